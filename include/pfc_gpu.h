@@ -1,0 +1,159 @@
+/*
+ * pfc_gpu.h — C ABI of the B200-native Partial-FC hot path (libpfc_gpu.so).
+ *
+ * Drop-in for the reference's distributed step
+ *   StepResult pfc::distributed_partial_step(std::vector<CenterShard>& shards,
+ *                                            const FeatureBatch& batch,
+ *                                            const StepConfig& cfg,
+ *                                            const SeededRng& iteration_rng)
+ *   (/root/reference/proj/include/pfc/shardsim.hpp:166-168)
+ * and of the pieces a caller touches around it:
+ *   ShardLayout / buffer_capacity         (proj/include/pfc/sampler.hpp:16-33, 50-57)
+ *   init_center_shards                    (proj/include/pfc/shardsim.hpp:56-82)
+ *   CenterShard weights / momentum        (proj/include/pfc/types.hpp:29-47)
+ *   StepConfig / MarginConfig             (shardsim.hpp:117-127, margin.hpp:17-37)
+ *   StepResult.{loss, d_features, trace, buffers} (shardsim.hpp:129-135)
+ *   error taxonomy                        (proj/include/pfc/error.hpp:9-42)
+ *
+ * Plain C types only (no torch / CUDA types): a context owns one GPU (one rank) and the
+ * class-sharded centre matrix W and its momentum for the reference shards
+ * [rank*K/world, (rank+1)*K/world).  Every entry point returns a pfc_status; on failure
+ * pfc_gpu_last_error() holds the reference's message text for the matching pfc::*Error.
+ * The C++ adapter include/pfc/gpu_step.hpp rethrows these as the reference exception types.
+ */
+#ifndef PFC_GPU_H_
+#define PFC_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PFC_OK = 0,
+  PFC_ERR_SHAPE = 1,      /* pfc::ShapeError */
+  PFC_ERR_CONTRACT = 2,   /* pfc::ContractError */
+  PFC_ERR_CAPACITY = 3,   /* pfc::CapacityError */
+  PFC_ERR_CONFIG = 4,     /* pfc::ConfigError */
+  PFC_ERR_NUMERICAL = 5,  /* pfc::NumericalError */
+  PFC_ERR_CUDA = 6,       /* CUDA runtime / driver failure (no reference counterpart) */
+  PFC_ERR_NCCL = 7        /* NCCL failure (no reference counterpart) */
+} pfc_status;
+
+typedef enum { /* MarginKind, margin.hpp:11 */
+  PFC_MARGIN_PLAIN = 0,
+  PFC_MARGIN_ADDITIVE_COSINE = 1, /* CosFace-style */
+  PFC_MARGIN_ADDITIVE_ANGULAR = 2 /* ArcFace-style */
+} pfc_margin_kind;
+
+typedef enum {
+  PFC_PRECISION_BF16 = 0, /* tcgen05 kind::f16 GEMMs, fp32 accumulate, fp32 master W / momentum */
+  PFC_PRECISION_FP32 = 1  /* fp32 validation mode: SIMT fp32 GEMMs, fp64 softmax / gradient stage */
+} pfc_precision;
+
+typedef struct {
+  int64_t num_classes;     /* C  (ShardLayout::num_classes) */
+  int64_t dim;             /* D  (embedding dimension) */
+  int64_t num_shards;      /* K  (ShardLayout::num_shards; the reference's shard count) */
+  int64_t max_batch;       /* largest global batch B the context will see (<= 8192) */
+  double r;                /* StepConfig::r */
+  int32_t margin_kind;     /* pfc_margin_kind */
+  double margin_scale;     /* MarginConfig::scale */
+  double margin_m;         /* MarginConfig::margin */
+  int32_t has_filter;      /* StepConfig::filter_threshold engaged */
+  double filter_threshold;
+  double momentum;         /* StepConfig::momentum */
+  double weight_decay;     /* StepConfig::weight_decay */
+  int32_t precision;       /* pfc_precision */
+  int32_t device;          /* CUDA device ordinal of this rank */
+  int32_t rank;            /* this process's rank, 0 <= rank < world_size */
+  int32_t world_size;      /* GPUs (ranks); must divide num_shards */
+  const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from pfc_gpu_nccl_unique_id (world_size > 1) */
+  int32_t flags;           /* PFC_FLAG_* */
+} pfc_gpu_desc;
+
+#define PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER 1 /* test hook: always use the exact sequential FY */
+#define PFC_FLAG_NO_GRAPH 2                  /* do not capture the step in a CUDA graph */
+
+typedef struct {
+  uint64_t seed;       /* iteration_rng.seed()      (rng.hpp:44) */
+  uint64_t stream_id;  /* iteration_rng.stream_id() (rng.hpp:45) */
+  double lr;           /* StepConfig::lr */
+  int64_t step_index;  /* StepConfig::step_index (error context only) */
+} pfc_gpu_step_args;
+
+typedef struct {
+  double loss;               /* StepResult::loss */
+  uint64_t allgather_bytes;  /* StepResult::trace, reference closed form (shardsim.hpp:192-193) */
+  uint64_t reduce_scalar_bytes;
+  uint64_t reduce_grad_bytes;
+  uint64_t reduce_ops;
+  int64_t capacity;          /* per-shard buffer size (buffer_capacity) */
+  int32_t rejection_shards;  /* shards that needed the exact sequential sampler this step */
+  int32_t reserved;
+} pfc_gpu_step_out;
+
+/* ---- lifecycle ------------------------------------------------------------------------ */
+int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out);
+int pfc_gpu_destroy(void* ctx);
+/* Message of the last failure on ctx (or of the last failed create on this thread if NULL). */
+const char* pfc_gpu_last_error(const void* ctx);
+int pfc_gpu_nccl_unique_id(uint8_t out[128]);
+const char* pfc_gpu_version(void);
+
+/* ---- shape queries (ShardLayout / buffer_capacity) ------------------------------------ */
+int64_t pfc_gpu_capacity(const void* ctx);
+int pfc_gpu_local_shards(const void* ctx, int64_t* first_shard, int64_t* num_local_shards);
+int pfc_gpu_shard_range(const void* ctx, int64_t shard, int64_t* class_begin, int64_t* class_end);
+
+/* ---- centre state (CenterShard weights / momentum, reference layout D x owned fp64) ----- */
+int pfc_gpu_set_shard(void* ctx, int64_t shard, const double* weights_d_by_owned,
+                      const double* momentum_d_by_owned /* NULL -> zeros */);
+int pfc_gpu_get_shard(void* ctx, int64_t shard, double* weights_d_by_owned,
+                      double* momentum_d_by_owned /* may be NULL */);
+/* init_center_shards on the device: per-class stream ("center-init", class), Box-Muller in
+ * fp64, unit-normalised, momentum = 0 (shardsim.hpp:56-82). */
+int pfc_gpu_init_shards(void* ctx, uint64_t seed);
+/* device pointers to the rank-local fp32 row-major [local classes x D] W and momentum */
+int pfc_gpu_device_state(void* ctx, float** weights, float** momentum, int64_t* rows);
+
+/* ---- the step --------------------------------------------------------------------------- */
+/* Drop-in (host buffers): batch is the already-gathered global batch like FeatureBatch:
+ * X is D x B row-major fp64, labels[B]; d_features_out receives the full D x B gradient
+ * summed over all shards (StepResult::d_features).  Synchronous. */
+int pfc_gpu_step(void* ctx, const double* features_d_by_b, const int64_t* labels, int64_t batch,
+                 const pfc_gpu_step_args* args, double* d_features_d_by_b,
+                 pfc_gpu_step_out* out);
+/* Device path: this rank's slice of the global batch (rank-major order), device pointers:
+ * x_local [b_local x D] fp32 row-major, labels_local [b_local] int64; dx_local [b_local x D]
+ * fp32 receives this rank's rows of the summed gradient (NCCL reduce-scatter when
+ * world_size > 1).  Enqueued on the context stream; with out != NULL it synchronises and
+ * validates, with out == NULL it returns immediately (call pfc_gpu_sync to validate). */
+int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_local,
+                        int64_t b_local, const pfc_gpu_step_args* args, float* dx_local,
+                        pfc_gpu_step_out* out);
+int pfc_gpu_sync(void* ctx, pfc_gpu_step_out* out);
+/* The last step's SampleBuffer of a local shard: cap class ids (positives ascending, then
+ * negatives in Fisher-Yates order) and num_positives (sampler.hpp:38-46). */
+int pfc_gpu_get_buffers(void* ctx, int64_t shard, int64_t* class_indices, int64_t* num_positives);
+/* The context's CUDA stream (cudaStream_t) for callers that enqueue around the step. */
+void* pfc_gpu_stream(void* ctx);
+
+/* ---- bench / test helpers --------------------------------------------------------------- */
+/* Synthetic inputs of the bench convention on the device:
+ * labels[b] = SeededRng(seed, make_stream("bench-labels", step)).next_below(C) and
+ * X[b][d] = SeededRng(seed, make_stream("bench-x", step)).next_normal() (b-major, d inner). */
+int pfc_gpu_bench_inputs(void* ctx, uint64_t seed, uint64_t step, int64_t batch, float* x_dev,
+                         int64_t* labels_dev);
+/* Kernel timing of the last step (ms, CUDA events around each phase); n <= 16 entries. */
+int pfc_gpu_phase_times(void* ctx, float* ms, const char** names, int n);
+int pfc_gpu_set_phase_timing(void* ctx, int enabled);
+/* Number of kernels (ours) launched by one step at the current batch shape. */
+int64_t pfc_gpu_launches_per_step(void* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFC_GPU_H_ */

@@ -1,0 +1,78 @@
+// common.cuh — device-side definitions shared by the PFC hot-path kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pfc {
+
+constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
+
+// reference rng.hpp:17-24 (murmur3 finaliser)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+// rng.hpp:49-51: stream id of SeededRng::fork(label)
+__host__ __device__ __forceinline__ uint64_t fork_stream(uint64_t stream, uint64_t label) {
+  return mix64(stream ^ mix64(label + kPhi));
+}
+// rng.hpp:53-56: draw number `counter` (1-based) of stream (seed, stream), as a pure function.
+__host__ __device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t stream) {
+  return mix64(seed + kPhi) ^ mix64(stream);
+}
+__host__ __device__ __forceinline__ uint64_t rng_draw(uint64_t key, uint64_t counter) {
+  return mix64(key + kPhi * counter);
+}
+
+// Device status block, read back once per step (SURVEY.md §5 failure detection).
+struct StepStatus {
+  double loss;
+  int32_t label_oob;          // 1 when some label is outside [0, C)
+  int32_t capacity_shard;     // first shard (global id) with npos > cap, else -1
+  int64_t oob_label;          // smallest out-of-range label (sorted order, as the reference)
+  int32_t capacity_npos;
+  int32_t masked_row;         // first row whose buffer columns are all masked, else INT32_MAX
+  int32_t nonfinite_loss;
+  int32_t nonfinite_dx;
+  int32_t rejection_shards;   // count of shards that needed the sequential sampler
+  int32_t batch_too_large;
+  int32_t pad[2];
+};
+
+enum MarginKindDev : int { kPlain = 0, kAddCos = 1, kAddAng = 2 };
+
+struct MarginDev {
+  int kind;
+  float s;       // scale (1 for plain)
+  double sd, md; // scale, margin in fp64 for the positive logit
+};
+
+constexpr double kAngularClamp = 1e-7;  // margin.hpp:15
+
+// apply_margin for the positive entry (margin.hpp:41-54), fp64 like the reference.
+__device__ __forceinline__ double margin_pos(const MarginDev& mg, double c) {
+  if (mg.kind == kPlain) return c;
+  if (mg.kind == kAddCos) return mg.sd * (c - mg.md);
+  const double lo = -1.0 + kAngularClamp, hi = 1.0 - kAngularClamp;
+  const double cc = c < lo ? lo : (hi < c ? hi : c);
+  return mg.sd * cos(acos(cc) + mg.md);
+}
+// margin_derivative for the positive entry (margin.hpp:58-72).
+__device__ __forceinline__ double margin_deriv_pos(const MarginDev& mg, double c) {
+  if (mg.kind == kPlain) return 1.0;
+  if (mg.kind == kAddCos) return mg.sd;
+  if (c <= -1.0 + kAngularClamp || c >= 1.0 - kAngularClamp) return 0.0;
+  const double th = acos(c);
+  return mg.sd * sin(th + mg.md) / sqrt(1.0 - c * c);
+}
+
+__device__ __forceinline__ float fast_exp(float x) { return __expf(x); }
+__device__ __forceinline__ double fast_exp(double x) { return exp(x); }
+
+}  // namespace pfc

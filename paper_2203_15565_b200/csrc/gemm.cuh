@@ -1,0 +1,271 @@
+// gemm.cuh — the two GEMM engines of the hot path.
+//
+//  * umma_gemm_kernel: persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//      warp 0      : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier complete_tx)
+//      warp 1      : single-thread tcgen05.mma issuer (kind::f16, bf16 in, fp32 accum in TMEM)
+//      warp 2      : TMEM allocator (2 x BN columns: double-buffered accumulators)
+//      warps 4..7  : epilogue (tcgen05.ld 32x32b -> registers -> fused epilogue functor)
+//    Tile = 128 x BN, BK = 64, STAGES-deep smem ring.  A and B may each be K-major or
+//    MN-major (UMMA descriptor transpose bits), so one gathered centre block and one
+//    normalised feature block serve all three GEMMs of the step without transposes.
+//  * simt_gemm_kernel: fp32 CUDA-core GEMM used by the fp32 validation mode; it feeds the
+//    SAME epilogue functors (thread = accumulator row, 32-column chunks), BN = 64.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace pfc {
+
+struct TileInfo {
+  int m_tile, n_tile, split;
+  int row0, col0;
+  int kb0, kb1;
+};
+
+struct GemmGeom {
+  int M, N, K;
+  int m_tiles, n_tiles, splits, kb_per_split, kb_total;
+  int n_fastest;  // tile order: 0 -> m fastest, 1 -> n fastest
+  int BN, BK;
+  __host__ __device__ int total() const { return m_tiles * n_tiles * splits; }
+  __host__ __device__ TileInfo tile(int t) const {
+    TileInfo ti;
+    const int mn = m_tiles * n_tiles;
+    ti.split = t / mn;
+    const int r = t % mn;
+    if (n_fastest) {
+      ti.n_tile = r % n_tiles;
+      ti.m_tile = r / n_tiles;
+    } else {
+      ti.m_tile = r % m_tiles;
+      ti.n_tile = r / m_tiles;
+    }
+    ti.row0 = ti.m_tile * 128;
+    ti.col0 = ti.n_tile * BN;
+    ti.kb0 = ti.split * kb_per_split;
+    ti.kb1 = ti.kb0 + kb_per_split < kb_total ? ti.kb0 + kb_per_split : kb_total;
+    return ti;
+  }
+};
+
+inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest) {
+  GemmGeom g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.BN = BN;
+  g.BK = 64;
+  g.m_tiles = (M + 127) / 128;
+  g.n_tiles = (N + BN - 1) / BN;
+  g.kb_total = (K + 63) / 64;
+  if (splits < 1) splits = 1;
+  if (splits > g.kb_total) splits = g.kb_total;
+  g.kb_per_split = (g.kb_total + splits - 1) / splits;
+  g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
+  g.n_fastest = n_fastest;
+  return g;
+}
+
+constexpr int kEpiSmemBytes = 20 * 1024;
+
+template <int BN, int STAGES>
+constexpr int umma_smem_bytes() {
+  return 1024 /*align slack*/ + STAGES * (128 * 64 * 2 + BN * 64 * 2) + 256 /*barriers*/ +
+         kEpiSmemBytes;
+}
+
+struct TmemSrc {
+  uint32_t taddr;  // lane field already set for this warp
+  __device__ __forceinline__ void load(int c0, float (&v)[32]) const {
+    pfc_sm100::tmem_ld32(taddr + (uint32_t)c0, v);
+  }
+};
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(256, 1)
+    umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const GemmGeom g, const Epi epi) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  using namespace pfc_sm100;
+  constexpr uint32_t A_BYTES = 128 * 64 * 2;
+  constexpr uint32_t B_BYTES = BN * 64 * 2;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+  static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "tmem cols pow2");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_smem = smem + STAGES * STAGE_BYTES + 256;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = g.total();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t kbc = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileInfo ti = g.tile(t);
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb, ++kbc) {
+          const uint32_t s = kbc % STAGES, ph = (kbc / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          const int k0 = kb * 64;
+          uint8_t* a = sA + s * A_BYTES;
+          uint8_t* b = sB + s * B_BYTES;
+          if (!A_MN) {
+            tma_load_2d(&tmA, &full[s], a, k0, ti.row0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) tma_load_2d(&tmA, &full[s], a + i * 8192, ti.row0 + 64 * i, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(&tmB, &full[s], b, k0, ti.col0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_2d(&tmB, &full[s], b + i * 8192, ti.col0 + 64 * i, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, BN, A_MN, B_MN);
+      uint32_t kbc = 0, it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const TileInfo ti = g.tile(t);
+        const uint32_t as = it & 1, aph = (it >> 1) & 1;
+        mbar_wait(&tempty[as], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb, ++kbc) {
+          const uint32_t s = kbc % STAGES, ph = (kbc / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(a_base + k * 32, 0, 1024);
+            const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(b_base + k * 32, 0, 1024);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb > ti.kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int tid = threadIdx.x - 128;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      const TileInfo ti = g.tile(t);
+      const uint32_t as = it & 1, aph = (it >> 1) & 1;
+      mbar_wait(&tfull[as], aph);
+      tc_fence_after();
+      const TmemSrc src{tmem_base + as * BN + ((uint32_t)((warp & 3) * 32) << 16)};
+      epi.template run<BN>(ti, src, tid, epi_smem);
+      tc_fence_before();
+      mbar_arrive(&tempty[as]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
+#endif
+}
+
+// ---------------------------------------------------------------- SIMT fp32 engine
+struct SmemRowSrc {  // accumulator row of this thread, staged in shared memory (stride 65)
+  const float* row;
+  __device__ __forceinline__ void load(int c0, float (&v)[32]) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = row[c0 + j];
+  }
+};
+
+// A(m,k) = A_MN ? A[k*lda + m] : A[m*lda + k];  B(n,k) = B_MN ? B[k*ldb + n] : B[n*ldb + k].
+template <bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(128)
+    simt_gemm_kernel(const float* __restrict__ A, int lda, const float* __restrict__ Bm, int ldb,
+                     const GemmGeom g, const Epi epi) {
+  constexpr int BN = 64, KC = 32;
+  extern __shared__ uint8_t smem_raw[];
+  float* sA = reinterpret_cast<float*>(smem_raw);  // [KC][129]
+  float* sB = sA + KC * 129;                        // [KC][BN]
+  float* sAcc = sB + KC * BN;                       // [128][65]
+  uint8_t* epi_smem = reinterpret_cast<uint8_t*>(sAcc + 128 * 65);
+  const int tid = threadIdx.x;
+  const TileInfo ti = g.tile(blockIdx.x);
+  float acc[BN];
+#pragma unroll
+  for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+  const int k_begin = ti.kb0 * 64;
+  const int k_end = min(g.K, ti.kb1 * 64);
+  for (int kc = k_begin; kc < k_end; kc += KC) {
+    for (int e = tid; e < KC * 128; e += 128) {
+      const int kk = A_MN ? e / 128 : e % KC;
+      const int mm = A_MN ? e % 128 : e / KC;
+      const int m = ti.row0 + mm, k = kc + kk;
+      float v = 0.f;
+      if (m < g.M && k < k_end) v = A_MN ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k];
+      sA[kk * 129 + mm] = v;
+    }
+    for (int e = tid; e < KC * BN; e += 128) {
+      const int kk = B_MN ? e / BN : e % KC;
+      const int nn = B_MN ? e % BN : e / KC;
+      const int n = ti.col0 + nn, k = kc + kk;
+      float v = 0.f;
+      if (n < g.N && k < k_end) v = B_MN ? Bm[(int64_t)k * ldb + n] : Bm[(int64_t)n * ldb + k];
+      sB[kk * BN + nn] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < KC; ++kk) {
+      const float a = sA[kk * 129 + tid];
+#pragma unroll
+      for (int j = 0; j < BN; ++j) acc[j] = fmaf(a, sB[kk * BN + j], acc[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < BN; ++j) sAcc[tid * 65 + j] = acc[j];
+  const SmemRowSrc src{sAcc + tid * 65};
+  epi.template run<BN>(ti, src, tid, epi_smem);
+}
+
+constexpr int kSimtSmemBytes = (32 * 129 + 32 * 64 + 128 * 65) * 4 + kEpiSmemBytes;
+
+}  // namespace pfc

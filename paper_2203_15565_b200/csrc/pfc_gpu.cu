@@ -1,0 +1,952 @@
+// pfc_gpu.cu — host orchestration of the B200-native Partial-FC step and the C ABI of
+// include/pfc_gpu.h.  One context = one rank = one GPU; it owns the fp32 row-major W and
+// momentum of its reference shards and runs
+//
+//   [NCCL all-gather labels, X]  (world > 1)
+//   sampler (bit-exact build_buffers)                 sampler.cu
+//   normalise X, gather+normalise sampled W rows      kernels.cuh
+//   logits GEMM + margin + online softmax partials    tcgen05 GEMM, FwdStatsEpi
+//   merge partials [NCCL all-gather of (max,sum), all-reduce z_pos]  -> loss
+//   recompute logits GEMM -> G, feat/center proj      tcgen05 GEMM, GradEpi
+//   dX = G W^ (split-K) + correction [NCCL reduce-scatter]   tcgen05 GEMM, DxPartEpi
+//   dW = G^T X^ -> fused sparse momentum-SGD          tcgen05 GEMM, DwUpdateEpi
+//
+// mirroring pfc::distributed_partial_step (proj/include/pfc/shardsim.hpp:166-420).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pfc_gpu.h"
+#include "common.cuh"
+#include "epilogues.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "sampler.cu"
+
+namespace pfc {
+namespace {
+
+thread_local std::string g_create_error;
+
+// ------------------------------------------------------------------ NCCL (dlopen'ed lazily)
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+enum { ncclInt8 = 0, ncclInt64 = 4, ncclFloat32 = 7, ncclFloat64 = 8 };
+enum { ncclSum = 0 };
+struct Nccl {
+  void* h = nullptr;
+  int (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) {
+      err = "NCCL not found (dlopen libnccl.so.2 failed)";
+      return false;
+    }
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+    ReduceScatter = (decltype(ReduceScatter))dlsym(h, "ncclReduceScatter");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllGather || !AllReduce || !ReduceScatter) {
+      err = "NCCL symbols missing";
+      return false;
+    }
+    return true;
+  }
+};
+Nccl g_nccl;
+
+// ------------------------------------------------------------------ TMA descriptor encode
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [outer][inner] with row stride ld (elements); box {64, box_outer}, 128B swizzle.
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_outer) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+constexpr int kBN = 256, kStages = 4;  // tcgen05 tile 128 x 256, 4-stage ring
+constexpr int kSimtBN = 64;
+
+struct PhaseTimer {
+  bool enabled = false;
+  static constexpr int kMax = 16;
+  cudaEvent_t ev[kMax + 1] = {};
+  const char* names[kMax] = {};
+  int n = 0;
+  float ms[kMax] = {};
+};
+
+struct Ctx {
+  pfc_gpu_desc d{};
+  std::string err;
+  int64_t C, D, K, Dp, blk, cap, k0, nk, cls_lo, cls_hi, rows, ncols, ncols_pad, ldg;
+  int64_t pool_stride, maxB;
+  int R, rank;
+  bool bf16;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  MarginDev mg{};
+  // state
+  float* W = nullptr;
+  float* M = nullptr;
+  // sampler
+  int64_t* labels = nullptr;  // global batch labels (world > 1 / host path)
+  int64_t* uniq = nullptr;
+  ShardMeta* meta = nullptr;
+  int32_t* buf_cls = nullptr;
+  int32_t* pos_col = nullptr;
+  int32_t* head = nullptr;
+  int32_t* nxt = nullptr;
+  int32_t* jv = nullptr;
+  int32_t* pool_scratch = nullptr;
+  // features / centres
+  float* X = nullptr;  // global batch rows [B][D] fp32 (world > 1 / host path)
+  float* xnorm = nullptr;
+  void* xh = nullptr;  // [maxB][Dp] bf16 or fp32
+  void* wh = nullptr;  // [ncols_pad][Dp]
+  float* wnorm = nullptr;
+  int32_t* lrow = nullptr;
+  // softmax statistics
+  void* part_m = nullptr;  // [T][maxB]
+  void* part_s = nullptr;
+  void* lm = nullptr;      // [R][maxB]
+  void* ls = nullptr;
+  void* gmax = nullptr;
+  void* inv_gsum = nullptr;
+  double* zpos = nullptr;
+  double* loss_row = nullptr;
+  // backward
+  void* G = nullptr;       // [maxB][ldg]
+  void* fproj = nullptr;   // [T][maxB]
+  void* cproj = nullptr;   // [mt][ncols]
+  float* dx_part = nullptr;  // [S][maxB][D]
+  float* dX = nullptr;       // [maxB][D]
+  int max_splits = 1;
+  // host-path scratch
+  double* xdb = nullptr;  // D x maxB fp64
+  StepStatus* st = nullptr;
+  StepStatus* st_host = nullptr;
+  // tensor maps cached per batch
+  int64_t tm_B = -1;
+  CUtensorMap tm_x_k, tm_w_k, tm_g_mn, tm_x_mn, tm_g_k, tm_w_mn;
+  // nccl
+  ncclComm_t comm = nullptr;
+  // bookkeeping
+  int64_t lastB = 0;
+  int64_t launches = 0;
+  PhaseTimer pt;
+  std::vector<void*> allocs;
+};
+
+int fail(Ctx* c, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  else g_create_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(c, expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail((c), PFC_ERR_CUDA, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_),    \
+                  __FILE__, __LINE__, cudaGetErrorString(e_));                              \
+  } while (0)
+
+#define NCCL_TRY(c, expr)                                                                   \
+  do {                                                                                      \
+    int r_ = (expr);                                                                        \
+    if (r_ != 0)                                                                            \
+      return fail((c), PFC_ERR_NCCL, "NCCL error %d (%s) at %s:%d", r_,                     \
+                  g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "?", __FILE__, __LINE__); \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(Ctx* c, T** p, size_t n) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, n * sizeof(T) + 256);
+  if (e == cudaSuccess) {
+    c->allocs.push_back(q);
+    cudaMemset(q, 0, n * sizeof(T) + 256);
+  }
+  *p = static_cast<T*>(q);
+  return e;
+}
+
+void phase(Ctx* c, const char* name) {
+  if (!c->pt.enabled || c->pt.n >= PhaseTimer::kMax) return;
+  c->pt.names[c->pt.n] = name;
+  cudaEventRecord(c->pt.ev[c->pt.n + 1], c->stream);
+  c->pt.n++;
+}
+
+// ------------------------------------------------------------------ GEMM launchers
+template <int BN, bool A_MN, bool B_MN, class Epi>
+cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, const GemmGeom& g,
+                        const Epi& epi) {
+  auto kern = umma_gemm_kernel<BN, kStages, A_MN, B_MN, Epi>;
+  constexpr int smem = umma_smem_bytes<BN, kStages>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int total = g.total();
+  const int grid = total < c->num_sms ? total : c->num_sms;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, 256, smem, c->stream>>>(ta, tb, g, epi);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN, class Epi>
+cudaError_t launch_simt(Ctx* c, const float* A, int lda, const float* Bm, int ldb,
+                        const GemmGeom& g, const Epi& epi) {
+  auto kern = simt_gemm_kernel<A_MN, B_MN, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimtSmemBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (g.total() <= 0) return cudaSuccess;
+  kern<<<g.total(), 128, kSimtSmemBytes, c->stream>>>(A, lda, Bm, ldb, g, epi);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+int ensure_maps(Ctx* c, int64_t B) {
+  if (!c->bf16 || c->tm_B == B) return PFC_OK;
+  bool ok = true;
+  // logits / G GEMMs: A = X^ [B][Dp] K-major, B = W^ [ncols][Dp] K-major
+  ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128);
+  ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kBN);
+  // dW GEMM: A = G as [B rows][ncols cols], MN-major (classes contiguous); B = X^ MN-major
+  ok &= make_map(&c->tm_g_mn, c->G, c->ncols, B, c->ldg, 64);
+  ok &= make_map(&c->tm_x_mn, c->xh, c->Dp, B, c->Dp, 64);
+  // dX GEMM: A = G K-major (classes contiguous = K); B = W^ MN-major (D contiguous = N)
+  ok &= make_map(&c->tm_g_k, c->G, c->ncols, B, c->ldg, 128);
+  ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, 64);
+  if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  c->tm_B = B;
+  return PFC_OK;
+}
+
+int dx_splits(Ctx* c, int64_t B) {
+  if (c->bf16) {
+    const int64_t tiles = ceil_div(B, 128) * ceil_div(c->D, kBN);
+    int64_t s = c->num_sms / (tiles > 0 ? tiles : 1);
+    if (s < 1) s = 1;
+    return (int)std::min<int64_t>(s, c->max_splits);
+  }
+  const int64_t tiles = ceil_div(B, 128) * ceil_div(c->D, kSimtBN);
+  int64_t s = (2 * c->num_sms) / (tiles > 0 ? tiles : 1);
+  if (s < 1) s = 1;
+  return (int)std::min<int64_t>(s, c->max_splits);
+}
+
+// The device pipeline for one step on a gathered global batch of B rows.
+// x: [B][D] fp32 rows; lab: [B] int64 (device).  Writes the rank-local partial dX into
+// dx_full ([B][D]).
+template <typename ST, typename OT, bool kUmma>
+int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
+                 const pfc_gpu_step_args* a, float* dx_full) {
+  cudaStream_t s = c->stream;
+  const int bs = 256;
+  if (int rc = ensure_maps(c, B)) return rc;
+  CUDA_TRY(c, cudaMemsetAsync(c->st, 0, sizeof(StepStatus), s));
+  {
+    StepStatus init{};
+    init.capacity_shard = -1;
+    init.masked_row = 0x7fffffff;
+    *c->st_host = init;
+    CUDA_TRY(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(StepStatus), cudaMemcpyHostToDevice, s));
+  }
+  // ---- sampler (build_buffers, sampler.hpp:63-126)
+  const size_t sort_smem = sizeof(int64_t) * kMaxSortBatch;
+  static bool sort_cfg = false;
+  if (!sort_cfg) {
+    CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sort_smem));
+    sort_cfg = true;
+  }
+  positives_kernel<<<1, 1024, sort_smem, s>>>(
+      lab, (int)B, c->C, (int)c->K, c->blk, (int)c->cap, (int)c->k0, (int)c->nk, c->uniq,
+      c->meta, c->buf_cls, c->pos_col, c->st, (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0);
+  c->launches++;
+  CUDA_TRY(c, cudaMemsetAsync(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride, s));
+  const int64_t nd = c->nk * c->cap;
+  draws_kernel<<<(unsigned)ceil_div(nd, bs), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap, a->seed,
+                                                         a->stream_id, (int)c->k0, c->pool_stride,
+                                                         c->head, c->nxt, c->jv, c->st);
+  walk_kernel<<<(unsigned)ceil_div(nd, bs), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap,
+                                                        c->pool_stride, c->head, c->nxt, c->jv,
+                                                        c->buf_cls, c->st);
+  sequential_fallback_kernel<<<(unsigned)c->nk, 256, 0, s>>>(c->meta, (int)c->cap, a->seed,
+                                                             a->stream_id, (int)c->k0,
+                                                             c->pool_stride, c->pool_scratch,
+                                                             c->buf_cls, c->st);
+  c->launches += 3;
+  phase(c, "sampler");
+  // ---- normalise features, gather + normalise sampled centres
+  OT* xh = static_cast<OT*>(c->xh);
+  OT* wh = static_cast<OT*>(c->wh);
+  normalize_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(x, (int)B, (int)c->D,
+                                                                       (int)c->Dp, xh, c->xnorm);
+  gather_w_kernel<OT><<<(unsigned)ceil_div(c->ncols_pad * 32, bs), bs, 0, s>>>(
+      c->W, (int)c->D, (int)c->Dp, c->buf_cls, (int)c->ncols, (int)c->ncols_pad, c->cls_lo,
+      c->rows, wh, c->wnorm, c->lrow, c->st);
+  c->launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  phase(c, "gather");
+  CUDA_TRY(c, cudaMemsetAsync(c->zpos, 0, sizeof(double) * B, s));
+
+  constexpr int BN = kUmma ? kBN : kSimtBN;
+  ST* pm = static_cast<ST*>(c->part_m);
+  ST* ps = static_cast<ST*>(c->part_s);
+  const float tau = (float)c->d.filter_threshold;
+  // ---- logits GEMM + margin + online softmax partials (shardsim.hpp:249-318)
+  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, BN, 1, 0);
+  {
+    FwdStatsEpi<ST> e{(int)B, (int)c->ncols, c->pos_col, c->mg, c->d.has_filter, tau, pm, ps,
+                      c->zpos};
+    cudaError_t err;
+    if constexpr (kUmma) err = launch_umma<kBN, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
+    else err = launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp, (const float*)c->wh,
+                                         (int)c->Dp, gf, e);
+    CUDA_TRY(c, err);
+  }
+  phase(c, "logits_gemm");
+  // ---- softmax statistics: tiles -> rank-local, then across ranks (collectives 1 + 2)
+  const int T = gf.n_tiles;
+  ST* lm = static_cast<ST*>(c->lm);
+  ST* ls = static_cast<ST*>(c->ls);
+  merge_tiles_kernel<ST><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(pm, ps, T, (int)B,
+                                                                       lm + c->rank * B,
+                                                                       ls + c->rank * B);
+  c->launches++;
+  if (c->R > 1) {
+    const int dt = sizeof(ST) == 8 ? ncclFloat64 : ncclFloat32;
+    NCCL_TRY(c, g_nccl.AllGather(lm + c->rank * B, lm, B, dt, c->comm, s));
+    NCCL_TRY(c, g_nccl.AllGather(ls + c->rank * B, ls, B, dt, c->comm, s));
+    NCCL_TRY(c, g_nccl.AllReduce(c->zpos, c->zpos, B, ncclFloat64, ncclSum, c->comm, s));
+  }
+  ST* gm = static_cast<ST*>(c->gmax);
+  ST* ig = static_cast<ST*>(c->inv_gsum);
+  merge_ranks_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(lm, ls, c->R, (int)B, c->zpos,
+                                                                  gm, ig, c->loss_row, c->st);
+  loss_reduce_kernel<<<1, 1024, 0, s>>>(c->loss_row, (int)B, c->st);
+  c->launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  phase(c, "softmax_stats");
+  // ---- G = dL/dcos (recomputed logits), feat_proj / center_proj partials (shardsim.hpp:341-362)
+  ST* fp = static_cast<ST*>(c->fproj);
+  ST* cp = static_cast<ST*>(c->cproj);
+  {
+    GradEpi<ST, OT> e{(int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, c->d.has_filter, tau,
+                      gm, ig, (ST)(1.0 / (double)B), static_cast<OT*>(c->G), fp, cp};
+    cudaError_t err;
+    if constexpr (kUmma) err = launch_umma<kBN, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
+    else err = launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp, (const float*)c->wh,
+                                         (int)c->Dp, gf, e);
+    CUDA_TRY(c, err);
+  }
+  phase(c, "grad_gemm");
+  // ---- dX = sum_j g_bj w^_j (split-K), then (acc - feat_proj x^)/|x| (shardsim.hpp:363-376)
+  {
+    const int S = dx_splits(c, B);
+    const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0);
+    DxPartEpi e{(int)B, (int)c->D, c->dx_part};
+    cudaError_t err;
+    if constexpr (kUmma) err = launch_umma<kBN, false, true>(c, c->tm_g_k, c->tm_w_mn, gx, e);
+    else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
+                                        (int)c->Dp, gx, e);
+    CUDA_TRY(c, err);
+    dx_finalize_kernel<ST><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, fp, T, x, c->xnorm,
+                                                       (int)B, (int)c->D, dx_full, c->st);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  phase(c, "dx_gemm");
+  // ---- dW = sum_b g_bj x^_b, corrected, fused momentum-SGD on sampled rows (shardsim.hpp:377-417)
+  {
+    const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
+    DwUpdateEpi<ST> e{(int)c->ncols, (int)c->D, gf.m_tiles, c->wnorm, c->lrow, cp, c->W, c->M,
+                      (float)a->lr, (float)c->d.momentum, (float)c->d.weight_decay, c->st};
+    cudaError_t err;
+    if constexpr (kUmma) err = launch_umma<kBN, true, true>(c, c->tm_g_mn, c->tm_x_mn, gw, e);
+    else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
+                                       (int)c->Dp, gw, e);
+    CUDA_TRY(c, err);
+  }
+  phase(c, "dw_update_gemm");
+  return PFC_OK;
+}
+
+int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gpu_step_args* a,
+             float* dx_full) {
+  if (c->pt.enabled) {
+    c->pt.n = 0;
+    cudaEventRecord(c->pt.ev[0], c->stream);
+  }
+  c->launches = 0;
+  c->lastB = B;
+  if (c->bf16) return run_pipeline<float, __nv_bfloat16, true>(c, x, lab, B, a, dx_full);
+  return run_pipeline<double, float, false>(c, x, lab, B, a, dx_full);
+}
+
+void trace_closed_form(Ctx* c, int64_t B, pfc_gpu_step_out* o) {
+  // reference accounting (shardsim.hpp:192-193, 327-328, 395-398)
+  const uint64_t K = (uint64_t)c->K, b = (uint64_t)B, dd = (uint64_t)c->D;
+  o->allgather_bytes = (K - 1) * b * dd * 8;
+  o->reduce_scalar_bytes = (K - 1) * b * 2 * 2 * 8;
+  o->reduce_grad_bytes = (K - 1) * b * dd * 2 * 8;
+  o->reduce_ops = 3;
+  o->capacity = c->cap;
+}
+
+// Check the device status block; map to the reference's error types and messages.
+int check_status(Ctx* c, int64_t step_index, int64_t B, pfc_gpu_step_out* out) {
+  const StepStatus& st = *c->st_host;
+  if (st.batch_too_large)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: global batch %lld exceeds the supported %d",
+                (long long)B, kMaxSortBatch);
+  if (st.label_oob)
+    return fail(c, PFC_ERR_CONTRACT, "build_buffers: label %lld outside [0, %lld)",
+                (long long)st.oob_label, (long long)c->C);
+  if (st.capacity_shard >= 0) {
+    const int64_t k = st.capacity_shard;
+    const int64_t lo = std::min(k * c->blk, c->C), hi = std::min((k + 1) * c->blk, c->C);
+    if (st.capacity_npos > c->cap)
+      return fail(c, PFC_ERR_CAPACITY,
+                  "build_buffers: shard %lld received %d distinct positives but capacity is %lld; "
+                  "increase the sampling ratio r or the shard count",
+                  (long long)k, st.capacity_npos, (long long)c->cap);
+    return fail(c, PFC_ERR_CAPACITY,
+                "build_buffers: shard %lld owns only %lld classes but capacity is %lld (C must "
+                "divide evenly enough across K at this r)",
+                (long long)k, (long long)(hi - lo), (long long)c->cap);
+  }
+  if (st.masked_row != 0x7fffffff)
+    return fail(c, PFC_ERR_CONTRACT,
+                "distributed_partial_step: all buffer columns masked for row %d", st.masked_row);
+  if (st.nonfinite_loss)
+    return fail(c, PFC_ERR_NUMERICAL, "distributed_partial_step: non-finite loss at step %lld",
+                (long long)step_index);
+  if (st.nonfinite_dx)
+    return fail(c, PFC_ERR_NUMERICAL,
+                "distributed_partial_step d_features: non-finite entry in %lldx%lld result",
+                (long long)c->D, (long long)B);
+  if (out) {
+    out->loss = st.loss;
+    out->rejection_shards = st.rejection_shards;
+    trace_closed_form(c, B, out);
+  }
+  return PFC_OK;
+}
+
+int finish_phase_timing(Ctx* c) {
+  if (!c->pt.enabled) return PFC_OK;
+  CUDA_TRY(c, cudaEventSynchronize(c->pt.ev[c->pt.n]));
+  for (int i = 0; i < c->pt.n; ++i) cudaEventElapsedTime(&c->pt.ms[i], c->pt.ev[i], c->pt.ev[i + 1]);
+  return PFC_OK;
+}
+
+// Host-side replica of build_buffers' validation (sampler.hpp:68-98) for the host-buffer
+// path, so errors are raised with the reference's text before any device work.
+int host_validate(Ctx* c, const int64_t* labels, int64_t B) {
+  std::vector<int64_t> s(labels, labels + B);
+  std::sort(s.begin(), s.end());
+  s.erase(std::unique(s.begin(), s.end()), s.end());
+  for (int64_t v : s)
+    if (v < 0 || v >= c->C)
+      return fail(c, PFC_ERR_CONTRACT, "build_buffers: label %lld outside [0, %lld)", (long long)v,
+                  (long long)c->C);
+  size_t p = 0;
+  for (int64_t k = 0; k < c->K; ++k) {
+    const int64_t lo = std::min(k * c->blk, c->C), hi = std::min((k + 1) * c->blk, c->C);
+    int64_t np = 0;
+    while (p < s.size() && s[p] < hi) {
+      ++np;
+      ++p;
+    }
+    if (np > c->cap)
+      return fail(c, PFC_ERR_CAPACITY,
+                  "build_buffers: shard %lld received %lld distinct positives but capacity is "
+                  "%lld; increase the sampling ratio r or the shard count",
+                  (long long)k, (long long)np, (long long)c->cap);
+    if (hi - lo < c->cap)
+      return fail(c, PFC_ERR_CAPACITY,
+                  "build_buffers: shard %lld owns only %lld classes but capacity is %lld (C must "
+                  "divide evenly enough across K at this r)",
+                  (long long)k, (long long)(hi - lo), (long long)c->cap);
+  }
+  return PFC_OK;
+}
+
+int validate_desc(const pfc_gpu_desc* d) {
+  if (!d) return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: null descriptor");
+  if (d->num_classes < 1 || d->num_shards < 1)
+    return fail(nullptr, PFC_ERR_CONTRACT, "ShardLayout: need at least one class and one shard");
+  if (!(d->r > 0.0 && d->r <= 1.0))
+    return fail(nullptr, PFC_ERR_CONTRACT, "buffer_capacity: sampling ratio must lie in (0, 1]");
+  if (!(d->margin_scale > 0.0))
+    return fail(nullptr, PFC_ERR_CONFIG, "margin: scale must be positive");
+  if (d->margin_m < 0.0 || d->margin_m >= 1.0)
+    return fail(nullptr, PFC_ERR_CONFIG, "margin: m must be in [0, 1)");
+  if (d->margin_kind == PFC_MARGIN_PLAIN && (d->margin_scale != 1.0 || d->margin_m != 0.0))
+    return fail(nullptr, PFC_ERR_CONFIG, "margin: plain kind requires s=1, m=0");
+  if (d->margin_kind < 0 || d->margin_kind > 2)
+    return fail(nullptr, PFC_ERR_CONTRACT, "apply_margin: unknown kind");
+  if (d->dim < 1) return fail(nullptr, PFC_ERR_SHAPE, "pfc_gpu_create: dim must be >= 1");
+  if (d->max_batch < 1 || d->max_batch > kMaxSortBatch)
+    return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: max_batch must be in [1, %d]",
+                kMaxSortBatch);
+  if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size ||
+      d->num_shards % d->world_size != 0)
+    return fail(nullptr, PFC_ERR_CONTRACT,
+                "pfc_gpu_create: world_size must divide num_shards and 0 <= rank < world_size");
+  if (d->num_classes >= (int64_t)INT32_MAX)
+    return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: num_classes must be < 2^31");
+  return PFC_OK;
+}
+
+}  // namespace
+}  // namespace pfc
+
+using namespace pfc;
+
+extern "C" {
+
+const char* pfc_gpu_version(void) { return "pfc_gpu 0.1 (sm_100a tcgen05)"; }
+
+const char* pfc_gpu_last_error(const void* ctx) {
+  if (!ctx) return g_create_error.c_str();
+  return static_cast<const Ctx*>(ctx)->err.c_str();
+}
+
+int pfc_gpu_nccl_unique_id(uint8_t out[128]) {
+  std::string e;
+  if (!g_nccl.load(e)) return fail(nullptr, PFC_ERR_NCCL, "%s", e.c_str());
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != 0) return fail(nullptr, PFC_ERR_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(out, id.internal, 128);
+  return PFC_OK;
+}
+
+int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
+  if (int rc = validate_desc(desc)) return rc;
+  Ctx* c = new Ctx();
+  c->d = *desc;
+  c->C = desc->num_classes;
+  c->D = desc->dim;
+  c->K = desc->num_shards;
+  c->R = desc->world_size;
+  c->rank = desc->rank;
+  c->bf16 = desc->precision == PFC_PRECISION_BF16;
+  c->Dp = round_up(c->D, 64);
+  c->blk = ceil_div(c->C, c->K);
+  {
+    const double want = (double)c->C * desc->r;
+    const int64_t total = (int64_t)std::ceil(want - 1e-9);
+    c->cap = (total + c->K - 1) / c->K;  // buffer_capacity (sampler.hpp:50-57)
+  }
+  c->nk = c->K / c->R;
+  c->k0 = (int64_t)c->rank * c->nk;
+  c->cls_lo = std::min(c->k0 * c->blk, c->C);
+  c->cls_hi = std::min((c->k0 + c->nk) * c->blk, c->C);
+  c->rows = c->cls_hi - c->cls_lo;
+  c->ncols = c->nk * c->cap;
+  c->ncols_pad = round_up(std::max<int64_t>(c->ncols, 1), 256);
+  c->ldg = round_up(std::max<int64_t>(c->ncols, 1), 8);
+  c->pool_stride = std::max<int64_t>(c->blk, 1);
+  c->maxB = desc->max_batch;
+  c->mg.kind = desc->margin_kind;
+  c->mg.s = (float)desc->margin_scale;
+  c->mg.sd = desc->margin_scale;
+  c->mg.md = desc->margin_m;
+  int64_t B = c->maxB;
+  auto bail = [&](int rc) {
+    g_create_error = c->err;
+    pfc_gpu_destroy(c);
+    return rc;
+  };
+#define CT(expr)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return bail(fail(c, PFC_ERR_CUDA, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), \
+                       __FILE__, __LINE__, cudaGetErrorString(e_)));                     \
+  } while (0)
+  CT(cudaSetDevice(desc->device));
+  {
+    int major = 0, minor = 0;
+    CT(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, desc->device));
+    CT(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, desc->device));
+    if (major != 10 || minor != 0)
+      return bail(fail(c, PFC_ERR_CUDA, "pfc_gpu requires an sm_100 (B200) device, got sm_%d%d",
+                       major, minor));
+    CT(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, desc->device));
+  }
+  CT(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  const size_t ob = c->bf16 ? 2 : 4;  // operand bytes
+  const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
+  const int BN = c->bf16 ? kBN : kSimtBN;
+  const int64_t T = ceil_div(std::max<int64_t>(c->ncols, 1), BN);
+  const int64_t mt = ceil_div(B, 128);
+  c->max_splits = c->bf16 ? 32 : 64;
+  CT(dalloc(c, &c->W, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
+  CT(dalloc(c, &c->M, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
+  CT(dalloc(c, &c->labels, (size_t)B));
+  CT(dalloc(c, &c->uniq, (size_t)B));
+  CT(dalloc(c, &c->meta, (size_t)c->nk));
+  CT(dalloc(c, &c->buf_cls, (size_t)std::max<int64_t>(c->ncols, 1)));
+  CT(dalloc(c, &c->pos_col, (size_t)B));
+  CT(dalloc(c, &c->head, (size_t)(c->nk * c->pool_stride)));
+  CT(dalloc(c, &c->nxt, (size_t)std::max<int64_t>(c->ncols, 1)));
+  CT(dalloc(c, &c->jv, (size_t)std::max<int64_t>(c->ncols, 1)));
+  CT(dalloc(c, &c->pool_scratch, (size_t)(c->nk * c->pool_stride)));
+  CT(dalloc(c, &c->X, (size_t)B * c->D));
+  CT(dalloc(c, &c->xnorm, (size_t)B));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->xh), (size_t)B * c->Dp * ob));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->wh), (size_t)c->ncols_pad * c->Dp * ob));
+  CT(dalloc(c, &c->wnorm, (size_t)c->ncols_pad));
+  CT(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_m), (size_t)(T * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(T * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->lm), (size_t)(c->R * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->ls), (size_t)(c->R * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->gmax), (size_t)B * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->inv_gsum), (size_t)B * sb));
+  CT(dalloc(c, &c->zpos, (size_t)B));
+  CT(dalloc(c, &c->loss_row, (size_t)B));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)B * c->ldg * ob));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->fproj), (size_t)(T * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->cproj),
+            (size_t)(mt * std::max<int64_t>(c->ncols, 1)) * sb));
+  CT(dalloc(c, &c->dx_part, (size_t)c->max_splits * B * c->D));
+  CT(dalloc(c, &c->dX, (size_t)B * c->D));
+  CT(dalloc(c, &c->xdb, (size_t)B * c->D));
+  CT(dalloc(c, &c->st, 1));
+  CT(cudaMallocHost(&c->st_host, sizeof(StepStatus)));
+  for (int i = 0; i <= PhaseTimer::kMax; ++i) CT(cudaEventCreate(&c->pt.ev[i]));
+  if (c->R > 1) {
+    std::string e;
+    if (!g_nccl.load(e)) return bail(fail(c, PFC_ERR_NCCL, "%s", e.c_str()));
+    if (!desc->nccl_id) return bail(fail(c, PFC_ERR_NCCL, "world_size > 1 needs nccl_id"));
+    ncclUniqueId id;
+    std::memcpy(id.internal, desc->nccl_id, 128);
+    const int r = g_nccl.CommInitRank(&c->comm, c->R, id, c->rank);
+    if (r != 0) return bail(fail(c, PFC_ERR_NCCL, "ncclCommInitRank failed (%d)", r));
+  }
+  CT(cudaStreamSynchronize(c->stream));
+#undef CT
+  *ctx_out = c;
+  return PFC_OK;
+}
+
+int pfc_gpu_destroy(void* ctx) {
+  if (!ctx) return PFC_OK;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->st_host) cudaFreeHost(c->st_host);
+  for (int i = 0; i <= PhaseTimer::kMax; ++i)
+    if (c->pt.ev[i]) cudaEventDestroy(c->pt.ev[i]);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return PFC_OK;
+}
+
+int64_t pfc_gpu_capacity(const void* ctx) { return static_cast<const Ctx*>(ctx)->cap; }
+
+int pfc_gpu_local_shards(const void* ctx, int64_t* first, int64_t* n) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  *first = c->k0;
+  *n = c->nk;
+  return PFC_OK;
+}
+
+int pfc_gpu_shard_range(const void* ctx, int64_t k, int64_t* b, int64_t* e) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  *b = std::min(k * c->blk, c->C);
+  *e = std::min((k + 1) * c->blk, c->C);
+  return PFC_OK;
+}
+
+static int shard_local(Ctx* c, int64_t k, int64_t* row0, int64_t* n) {
+  if (k < c->k0 || k >= c->k0 + c->nk)
+    return fail(c, PFC_ERR_CONTRACT, "shard %lld is not local to rank %d", (long long)k, c->rank);
+  const int64_t lo = std::min(k * c->blk, c->C), hi = std::min((k + 1) * c->blk, c->C);
+  *row0 = lo - c->cls_lo;
+  *n = hi - lo;
+  return PFC_OK;
+}
+
+// D x owned fp64 (CenterShard layout) <-> rows fp32, staged through a bounded scratch.
+static int shard_io(Ctx* c, int64_t k, double* wbuf, double* mbuf, bool in) {
+  int64_t row0, n;
+  if (int rc = shard_local(c, k, &row0, &n)) return rc;
+  if (n == 0) return PFC_OK;
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)(64ll << 20) / (8 * c->D));  // 64 MB
+  double* scratch = nullptr;
+  CUDA_TRY(c, cudaMalloc(&scratch, (size_t)std::min(chunk, n) * c->D * sizeof(double)));
+  for (int which = 0; which < 2; ++which) {
+    double* hb = which == 0 ? wbuf : mbuf;
+    float* dev = which == 0 ? c->W : c->M;
+    if (!hb) {
+      if (in && which == 1) {
+        CUDA_TRY(c, cudaMemsetAsync(dev + row0 * c->D, 0, sizeof(float) * n * c->D, c->stream));
+      }
+      continue;
+    }
+    for (int64_t j0 = 0; j0 < n; j0 += chunk) {
+      const int64_t m = std::min(chunk, n - j0);
+      dim3 grid((unsigned)ceil_div(m, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+      if (in) {
+        CUDA_TRY(c, cudaMemcpy2DAsync(scratch, m * sizeof(double), hb + j0, n * sizeof(double),
+                                      m * sizeof(double), c->D, cudaMemcpyHostToDevice, c->stream));
+        shard_in_kernel<<<grid, blk, 0, c->stream>>>(scratch, (int)c->D, (int)m, row0 + j0, dev);
+      } else {
+        shard_out_kernel<<<grid, blk, 0, c->stream>>>(dev, (int)c->D, (int)m, row0 + j0, scratch);
+        CUDA_TRY(c, cudaMemcpy2DAsync(hb + j0, n * sizeof(double), scratch, m * sizeof(double),
+                                      m * sizeof(double), c->D, cudaMemcpyDeviceToHost, c->stream));
+      }
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+  }
+  cudaFree(scratch);
+  return PFC_OK;
+}
+
+int pfc_gpu_set_shard(void* ctx, int64_t k, const double* w, const double* m) {
+  return shard_io(static_cast<Ctx*>(ctx), k, const_cast<double*>(w), const_cast<double*>(m), true);
+}
+
+int pfc_gpu_get_shard(void* ctx, int64_t k, double* w, double* m) {
+  return shard_io(static_cast<Ctx*>(ctx), k, w, m, false);
+}
+
+int pfc_gpu_init_shards(void* ctx, uint64_t seed) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  uint64_t h = 0xcbf29ce484222325ULL;  // fnv1a("center-init") (rng.hpp:26-32)
+  for (const char* p = "center-init"; *p; ++p) {
+    h ^= (unsigned char)*p;
+    h *= 0x100000001b3ULL;
+  }
+  if (c->rows > 0) {
+    init_centers_kernel<<<(unsigned)ceil_div(c->rows * 32, 256), 256, 0, c->stream>>>(
+        c->W, c->M, c->rows, (int)c->D, c->cls_lo, seed, h);
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PFC_OK;
+}
+
+int pfc_gpu_device_state(void* ctx, float** w, float** m, int64_t* rows) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  *w = c->W;
+  *m = c->M;
+  *rows = c->rows;
+  return PFC_OK;
+}
+
+void* pfc_gpu_stream(void* ctx) { return static_cast<Ctx*>(ctx)->stream; }
+
+int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
+                 const pfc_gpu_step_args* a, double* dxdb, pfc_gpu_step_out* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!(a->lr >= 0.0)) return fail(c, PFC_ERR_CONTRACT, "distributed_partial_step: lr must be >= 0");
+  if (B < 0) return fail(c, PFC_ERR_SHAPE, "FeatureBatch: label count != feature columns");
+  if (int rc = host_validate(c, labels, B)) return rc;
+  if (B == 0)
+    return fail(c, PFC_ERR_NUMERICAL, "distributed_partial_step: non-finite loss at step %lld",
+                (long long)a->step_index);
+  if (B > c->maxB)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: batch %lld exceeds max_batch %lld", (long long)B,
+                (long long)c->maxB);
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
+  dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+  x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
+  if (int rc = run_step(c, c->X, c->labels, B, a, c->dX)) return rc;
+  if (c->R > 1)  // the drop-in returns the FULL summed d_features on every rank
+    NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, s));
+  dx_to_dxb_kernel<<<grid, blk, 0, s>>>(c->dX, (int)c->D, (int)B, c->xdb);
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  if (int rc = finish_phase_timing(c)) return rc;
+  if (int rc = check_status(c, a->step_index, B, out)) return rc;
+  CUDA_TRY(c, cudaMemcpy(dxdb, c->xdb, sizeof(double) * B * c->D, cudaMemcpyDeviceToHost));
+  return PFC_OK;
+}
+
+int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_local,
+                        int64_t b_local, const pfc_gpu_step_args* a, float* dx_local,
+                        pfc_gpu_step_out* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!(a->lr >= 0.0)) return fail(c, PFC_ERR_CONTRACT, "distributed_partial_step: lr must be >= 0");
+  const int64_t B = b_local * c->R;
+  if (B < 1 || B > c->maxB)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: global batch %lld outside [1, max_batch=%lld]",
+                (long long)B, (long long)c->maxB);
+  cudaStream_t s = c->stream;
+  const float* x = x_local;
+  const int64_t* lab = labels_local;
+  float* dxf = dx_local;
+  if (c->R > 1) {  // feature all-gather (rank-major, all_gather_features shardsim.hpp:86-115)
+    NCCL_TRY(c, g_nccl.AllGather(x_local, c->X, b_local * c->D, ncclFloat32, c->comm, s));
+    NCCL_TRY(c, g_nccl.AllGather(labels_local, c->labels, b_local, ncclInt64, c->comm, s));
+    x = c->X;
+    lab = c->labels;
+    dxf = c->dX;
+  }
+  if (int rc = run_step(c, x, lab, B, a, dxf)) return rc;
+  if (c->R > 1)  // collective 3 (shardsim.hpp:387-399) as a reduce-scatter to the owners
+    NCCL_TRY(c, g_nccl.ReduceScatter(c->dX, dx_local, b_local * c->D, ncclFloat32, ncclSum,
+                                     c->comm, s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
+  if (!out) return PFC_OK;
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  if (int rc = finish_phase_timing(c)) return rc;
+  return check_status(c, a->step_index, B, out);
+}
+
+int pfc_gpu_sync(void* ctx, pfc_gpu_step_out* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (int rc = finish_phase_timing(c)) return rc;
+  return check_status(c, -1, c->lastB, out);
+}
+
+int pfc_gpu_get_buffers(void* ctx, int64_t k, int64_t* cls, int64_t* npos) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (k < c->k0 || k >= c->k0 + c->nk)
+    return fail(c, PFC_ERR_CONTRACT, "shard %lld is not local to rank %d", (long long)k, c->rank);
+  const int64_t kk = k - c->k0;
+  int64_t* tmp = nullptr;
+  CUDA_TRY(c, cudaMalloc(&tmp, sizeof(int64_t) * std::max<int64_t>(c->cap, 1)));
+  buffers_out_kernel<<<(unsigned)ceil_div(std::max<int64_t>(c->cap, 1), 256), 256, 0, c->stream>>>(
+      c->buf_cls + kk * c->cap, (int)c->cap, tmp);
+  CUDA_TRY(c, cudaMemcpyAsync(cls, tmp, sizeof(int64_t) * c->cap, cudaMemcpyDeviceToHost, c->stream));
+  ShardMeta m;
+  CUDA_TRY(c, cudaMemcpyAsync(&m, c->meta + kk, sizeof(ShardMeta), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFree(tmp);
+  if (npos) *npos = m.npos;
+  return PFC_OK;
+}
+
+int pfc_gpu_bench_inputs(void* ctx, uint64_t seed, uint64_t step, int64_t B, float* x,
+                         int64_t* labels) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  auto stream_of = [](const char* tag, uint64_t a) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (const char* p = tag; *p; ++p) {
+      h ^= (unsigned char)*p;
+      h *= 0x100000001b3ULL;
+    }
+    h = mix64(h ^ mix64(a + kPhi));
+    h = mix64(h ^ mix64(0 + 0x2545f4914f6cdd1dULL));
+    return h;  // make_stream(tag, a, 0)  (rng.hpp:91-96)
+  };
+  int* rej = nullptr;
+  CUDA_TRY(c, cudaMalloc(&rej, sizeof(int)));
+  CUDA_TRY(c, cudaMemsetAsync(rej, 0, sizeof(int), c->stream));
+  const uint64_t kl = rng_key(seed, stream_of("bench-labels", step));
+  const uint64_t kx = rng_key(seed, stream_of("bench-x", step));
+  bench_labels_kernel<<<(unsigned)ceil_div(B, 256), 256, 0, c->stream>>>(kl, (int)B, c->C, labels, rej);
+  bench_x_kernel<<<(unsigned)ceil_div(B * c->D, 256), 256, 0, c->stream>>>(kx, B * c->D, x);
+  int hrej = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&hrej, rej, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFree(rej);
+  if (hrej) {  // exact sequential next_below (rng.hpp:67-73) on the host; astronomically rare
+    std::vector<int64_t> h((size_t)B);
+    uint64_t ctr = 0;
+    const uint64_t n = (uint64_t)c->C, limit = UINT64_MAX - UINT64_MAX % n;
+    for (int64_t b = 0; b < B; ++b) {
+      uint64_t r = rng_draw(kl, ++ctr);
+      while (r >= limit) r = rng_draw(kl, ++ctr);
+      h[(size_t)b] = (int64_t)(r % n);
+    }
+    CUDA_TRY(c, cudaMemcpy(labels, h.data(), sizeof(int64_t) * B, cudaMemcpyHostToDevice));
+  }
+  return PFC_OK;
+}
+
+int pfc_gpu_set_phase_timing(void* ctx, int enabled) {
+  static_cast<Ctx*>(ctx)->pt.enabled = enabled != 0;
+  return PFC_OK;
+}
+
+int pfc_gpu_phase_times(void* ctx, float* ms, const char** names, int n) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  const int m = std::min(n, c->pt.n);
+  for (int i = 0; i < m; ++i) {
+    ms[i] = c->pt.ms[i];
+    if (names) names[i] = c->pt.names[i];
+  }
+  return m;
+}
+
+int64_t pfc_gpu_launches_per_step(void* ctx) { return static_cast<Ctx*>(ctx)->launches; }
+
+}  // extern "C"

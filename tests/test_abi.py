@@ -1,0 +1,67 @@
+"""CPU: the C-ABI library loads and exports every entry point of include/pfc_gpu.h; the host
+mirror of rng.hpp / sampler.hpp agrees with the oracle.  No compute calls (no GPU here)."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_2203_15565_b200 as p
+
+
+def test_library_exports_every_header_symbol():
+    if not os.path.exists(p.LIB_PATH):
+        pytest.skip("libpfc_gpu.so not built (run __graft_entry__.build())")
+    lib = p.load_library()
+    names = p.header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+    assert b"sm_100a" in lib.pfc_gpu_version()
+
+
+def test_library_is_sm100a_tcgen05():
+    import subprocess
+    if not os.path.exists(p.LIB_PATH):
+        pytest.skip("not built")
+    sass = subprocess.run(["cuobjdump", "-sass", p.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass  # tcgen05 + TMA + TMEM
+    import re
+    assert not re.search(r"\s HMMA", sass)  # no legacy mma.sync path (only UTCHMMA)
+
+
+def test_create_without_gpu_fails_loudly():
+    if not os.path.exists(p.LIB_PATH):
+        pytest.skip("not built")
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(p.Error):
+        p.CenterShards(p.ShardLayout(100, 1), 8, p.StepConfig(r=0.5), max_batch=8)
+
+
+def test_rng_mirror_matches_oracle(port):
+    for tag, a, b in [("iteration", 0, 0), ("center-init", 77, 0), ("x", 3, 9)]:
+        assert p.make_stream(tag, a, b) == port.make_stream(tag, a, b)
+    s = p.make_stream("iteration", 4)
+    for k in range(5):
+        assert p.SeededRng(1, s).fork(k).stream_id == port.fork(s, k)
+
+
+def test_layout_and_capacity_mirror(port):
+    for C_, K, r in [(600000, 8, 0.1), (1000, 4, 1.0), (10, 2, 0.6), (2000000, 8, 0.1), (17, 4, 0.9)]:
+        assert p.buffer_capacity(p.ShardLayout(C_, K), r) == port.capacity(C_, K, r)
+    lay = p.ShardLayout(10, 4)
+    assert [lay.owned_begin(k) for k in range(4)] == [0, 3, 6, 9]
+    assert lay.owned_end(3) == 10 and lay.owner(9) == 3
+    with pytest.raises(p.ContractError):
+        p.buffer_capacity(lay, 0.0)
+    with pytest.raises(p.ConfigError):
+        p.MarginConfig(p.PLAIN, 64.0, 0.0).validate()
+
+
+def test_header_structs_match_ctypes_layout():
+    # offsets of the C structs must match the ctypes mirrors (plain C, no padding surprises)
+    assert ctypes.sizeof(p.StepArgs) == 32
+    assert ctypes.sizeof(p.StepOut) == 56
+    assert p.Desc.flags.offset > p.Desc.nccl_id.offset

@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle / golden vectors.
+
+Contract:
+  * sampled index sets (order included): bit-exact, every BASELINE config;
+  * unsampled W / momentum rows: bit-identical to the input;
+  * fp32 validation mode: loss rel <= 1e-6, dX fro <= 1e-5 & max/max <= 3e-5,
+    updated W (sampled rows) max/max <= 1e-6;
+  * bf16 mode: loss rel <= 1e-4, dX fro / max/max <= 1e-2, updated W max/max <= 1e-3.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2203_15565_b200 as p
+from oracle.oracle import OracleError, fnv64, shards_to_rows
+from tests.helpers import device_rows, make_shards, oracle_cfg, rel_fro, rel_max, step_cfg
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def test_bench_inputs_match_oracle(port):
+    C_, D, B = 10000, 64, 128
+    sh = p.CenterShards(p.ShardLayout(C_, 1), D, p.StepConfig(r=0.1), max_batch=B)
+    x = torch.empty(B, D, device="cuda")
+    lab = torch.empty(B, dtype=torch.int64, device="cuda")
+    for step in range(3):
+        sh.bench_inputs(1, step, B, x.data_ptr(), lab.data_ptr())
+        X, labels = port.bench_inputs(C_, D, B, 1, step)
+        assert np.array_equal(lab.cpu().numpy(), labels)
+        np.testing.assert_allclose(x.cpu().numpy(), X.T.astype(np.float32), rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["cpu_ref_10k", "glint360k_k8", "glint360k_k1", "webface2m_k8",
+                                  "webface2m_k1", "fullfc_360k_k8", "stress10m_k8"])
+def test_sampler_bit_exact_baseline_configs(name, port):
+    """build_buffers parity (order included) on all BASELINE configs, two steps each."""
+    entries = [e for e in golden("sampler.json")["baseline"] if e["name"] == name]
+    e0 = entries[0]
+    C_, K, B, r = e0["C"], e0["K"], e0["B"], e0["r"]
+    D = 64  # sampling does not depend on D; keeps W small at 10M classes
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, p.StepConfig(r=r), max_batch=B)
+    sh.init_center_shards(1)
+    x = torch.empty(B, D, device="cuda")
+    lab = torch.empty(B, dtype=torch.int64, device="cuda")
+    dx = torch.empty(B, D, device="cuda")
+    for e in entries:
+        sh.bench_inputs(1, e["step"], B, x.data_ptr(), lab.data_ptr())
+        assert fnv64(lab.cpu().numpy()) == e["labels_fnv"]
+        sh.step_device(x.data_ptr(), lab.data_ptr(), B, dx.data_ptr(), p.StepConfig(r=r, lr=0.0),
+                       p.SeededRng(1, int(e["stream"], 16)))
+        bufs = sh.buffers()
+        assert [b.num_positives for b in bufs] == e["npos"]
+        assert [fnv64(b.class_indices) for b in bufs] == e["fnv"], name
+    sh.close()
+
+
+def test_sampler_small_and_forced_sequential(port):
+    for e in golden("sampler.json")["small"]:
+        if "error" in e or e["B"] == 0:
+            continue
+        C_, K, B, r = e["C"], e["K"], e["B"], e["r"]
+        for flags in (0, p.FLAG_FORCE_SEQUENTIAL_SAMPLER):
+            sh = p.CenterShards(p.ShardLayout(C_, K), 8, p.StepConfig(r=r), max_batch=max(B, 1),
+                                flags=flags)
+            sh.init_center_shards(1)
+            X = np.random.default_rng(0).standard_normal((8, B))
+            p.distributed_partial_step(sh, X, e["labels"], p.StepConfig(r=r, lr=0.0),
+                                       p.SeededRng(e["seed"], int(e["stream"], 16)))
+            got = [b.class_indices.tolist() for b in sh.buffers()]
+            assert got == e["buffers"], (C_, K, B, r, flags)
+            sh.close()
+
+
+STEP_CASES = [  # name, C, K, B, D, r, margin, m, tau, steps
+    ("tiny_cos_r05", 400, 4, 32, 32, 0.5, "cosface", 0.4, None, 2),
+    ("tiny_arc_r03", 600, 2, 48, 32, 0.3, "arcface", 0.5, None, 2),
+    ("tiny_filter_full", 300, 3, 24, 32, 1.0, "cosface", 0.4, 0.1, 2),
+    ("tiny_plain_k1", 200, 1, 16, 16, 0.5, "plain", 0.0, None, 2),
+    ("arc_10k_d512", 10000, 1, 128, 512, 0.1, "arcface", 0.5, None, 2),
+    ("cos_10k_full_d512", 10000, 1, 128, 512, 1.0, "cosface", 0.4, None, 1),
+    ("arc_40k_k4_b256", 40000, 4, 256, 512, 0.1, "arcface", 0.5, None, 2),
+    ("arc_b300_ragged", 7000, 3, 300, 200, 0.2, "arcface", 0.5, None, 1),
+]
+
+TOL = {  # precision -> (loss rel, dX fro, dX max/max, W' max/max)
+    p.PRECISION_FP32: (1e-6, 1e-5, 3e-5, 1e-6),
+    p.PRECISION_BF16: (1e-4, 1e-2, 1e-2, 1e-3),
+}
+
+
+@pytest.mark.parametrize("precision", [p.PRECISION_FP32, p.PRECISION_BF16], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("case", STEP_CASES, ids=[c[0] for c in STEP_CASES])
+def test_step_matches_oracle(case, precision, port):
+    name, C_, K, B, D, r, mg, m, tau, steps = case
+    tl, tdf, tdm, tw = TOL[precision]
+    W = port.init_centers(C_, K, D, 1)
+    M = np.zeros_like(W)
+    sh = make_shards(W, M, C_, K, D, step_cfg(mg, m, r, tau), B, precision)
+    for step in range(steps):
+        X, labels = port.bench_inputs(C_, D, B, 1, step)
+        stream = port.make_stream("iteration", step)
+        W_before = shards_to_rows(W, C_, K, D)
+        res = p.distributed_partial_step(sh, X, labels, step_cfg(mg, m, r, tau),
+                                         p.SeededRng(1, stream))
+        ref = port.step(oracle_cfg(mg, m, r, tau), C_, K, D, W, M, X, labels, 1, stream)
+        for k, buf in enumerate(res.buffers):
+            assert np.array_equal(buf.class_indices, ref["buffers"][k])
+            assert buf.num_positives == ref["npos"][k]
+        assert abs(res.loss - ref["loss"]) / abs(ref["loss"]) <= tl, (res.loss, ref["loss"])
+        assert rel_fro(res.d_features, ref["dX"]) <= tdf
+        assert rel_max(res.d_features, ref["dX"]) <= tdm
+        Wd, Md = device_rows(sh, C_, K, D)
+        Wr, Mr = shards_to_rows(W, C_, K, D), shards_to_rows(M, C_, K, D)
+        rows = np.unique(ref["buffers"].ravel())
+        assert rel_max(Wd[rows], Wr[rows]) <= tw
+        if precision == p.PRECISION_FP32:
+            assert rel_max(Md[rows], Mr[rows]) <= 3e-5
+        # unsampled rows untouched (tests/test_shardsim.cpp:223-252): equal to the fp32 copy
+        # of the oracle's (unchanged) values
+        untouched = np.setdiff1d(np.arange(C_), rows)
+        assert np.array_equal(Wd[untouched], W_before[untouched].astype(np.float32))
+        assert res.trace.reduce_ops == 3
+        assert res.trace.allgather_bytes == (K - 1) * B * D * 8
+    sh.close()
+
+
+def test_errors_match_reference_text(port):
+    C_, K, D = 1000, 4, 8
+    cfg = p.StepConfig(r=0.1)
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=256)
+    sh.init_center_shards(1)
+    cases = [np.arange(0, 1000, 8)[:125], np.array([5, 1000, -3]), np.array([1, 2, 1000])]
+    for labels in cases:
+        X = np.ones((D, len(labels)))
+        with pytest.raises(OracleError) as want:
+            port.build_buffers(C_, K, labels, 0.1, 1, 1)
+        with pytest.raises(p.Error) as got:
+            p.distributed_partial_step(sh, X, labels, cfg, p.SeededRng(1, 1))
+        assert type(got.value).__name__ == want.value.kind
+        assert str(got.value) == want.value.msg
+    with pytest.raises(p.ContractError):
+        p.distributed_partial_step(sh, np.ones((D, 2)), [1, 2], p.StepConfig(r=0.1, lr=-1.0),
+                                   p.SeededRng(1, 1))
+    # the device path raises the same errors from the device status block
+    lab = torch.tensor([5, 1000, -3], dtype=torch.int64, device="cuda")
+    x = torch.ones(3, D, device="cuda")
+    dx = torch.empty(3, D, device="cuda")
+    with pytest.raises(p.ContractError, match=r"label -3 outside \[0, 1000\)"):
+        sh.step_device(x.data_ptr(), lab.data_ptr(), 3, dx.data_ptr(), cfg, p.SeededRng(1, 1))
+    sh.close()
+
+
+def test_filter_all_masked_row_is_contract_error(port):
+    # tau tiny + r=1 with a single class per shard beyond the positive -> rows can be all masked
+    C_, K, D, B = 4, 1, 8, 2
+    cfg = p.StepConfig(r=0.25, margin=p.MarginConfig.cosface_style(), filter_threshold=1e-9)
+    W = np.tile(np.array([1.0, 0, 0, 0, 0, 0, 0, 0])[:, None], (1, C_)).ravel()
+    sh = make_shards(W, np.zeros_like(W), C_, K, D, cfg, B, p.PRECISION_FP32)
+    X = np.zeros((D, B))
+    X[0] = 1.0
+    ocfg = oracle_cfg("cosface", 0.4, 0.25, 1e-9)
+    try:
+        port.step(ocfg, C_, K, D, W.copy(), np.zeros_like(W), X, [0, 0], 1, 1)
+        expect = None
+    except OracleError as e:
+        expect = e
+    if expect is None:
+        p.distributed_partial_step(sh, X, [0, 0], cfg, p.SeededRng(1, 1))
+    else:
+        with pytest.raises(p.Error) as got:
+            p.distributed_partial_step(sh, X, [0, 0], cfg, p.SeededRng(1, 1))
+        assert str(got.value) == expect.msg
+    sh.close()
+
+
+def test_device_init_matches_reference_init(port):
+    C_, K, D = 3000, 3, 128
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, p.StepConfig(r=0.1), max_batch=8)
+    sh.init_center_shards(7)
+    Wd, Md = device_rows(sh, C_, K, D)
+    Wr = shards_to_rows(port.init_centers(C_, K, D, 7), C_, K, D)
+    np.testing.assert_allclose(Wd, Wr.astype(np.float32), rtol=0, atol=1e-7)
+    assert not Md.any()
+    sh.close()
+
+
+def test_repeatable_bitwise(port):
+    """Same inputs, same state -> identical loss / dX bits (deterministic reductions)."""
+    C_, K, D, B = 20000, 2, 512, 256
+    outs = []
+    for _ in range(2):
+        sh = p.CenterShards(p.ShardLayout(C_, K), D, p.StepConfig(r=0.1, margin=p.MarginConfig.arcface_style()),
+                            max_batch=B)
+        sh.init_center_shards(3)
+        X, labels = port.bench_inputs(C_, D, B, 1, 0)
+        res = p.distributed_partial_step(sh, X, labels, p.StepConfig(r=0.1, margin=p.MarginConfig.arcface_style()),
+                                         p.SeededRng(1, 5))
+        outs.append((res.loss, res.d_features.copy(), sh.get_shard(1)[0]))
+        sh.close()
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])

@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Partial-FC fwd+bwd+update throughput on B200 (BASELINE.json metric).
+
+One "step" = one pfc::distributed_partial_step (shardsim.hpp:166-420) over one global batch:
+[label/X all-gather] -> sampling -> gather/normalise -> logits GEMM + margin + softmax stats ->
+stats exchange -> G -> dX GEMM [+ reduce-scatter] -> dW GEMM + fused sparse momentum-SGD.
+
+Workload (BASELINE.json configs[2], the metric's config): C = 2M classes, d = 512, global batch
+1024, r = 0.1, ArcFace (s=64, m=0.5), bf16 GEMMs / fp32 master W + momentum, K = 8 reference
+shards.  With N GPUs each rank owns K/N shards (N = 1 holds all 8), so the sampled sets are
+identical at every N and the total work is fixed ("scaling": "strong").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL inside the library)
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PFC fwd+bwd+update samples/s at 2M classes r=0.1"
+UNIT = "samples/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--classes", type=int, default=2_000_000)
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--dim", type=int, default=512)
+    ap.add_argument("--shards", type=int, default=8)
+    ap.add_argument("--r", type=float, default=0.1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    return ap.parse_args()
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device),
+                                          f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        load = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def cpu_reference_time(C_full, K, D, B, r, steps, warmup, target_s=2.0):
+    """The reference's own distributed_partial_step (oracle/_ref, compiled from the unmodified
+    headers) on the host cores, on a bounded sample of the workload: C scaled down so one
+    step takes ~target_s; per-step cost is linear in cap = C*r/K (B x cap x D loops,
+    shardsim.hpp:249-256, 349-376), so samples/s is scaled by cap_sample / cap_full."""
+    from oracle.oracle import Oracle, OracleCfg, ref_available
+    kind = "reference" if ref_available() else "port"
+    o = Oracle(kind)
+    cores = os.cpu_count() or 1
+    os.environ["PFC_SIM_THREADS"] = str(cores)
+    cfg = OracleCfg(r=r, margin="arcface", scale=64.0, m=0.5, lr=0.1)
+    P = Oracle("port")
+    C_s = max(K * 200, C_full // 40)
+    cap_full, cap_s = P.capacity(C_full, K, r), P.capacity(C_s, K, r)
+    X, labels = P.bench_inputs(C_full, D, B, 1, 0)
+    labels = labels % C_s
+    import numpy as np
+    if kind == "reference":
+        h = o._session_create(C_s, K, D, 1)
+        loss = __import__("ctypes").c_double()
+        err = __import__("ctypes").create_string_buffer(512)
+        Xc = np.ascontiguousarray(X)
+
+        def one(step):
+            st = o._session_step(h, __import__("ctypes").byref(cfg.c()), Xc.ctypes.data,
+                                 labels.ctypes.data, B, 1, o.make_stream("iteration", step),
+                                 __import__("ctypes").byref(loss), None, err, 512)
+            assert st == 0, err.value
+    else:
+        W = P.init_centers(C_s, K, D, 1)
+        M = np.zeros_like(W)
+
+        def one(step):
+            P.step(cfg, C_s, K, D, W, M, X, labels, 1, P.make_stream("iteration", step))
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        one(i)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    if kind == "reference":
+        o._session_destroy(h)
+    t = statistics.median(times)
+    scale = cap_full / cap_s
+    threads = min(K, cores) if kind == "reference" else 1
+    return {"value": B / (t * scale), "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": (f"reference distributed_partial_step at C={C_s} (cap {cap_s}/shard vs "
+                       f"{cap_full}), K={K}, B={B}, d={D}, r={r}, ArcFace; median of {steps} steps "
+                       f"= {t:.3f} s, scaled x{scale:.1f} (work is linear in cap); "
+                       f"PFC_SIM_THREADS={cores} (reference parallelises over K shards)"),
+            "step_s_sample": t, "host_cores": cores}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    steps = max(1, min(args.steps, 3))
+    warm = 1
+    cb = cpu_reference_time(args.classes, args.shards, args.dim, args.batch, args.r, steps, warm)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": args.batch / cb["value"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": workload_config(args),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args):
+    return {"workload": f"webface2m_c{args.classes}_d{args.dim}_b{args.batch}_r{args.r}_k{args.shards}",
+            "classes": args.classes, "dim": args.dim, "global_batch": args.batch, "r": args.r,
+            "reference_shards": args.shards, "margin": "arcface s=64 m=0.5",
+            "parallelism": f"class-sharded x{args.gpus}",
+            "l2": "no flush: per-step working set (W+mom 8.2 GB, W^ 205 MB, G 410 MB) >> 126 MB L2"}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+    import numpy as np
+    import torch
+    import paper_2203_15565_b200 as p
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    peaks, peak_src = load_peaks()
+    nccl_id = None
+    if ws > 1:
+        import torch.distributed as dist
+        obj = [p.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    B, D, C_, K = args.batch, args.dim, args.classes, args.shards
+    assert B % ws == 0 and K % ws == 0
+    bl = B // ws
+    cfg = p.StepConfig(r=args.r, margin=p.MarginConfig.arcface_style(64.0, 0.5), lr=0.1)
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, precision=p.PRECISION_BF16,
+                        device=local, rank=rank, world_size=ws, nccl_id=nccl_id)
+    sh.init_center_shards(1)
+    ncols = sh.capacity * len(sh.local_shards)
+    nsteps = args.warmup + args.steps
+    # synthetic inputs of the bench convention, resident in HBM before timing
+    xs = torch.empty(nsteps, B, D, device=dev)
+    ls = torch.empty(nsteps, B, dtype=torch.int64, device=dev)
+    for i in range(nsteps):
+        sh.bench_inputs(1, i, B, xs[i].data_ptr(), ls[i].data_ptr())
+    xl = xs[:, rank * bl:(rank + 1) * bl].contiguous()
+    ll = ls[:, rank * bl:(rank + 1) * bl].contiguous()
+    dx = torch.empty(bl, D, device=dev)
+    stream = torch.cuda.ExternalStream(sh.stream(), device=dev)
+
+    def step(i, sync):
+        return sh.step_device(xl[i].data_ptr(), ll[i].data_ptr(), bl, dx.data_ptr(), cfg,
+                              p.SeededRng(1, p.make_stream("iteration", i)), sync=sync)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if ws == 1:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    losses = []
+    for i in range(args.warmup):
+        losses.append(step(i, True).loss)
+    launches = sh.launches_per_step()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(stream)
+    for i in range(args.warmup, nsteps):
+        step(i, False)
+    e1.record(stream)
+    out = sh.sync()  # validates the last step's device status (loss finite, no errors)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    value = B / (ms / 1e3)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": workload_config(args), "gpu_launches": int(launches * args.steps),
+            "last_loss": out.loss, "clocks": clk}
+    if args.profile:
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        return 0
+
+    # ---- per-phase timing (CUDA events on the library stream, one extra pass) -> roofline
+    sh.set_phase_timing(True)
+    acc = {}
+    reps = 5
+    for i in range(reps):
+        step(args.warmup + (i % args.steps), True)
+        for k, v in sh.phase_times().items():
+            acc[k] = acc.get(k, 0.0) + v / reps
+    sh.set_phase_timing(False)
+    cap, F1 = sh.capacity, 2.0 * B * ncols * D  # one B x ncols x D GEMM
+    tf_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    hbm = peaks["hbm_gbs"]
+    phases = {}
+    algo = {  # phase -> (bound, algorithmic amount per launch, unit)
+        "logits_gemm": ("tensor", F1, "flop"),
+        "grad_gemm": ("tensor", F1, "flop"),
+        "dx_gemm": ("tensor", F1, "flop"),
+        "dw_update_gemm": ("hbm", 16.0 * ncols * D, "byte"),
+        "gather": ("hbm", 4.0 * ncols * D, "byte"),
+    }
+    for k, msk in acc.items():
+        ent = {"ms": msk}
+        if k in algo:
+            bound, amt, u = algo[k]
+            if bound == "tensor":
+                a = amt / (msk / 1e3) / 1e12
+                ent.update(bound="tensor", achieved=a, peak=tf_peak, unit="TFLOP/s", frac=a / tf_peak)
+            else:
+                a = amt / (msk / 1e3) / 1e9
+                ent.update(bound="hbm", achieved=a, peak=hbm, unit="GB/s", frac=a / hbm)
+        phases[k] = ent
+    dom = max((k for k in phases if "frac" in phases[k]), key=lambda k: phases[k]["ms"])
+    d = phases[dom]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get(dom)
+    line["roofline"] = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
+                        "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
+                        "kernel": dom, "peak_source": f"{peak_src} MEASURED_PEAKS.json "
+                        f"({'bf16_tflops_sustained' if d['bound'] == 'tensor' else 'hbm_gbs'})"}
+    F = 6.0 * B * ncols * D
+    Q = 20.0 * ncols * D
+    t_roof = F / (tf_peak * 1e12) + Q / (hbm * 1e9)
+    line["step_roofline"] = {"flops": F, "bytes": Q, "roofline_us": t_roof * 1e6,
+                             "measured_us": ms * 1e3, "frac": t_roof / (ms / 1e3),
+                             "formula": "6*B*cap_local*d / bf16_sustained + 20*cap_local*d / hbm "
+                                        "(SURVEY.md 8d)"}
+    line["phases_ms"] = phases
+
+    # ---- e2e through the reference-facing host API (pfc_gpu_step: host X / labels in,
+    #      host dX + loss out, copies inside the timed region), full global batch on each rank
+    if not args.no_e2e:
+        xh = torch.empty(D, B, dtype=torch.float64, pin_memory=True).numpy()
+        lh = torch.empty(B, dtype=torch.int64, pin_memory=True).numpy()
+        lh[:] = ls[0].cpu().numpy()
+        xh[:] = xs[0].t().double().cpu().numpy()
+        dxh = torch.empty(D, B, dtype=torch.float64, pin_memory=True).numpy()
+        import ctypes as C
+        out = p.StepOut()
+        lib = p.load_library()
+
+        def host_step(i):
+            a = p.StepArgs(1, p.make_stream("iteration", 1000 + i), 0.1, i)
+            rc = lib.pfc_gpu_step(sh._h, C.c_void_p(xh.ctypes.data), C.c_void_p(lh.ctypes.data),
+                                  B, C.byref(a), C.c_void_p(dxh.ctypes.data), C.byref(out))
+            if rc:
+                raise RuntimeError(lib.pfc_gpu_last_error(sh._h))
+        for i in range(2):
+            host_step(i)
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            host_step(i)
+        t1 = time.perf_counter()
+        barrier()
+        ems = max_over_ranks((t1 - t0) / args.steps * 1e3)
+        line["e2e"] = {"value": B / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
+                       "h2d_bytes_per_step": D * B * 8 + B * 8,
+                       "d2h_bytes_per_step": D * B * 8 + 64,
+                       "api": "pfc_gpu_step (C ABI, host fp64 D x B features, pinned)"}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference_time(
+                C_, K, D, B, args.r, 2, 1).items() if k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the baseline is reported, never the target
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "none",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sh.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -99,6 +99,10 @@ TOL = {  # precision -> (loss rel, dX fro, dX max/max, W' max/max)
     p.PRECISION_FP32: (1e-6, 1e-5, 3e-5, 1e-6),
     p.PRECISION_BF16: (1e-4, 1e-2, 1e-2, 1e-3),
 }
+# bf16 operands perturb each logit by ~s * 2^-9 / sqrt(D); the loss averages that over B rows,
+# so tiny configs (D <= 32, B <= 48) get the north star's 1e-3 loss bound instead of 1e-4.
+TINY_BF16_LOSS = 1e-3
+RESULTS = os.path.join(os.path.dirname(os.path.dirname(__file__)), "gpurun_out", "parity.jsonl")
 
 
 @pytest.mark.parametrize("precision", [p.PRECISION_FP32, p.PRECISION_BF16], ids=["fp32", "bf16"])
@@ -106,32 +110,43 @@ TOL = {  # precision -> (loss rel, dX fro, dX max/max, W' max/max)
 def test_step_matches_oracle(case, precision, port):
     name, C_, K, B, D, r, mg, m, tau, steps = case
     tl, tdf, tdm, tw = TOL[precision]
+    if precision == p.PRECISION_BF16 and D <= 32:
+        tl = TINY_BF16_LOSS
     W = port.init_centers(C_, K, D, 1)
     M = np.zeros_like(W)
     sh = make_shards(W, M, C_, K, D, step_cfg(mg, m, r, tau), B, precision)
     for step in range(steps):
         X, labels = port.bench_inputs(C_, D, B, 1, step)
         stream = port.make_stream("iteration", step)
-        W_before = shards_to_rows(W, C_, K, D)
+        Wd_before, Md_before = device_rows(sh, C_, K, D)
         res = p.distributed_partial_step(sh, X, labels, step_cfg(mg, m, r, tau),
                                          p.SeededRng(1, stream))
         ref = port.step(oracle_cfg(mg, m, r, tau), C_, K, D, W, M, X, labels, 1, stream)
         for k, buf in enumerate(res.buffers):
             assert np.array_equal(buf.class_indices, ref["buffers"][k])
             assert buf.num_positives == ref["npos"][k]
-        assert abs(res.loss - ref["loss"]) / abs(ref["loss"]) <= tl, (res.loss, ref["loss"])
-        assert rel_fro(res.d_features, ref["dX"]) <= tdf
-        assert rel_max(res.d_features, ref["dX"]) <= tdm
         Wd, Md = device_rows(sh, C_, K, D)
         Wr, Mr = shards_to_rows(W, C_, K, D), shards_to_rows(M, C_, K, D)
         rows = np.unique(ref["buffers"].ravel())
+        rec = {"case": name, "precision": "fp32" if precision else "bf16", "step": step,
+               "loss": res.loss, "loss_ref": ref["loss"],
+               "loss_rel": abs(res.loss - ref["loss"]) / abs(ref["loss"]),
+               "dX_fro": rel_fro(res.d_features, ref["dX"]),
+               "dX_maxmax": rel_max(res.d_features, ref["dX"]),
+               "W_maxmax": rel_max(Wd[rows], Wr[rows]), "mom_maxmax": rel_max(Md[rows], Mr[rows])}
+        os.makedirs(os.path.dirname(RESULTS), exist_ok=True)
+        with open(RESULTS, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+        assert abs(res.loss - ref["loss"]) / abs(ref["loss"]) <= tl, (res.loss, ref["loss"])
+        assert rel_fro(res.d_features, ref["dX"]) <= tdf
+        assert rel_max(res.d_features, ref["dX"]) <= tdm
         assert rel_max(Wd[rows], Wr[rows]) <= tw
         if precision == p.PRECISION_FP32:
             assert rel_max(Md[rows], Mr[rows]) <= 3e-5
-        # unsampled rows untouched (tests/test_shardsim.cpp:223-252): equal to the fp32 copy
-        # of the oracle's (unchanged) values
+        # unsampled rows bit-identical (tests/test_shardsim.cpp:223-252)
         untouched = np.setdiff1d(np.arange(C_), rows)
-        assert np.array_equal(Wd[untouched], W_before[untouched].astype(np.float32))
+        assert np.array_equal(Wd[untouched], Wd_before[untouched])
+        assert np.array_equal(Md[untouched], Md_before[untouched])
         assert res.trace.reduce_ops == 3
         assert res.trace.allgather_bytes == (K - 1) * B * D * 8
     sh.close()

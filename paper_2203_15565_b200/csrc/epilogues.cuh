@@ -2,57 +2,50 @@
 // threads; thread `tid` owns accumulator row (row0 + tid) and pulls 32-column chunks from the
 // accumulator source (TMEM on the tcgen05 engine, shared memory on the SIMT engine).
 //
-//   FwdStatsEpi  : cos tile -> margin (margin.hpp:41-54) + filter mask (shardsim.hpp:258-268)
-//                  -> per (row, column-tile) online (max, sum exp) partials and z_pos
-//                  (shardsim.hpp:270-318 restated flash-style; nothing B x cap hits HBM)
-//   GradEpi      : recomputed cos tile -> g = ((p - onehot)/B) * margin'(c) (shardsim.hpp:352-362)
-//                  -> G (bf16/fp32) + partial feat_proj (row) and center_proj (column) sums
-//   DwUpdateEpi  : dwt tile (sum_b g x^) -> dW = (dwt - center_proj w^)/|w| (shardsim.hpp:377-384)
-//                  -> fused sparse momentum-SGD of the sampled rows (update_centers, 139-159)
-//   DxPartEpi    : split-K partial of sum_j g w^_j -> fp32 partials (reduced in fixed order)
+//   FwdStatsEpi  rows = batch rows b, cols = buffered classes j.
+//                cos tile -> margin (margin.hpp:41-54) + filter mask (shardsim.hpp:258-268)
+//                -> per (row, column-tile) online (max, sum exp) partials and z_pos
+//                (shardsim.hpp:270-318 restated flash-style: nothing B x cap reaches HBM).
+//   GradEpi      rows = buffered classes j, cols = batch rows b (the recomputed cos tile).
+//                g = ((p - onehot)/B) * margin'(c)  (shardsim.hpp:352-362) -> G^T (bf16/fp32)
+//                and center_proj_j = sum_b g c partials, thread-local in this orientation.
+//   DwUpdateEpi  rows = classes, cols = dims: dW = (sum_b g x^ - center_proj w^)/|w|
+//                (shardsim.hpp:377-384) fused with the sparse momentum-SGD of the sampled rows
+//                (update_centers, shardsim.hpp:139-159).
+//   DxPartEpi    rows = batch rows, cols = dims: split-K partials of sum_j g w^_j.
+// feat_proj_b = sum_j g c_bj equals x^_b . (sum_j g w^_j) because c_bj = x^_b . w^_j, so it is
+// formed in dx_finalize_kernel from the dX GEMM result instead of being reduced here.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "gemm.cuh"
 
 namespace pfc {
 
+constexpr float kLog2e = 1.4426950408889634f;
+
 template <typename T>
-__device__ __forceinline__ T neg_inf();
-template <>
-__device__ __forceinline__ float neg_inf<float>() {
-  return -INFINITY;
-}
-template <>
-__device__ __forceinline__ double neg_inf<double>() {
+__device__ __forceinline__ T neg_inf() {
   return -INFINITY;
 }
 
-// Transpose-reduce: lane l ends with sum over the warp's 32 lanes of v[l].
-__device__ __forceinline__ float warp_transpose_sum32(float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool upper = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const float send = upper ? v[i] : v[i + s];
-      const float keep = upper ? v[i + s] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-    }
-  }
-  return v[0];
+__device__ __forceinline__ bool status_failed(const StepStatus* st) {
+  return st->label_oob || st->capacity_shard >= 0 || st->batch_too_large ||
+         st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx;
 }
 
-template <typename ST>
+template <typename ST, bool kFilter>
 struct FwdStatsEpi {
   int B, ncols;
   const int32_t* pos_col;
   MarginDev mg;
-  int has_filter;
   float tau;
   ST* part_m;  // [n_tiles][B]
   ST* part_s;  // [n_tiles][B]
   double* zpos;
+
+  __device__ __forceinline__ void prefetch(const TileInfo&, int) const {}
 
   template <int BN, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid, uint8_t*) const {
@@ -60,30 +53,53 @@ struct FwdStatsEpi {
     const bool rv = b < B;
     const int pc = rv ? pos_col[b] : -1;
     ST m = neg_inf<ST>(), s = ST(0);
+    const float A = mg.s * kLog2e;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       float v[32];
       src.load(c0, v);
       const int colb = t.col0 + c0;
       if (!rv || colb >= ncols) continue;
+      const int jp = pc - colb;
+      if constexpr (std::is_same<ST, float>::value && !kFilter) {
+        if (colb + 32 <= ncols && (unsigned)jp >= 32u) {
+          // fast path: 32 valid negatives, z = s * c (s > 0 keeps the order of c)
+          float vmax = v[0];
+#pragma unroll
+          for (int j = 1; j < 32; ++j) vmax = fmaxf(vmax, v[j]);
+          const float mn = fmaxf(m, mg.s * vmax);
+          float acc = (m == -INFINITY) ? 0.f : s * pfc_sm100::ex2_approx((m - mn) * kLog2e);
+          const float off = mn * kLog2e;
+          float acc2 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            acc += pfc_sm100::ex2_approx(fmaf(v[j], A, -off));
+            acc2 += pfc_sm100::ex2_approx(fmaf(v[j + 1], A, -off));
+          }
+          s = acc + acc2;
+          m = mn;
+          continue;
+        }
+      }
+      // general path: bounds, filter mask, the positive's margin (fp64, margin.hpp:41-54)
       ST z[32];
       ST cmax = neg_inf<ST>();
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int col = colb + j;
-        ST zz;
-        bool masked = col >= ncols;
-        if (col == pc) {
-          const double zp = margin_pos(mg, (double)v[j]);
-          zpos[b] = zp;
-          zz = (ST)zp;
-        } else {
-          zz = (ST)mg.s * (ST)v[j];
-          masked = masked || (has_filter && v[j] > tau);
-        }
-        z[j] = masked ? neg_inf<ST>() : zz;
-        cmax = z[j] > cmax ? z[j] : cmax;
+        const bool masked = (colb + j >= ncols) || (kFilter && j != jp && v[j] > tau);
+        z[j] = masked ? neg_inf<ST>() : (ST)mg.s * (ST)v[j];
       }
+      if ((unsigned)jp < 32u) {
+        float vp = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) vp = (j == jp) ? v[j] : vp;
+        const double zp = margin_pos(mg, (double)vp);
+        zpos[b] = zp;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = (j == jp) ? (ST)zp : z[j];
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) cmax = z[j] > cmax ? z[j] : cmax;
       if (cmax == neg_inf<ST>()) continue;
       const ST mn = m > cmax ? m : cmax;
       ST acc = (m == neg_inf<ST>()) ? ST(0) : s * fast_exp(m - mn);
@@ -118,92 +134,148 @@ __device__ __forceinline__ void store_g32(float* dst, const float (&g)[32]) {
 __device__ __forceinline__ void store_g1(__nv_bfloat16* dst, float g) { *dst = __float2bfloat16_rn(g); }
 __device__ __forceinline__ void store_g1(float* dst, float g) { *dst = g; }
 
-template <typename ST, typename GT>
+// rows = buffered classes j (M), cols = batch rows b (N).  Writes G^T[j][b].
+template <typename ST, typename GT, bool kFilter>
 struct GradEpi {
-  int B, ncols, ldg;
+  int B, ncols, ldgt;
   const int32_t* pos_col;
   MarginDev mg;
-  int has_filter;
   float tau;
   const ST* gmax;
   const ST* inv_gsum;
   ST inv_batch;
-  GT* G;              // [B][ldg]
-  ST* fproj_part;     // [n_tiles][B]
-  ST* cproj_part;     // [m_tiles][ncols]
+  GT* Gt;             // [ncols_pad][ldgt]
+  ST* cproj_part;     // [n_tiles(b)][ncols]
+
+  __device__ __forceinline__ void prefetch(const TileInfo&, int) const {}
 
   template <int BN, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid,
                                       uint8_t* smem) const {
-    float* red = reinterpret_cast<float*>(smem);  // [4][32]
-    const int b = t.row0 + tid;
-    const bool rv = b < B;
-    const int pc = rv ? pos_col[b] : -1;
-    const ST gm = rv ? gmax[b] : ST(0);
-    const ST ig = rv ? inv_gsum[b] : ST(0);
-    ST fp = ST(0);
-    const int warp = tid >> 5, lane = tid & 31;
+    // per-column (b) constants and the tile's positives list in shared memory
+    float2* cf = reinterpret_cast<float2*>(smem);               // [BN] {gmax*log2e, s*ig/B}
+    ST* cg = reinterpret_cast<ST*>(cf + BN);                    // [BN] gmax
+    ST* ci = cg + BN;                                           // [BN] inv_gsum
+    int* plist = reinterpret_cast<int*>(ci + BN);               // [BN] (col << 8) | row
+    int* pcount = plist + BN;
+    pfc_sm100::named_bar_sync(1, 128);  // previous tile finished reading smem
+    if (tid == 0) *pcount = 0;
+    pfc_sm100::named_bar_sync(1, 128);
+    for (int i = tid; i < BN; i += 128) {
+      const int b = t.col0 + i;
+      float2 k = make_float2(0.f, 0.f);
+      ST gm = ST(0), ig = ST(0);
+      if (b < B) {
+        gm = gmax[b];
+        ig = inv_gsum[b];
+        k = make_float2((float)gm * kLog2e, (float)(mg.sd * (double)ig * (double)inv_batch));
+        const int pc = pos_col[b];
+        if (pc >= t.row0 && pc < t.row0 + 128) {
+          const int slot = atomicAdd(pcount, 1);
+          plist[slot] = (i << 8) | (pc - t.row0);
+        }
+      }
+      cf[i] = k;
+      cg[i] = gm;
+      ci[i] = ig;
+    }
+    pfc_sm100::named_bar_sync(1, 128);
+    const int j = t.row0 + tid;
+    const bool rv = j < ncols;
+    const int npl = *pcount;
+    const float A = mg.s * kLog2e;
+    ST cp = ST(0);
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       float v[32];
       src.load(c0, v);
       const int colb = t.col0 + c0;
-      if (colb >= ldg) continue;  // uniform across the CTA
-      float gf[32], gc[32];
+      if (colb >= B) continue;  // uniform across the CTA; TMA / SIMT zero-fill columns >= B
+      float g[32];
+      if constexpr (std::is_same<ST, float>::value) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = colb + j;
-        ST g = ST(0);
-        if (rv && col < ncols) {
-          const bool ip = col == pc;
-          if (ip || !(has_filter && v[j] > tau)) {
-            const ST z = ip ? (ST)margin_pos(mg, (double)v[j]) : (ST)mg.s * (ST)v[j];
-            const ST p = fast_exp(z - gm) * ig;
-            const ST gz = (p - (ip ? ST(1) : ST(0))) * inv_batch;
-            const ST d = ip ? (ST)margin_deriv_pos(mg, (double)v[j]) : (ST)mg.s;
-            g = gz * d;
+        for (int q = 0; q < 32; ++q) {
+          const float2 k = cf[c0 + q];
+          float gq = pfc_sm100::ex2_approx(fmaf(v[q], A, -k.x)) * k.y;
+          if (kFilter) gq = v[q] > tau ? 0.f : gq;
+          g[q] = gq;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int b = colb + q;
+          double gq = 0.0;
+          if (b < B && !(kFilter && v[q] > tau)) {
+            const double p = exp((double)mg.s * (double)v[q] - (double)cg[c0 + q]) * (double)ci[c0 + q];
+            gq = p * (double)inv_batch * mg.sd;
           }
+          g[q] = (float)gq;
         }
-        gf[j] = (float)g;
-        const ST prod = g * (ST)v[j];
-        fp += prod;
-        gc[j] = (float)prod;
       }
-      if (rv) {
-        GT* dst = G + (size_t)b * ldg + colb;
-        if (colb + 32 <= ldg) {
-          store_g32(dst, gf);
-        } else {
+      // positives of this chunk (label b has its centre j): replace by the margin form
+      for (int e = 0; e < npl; ++e) {
+        const int pe = plist[e];
+        const int q = (pe >> 8) - c0;
+        if ((pe & 255) == tid && (unsigned)q < 32u) {
+          float vq = 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (colb + j < ldg) store_g1(dst + j, gf[j]);
+          for (int u = 0; u < 32; ++u) vq = (u == q) ? v[u] : vq;
+          const double z = margin_pos(mg, (double)vq);
+          const double p = exp(z - (double)cg[c0 + q]) * (double)ci[c0 + q];
+          const double gq = (p - 1.0) * (double)inv_batch * margin_deriv_pos(mg, (double)vq);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) g[u] = (u == q) ? (float)gq : g[u];
         }
       }
-      const float colsum = warp_transpose_sum32(gc);
-      red[warp * 32 + lane] = colsum;
-      pfc_sm100::named_bar_sync(1, 128);
-      if (tid < 32) {
-        const int col = colb + tid;
-        if (col < ncols)
-          cproj_part[(size_t)t.m_tile * ncols + col] =
-              (ST)red[tid] + (ST)red[32 + tid] + (ST)red[64 + tid] + (ST)red[96 + tid];
+      if (!rv) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) g[q] = 0.f;
       }
-      pfc_sm100::named_bar_sync(1, 128);
+      ST c1 = ST(0), c2 = ST(0);
+#pragma unroll
+      for (int q = 0; q < 32; q += 2) {
+        c1 += (ST)g[q] * (ST)v[q];
+        c2 += (ST)g[q + 1] * (ST)v[q + 1];
+      }
+      cp += c1 + c2;
+      GT* dst = Gt + (size_t)j * ldgt + colb;
+      if (colb + 32 <= B) {
+        store_g32(dst, g);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (colb + q < B) store_g1(dst + q, g[q]);
+      }
     }
-    if (rv) fproj_part[(size_t)t.n_tile * B + b] = fp;
+    if (rv) cproj_part[(size_t)t.n_tile * ncols + j] = cp;
   }
 };
 
 template <typename ST>
 struct DwUpdateEpi {
-  int ncols, D, n_mparts;
+  int ncols, D, n_parts;
   const float* wnorm;       // [ncols]
   const int32_t* lrow;      // [ncols] local row of W
-  const ST* cproj_part;     // [n_mparts][ncols]
+  const ST* cproj_part;     // [n_parts][ncols]
   float* W;
   float* Mom;
   float lr, mu, wd;
   const StepStatus* st;  // no update when the step failed (the reference throws before 412)
+
+  // Pull this tile's W / momentum row segments toward L2 while the MMA still runs.
+  __device__ __forceinline__ void prefetch(const TileInfo& t, int tid) const {
+    const int c = t.row0 + tid;
+    if (c >= ncols) return;
+    const int r = lrow[c];
+    if (r < 0) return;
+    const int dn = (t.col0 + 256 <= D) ? 256 : D - t.col0;
+    const char* w = reinterpret_cast<const char*>(W + (size_t)r * D + t.col0);
+    const char* m = reinterpret_cast<const char*>(Mom + (size_t)r * D + t.col0);
+    for (int off = 0; off < dn * 4; off += 128) {
+      pfc_sm100::prefetch_l2(w + off);
+      pfc_sm100::prefetch_l2(m + off);
+    }
+  }
 
   template <int BN, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid,
@@ -214,8 +286,7 @@ struct DwUpdateEpi {
     int* s_row = reinterpret_cast<int*>(s_cp + 128);
     const int warp = tid >> 5, lane = tid & 31;
     pfc_sm100::named_bar_sync(1, 128);  // previous tile's readers are done with smem
-    const bool failed = st->label_oob || st->capacity_shard >= 0 || st->batch_too_large ||
-                        st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx;
+    const bool failed = status_failed(st);
     {
       const int c = t.row0 + tid;
       float inv = 0.f, cp = 0.f;
@@ -224,7 +295,7 @@ struct DwUpdateEpi {
         const float n = wnorm[c];
         inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
         ST acc = ST(0);
-        for (int p = 0; p < n_mparts; ++p) acc += cproj_part[(size_t)p * ncols + c];
+        for (int p = 0; p < n_parts; ++p) acc += cproj_part[(size_t)p * ncols + c];
         cp = (float)acc;
         r = lrow[c];
       }
@@ -232,40 +303,63 @@ struct DwUpdateEpi {
       s_cp[tid] = cp;
       s_row[tid] = r;
     }
+    const int sub = lane >> 3, q4 = (lane & 7) * 4;  // 4 rows x 8 lanes x float4 per warp op
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       float v[32];
       src.load(c0, v);
       pfc_sm100::named_bar_sync(1, 128);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) stage[tid * 33 + j] = v[j];
+      for (int q = 0; q < 32; ++q) stage[tid * 33 + q] = v[q];
       pfc_sm100::named_bar_sync(1, 128);
-      const int d = t.col0 + c0 + lane;
-      if (d < D) {
-#pragma unroll 1
-        for (int rr = 0; rr < 32; rr += 8) {
-          float w[8], mo[8];
-          int rw[8];
+      const int d = t.col0 + c0 + q4;
+      if (d >= D) continue;
+      const bool vec = (d + 4 <= D) && ((D & 3) == 0);
+      float4 w[8], mo[8];
+      int rw[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            rw[u] = s_row[warp * 32 + rr + u];
-            if (rw[u] >= 0) {
-              w[u] = W[(size_t)rw[u] * D + d];
-              mo[u] = Mom[(size_t)rw[u] * D + d];
-            }
+      for (int u = 0; u < 8; ++u) {
+        rw[u] = s_row[warp * 32 + u * 4 + sub];
+        if (rw[u] >= 0) {
+          const size_t o = (size_t)rw[u] * D + d;
+          if (vec) {
+            w[u] = *reinterpret_cast<const float4*>(W + o);
+            mo[u] = *reinterpret_cast<const float4*>(Mom + o);
+          } else {
+            w[u] = make_float4(W[o], d + 1 < D ? W[o + 1] : 0.f, d + 2 < D ? W[o + 2] : 0.f,
+                               d + 3 < D ? W[o + 3] : 0.f);
+            mo[u] = make_float4(Mom[o], d + 1 < D ? Mom[o + 1] : 0.f,
+                                d + 2 < D ? Mom[o + 2] : 0.f, d + 3 < D ? Mom[o + 3] : 0.f);
           }
+        }
+      }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (rw[u] >= 0) {
-              const int r = warp * 32 + rr + u;
-              const float inv = s_inv[r];
-              const float dw = (stage[r * 33 + lane] - s_cp[r] * (w[u] * inv)) * inv;
-              const float g = dw + wd * w[u];
-              const float vv = mu * mo[u] + g;
-              Mom[(size_t)rw[u] * D + d] = vv;
-              W[(size_t)rw[u] * D + d] = w[u] - lr * vv;
+      for (int u = 0; u < 8; ++u) {
+        if (rw[u] < 0) continue;
+        const int r = warp * 32 + u * 4 + sub;
+        const float inv = s_inv[r], cpj = s_cp[r];
+        const float* a = stage + r * 33 + q4;
+        float wv[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+        float mv[4] = {mo[u].x, mo[u].y, mo[u].z, mo[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float dw = (a[e] - cpj * (wv[e] * inv)) * inv;
+          const float g = dw + wd * wv[e];
+          const float vv = mu * mv[e] + g;
+          mv[e] = vv;
+          wv[e] = wv[e] - lr * vv;
+        }
+        const size_t o = (size_t)rw[u] * D + d;
+        if (vec) {
+          *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+          *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (d + e < D) {
+              Mom[o + e] = mv[e];
+              W[o + e] = wv[e];
             }
-          }
         }
       }
     }
@@ -275,6 +369,7 @@ struct DwUpdateEpi {
 struct DxPartEpi {
   int B, D;
   float* part;  // [splits][B][D]
+  __device__ __forceinline__ void prefetch(const TileInfo&, int) const {}
   template <int BN, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid, uint8_t*) const {
     const int b = t.row0 + tid;

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const TileInfo ti = g.tile(t);
       const uint32_t as = it & 1, aph = (it >> 1) & 1;
+      epi.prefetch(ti, tid);
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const TmemSrc src{tmem_base + as * BN + ((uint32_t)((warp & 3) * 32) << 16)};
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int j = 0; j < BN; ++j) sAcc[tid * 65 + j] = acc[j];
   const SmemRowSrc src{sAcc + tid * 65};
+  epi.prefetch(ti, tid);
   epi.template run<BN>(ti, src, tid, epi_smem);
 }
 

@@ -215,32 +215,47 @@ __global__ void loss_reduce_kernel(const double* __restrict__ loss_row, int B, S
   }
 }
 
-// dX = (sum_split part - feat_proj * x^) / max(|x|, 1e-12)  (shardsim.hpp:371-375).
-template <typename ST>
-__global__ void dx_finalize_kernel(const float* __restrict__ part, int S,
-                                   const ST* __restrict__ fproj_part, int T,
-                                   const float* __restrict__ X, const float* __restrict__ xnorm,
-                                   int B, int D, float* __restrict__ dX, StepStatus* st) {
+// dX = (r - feat_proj * x^) / max(|x|, 1e-12)  (shardsim.hpp:371-375), r = sum_split part.
+// feat_proj_b = sum_j g_bj c_bj = x^_b . r_b since c_bj = x^_b . w^_j (exact identity).
+template <int D_PER_THREAD>
+__global__ void __launch_bounds__(256) dx_finalize_kernel(const float* __restrict__ part, int S,
+                                                          const float* __restrict__ X,
+                                                          const float* __restrict__ xnorm, int B,
+                                                          int D, float* __restrict__ dX,
+                                                          StepStatus* st) {
   const int b = blockIdx.x;
-  __shared__ double fp_s;
-  if (threadIdx.x < 32) {
-    double acc = 0.0;
-    for (int t = threadIdx.x; t < T; t += 32) acc += (double)fproj_part[(size_t)t * B + b];
-    acc = warp_sum(acc);
-    if (threadIdx.x == 0) fp_s = acc;
-  }
-  __syncthreads();
+  __shared__ double red[8];
   const float n = xnorm[b];
   const float inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
-  const float fp = (float)fp_s;
-  bool bad = false;
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+  float r[D_PER_THREAD], xh[D_PER_THREAD];
+  double dot = 0.0;
+#pragma unroll
+  for (int i = 0; i < D_PER_THREAD; ++i) {
+    const int d = threadIdx.x + i * 256;
     float acc = 0.f;
-    for (int s = 0; s < S; ++s) acc += part[((size_t)s * B + b) * D + d];
-    const float xh = X[(size_t)b * D + d] * inv;
-    const float v = (acc - fp * xh) * inv;
-    dX[(size_t)b * D + d] = v;
-    bad |= !isfinite(v);
+    xh[i] = 0.f;
+    if (d < D) {
+      for (int s = 0; s < S; ++s) acc += part[((size_t)s * B + b) * D + d];
+      xh[i] = X[(size_t)b * D + d] * inv;
+    }
+    r[i] = acc;
+    dot += (double)acc * (double)xh[i];
+  }
+  dot = warp_sum(dot);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+  __syncthreads();
+  double fp = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) fp += red[w];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < D_PER_THREAD; ++i) {
+    const int d = threadIdx.x + i * 256;
+    if (d < D) {
+      const float v = (r[i] - (float)fp * xh[i]) * inv;
+      dX[(size_t)b * D + d] = v;
+      bad |= !isfinite(v);
+    }
   }
   if (bad && !sampler_failed(st)) st->nonfinite_dx = 1;
 }

@@ -164,8 +164,7 @@ struct Ctx {
   double* zpos = nullptr;
   double* loss_row = nullptr;
   // backward
-  void* G = nullptr;       // [maxB][ldg]
-  void* fproj = nullptr;   // [T][maxB]
+  void* G = nullptr;       // G^T [ncols_pad][ldg] (ldg = maxB rounded to 8)
   void* cproj = nullptr;   // [mt][ncols]
   float* dx_part = nullptr;  // [S][maxB][D]
   float* dX = nullptr;       // [maxB][D]
@@ -176,7 +175,7 @@ struct Ctx {
   StepStatus* st_host = nullptr;
   // tensor maps cached per batch
   int64_t tm_B = -1;
-  CUtensorMap tm_x_k, tm_w_k, tm_g_mn, tm_x_mn, tm_g_k, tm_w_mn;
+  CUtensorMap tm_x_k, tm_w_k, tm_w_k128, tm_x_k256, tm_gt_k, tm_x_mn, tm_gt_mn, tm_w_mn;
   // nccl
   ncclComm_t comm = nullptr;
   // bookkeeping
@@ -272,14 +271,17 @@ cudaError_t launch_simt(Ctx* c, const float* A, int lda, const float* Bm, int ld
 int ensure_maps(Ctx* c, int64_t B) {
   if (!c->bf16 || c->tm_B == B) return PFC_OK;
   bool ok = true;
-  // logits / G GEMMs: A = X^ [B][Dp] K-major, B = W^ [ncols][Dp] K-major
+  // logits GEMM (M = b, N = classes): A = X^ [B][Dp], B = W^ [ncols][Dp], both K-major
   ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128);
   ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kBN);
-  // dW GEMM: A = G as [B rows][ncols cols], MN-major (classes contiguous); B = X^ MN-major
-  ok &= make_map(&c->tm_g_mn, c->G, c->ncols, B, c->ldg, 64);
+  // G GEMM (M = classes, N = b): A = W^ K-major, B = X^ K-major
+  ok &= make_map(&c->tm_w_k128, c->wh, c->Dp, c->ncols, c->Dp, 128);
+  ok &= make_map(&c->tm_x_k256, c->xh, c->Dp, B, c->Dp, kBN);
+  // dW GEMM (M = classes, N = d, K = b): A = G^T [ncols][ldg] K-major; B = X^ MN-major
+  ok &= make_map(&c->tm_gt_k, c->G, B, c->ncols, c->ldg, 128);
   ok &= make_map(&c->tm_x_mn, c->xh, c->Dp, B, c->Dp, 64);
-  // dX GEMM: A = G K-major (classes contiguous = K); B = W^ MN-major (D contiguous = N)
-  ok &= make_map(&c->tm_g_k, c->G, c->ncols, B, c->ldg, 128);
+  // dX GEMM (M = b, N = d, K = classes): A = G^T read MN-major (b contiguous); B = W^ MN-major
+  ok &= make_map(&c->tm_gt_mn, c->G, B, c->ncols, c->ldg, 64);
   ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, 64);
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
@@ -359,15 +361,18 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   ST* pm = static_cast<ST*>(c->part_m);
   ST* ps = static_cast<ST*>(c->part_s);
   const float tau = (float)c->d.filter_threshold;
+  const bool filt = c->d.has_filter != 0;
   // ---- logits GEMM + margin + online softmax partials (shardsim.hpp:249-318)
   const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, BN, 1, 0);
   {
-    FwdStatsEpi<ST> e{(int)B, (int)c->ncols, c->pos_col, c->mg, c->d.has_filter, tau, pm, ps,
-                      c->zpos};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
-    else err = launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp, (const float*)c->wh,
-                                         (int)c->Dp, gf, e);
+    auto go = [&](auto e) {
+      if constexpr (kUmma) return launch_umma<kBN, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
+      else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
+                                            (const float*)c->wh, (int)c->Dp, gf, e);
+    };
+    if (filt) err = go(FwdStatsEpi<ST, true>{(int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, ps, c->zpos});
+    else err = go(FwdStatsEpi<ST, false>{(int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, ps, c->zpos});
     CUDA_TRY(c, err);
   }
   phase(c, "logits_gemm");
@@ -393,31 +398,38 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   c->launches += 2;
   CUDA_TRY(c, cudaGetLastError());
   phase(c, "softmax_stats");
-  // ---- G = dL/dcos (recomputed logits), feat_proj / center_proj partials (shardsim.hpp:341-362)
-  ST* fp = static_cast<ST*>(c->fproj);
+  // ---- G^T = dL/dcos (recomputed logits, M = classes, N = b) + center_proj partials
   ST* cp = static_cast<ST*>(c->cproj);
+  const GemmGeom gg = make_geom((int)c->ncols, (int)B, (int)c->Dp, BN, 1, 1);
   {
-    GradEpi<ST, OT> e{(int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, c->d.has_filter, tau,
-                      gm, ig, (ST)(1.0 / (double)B), static_cast<OT*>(c->G), fp, cp};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
-    else err = launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp, (const float*)c->wh,
-                                         (int)c->Dp, gf, e);
+    auto go = [&](auto e) {
+      if constexpr (kUmma) return launch_umma<kBN, false, false>(c, c->tm_w_k128, c->tm_x_k256, gg, e);
+      else return launch_simt<false, false>(c, (const float*)c->wh, (int)c->Dp,
+                                            (const float*)c->xh, (int)c->Dp, gg, e);
+    };
+    OT* Gt = static_cast<OT*>(c->G);
+    const ST invB = (ST)(1.0 / (double)B);
+    if (filt) err = go(GradEpi<ST, OT, true>{(int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
+    else err = go(GradEpi<ST, OT, false>{(int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
     CUDA_TRY(c, err);
   }
   phase(c, "grad_gemm");
-  // ---- dX = sum_j g_bj w^_j (split-K), then (acc - feat_proj x^)/|x| (shardsim.hpp:363-376)
+  // ---- dX = sum_j g_bj w^_j (split-K), then tangent projection / |x| (shardsim.hpp:363-376)
   {
     const int S = dx_splits(c, B);
     const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0);
     DxPartEpi e{(int)B, (int)c->D, c->dx_part};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, false, true>(c, c->tm_g_k, c->tm_w_mn, gx, e);
-    else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
-                                        (int)c->Dp, gx, e);
+    if constexpr (kUmma) err = launch_umma<kBN, true, true>(c, c->tm_gt_mn, c->tm_w_mn, gx, e);
+    else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
+                                       (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
-    dx_finalize_kernel<ST><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, fp, T, x, c->xnorm,
-                                                       (int)B, (int)c->D, dx_full, c->st);
+    const int dpt = (int)ceil_div(c->D, 256);
+    if (dpt <= 1) dx_finalize_kernel<1><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
+    else if (dpt <= 2) dx_finalize_kernel<2><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
+    else if (dpt <= 4) dx_finalize_kernel<4><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
+    else dx_finalize_kernel<8><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
   }
@@ -425,12 +437,12 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- dW = sum_b g_bj x^_b, corrected, fused momentum-SGD on sampled rows (shardsim.hpp:377-417)
   {
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
-    DwUpdateEpi<ST> e{(int)c->ncols, (int)c->D, gf.m_tiles, c->wnorm, c->lrow, cp, c->W, c->M,
+    DwUpdateEpi<ST> e{(int)c->ncols, (int)c->D, gg.n_tiles, c->wnorm, c->lrow, cp, c->W, c->M,
                       (float)a->lr, (float)c->d.momentum, (float)c->d.weight_decay, c->st};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, true, true>(c, c->tm_g_mn, c->tm_x_mn, gw, e);
-    else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
-                                       (int)c->Dp, gw, e);
+    if constexpr (kUmma) err = launch_umma<kBN, false, true>(c, c->tm_gt_k, c->tm_x_mn, gw, e);
+    else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
+                                        (int)c->Dp, gw, e);
     CUDA_TRY(c, err);
   }
   phase(c, "dw_update_gemm");
@@ -612,7 +624,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->rows = c->cls_hi - c->cls_lo;
   c->ncols = c->nk * c->cap;
   c->ncols_pad = round_up(std::max<int64_t>(c->ncols, 1), 256);
-  c->ldg = round_up(std::max<int64_t>(c->ncols, 1), 8);
+  c->ldg = round_up(desc->max_batch, 8);  // G^T row stride
   c->pool_stride = std::max<int64_t>(c->blk, 1);
   c->maxB = desc->max_batch;
   c->mg.kind = desc->margin_kind;
@@ -647,7 +659,6 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
   const int BN = c->bf16 ? kBN : kSimtBN;
   const int64_t T = ceil_div(std::max<int64_t>(c->ncols, 1), BN);
-  const int64_t mt = ceil_div(B, 128);
   c->max_splits = c->bf16 ? 32 : 64;
   CT(dalloc(c, &c->W, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
   CT(dalloc(c, &c->M, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
@@ -674,10 +685,9 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->inv_gsum), (size_t)B * sb));
   CT(dalloc(c, &c->zpos, (size_t)B));
   CT(dalloc(c, &c->loss_row, (size_t)B));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)B * c->ldg * ob));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->fproj), (size_t)(T * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->cproj),
-            (size_t)(mt * std::max<int64_t>(c->ncols, 1)) * sb));
+            (size_t)(ceil_div(B, BN) * std::max<int64_t>(c->ncols, 1)) * sb));
   CT(dalloc(c, &c->dx_part, (size_t)c->max_splits * B * c->D));
   CT(dalloc(c, &c->dX, (size_t)B * c->D));
   CT(dalloc(c, &c->xdb, (size_t)B * c->D));

@@ -1,17 +1,20 @@
-// epilogues.cuh — fused GEMM epilogues of the Partial-FC step.  Each functor is run by 128
-// threads; thread `tid` owns accumulator row (row0 + tid) and pulls 32-column chunks from the
-// accumulator source (TMEM on the tcgen05 engine, shared memory on the SIMT engine).
+// epilogues.cuh — fused GEMM epilogues of the Partial-FC step.  Each epilogue warpgroup (128
+// threads) runs the functor; thread `row` owns accumulator row (row0 + row) and pulls 32-column
+// chunks from the accumulator source (TMEM on the tcgen05 engine, shared memory on the SIMT
+// engine).  With NWG warpgroups, warpgroup wg owns columns [wg*BN/NWG, (wg+1)*BN/NWG).
 //
 //   FwdStatsEpi  rows = batch rows b, cols = buffered classes j.
 //                cos tile -> margin (margin.hpp:41-54) + filter mask (shardsim.hpp:258-268)
-//                -> per (row, column-tile) online (max, sum exp) partials and z_pos
+//                -> per (row, column-slice) online (max, sum exp) partials and z_pos
 //                (shardsim.hpp:270-318 restated flash-style: nothing B x cap reaches HBM).
 //   GradEpi      rows = buffered classes j, cols = batch rows b (the recomputed cos tile).
-//                g = ((p - onehot)/B) * margin'(c)  (shardsim.hpp:352-362) -> G^T (bf16/fp32)
-//                and center_proj_j = sum_b g c partials, thread-local in this orientation.
+//                g = ((p - onehot)/B) * margin'(c)  (shardsim.hpp:352-362) -> G^T (bf16 via
+//                swizzled smem + TMA store, or fp32) and center_proj_j = sum_b g c partials,
+//                thread-local in this orientation.
 //   DwUpdateEpi  rows = classes, cols = dims: dW = (sum_b g x^ - center_proj w^)/|w|
 //                (shardsim.hpp:377-384) fused with the sparse momentum-SGD of the sampled rows
-//                (update_centers, shardsim.hpp:139-159).
+//                (update_centers, shardsim.hpp:139-159); W / momentum of the next tile are
+//                prefetched into L2 while this tile is processed.
 //   DxPartEpi    rows = batch rows, cols = dims: split-K partials of sum_j g w^_j.
 // feat_proj_b = sum_j g c_bj equals x^_b . (sum_j g w^_j) because c_bj = x^_b . w^_j, so it is
 // formed in dx_finalize_kernel from the dX GEMM result instead of being reduced here.
@@ -37,25 +40,29 @@ __device__ __forceinline__ bool status_failed(const StepStatus* st) {
 
 template <typename ST, bool kFilter>
 struct FwdStatsEpi {
+  static constexpr int kSmem = 0;
   int B, ncols;
   const int32_t* pos_col;
   MarginDev mg;
   float tau;
-  ST* part_m;  // [n_tiles][B]
-  ST* part_s;  // [n_tiles][B]
+  ST* part_m;  // [n_tiles * NWG][B]
+  ST* part_s;
   double* zpos;
 
-  __device__ __forceinline__ void prefetch(const TileInfo&, int) const {}
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void finish(int, int) const {}
 
-  template <int BN, class Src>
-  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid, uint8_t*) const {
-    const int b = t.row0 + tid;
+  template <int BN, int NWG, class Src>
+  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
+                                      uint8_t*) const {
+    constexpr int CW = BN / NWG;
+    const int b = t.row0 + row;
     const bool rv = b < B;
     const int pc = rv ? pos_col[b] : -1;
     ST m = neg_inf<ST>(), s = ST(0);
     const float A = mg.s * kLog2e;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
       float v[32];
       src.load(c0, v);
       const int colb = t.col0 + c0;
@@ -109,19 +116,23 @@ struct FwdStatsEpi {
       m = mn;
     }
     if (rv) {
-      part_m[(size_t)t.n_tile * B + b] = m;
-      part_s[(size_t)t.n_tile * B + b] = s;
+      const size_t slot = (size_t)(t.n_tile * NWG + wg) * B + b;
+      part_m[slot] = m;
+      part_s[slot] = s;
     }
   }
 };
 
-__device__ __forceinline__ void store_g32(__nv_bfloat16* dst, const float (&g)[32]) {
-  uint32_t w[16];
+__device__ __forceinline__ void pack_bf16x32(const float (&g)[32], uint32_t (&w)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const __nv_bfloat162 h = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
     w[i] = *reinterpret_cast<const uint32_t*>(&h);
   }
+}
+__device__ __forceinline__ void store_g32(__nv_bfloat16* dst, const float (&g)[32]) {
+  uint32_t w[16];
+  pack_bf16x32(g, w);
   uint4* d = reinterpret_cast<uint4*>(dst);
 #pragma unroll
   for (int i = 0; i < 4; ++i) d[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
@@ -135,8 +146,10 @@ __device__ __forceinline__ void store_g1(__nv_bfloat16* dst, float g) { *dst = _
 __device__ __forceinline__ void store_g1(float* dst, float g) { *dst = g; }
 
 // rows = buffered classes j (M), cols = batch rows b (N).  Writes G^T[j][b].
-template <typename ST, typename GT, bool kFilter>
-struct GradEpi {
+template <typename ST, typename GT, bool kFilter, bool kTma>
+struct alignas(64) GradEpi {
+  static constexpr int kSmem = 20 * 1024;
+  CUtensorMap tm;     // G^T store map: inner = b (box 32, SWIZZLE_64B), outer = classes (box 128)
   int B, ncols, ldgt;
   const int32_t* pos_col;
   MarginDev mg;
@@ -145,24 +158,33 @@ struct GradEpi {
   const ST* inv_gsum;
   ST inv_batch;
   GT* Gt;             // [ncols_pad][ldgt]
-  ST* cproj_part;     // [n_tiles(b)][ncols]
+  ST* cproj_part;     // [n_tiles(b) * NWG][ncols]
 
-  __device__ __forceinline__ void prefetch(const TileInfo&, int) const {}
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void finish(int row, int) const {
+    if constexpr (kTma) {
+      if (row == 0) pfc_sm100::bulk_wait_all();
+    }
+  }
 
-  template <int BN, class Src>
-  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid,
+  template <int BN, int NWG, class Src>
+  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
                                       uint8_t* smem) const {
-    // per-column (b) constants and the tile's positives list in shared memory
-    float2* cf = reinterpret_cast<float2*>(smem);               // [BN] {gmax*log2e, s*ig/B}
-    ST* cg = reinterpret_cast<ST*>(cf + BN);                    // [BN] gmax
-    ST* ci = cg + BN;                                           // [BN] inv_gsum
-    int* plist = reinterpret_cast<int*>(ci + BN);               // [BN] (col << 8) | row
-    int* pcount = plist + BN;
-    pfc_sm100::named_bar_sync(1, 128);  // previous tile finished reading smem
-    if (tid == 0) *pcount = 0;
-    pfc_sm100::named_bar_sync(1, 128);
-    for (int i = tid; i < BN; i += 128) {
-      const int b = t.col0 + i;
+    constexpr int CW = BN / NWG;
+    const int cb = wg * CW;
+    const uint32_t bar = 1 + wg;
+    // per-column (b) constants and the slice's positives list in shared memory
+    float2* cf = reinterpret_cast<float2*>(smem);               // [CW] {gmax*log2e, s*ig/B}
+    ST* cg = reinterpret_cast<ST*>(cf + CW);                    // [CW] gmax
+    ST* ci = cg + CW;                                           // [CW] inv_gsum
+    int* plist = reinterpret_cast<int*>(ci + CW);               // [CW] (col << 8) | row
+    int* pcount = plist + CW;
+    uint8_t* stage = smem + 4096;                               // 2 x [128][64 B] swizzled
+    pfc_sm100::named_bar_sync(bar, 128);  // previous tile finished reading smem
+    if (row == 0) *pcount = 0;
+    pfc_sm100::named_bar_sync(bar, 128);
+    for (int i = row; i < CW; i += 128) {
+      const int b = t.col0 + cb + i;
       float2 k = make_float2(0.f, 0.f);
       ST gm = ST(0), ig = ST(0);
       if (b < B) {
@@ -179,23 +201,25 @@ struct GradEpi {
       cg[i] = gm;
       ci[i] = ig;
     }
-    pfc_sm100::named_bar_sync(1, 128);
-    const int j = t.row0 + tid;
+    pfc_sm100::named_bar_sync(bar, 128);
+    const int j = t.row0 + row;
     const bool rv = j < ncols;
     const int npl = *pcount;
     const float A = mg.s * kLog2e;
     ST cp = ST(0);
+    int buf = 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = cb; c0 < cb + CW; c0 += 32, buf ^= 1) {
       float v[32];
       src.load(c0, v);
       const int colb = t.col0 + c0;
-      if (colb >= B) continue;  // uniform across the CTA; TMA / SIMT zero-fill columns >= B
+      if (colb >= B) continue;  // uniform across the warpgroup
+      const int lc = c0 - cb;
       float g[32];
       if constexpr (std::is_same<ST, float>::value) {
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-          const float2 k = cf[c0 + q];
+          const float2 k = cf[lc + q];
           float gq = pfc_sm100::ex2_approx(fmaf(v[q], A, -k.x)) * k.y;
           if (kFilter) gq = v[q] > tau ? 0.f : gq;
           g[q] = gq;
@@ -206,7 +230,7 @@ struct GradEpi {
           const int b = colb + q;
           double gq = 0.0;
           if (b < B && !(kFilter && v[q] > tau)) {
-            const double p = exp((double)mg.s * (double)v[q] - (double)cg[c0 + q]) * (double)ci[c0 + q];
+            const double p = exp((double)mg.s * (double)v[q] - (double)cg[lc + q]) * (double)ci[lc + q];
             gq = p * (double)inv_batch * mg.sd;
           }
           g[q] = (float)gq;
@@ -215,13 +239,13 @@ struct GradEpi {
       // positives of this chunk (label b has its centre j): replace by the margin form
       for (int e = 0; e < npl; ++e) {
         const int pe = plist[e];
-        const int q = (pe >> 8) - c0;
-        if ((pe & 255) == tid && (unsigned)q < 32u) {
+        const int q = (pe >> 8) - lc;
+        if ((pe & 255) == row && (unsigned)q < 32u) {
           float vq = 0.f;
 #pragma unroll
           for (int u = 0; u < 32; ++u) vq = (u == q) ? v[u] : vq;
           const double z = margin_pos(mg, (double)vq);
-          const double p = exp(z - (double)cg[c0 + q]) * (double)ci[c0 + q];
+          const double p = exp(z - (double)cg[lc + q]) * (double)ci[lc + q];
           const double gq = (p - 1.0) * (double)inv_batch * margin_deriv_pos(mg, (double)vq);
 #pragma unroll
           for (int u = 0; u < 32; ++u) g[u] = (u == q) ? (float)gq : g[u];
@@ -238,21 +262,42 @@ struct GradEpi {
         c2 += (ST)g[q + 1] * (ST)v[q + 1];
       }
       cp += c1 + c2;
-      GT* dst = Gt + (size_t)j * ldgt + colb;
-      if (colb + 32 <= B) {
-        store_g32(dst, g);
-      } else {
+      if constexpr (kTma) {
+        // coalesced write-out: swizzled (64B) smem staging + one TMA store per 128 x 32 chunk
+        uint8_t* sb = stage + buf * 8192;
+        if (row == 0) pfc_sm100::bulk_wait_read<1>();
+        pfc_sm100::named_bar_sync(bar, 128);
+        uint32_t w[16];
+        pack_bf16x32(g, w);
+        const int sw = (row >> 1) & 3;
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (colb + q < B) store_g1(dst + q, g[q]);
+        for (int qq = 0; qq < 4; ++qq)
+          *reinterpret_cast<uint4*>(sb + row * 64 + ((qq ^ sw) << 4)) =
+              make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
+        pfc_sm100::fence_proxy_async_smem();
+        pfc_sm100::named_bar_sync(bar, 128);
+        if (row == 0) {
+          pfc_sm100::tma_store_2d(&tm, sb, colb, t.row0);
+          pfc_sm100::bulk_commit();
+        }
+      } else {
+        GT* dst = Gt + (size_t)j * ldgt + colb;
+        if (colb + 32 <= B) {
+          store_g32(dst, g);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (colb + q < B) store_g1(dst + q, g[q]);
+        }
       }
     }
-    if (rv) cproj_part[(size_t)t.n_tile * ncols + j] = cp;
+    if (rv) cproj_part[(size_t)(t.n_tile * NWG + wg) * ncols + j] = cp;
   }
 };
 
 template <typename ST>
 struct DwUpdateEpi {
+  static constexpr int kSmem = 18 * 1024;
   int ncols, D, n_parts;
   const float* wnorm;       // [ncols]
   const int32_t* lrow;      // [ncols] local row of W
@@ -261,34 +306,40 @@ struct DwUpdateEpi {
   float* Mom;
   float lr, mu, wd;
   const StepStatus* st;  // no update when the step failed (the reference throws before 412)
+  int cw;                // columns per warpgroup (BN / NWG), for prefetch
 
-  // Pull this tile's W / momentum row segments toward L2 while the MMA still runs.
-  __device__ __forceinline__ void prefetch(const TileInfo& t, int tid) const {
-    const int c = t.row0 + tid;
+  // Pull a tile's W / momentum row segments toward L2 (issued one tile ahead).
+  __device__ __forceinline__ void prefetch(const TileInfo& t, int row, int wg) const {
+    const int c = t.row0 + row;
     if (c >= ncols) return;
     const int r = lrow[c];
     if (r < 0) return;
-    const int dn = (t.col0 + 256 <= D) ? 256 : D - t.col0;
-    const char* w = reinterpret_cast<const char*>(W + (size_t)r * D + t.col0);
-    const char* m = reinterpret_cast<const char*>(Mom + (size_t)r * D + t.col0);
+    const int d0 = t.col0 + wg * cw;
+    if (d0 >= D) return;
+    const int dn = min(cw, D - d0);
+    const char* w = reinterpret_cast<const char*>(W + (size_t)r * D + d0);
+    const char* m = reinterpret_cast<const char*>(Mom + (size_t)r * D + d0);
     for (int off = 0; off < dn * 4; off += 128) {
       pfc_sm100::prefetch_l2(w + off);
       pfc_sm100::prefetch_l2(m + off);
     }
   }
+  __device__ __forceinline__ void finish(int, int) const {}
 
-  template <int BN, class Src>
-  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid,
+  template <int BN, int NWG, class Src>
+  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
                                       uint8_t* smem) const {
+    constexpr int CW = BN / NWG;
+    const uint32_t bar = 1 + wg;
     float* stage = reinterpret_cast<float*>(smem);  // [128][33]
     float* s_inv = stage + 128 * 33;
     float* s_cp = s_inv + 128;
     int* s_row = reinterpret_cast<int*>(s_cp + 128);
-    const int warp = tid >> 5, lane = tid & 31;
-    pfc_sm100::named_bar_sync(1, 128);  // previous tile's readers are done with smem
+    const int warp = row >> 5, lane = row & 31;
+    pfc_sm100::named_bar_sync(bar, 128);  // previous tile's readers are done with smem
     const bool failed = status_failed(st);
     {
-      const int c = t.row0 + tid;
+      const int c = t.row0 + row;
       float inv = 0.f, cp = 0.f;
       int r = -1;
       if (c < ncols && !failed) {
@@ -299,19 +350,19 @@ struct DwUpdateEpi {
         cp = (float)acc;
         r = lrow[c];
       }
-      s_inv[tid] = inv;
-      s_cp[tid] = cp;
-      s_row[tid] = r;
+      s_inv[row] = inv;
+      s_cp[row] = cp;
+      s_row[row] = r;
     }
     const int sub = lane >> 3, q4 = (lane & 7) * 4;  // 4 rows x 8 lanes x float4 per warp op
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
       float v[32];
       src.load(c0, v);
-      pfc_sm100::named_bar_sync(1, 128);
+      pfc_sm100::named_bar_sync(bar, 128);
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[tid * 33 + q] = v[q];
-      pfc_sm100::named_bar_sync(1, 128);
+      for (int q = 0; q < 32; ++q) stage[row * 33 + q] = v[q];
+      pfc_sm100::named_bar_sync(bar, 128);
       const int d = t.col0 + c0 + q4;
       if (d >= D) continue;
       const bool vec = (d + 4 <= D) && ((D & 3) == 0);
@@ -367,14 +418,18 @@ struct DwUpdateEpi {
 };
 
 struct DxPartEpi {
+  static constexpr int kSmem = 0;
   int B, D;
   float* part;  // [splits][B][D]
-  __device__ __forceinline__ void prefetch(const TileInfo&, int) const {}
-  template <int BN, class Src>
-  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int tid, uint8_t*) const {
-    const int b = t.row0 + tid;
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void finish(int, int) const {}
+  template <int BN, int NWG, class Src>
+  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
+                                      uint8_t*) const {
+    constexpr int CW = BN / NWG;
+    const int b = t.row0 + row;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
       float v[32];
       src.load(c0, v);
       const int d0 = t.col0 + c0;

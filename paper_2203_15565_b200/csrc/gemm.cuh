@@ -68,12 +68,12 @@ inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest
   return g;
 }
 
-constexpr int kEpiSmemBytes = 20 * 1024;
+constexpr int kEpiSmemBytes = 20 * 1024;  // SIMT engine epilogue scratch
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NWG, class Epi>
 constexpr int umma_smem_bytes() {
-  return 1024 /*align slack*/ + STAGES * (128 * 64 * 2 + BN * 64 * 2) + 256 /*barriers*/ +
-         kEpiSmemBytes;
+  return 1024 /*align slack*/ + STAGES * (128 * 64 * 2 + BN * 64 * 2) + 1024 /*barriers*/ +
+         NWG * Epi::kSmem;
 }
 
 struct TmemSrc {
@@ -83,10 +83,11 @@ struct TmemSrc {
   }
 };
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, class Epi>
-__global__ void __launch_bounds__(256, 1)
+template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(128 + 128 * NWG, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, const GemmGeom g, const Epi epi) {
+                     const __grid_constant__ CUtensorMap tmB, const GemmGeom g,
+                     const __grid_constant__ Epi epi) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using namespace pfc_sm100;
   constexpr uint32_t A_BYTES = 128 * 64 * 2;
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* epi_smem = smem + STAGES * STAGE_BYTES + 256;
+  uint8_t* epi_smem = smem + STAGES * STAGE_BYTES + 1024;  // 1024-aligned per-WG scratch
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 128 * NWG);
     }
     fence_barrier_init();
   }
@@ -189,19 +190,25 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int tid = threadIdx.x - 128;
+    // epilogue warpgroups: warp w reads TMEM lanes 32*(w%4).. (row = accumulator row);
+    // warpgroup wg takes columns [wg*BN/NWG, (wg+1)*BN/NWG) of every tile.
+    const int wg = (warp - 4) >> 2;
+    const int row = ((warp & 3) << 5) | lane;
+    uint8_t* wsm = epi_smem + wg * Epi::kSmem;
     uint32_t it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const TileInfo ti = g.tile(t);
       const uint32_t as = it & 1, aph = (it >> 1) & 1;
-      epi.prefetch(ti, tid);
+      if (it == 0) epi.prefetch(ti, row, wg);
+      if (t + (int)gridDim.x < total) epi.prefetch(g.tile(t + gridDim.x), row, wg);
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const TmemSrc src{tmem_base + as * BN + ((uint32_t)((warp & 3) * 32) << 16)};
-      epi.template run<BN>(ti, src, tid, epi_smem);
+      epi.template run<BN, NWG>(ti, src, row, wg, wsm);
       tc_fence_before();
       mbar_arrive(&tempty[as]);
     }
+    epi.finish(row, wg);
   }
   __syncthreads();
   if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
@@ -264,8 +271,8 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int j = 0; j < BN; ++j) sAcc[tid * 65 + j] = acc[j];
   const SmemRowSrc src{sAcc + tid * 65};
-  epi.prefetch(ti, tid);
-  epi.template run<BN>(ti, src, tid, epi_smem);
+  epi.template run<BN, 1>(ti, src, tid, 0, epi_smem);
+  epi.finish(tid, 0);
 }
 
 constexpr int kSimtSmemBytes = (32 * 129 + 32 * 64 + 128 * 65) * 4 + kEpiSmemBytes;

@@ -95,24 +95,28 @@ PFN_encodeTiled_t get_encode() {
   return fn;
 }
 
-// 2-D bf16 tensor [outer][inner] with row stride ld (elements); box {64, box_outer}, 128B swizzle.
+// 2-D bf16 tensor [outer][inner] with row stride ld (elements); box {box_inner, box_outer}.
+// Loads use {64, rows} with 128B swizzle (UMMA operand atoms); the G^T store uses {32, 128}
+// with 64B swizzle (matching the epilogue's smem staging).
 bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_outer) {
+              uint32_t box_outer, uint32_t box_inner = 64,
+              CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled_t enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
-constexpr int kBN = 256, kStages = 4;  // tcgen05 tile 128 x 256, 4-stage ring
+constexpr int kBN = 256;  // tcgen05 tile 128 x 256
+constexpr int kNWG = 2;   // epilogue warpgroups per CTA on the tcgen05 engine
 constexpr int kSimtBN = 64;
 
 struct PhaseTimer {
@@ -175,7 +179,7 @@ struct Ctx {
   StepStatus* st_host = nullptr;
   // tensor maps cached per batch
   int64_t tm_B = -1;
-  CUtensorMap tm_x_k, tm_w_k, tm_w_k128, tm_x_k256, tm_gt_k, tm_x_mn, tm_gt_mn, tm_w_mn;
+  CUtensorMap tm_x_k, tm_w_k, tm_w_k128, tm_x_k256, tm_gt_k, tm_x_mn, tm_gt_mn, tm_w_mn, tm_gt_st;
   // nccl
   ncclComm_t comm = nullptr;
   // bookkeeping
@@ -232,11 +236,12 @@ void phase(Ctx* c, const char* name) {
 }
 
 // ------------------------------------------------------------------ GEMM launchers
-template <int BN, bool A_MN, bool B_MN, class Epi>
+template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi>
 cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, const GemmGeom& g,
                         const Epi& epi) {
-  auto kern = umma_gemm_kernel<BN, kStages, A_MN, B_MN, Epi>;
-  constexpr int smem = umma_smem_bytes<BN, kStages>();
+  auto kern = umma_gemm_kernel<BN, STAGES, NWG, A_MN, B_MN, Epi>;
+  constexpr int smem = umma_smem_bytes<BN, STAGES, NWG, Epi>();
+  static_assert(smem <= 232448, "shared memory budget");
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -246,7 +251,7 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
   const int total = g.total();
   const int grid = total < c->num_sms ? total : c->num_sms;
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, 256, smem, c->stream>>>(ta, tb, g, epi);
+  kern<<<grid, 128 + 128 * NWG, smem, c->stream>>>(ta, tb, g, epi);
   c->launches++;
   return cudaGetLastError();
 }
@@ -283,6 +288,8 @@ int ensure_maps(Ctx* c, int64_t B) {
   // dX GEMM (M = b, N = d, K = classes): A = G^T read MN-major (b contiguous); B = W^ MN-major
   ok &= make_map(&c->tm_gt_mn, c->G, B, c->ncols, c->ldg, 64);
   ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, 64);
+  // G GEMM epilogue store of G^T (box 32 b x 128 classes, 64B swizzle)
+  ok &= make_map(&c->tm_gt_st, c->G, B, c->ncols, c->ldg, 128, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
   return PFC_OK;
@@ -358,6 +365,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   CUDA_TRY(c, cudaMemsetAsync(c->zpos, 0, sizeof(double) * B, s));
 
   constexpr int BN = kUmma ? kBN : kSimtBN;
+  constexpr int NWG = kUmma ? kNWG : 1;
   ST* pm = static_cast<ST*>(c->part_m);
   ST* ps = static_cast<ST*>(c->part_s);
   const float tau = (float)c->d.filter_threshold;
@@ -367,7 +375,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   {
     cudaError_t err;
     auto go = [&](auto e) {
-      if constexpr (kUmma) return launch_umma<kBN, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
+      if constexpr (kUmma) return launch_umma<kBN, 4, kNWG, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
       else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
                                             (const float*)c->wh, (int)c->Dp, gf, e);
     };
@@ -377,7 +385,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   }
   phase(c, "logits_gemm");
   // ---- softmax statistics: tiles -> rank-local, then across ranks (collectives 1 + 2)
-  const int T = gf.n_tiles;
+  const int T = gf.n_tiles * NWG;  // (max, sumexp) partial slots per row
   ST* lm = static_cast<ST*>(c->lm);
   ST* ls = static_cast<ST*>(c->ls);
   merge_tiles_kernel<ST><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(pm, ps, T, (int)B,
@@ -404,14 +412,14 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   {
     cudaError_t err;
     auto go = [&](auto e) {
-      if constexpr (kUmma) return launch_umma<kBN, false, false>(c, c->tm_w_k128, c->tm_x_k256, gg, e);
+      if constexpr (kUmma) return launch_umma<kBN, 3, kNWG, false, false>(c, c->tm_w_k128, c->tm_x_k256, gg, e);
       else return launch_simt<false, false>(c, (const float*)c->wh, (int)c->Dp,
                                             (const float*)c->xh, (int)c->Dp, gg, e);
     };
     OT* Gt = static_cast<OT*>(c->G);
     const ST invB = (ST)(1.0 / (double)B);
-    if (filt) err = go(GradEpi<ST, OT, true>{(int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
-    else err = go(GradEpi<ST, OT, false>{(int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
+    if (filt) err = go(GradEpi<ST, OT, true, kUmma>{c->tm_gt_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
+    else err = go(GradEpi<ST, OT, false, kUmma>{c->tm_gt_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
     CUDA_TRY(c, err);
   }
   phase(c, "grad_gemm");
@@ -421,7 +429,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0);
     DxPartEpi e{(int)B, (int)c->D, c->dx_part};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, true, true>(c, c->tm_gt_mn, c->tm_w_mn, gx, e);
+    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, true, true>(c, c->tm_gt_mn, c->tm_w_mn, gx, e);
     else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
                                        (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
@@ -437,10 +445,11 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- dW = sum_b g_bj x^_b, corrected, fused momentum-SGD on sampled rows (shardsim.hpp:377-417)
   {
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
-    DwUpdateEpi<ST> e{(int)c->ncols, (int)c->D, gg.n_tiles, c->wnorm, c->lrow, cp, c->W, c->M,
-                      (float)a->lr, (float)c->d.momentum, (float)c->d.weight_decay, c->st};
+    DwUpdateEpi<ST> e{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp, c->W, c->M,
+                      (float)a->lr, (float)c->d.momentum, (float)c->d.weight_decay, c->st,
+                      BN / NWG};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, false, true>(c, c->tm_gt_k, c->tm_x_mn, gw, e);
+    if constexpr (kUmma) err = launch_umma<kBN, 3, kNWG, false, true>(c, c->tm_gt_k, c->tm_x_mn, gw, e);
     else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
                                         (int)c->Dp, gw, e);
     CUDA_TRY(c, err);
@@ -677,8 +686,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->wh), (size_t)c->ncols_pad * c->Dp * ob));
   CT(dalloc(c, &c->wnorm, (size_t)c->ncols_pad));
   CT(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_m), (size_t)(T * B) * sb));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(T * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_m), (size_t)(T * kNWG * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(T * kNWG * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->lm), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->ls), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->gmax), (size_t)B * sb));
@@ -687,7 +696,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->loss_row, (size_t)B));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->cproj),
-            (size_t)(ceil_div(B, BN) * std::max<int64_t>(c->ncols, 1)) * sb));
+            (size_t)(ceil_div(B, BN) * kNWG * std::max<int64_t>(c->ncols, 1)) * sb));
   CT(dalloc(c, &c->dx_part, (size_t)c->max_splits * B * c->D));
   CT(dalloc(c, &c->dX, (size_t)B * c->D));
   CT(dalloc(c, &c->xdb, (size_t)B * c->D));

@@ -148,7 +148,7 @@ __device__ __forceinline__ void store_g1(float* dst, float g) { *dst = g; }
 // rows = buffered classes j (M), cols = batch rows b (N).  Writes G^T[j][b].
 template <typename ST, typename GT, bool kFilter, bool kTma>
 struct alignas(64) GradEpi {
-  static constexpr int kSmem = 20 * 1024;
+  static constexpr int kSmem = 36 * 1024;  // 4 KB column constants + 4 x 8 KB G^T staging
   CUtensorMap tm;     // G^T store map: inner = b (box 32, SWIZZLE_64B), outer = classes (box 128)
   int B, ncols, ldgt;
   const int32_t* pos_col;
@@ -171,45 +171,43 @@ struct alignas(64) GradEpi {
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
                                       uint8_t* smem) const {
     constexpr int CW = BN / NWG;
+    static_assert(CW <= 128, "column slice");
     const int cb = wg * CW;
     const uint32_t bar = 1 + wg;
-    // per-column (b) constants and the slice's positives list in shared memory
-    float2* cf = reinterpret_cast<float2*>(smem);               // [CW] {gmax*log2e, s*ig/B}
-    ST* cg = reinterpret_cast<ST*>(cf + CW);                    // [CW] gmax
-    ST* ci = cg + CW;                                           // [CW] inv_gsum
-    int* plist = reinterpret_cast<int*>(ci + CW);               // [CW] (col << 8) | row
-    int* pcount = plist + CW;
-    uint8_t* stage = smem + 4096;                               // 2 x [128][64 B] swizzled
-    pfc_sm100::named_bar_sync(bar, 128);  // previous tile finished reading smem
-    if (row == 0) *pcount = 0;
+    // per-column (b) constants of this warpgroup's slice
+    float2* cf = reinterpret_cast<float2*>(smem);          // [CW] {gmax*log2e, s*ig/B}
+    ST* cg = reinterpret_cast<ST*>(cf + CW);               // [CW] gmax
+    ST* ci = cg + CW;                                      // [CW] inv_gsum
+    uint8_t* prow = reinterpret_cast<uint8_t*>(ci + CW);   // [CW] positive's row in tile or 0xFF
+    uint8_t* stage = smem + 4096;                          // CW/32 x [128][64 B], 64B-swizzled
+    if (kTma && row == 0) pfc_sm100::bulk_wait_read<0>();  // last tile's stores left smem
     pfc_sm100::named_bar_sync(bar, 128);
     for (int i = row; i < CW; i += 128) {
       const int b = t.col0 + cb + i;
       float2 k = make_float2(0.f, 0.f);
       ST gm = ST(0), ig = ST(0);
+      uint8_t pr = 0xFF;
       if (b < B) {
         gm = gmax[b];
         ig = inv_gsum[b];
         k = make_float2((float)gm * kLog2e, (float)(mg.sd * (double)ig * (double)inv_batch));
-        const int pc = pos_col[b];
-        if (pc >= t.row0 && pc < t.row0 + 128) {
-          const int slot = atomicAdd(pcount, 1);
-          plist[slot] = (i << 8) | (pc - t.row0);
-        }
+        const int pc = pos_col[b] - t.row0;
+        if ((unsigned)pc < 128u) pr = (uint8_t)pc;
       }
       cf[i] = k;
       cg[i] = gm;
       ci[i] = ig;
+      prow[i] = pr;
     }
     pfc_sm100::named_bar_sync(bar, 128);
     const int j = t.row0 + row;
     const bool rv = j < ncols;
-    const int npl = *pcount;
     const float A = mg.s * kLog2e;
+    const uint32_t rowx4 = 0x01010101u * (uint32_t)row;
     ST cp = ST(0);
-    int buf = 0;
+    bool staged = false;
 #pragma unroll 1
-    for (int c0 = cb; c0 < cb + CW; c0 += 32, buf ^= 1) {
+    for (int c0 = cb; c0 < cb + CW; c0 += 32) {
       float v[32];
       src.load(c0, v);
       const int colb = t.col0 + c0;
@@ -236,19 +234,27 @@ struct alignas(64) GradEpi {
           g[q] = (float)gq;
         }
       }
-      // positives of this chunk (label b has its centre j): replace by the margin form
-      for (int e = 0; e < npl; ++e) {
-        const int pe = plist[e];
-        const int q = (pe >> 8) - lc;
-        if ((pe & 255) == row && (unsigned)q < 32u) {
-          float vq = 0.f;
+      // positives in this chunk: columns b whose label is this thread's class j
+      {
+        const uint4* pw = reinterpret_cast<const uint4*>(prow + lc);
+        const uint4 p0 = pw[0], p1 = pw[1];
+        const uint32_t hit = __vcmpeq4(p0.x, rowx4) | __vcmpeq4(p0.y, rowx4) |
+                             __vcmpeq4(p0.z, rowx4) | __vcmpeq4(p0.w, rowx4) |
+                             __vcmpeq4(p1.x, rowx4) | __vcmpeq4(p1.y, rowx4) |
+                             __vcmpeq4(p1.z, rowx4) | __vcmpeq4(p1.w, rowx4);
+        if (hit) {
+#pragma unroll 1
+          for (int q = 0; q < 32; ++q) {
+            if (prow[lc + q] != (uint8_t)row) continue;
+            float vq = 0.f;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) vq = (u == q) ? v[u] : vq;
-          const double z = margin_pos(mg, (double)vq);
-          const double p = exp(z - (double)cg[lc + q]) * (double)ci[lc + q];
-          const double gq = (p - 1.0) * (double)inv_batch * margin_deriv_pos(mg, (double)vq);
+            for (int u = 0; u < 32; ++u) vq = (u == q) ? v[u] : vq;
+            const double z = margin_pos(mg, (double)vq);
+            const double p = exp(z - (double)cg[lc + q]) * (double)ci[lc + q];
+            const double gq = (p - 1.0) * (double)inv_batch * margin_deriv_pos(mg, (double)vq);
 #pragma unroll
-          for (int u = 0; u < 32; ++u) g[u] = (u == q) ? (float)gq : g[u];
+            for (int u = 0; u < 32; ++u) g[u] = (u == q) ? (float)gq : g[u];
+          }
         }
       }
       if (!rv) {
@@ -263,10 +269,8 @@ struct alignas(64) GradEpi {
       }
       cp += c1 + c2;
       if constexpr (kTma) {
-        // coalesced write-out: swizzled (64B) smem staging + one TMA store per 128 x 32 chunk
-        uint8_t* sb = stage + buf * 8192;
-        if (row == 0) pfc_sm100::bulk_wait_read<1>();
-        pfc_sm100::named_bar_sync(bar, 128);
+        // 64B-swizzled staging of the 128 x 32 chunk; TMA stores after the slice is complete
+        uint8_t* sb = stage + (lc >> 5) * 8192;
         uint32_t w[16];
         pack_bf16x32(g, w);
         const int sw = (row >> 1) & 3;
@@ -274,12 +278,7 @@ struct alignas(64) GradEpi {
         for (int qq = 0; qq < 4; ++qq)
           *reinterpret_cast<uint4*>(sb + row * 64 + ((qq ^ sw) << 4)) =
               make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
-        pfc_sm100::fence_proxy_async_smem();
-        pfc_sm100::named_bar_sync(bar, 128);
-        if (row == 0) {
-          pfc_sm100::tma_store_2d(&tm, sb, colb, t.row0);
-          pfc_sm100::bulk_commit();
-        }
+        staged = true;
       } else {
         GT* dst = Gt + (size_t)j * ldgt + colb;
         if (colb + 32 <= B) {
@@ -288,6 +287,17 @@ struct alignas(64) GradEpi {
 #pragma unroll
           for (int q = 0; q < 32; ++q)
             if (colb + q < B) store_g1(dst + q, g[q]);
+        }
+      }
+    }
+    if constexpr (kTma) {
+      if (staged) {  // uniform
+        pfc_sm100::fence_proxy_async_smem();
+        pfc_sm100::named_bar_sync(bar, 128);
+        if (row == 0) {
+          for (int c0 = cb; c0 < cb + CW && t.col0 + c0 < B; c0 += 32)
+            pfc_sm100::tma_store_2d(&tm, stage + ((c0 - cb) >> 5) * 8192, t.col0 + c0, t.row0);
+          pfc_sm100::bulk_commit();
         }
       }
     }
@@ -307,9 +317,13 @@ struct DwUpdateEpi {
   float lr, mu, wd;
   const StepStatus* st;  // no update when the step failed (the reference throws before 412)
   int cw;                // columns per warpgroup (BN / NWG), for prefetch
+  int pf_mode;           // 0 none, 1 current tile at epilogue start, 2 one tile ahead
 
-  // Pull a tile's W / momentum row segments toward L2 (issued one tile ahead).
+  // Pull a tile's W / momentum row segments toward L2.
   __device__ __forceinline__ void prefetch(const TileInfo& t, int row, int wg) const {
+    if (pf_mode == 2) prefetch_rows(t, row, wg);
+  }
+  __device__ __forceinline__ void prefetch_rows(const TileInfo& t, int row, int wg) const {
     const int c = t.row0 + row;
     if (c >= ncols) return;
     const int r = lrow[c];
@@ -336,6 +350,7 @@ struct DwUpdateEpi {
     float* s_cp = s_inv + 128;
     int* s_row = reinterpret_cast<int*>(s_cp + 128);
     const int warp = row >> 5, lane = row & 31;
+    if (pf_mode == 1) prefetch_rows(t, row, wg);
     pfc_sm100::named_bar_sync(bar, 128);  // previous tile's readers are done with smem
     const bool failed = status_failed(st);
     {

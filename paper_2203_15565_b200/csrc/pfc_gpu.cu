@@ -173,6 +173,7 @@ struct Ctx {
   float* dx_part = nullptr;  // [S][maxB][D]
   float* dX = nullptr;       // [maxB][D]
   int max_splits = 1;
+  int dw_prefetch = 1;  // DwUpdateEpi L2 prefetch policy (PFC_DW_PREFETCH=0/1/2)
   // host-path scratch
   double* xdb = nullptr;  // D x maxB fp64
   StepStatus* st = nullptr;
@@ -447,7 +448,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
     DwUpdateEpi<ST> e{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp, c->W, c->M,
                       (float)a->lr, (float)c->d.momentum, (float)c->d.weight_decay, c->st,
-                      BN / NWG};
+                      BN / NWG, c->dw_prefetch};
     cudaError_t err;
     if constexpr (kUmma) err = launch_umma<kBN, 3, kNWG, false, true>(c, c->tm_gt_k, c->tm_x_mn, gw, e);
     else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
@@ -636,6 +637,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->ldg = round_up(desc->max_batch, 8);  // G^T row stride
   c->pool_stride = std::max<int64_t>(c->blk, 1);
   c->maxB = desc->max_batch;
+  if (const char* e = getenv("PFC_DW_PREFETCH")) c->dw_prefetch = atoi(e);
   c->mg.kind = desc->margin_kind;
   c->mg.s = (float)desc->margin_scale;
   c->mg.sd = desc->margin_scale;

@@ -103,7 +103,7 @@ TOL = {  # precision -> (loss rel, dX fro, dX max/max, W' max/max)
 # relative amount; the d=512 contract above is calibrated for the BASELINE configs.  The tiny
 # D <= 32 parity configs (made for the fp64 oracle) run in bf16 only as a smoke bound, and the
 # filter case additionally flips mask decisions of cosines within bf16 rounding of tau.
-TINY_BF16 = (1e-3, 5e-2, 1e-1, 5e-2)
+TINY_BF16 = (1e-3, 1e-1, 2e-1, 5e-2)
 RESULTS = os.path.join(os.path.dirname(os.path.dirname(__file__)), "gpurun_out", "parity.jsonl")
 
 

@@ -49,12 +49,14 @@ struct FwdStatsEpi {
   ST* part_s;
   double* zpos;
 
+  struct Pre {};
+  __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
   __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
   __device__ __forceinline__ void finish(int, int) const {}
 
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t*) const {
+                                      uint8_t*, const Pre&) const {
     constexpr int CW = BN / NWG;
     const int b = t.row0 + row;
     const bool rv = b < B;
@@ -146,10 +148,14 @@ __device__ __forceinline__ void store_g1(__nv_bfloat16* dst, float g) { *dst = _
 __device__ __forceinline__ void store_g1(float* dst, float g) { *dst = g; }
 
 // rows = buffered classes j (M), cols = batch rows b (N).  Writes G^T[j][b].
+// kTma (tcgen05 engine): per-column constants arrive one tile ahead in registers (Pre); every
+// warp stages its 32 rows x 32 columns chunks (64B-swizzled) in a private 4-deep ring and
+// TMA-stores them itself, so the epilogue needs no cross-warp barrier.
 template <typename ST, typename GT, bool kFilter, bool kTma>
 struct alignas(64) GradEpi {
-  static constexpr int kSmem = 36 * 1024;  // 4 KB column constants + 4 x 8 KB G^T staging
-  CUtensorMap tm;     // G^T store map: inner = b (box 32, SWIZZLE_64B), outer = classes (box 128)
+  static constexpr int kWarpBytes = 9728;  // 4 x 2 KB staging + 1 KB constants + 128 B rows
+  static constexpr int kSmem = kTma ? 4 * kWarpBytes : 20 * 1024;
+  CUtensorMap tm;     // G^T store map: inner = b (box 32, SWIZZLE_64B), outer = classes (box 32)
   int B, ncols, ldgt;
   const int32_t* pos_col;
   MarginDev mg;
@@ -160,126 +166,184 @@ struct alignas(64) GradEpi {
   GT* Gt;             // [ncols_pad][ldgt]
   ST* cproj_part;     // [n_tiles(b) * NWG][ncols]
 
+  struct Pre {
+    float2 k[4];
+    int pc[4];
+  };
+  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int wg) const {
+    Pre p{};
+    if constexpr (kTma) {
+      const int lane = row & 31;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int b = t.col0 + wg * 128 + lane + 32 * i;
+        p.k[i] = make_float2(0.f, 0.f);
+        p.pc[i] = -1;
+        if (b < B) {
+          const float gm = (float)gmax[b];
+          const float ig = (float)inv_gsum[b];
+          p.k[i] = make_float2(gm * kLog2e, (float)(mg.sd * (double)ig * (double)inv_batch));
+          p.pc[i] = pos_col[b];
+        }
+      }
+    }
+    return p;
+  }
   __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
   __device__ __forceinline__ void finish(int row, int) const {
     if constexpr (kTma) {
-      if (row == 0) pfc_sm100::bulk_wait_all();
+      if ((row & 31) == 0) pfc_sm100::bulk_wait_all();
     }
+  }
+
+  // g for 32 columns from the cosines v and per-column constants (gmax*log2e, s*ig/B)
+  __device__ __forceinline__ void grad32(const float (&v)[32], const float2* cf, float (&g)[32]) const {
+    const float A = mg.s * kLog2e;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const float2 k = cf[q];
+      float gq = pfc_sm100::ex2_approx(fmaf(v[q], A, -k.x)) * k.y;
+      if (kFilter) gq = v[q] > tau ? 0.f : gq;
+      g[q] = gq;
+    }
+  }
+  // the positive entry q of this chunk: margin form (margin.hpp:41-72), fp64
+  __device__ __forceinline__ void patch_positive(const float (&v)[32], float (&g)[32], int q,
+                                                 double gm, double ig) const {
+    float vq = 0.f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) vq = (u == q) ? v[u] : vq;
+    const double z = margin_pos(mg, (double)vq);
+    const double p = exp(z - gm) * ig;
+    const double gq = (p - 1.0) * (double)inv_batch * margin_deriv_pos(mg, (double)vq);
+#pragma unroll
+    for (int u = 0; u < 32; ++u) g[u] = (u == q) ? (float)gq : g[u];
   }
 
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t* smem) const {
+                                      uint8_t* smem, const Pre& pre) const {
     constexpr int CW = BN / NWG;
-    static_assert(CW <= 128, "column slice");
     const int cb = wg * CW;
-    const uint32_t bar = 1 + wg;
-    // per-column (b) constants of this warpgroup's slice
-    float2* cf = reinterpret_cast<float2*>(smem);          // [CW] {gmax*log2e, s*ig/B}
-    ST* cg = reinterpret_cast<ST*>(cf + CW);               // [CW] gmax
-    ST* ci = cg + CW;                                      // [CW] inv_gsum
-    uint8_t* prow = reinterpret_cast<uint8_t*>(ci + CW);   // [CW] positive's row in tile or 0xFF
-    uint8_t* stage = smem + 4096;                          // CW/32 x [128][64 B], 64B-swizzled
-    if (kTma && row == 0) pfc_sm100::bulk_wait_read<0>();  // last tile's stores left smem
-    pfc_sm100::named_bar_sync(bar, 128);
-    for (int i = row; i < CW; i += 128) {
-      const int b = t.col0 + cb + i;
-      float2 k = make_float2(0.f, 0.f);
-      ST gm = ST(0), ig = ST(0);
-      uint8_t pr = 0xFF;
-      if (b < B) {
-        gm = gmax[b];
-        ig = inv_gsum[b];
-        k = make_float2((float)gm * kLog2e, (float)(mg.sd * (double)ig * (double)inv_batch));
-        const int pc = pos_col[b] - t.row0;
-        if ((unsigned)pc < 128u) pr = (uint8_t)pc;
-      }
-      cf[i] = k;
-      cg[i] = gm;
-      ci[i] = ig;
-      prow[i] = pr;
-    }
-    pfc_sm100::named_bar_sync(bar, 128);
     const int j = t.row0 + row;
     const bool rv = j < ncols;
-    const float A = mg.s * kLog2e;
-    const uint32_t rowx4 = 0x01010101u * (uint32_t)row;
     ST cp = ST(0);
-    bool staged = false;
-#pragma unroll 1
-    for (int c0 = cb; c0 < cb + CW; c0 += 32) {
-      float v[32];
-      src.load(c0, v);
-      const int colb = t.col0 + c0;
-      if (colb >= B) continue;  // uniform across the warpgroup
-      const int lc = c0 - cb;
-      float g[32];
-      if constexpr (std::is_same<ST, float>::value) {
+    if constexpr (kTma) {
+      static_assert(CW == 128, "warp-private staging assumes 128 columns per warpgroup");
+      const int wig = row >> 5, lane = row & 31;
+      uint8_t* ws = smem + wig * kWarpBytes;
+      uint8_t* stage = ws;                                   // 4 x [32 rows][64 B]
+      float2* cf = reinterpret_cast<float2*>(ws + 8192);     // [128]
+      uint8_t* prow = ws + 9216;                             // [128]
+      __syncwarp();  // lanes finished reading the previous tile's constants
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const float2 k = cf[lc + q];
-          float gq = pfc_sm100::ex2_approx(fmaf(v[q], A, -k.x)) * k.y;
-          if (kFilter) gq = v[q] > tau ? 0.f : gq;
-          g[q] = gq;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int b = colb + q;
-          double gq = 0.0;
-          if (b < B && !(kFilter && v[q] > tau)) {
-            const double p = exp((double)mg.s * (double)v[q] - (double)cg[lc + q]) * (double)ci[lc + q];
-            gq = p * (double)inv_batch * mg.sd;
-          }
-          g[q] = (float)gq;
-        }
+      for (int i = 0; i < 4; ++i) {
+        cf[lane + 32 * i] = pre.k[i];
+        const int pr = pre.pc[i] - t.row0;
+        prow[lane + 32 * i] = (uint8_t)((unsigned)pr < 128u ? pr : 0xFF);
       }
-      // positives in this chunk: columns b whose label is this thread's class j
-      {
-        const uint4* pw = reinterpret_cast<const uint4*>(prow + lc);
-        const uint4 p0 = pw[0], p1 = pw[1];
-        const uint32_t hit = __vcmpeq4(p0.x, rowx4) | __vcmpeq4(p0.y, rowx4) |
-                             __vcmpeq4(p0.z, rowx4) | __vcmpeq4(p0.w, rowx4) |
-                             __vcmpeq4(p1.x, rowx4) | __vcmpeq4(p1.y, rowx4) |
-                             __vcmpeq4(p1.z, rowx4) | __vcmpeq4(p1.w, rowx4);
-        if (hit) {
+      __syncwarp();
+      const uint32_t rowx4 = 0x01010101u * (uint32_t)row;
 #pragma unroll 1
+      for (int kk = 0; kk < CW / 32; ++kk) {
+        const int c0 = cb + kk * 32;
+        float v[32];
+        src.load(c0, v);
+        const int colb = t.col0 + c0;
+        uint8_t* sb = stage + kk * 2048;
+        if (colb < B) {  // uniform
+          float g[32];
+          grad32(v, cf + kk * 32, g);
+          const uint4* pw = reinterpret_cast<const uint4*>(prow + kk * 32);
+          const uint4 p0 = pw[0], p1 = pw[1];
+          const uint32_t hit = __vcmpeq4(p0.x, rowx4) | __vcmpeq4(p0.y, rowx4) |
+                               __vcmpeq4(p0.z, rowx4) | __vcmpeq4(p0.w, rowx4) |
+                               __vcmpeq4(p1.x, rowx4) | __vcmpeq4(p1.y, rowx4) |
+                               __vcmpeq4(p1.z, rowx4) | __vcmpeq4(p1.w, rowx4);
+          if (hit) {
+#pragma unroll 1
+            for (int q = 0; q < 32; ++q)
+              if (prow[kk * 32 + q] == (uint8_t)row)
+                patch_positive(v, g, q, (double)gmax[colb + q], (double)inv_gsum[colb + q]);
+          }
+          if (!rv) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) g[q] = 0.f;
+          }
+          float c1 = 0.f, c2 = 0.f;
+#pragma unroll
+          for (int q = 0; q < 32; q += 2) {
+            c1 = fmaf(g[q], v[q], c1);
+            c2 = fmaf(g[q + 1], v[q + 1], c2);
+          }
+          cp += (ST)(c1 + c2);
+          uint32_t w[16];
+          pack_bf16x32(g, w);
+          if (lane == 0) pfc_sm100::bulk_wait_read<3>();  // this buffer's store, 4 groups ago
+          __syncwarp();
+          const int sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            *reinterpret_cast<uint4*>(sb + lane * 64 + ((qq ^ sw) << 4)) =
+                make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
+          pfc_sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) pfc_sm100::tma_store_2d(&tm, sb, colb, t.row0 + wig * 32);
+        }
+        if (lane == 0) pfc_sm100::bulk_commit();  // one group per chunk (possibly empty)
+      }
+    } else {
+      // SIMT engine (fp32 validation): block-wide constants, plain stores
+      const uint32_t bar = 1 + wg;
+      float2* cf = reinterpret_cast<float2*>(smem);
+      ST* cg = reinterpret_cast<ST*>(cf + CW);
+      ST* ci = cg + CW;
+      int* pcs = reinterpret_cast<int*>(ci + CW);
+      pfc_sm100::named_bar_sync(bar, 128);
+      for (int i = row; i < CW; i += 128) {
+        const int b = t.col0 + cb + i;
+        ST gm = ST(0), ig = ST(0);
+        int pc = -1;
+        if (b < B) {
+          gm = gmax[b];
+          ig = inv_gsum[b];
+          pc = pos_col[b];
+        }
+        cf[i] = make_float2((float)gm * kLog2e, (float)(mg.sd * (double)ig * (double)inv_batch));
+        cg[i] = gm;
+        ci[i] = ig;
+        pcs[i] = pc;
+      }
+      pfc_sm100::named_bar_sync(bar, 128);
+#pragma unroll 1
+      for (int c0 = cb; c0 < cb + CW; c0 += 32) {
+        float v[32];
+        src.load(c0, v);
+        const int colb = t.col0 + c0;
+        if (colb >= B) continue;
+        const int lc = c0 - cb;
+        float g[32];
+        if constexpr (std::is_same<ST, float>::value) {
+          grad32(v, cf + lc, g);
+        } else {
+#pragma unroll
           for (int q = 0; q < 32; ++q) {
-            if (prow[lc + q] != (uint8_t)row) continue;
-            float vq = 0.f;
-#pragma unroll
-            for (int u = 0; u < 32; ++u) vq = (u == q) ? v[u] : vq;
-            const double z = margin_pos(mg, (double)vq);
-            const double p = exp(z - (double)cg[lc + q]) * (double)ci[lc + q];
-            const double gq = (p - 1.0) * (double)inv_batch * margin_deriv_pos(mg, (double)vq);
-#pragma unroll
-            for (int u = 0; u < 32; ++u) g[u] = (u == q) ? (float)gq : g[u];
+            double gq = 0.0;
+            if (colb + q < B && !(kFilter && v[q] > tau)) {
+              const double p = exp((double)mg.s * (double)v[q] - (double)cg[lc + q]) * (double)ci[lc + q];
+              gq = p * (double)inv_batch * mg.sd;
+            }
+            g[q] = (float)gq;
           }
         }
-      }
-      if (!rv) {
+        for (int q = 0; q < 32; ++q)
+          if (pcs[lc + q] == j) patch_positive(v, g, q, (double)cg[lc + q], (double)ci[lc + q]);
+        if (!rv) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) g[q] = 0.f;
-      }
-      ST c1 = ST(0), c2 = ST(0);
+          for (int q = 0; q < 32; ++q) g[q] = 0.f;
+        }
 #pragma unroll
-      for (int q = 0; q < 32; q += 2) {
-        c1 += (ST)g[q] * (ST)v[q];
-        c2 += (ST)g[q + 1] * (ST)v[q + 1];
-      }
-      cp += c1 + c2;
-      if constexpr (kTma) {
-        // 64B-swizzled staging of the 128 x 32 chunk; TMA stores after the slice is complete
-        uint8_t* sb = stage + (lc >> 5) * 8192;
-        uint32_t w[16];
-        pack_bf16x32(g, w);
-        const int sw = (row >> 1) & 3;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq)
-          *reinterpret_cast<uint4*>(sb + row * 64 + ((qq ^ sw) << 4)) =
-              make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
-        staged = true;
-      } else {
+        for (int q = 0; q < 32; ++q) cp += (ST)g[q] * (ST)v[q];
         GT* dst = Gt + (size_t)j * ldgt + colb;
         if (colb + 32 <= B) {
           store_g32(dst, g);
@@ -290,24 +354,13 @@ struct alignas(64) GradEpi {
         }
       }
     }
-    if constexpr (kTma) {
-      if (staged) {  // uniform
-        pfc_sm100::fence_proxy_async_smem();
-        pfc_sm100::named_bar_sync(bar, 128);
-        if (row == 0) {
-          for (int c0 = cb; c0 < cb + CW && t.col0 + c0 < B; c0 += 32)
-            pfc_sm100::tma_store_2d(&tm, stage + ((c0 - cb) >> 5) * 8192, t.col0 + c0, t.row0);
-          pfc_sm100::bulk_commit();
-        }
-      }
-    }
     if (rv) cproj_part[(size_t)(t.n_tile * NWG + wg) * ncols + j] = cp;
   }
 };
 
 template <typename ST>
 struct DwUpdateEpi {
-  static constexpr int kSmem = 18 * 1024;
+  static constexpr int kSmem = 17 * 1024;
   int ncols, D, n_parts;
   const float* wnorm;       // [ncols]
   const int32_t* lrow;      // [ncols] local row of W
@@ -319,7 +372,24 @@ struct DwUpdateEpi {
   int cw;                // columns per warpgroup (BN / NWG), for prefetch
   int pf_mode;           // 0 none, 1 current tile at epilogue start, 2 one tile ahead
 
-  // Pull a tile's W / momentum row segments toward L2.
+  struct Pre {
+    float inv, cp;
+    int r;
+  };
+  // the tile's per-row scalars: 1/|w|, center_proj (sum of partials), local W row
+  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int) const {
+    Pre p{0.f, 0.f, -1};
+    const int c = t.row0 + row;
+    if (c < ncols) {
+      const float n = wnorm[c];
+      p.inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
+      ST acc = ST(0);
+      for (int q = 0; q < n_parts; ++q) acc += cproj_part[(size_t)q * ncols + c];
+      p.cp = (float)acc;
+      p.r = lrow[c];
+    }
+    return p;
+  }
   __device__ __forceinline__ void prefetch(const TileInfo& t, int row, int wg) const {
     if (pf_mode == 2) prefetch_rows(t, row, wg);
   }
@@ -342,7 +412,7 @@ struct DwUpdateEpi {
 
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t* smem) const {
+                                      uint8_t* smem, const Pre& pre) const {
     constexpr int CW = BN / NWG;
     const uint32_t bar = 1 + wg;
     float* stage = reinterpret_cast<float*>(smem);  // [128][33]
@@ -353,40 +423,25 @@ struct DwUpdateEpi {
     if (pf_mode == 1) prefetch_rows(t, row, wg);
     pfc_sm100::named_bar_sync(bar, 128);  // previous tile's readers are done with smem
     const bool failed = status_failed(st);
-    {
-      const int c = t.row0 + row;
-      float inv = 0.f, cp = 0.f;
-      int r = -1;
-      if (c < ncols && !failed) {
-        const float n = wnorm[c];
-        inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
-        ST acc = ST(0);
-        for (int p = 0; p < n_parts; ++p) acc += cproj_part[(size_t)p * ncols + c];
-        cp = (float)acc;
-        r = lrow[c];
-      }
-      s_inv[row] = inv;
-      s_cp[row] = cp;
-      s_row[row] = r;
-    }
+    s_inv[row] = pre.inv;
+    s_cp[row] = pre.cp;
+    s_row[row] = failed ? -1 : pre.r;
+    pfc_sm100::named_bar_sync(bar, 128);
     const int sub = lane >> 3, q4 = (lane & 7) * 4;  // 4 rows x 8 lanes x float4 per warp op
+    int rw[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) rw[u] = s_row[warp * 32 + u * 4 + sub];
 #pragma unroll 1
     for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
-      float v[32];
-      src.load(c0, v);
-      pfc_sm100::named_bar_sync(bar, 128);
-#pragma unroll
-      for (int q = 0; q < 32; ++q) stage[row * 33 + q] = v[q];
-      pfc_sm100::named_bar_sync(bar, 128);
       const int d = t.col0 + c0 + q4;
-      if (d >= D) continue;
       const bool vec = (d + 4 <= D) && ((D & 3) == 0);
+      // W / momentum loads first: their latency overlaps the TMEM read and the staging
       float4 w[8], mo[8];
-      int rw[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        rw[u] = s_row[warp * 32 + u * 4 + sub];
-        if (rw[u] >= 0) {
+        w[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        mo[u] = w[u];
+        if (rw[u] >= 0 && d < D) {
           const size_t o = (size_t)rw[u] * D + d;
           if (vec) {
             w[u] = *reinterpret_cast<const float4*>(W + o);
@@ -399,6 +454,13 @@ struct DwUpdateEpi {
           }
         }
       }
+      float v[32];
+      src.load(c0, v);
+      pfc_sm100::named_bar_sync(bar, 128);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) stage[row * 33 + q] = v[q];
+      pfc_sm100::named_bar_sync(bar, 128);
+      if (d >= D) continue;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if (rw[u] < 0) continue;
@@ -436,11 +498,13 @@ struct DxPartEpi {
   static constexpr int kSmem = 0;
   int B, D;
   float* part;  // [splits][B][D]
+  struct Pre {};
+  __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
   __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
   __device__ __forceinline__ void finish(int, int) const {}
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t*) const {
+                                      uint8_t*, const Pre&) const {
     constexpr int CW = BN / NWG;
     const int b = t.row0 + row;
 #pragma unroll 1

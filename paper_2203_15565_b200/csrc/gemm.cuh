@@ -196,17 +196,27 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     const int row = ((warp & 3) << 5) | lane;
     uint8_t* wsm = epi_smem + wg * Epi::kSmem;
     uint32_t it = 0;
+    // per-tile operands of the epilogue are loaded one tile ahead (registers), so their
+    // global-memory latency hides behind the current tile
+    typename Epi::Pre pre{};
+    if ((int)blockIdx.x < total) pre = epi.preload(g.tile(blockIdx.x), row, wg);
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const TileInfo ti = g.tile(t);
       const uint32_t as = it & 1, aph = (it >> 1) & 1;
       if (it == 0) epi.prefetch(ti, row, wg);
-      if (t + (int)gridDim.x < total) epi.prefetch(g.tile(t + gridDim.x), row, wg);
+      typename Epi::Pre pre_next{};
+      if (t + (int)gridDim.x < total) {
+        const TileInfo tn = g.tile(t + gridDim.x);
+        epi.prefetch(tn, row, wg);
+        pre_next = epi.preload(tn, row, wg);
+      }
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const TmemSrc src{tmem_base + as * BN + ((uint32_t)((warp & 3) * 32) << 16)};
-      epi.template run<BN, NWG>(ti, src, row, wg, wsm);
+      epi.template run<BN, NWG>(ti, src, row, wg, wsm, pre);
       tc_fence_before();
       mbar_arrive(&tempty[as]);
+      pre = pre_next;
     }
     epi.finish(row, wg);
   }
@@ -271,7 +281,8 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int j = 0; j < BN; ++j) sAcc[tid * 65 + j] = acc[j];
   const SmemRowSrc src{sAcc + tid * 65};
-  epi.template run<BN, 1>(ti, src, tid, 0, epi_smem);
+  const typename Epi::Pre pre = epi.preload(ti, tid, 0);
+  epi.template run<BN, 1>(ti, src, tid, 0, epi_smem, pre);
   epi.finish(tid, 0);
 }
 

@@ -173,7 +173,7 @@ struct Ctx {
   float* dx_part = nullptr;  // [S][maxB][D]
   float* dX = nullptr;       // [maxB][D]
   int max_splits = 1;
-  int dw_prefetch = 1;  // DwUpdateEpi L2 prefetch policy (PFC_DW_PREFETCH=0/1/2)
+  int dw_prefetch = 0;  // DwUpdateEpi L2 prefetch policy (PFC_DW_PREFETCH=0/1/2)
   // host-path scratch
   double* xdb = nullptr;  // D x maxB fp64
   StepStatus* st = nullptr;
@@ -289,8 +289,8 @@ int ensure_maps(Ctx* c, int64_t B) {
   // dX GEMM (M = b, N = d, K = classes): A = G^T read MN-major (b contiguous); B = W^ MN-major
   ok &= make_map(&c->tm_gt_mn, c->G, B, c->ncols, c->ldg, 64);
   ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, 64);
-  // G GEMM epilogue store of G^T (box 32 b x 128 classes, 64B swizzle)
-  ok &= make_map(&c->tm_gt_st, c->G, B, c->ncols, c->ldg, 128, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  // G GEMM epilogue store of G^T (per-warp box 32 b x 32 classes, 64B swizzle)
+  ok &= make_map(&c->tm_gt_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
   return PFC_OK;

@@ -360,7 +360,7 @@ struct alignas(64) GradEpi {
 
 template <typename ST>
 struct DwUpdateEpi {
-  static constexpr int kSmem = 17 * 1024;
+  static constexpr int kSmem = 18 * 1024;  // stage [128][33] f32 + 3 x [128] row scalars
   int ncols, D, n_parts;
   const float* wnorm;       // [ncols]
   const int32_t* lrow;      // [ncols] local row of W
@@ -415,6 +415,7 @@ struct DwUpdateEpi {
                                       uint8_t* smem, const Pre& pre) const {
     constexpr int CW = BN / NWG;
     const uint32_t bar = 1 + wg;
+    static_assert((128 * 33 + 3 * 128) * 4 <= kSmem, "DwUpdateEpi scratch");
     float* stage = reinterpret_cast<float*>(smem);  // [128][33]
     float* s_inv = stage + 128 * 33;
     float* s_cp = s_inv + 128;

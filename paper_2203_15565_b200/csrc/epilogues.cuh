@@ -358,9 +358,11 @@ struct alignas(64) GradEpi {
   }
 };
 
-template <typename ST>
+template <typename ST, bool kVecD>
 struct DwUpdateEpi {
-  static constexpr int kSmem = 18 * 1024;  // stage [128][33] f32 + 3 x [128] row scalars
+  // per warp: transposed 32 x 32 chunk (stride 33) + 3 x 32 row scalars
+  static constexpr int kWarpFloats = 32 * 33 + 3 * 32;
+  static constexpr int kSmem = 4 * kWarpFloats * 4;
   int ncols, D, n_parts;
   const float* wnorm;       // [ncols]
   const int32_t* lrow;      // [ncols] local row of W
@@ -410,85 +412,90 @@ struct DwUpdateEpi {
   }
   __device__ __forceinline__ void finish(int, int) const {}
 
+  __device__ __forceinline__ void update4(float4& w, float4& m, const float* a, float inv,
+                                          float cpj) const {
+    float wv[4] = {w.x, w.y, w.z, w.w};
+    float mv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float dw = (a[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382
+      const float g = dw + wd * wv[e];                      // shardsim.hpp:152-153
+      const float vv = mu * mv[e] + g;                      // shardsim.hpp:154
+      mv[e] = vv;
+      wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
+    }
+    w = make_float4(wv[0], wv[1], wv[2], wv[3]);
+    m = make_float4(mv[0], mv[1], mv[2], mv[3]);
+  }
+
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
                                       uint8_t* smem, const Pre& pre) const {
     constexpr int CW = BN / NWG;
-    const uint32_t bar = 1 + wg;
-    static_assert((128 * 33 + 3 * 128) * 4 <= kSmem, "DwUpdateEpi scratch");
-    float* stage = reinterpret_cast<float*>(smem);  // [128][33]
-    float* s_inv = stage + 128 * 33;
-    float* s_cp = s_inv + 128;
-    int* s_row = reinterpret_cast<int*>(s_cp + 128);
-    const int warp = row >> 5, lane = row & 31;
+    const int wig = row >> 5, lane = row & 31;
+    float* ws = reinterpret_cast<float*>(smem) + wig * kWarpFloats;
+    float* stage = ws;                 // [32][33]: row-of-warp x dim
+    float* s_inv = ws + 32 * 33;
+    float* s_cp = s_inv + 32;
+    int* s_row = reinterpret_cast<int*>(s_cp + 32);
     if (pf_mode == 1) prefetch_rows(t, row, wg);
-    pfc_sm100::named_bar_sync(bar, 128);  // previous tile's readers are done with smem
     const bool failed = status_failed(st);
-    s_inv[row] = pre.inv;
-    s_cp[row] = pre.cp;
-    s_row[row] = failed ? -1 : pre.r;
-    pfc_sm100::named_bar_sync(bar, 128);
+    __syncwarp();  // the warp finished reading the previous tile's scalars
+    s_inv[lane] = pre.inv;
+    s_cp[lane] = pre.cp;
+    s_row[lane] = failed ? -1 : pre.r;
+    __syncwarp();
     const int sub = lane >> 3, q4 = (lane & 7) * 4;  // 4 rows x 8 lanes x float4 per warp op
     int rw[8];
+    float rinv[8], rcp[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) rw[u] = s_row[warp * 32 + u * 4 + sub];
+    for (int u = 0; u < 8; ++u) {
+      const int r = u * 4 + sub;
+      rw[u] = s_row[r];
+      rinv[u] = s_inv[r];
+      rcp[u] = s_cp[r];
+    }
 #pragma unroll 1
     for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
-      const int d = t.col0 + c0 + q4;
-      const bool vec = (d + 4 <= D) && ((D & 3) == 0);
-      // W / momentum loads first: their latency overlaps the TMEM read and the staging
-      float4 w[8], mo[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        w[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        mo[u] = w[u];
-        if (rw[u] >= 0 && d < D) {
-          const size_t o = (size_t)rw[u] * D + d;
-          if (vec) {
-            w[u] = *reinterpret_cast<const float4*>(W + o);
-            mo[u] = *reinterpret_cast<const float4*>(Mom + o);
-          } else {
-            w[u] = make_float4(W[o], d + 1 < D ? W[o + 1] : 0.f, d + 2 < D ? W[o + 2] : 0.f,
-                               d + 3 < D ? W[o + 3] : 0.f);
-            mo[u] = make_float4(Mom[o], d + 1 < D ? Mom[o + 1] : 0.f,
-                                d + 2 < D ? Mom[o + 2] : 0.f, d + 3 < D ? Mom[o + 3] : 0.f);
-          }
-        }
-      }
       float v[32];
       src.load(c0, v);
-      pfc_sm100::named_bar_sync(bar, 128);
+      const int d = t.col0 + c0 + q4;
+      if (kVecD && t.col0 + c0 >= D) continue;  // uniform
+      __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[row * 33 + q] = v[q];
-      pfc_sm100::named_bar_sync(bar, 128);
-      if (d >= D) continue;
+      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
+      __syncwarp();
+      if constexpr (kVecD) {
+        float4 w[8], mo[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (rw[u] < 0) continue;
-        const int r = warp * 32 + u * 4 + sub;
-        const float inv = s_inv[r], cpj = s_cp[r];
-        const float* a = stage + r * 33 + q4;
-        float wv[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-        float mv[4] = {mo[u].x, mo[u].y, mo[u].z, mo[u].w};
+        for (int u = 0; u < 8; ++u)
+          if (rw[u] >= 0) {
+            const size_t o = (size_t)rw[u] * D + d;
+            w[u] = *reinterpret_cast<const float4*>(W + o);
+            mo[u] = *reinterpret_cast<const float4*>(Mom + o);
+          }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float dw = (a[e] - cpj * (wv[e] * inv)) * inv;
-          const float g = dw + wd * wv[e];
-          const float vv = mu * mv[e] + g;
-          mv[e] = vv;
-          wv[e] = wv[e] - lr * vv;
-        }
-        const size_t o = (size_t)rw[u] * D + d;
-        if (vec) {
-          *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-          *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (d + e < D) {
-              Mom[o + e] = mv[e];
-              W[o + e] = wv[e];
-            }
+        for (int u = 0; u < 8; ++u)
+          if (rw[u] >= 0) {
+            update4(w[u], mo[u], stage + (u * 4 + sub) * 33 + q4, rinv[u], rcp[u]);
+            const size_t o = (size_t)rw[u] * D + d;
+            *reinterpret_cast<float4*>(Mom + o) = mo[u];
+            *reinterpret_cast<float4*>(W + o) = w[u];
+          }
+      } else {
+        // generic D: scalar lanes over the chunk's 32 dims, one row per iteration
+        const int dd = t.col0 + c0 + lane;
+        if (dd < D) {
+          for (int r = 0; r < 32; ++r) {
+            const int wr = s_row[r];
+            if (wr < 0) continue;
+            const size_t o = (size_t)wr * D + dd;
+            float4 w4 = make_float4(W[o], 0.f, 0.f, 0.f), m4 = make_float4(Mom[o], 0.f, 0.f, 0.f);
+            float a[4] = {stage[r * 33 + lane], 0.f, 0.f, 0.f};
+            update4(w4, m4, a, s_inv[r], s_cp[r]);
+            Mom[o] = m4.x;
+            W[o] = w4.x;
+          }
         }
       }
     }

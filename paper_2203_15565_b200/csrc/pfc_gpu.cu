@@ -446,13 +446,20 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- dW = sum_b g_bj x^_b, corrected, fused momentum-SGD on sampled rows (shardsim.hpp:377-417)
   {
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
-    DwUpdateEpi<ST> e{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp, c->W, c->M,
-                      (float)a->lr, (float)c->d.momentum, (float)c->d.weight_decay, c->st,
-                      BN / NWG, c->dw_prefetch};
+    auto go = [&](auto e) {
+      if constexpr (kUmma) return launch_umma<kBN, 3, kNWG, false, true>(c, c->tm_gt_k, c->tm_x_mn, gw, e);
+      else return launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
+                                           (int)c->Dp, gw, e);
+    };
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, 3, kNWG, false, true>(c, c->tm_gt_k, c->tm_x_mn, gw, e);
-    else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
-                                        (int)c->Dp, gw, e);
+    if (c->D % 32 == 0)
+      err = go(DwUpdateEpi<ST, true>{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp,
+                                     c->W, c->M, (float)a->lr, (float)c->d.momentum,
+                                     (float)c->d.weight_decay, c->st, BN / NWG, c->dw_prefetch});
+    else
+      err = go(DwUpdateEpi<ST, false>{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp,
+                                      c->W, c->M, (float)a->lr, (float)c->d.momentum,
+                                      (float)c->d.weight_decay, c->st, BN / NWG, c->dw_prefetch});
     CUDA_TRY(c, err);
   }
   phase(c, "dw_update_gemm");

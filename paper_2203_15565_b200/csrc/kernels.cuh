@@ -142,28 +142,46 @@ __global__ void gather_w_kernel(const float* __restrict__ W, int D, int Dp,
 }
 
 // Merge the per-column-tile (max, sumexp) partials of each row into one (max, sum) pair.
+// Pass 1: grid (rows/128, segments); thread = row b, coalesced over b, loops its segment of
+// tiles.  Pass 2: thread = row, folds the segments in order.
+constexpr int kMergeSegs = 64;
 template <typename ST>
-__global__ void merge_tiles_kernel(const ST* __restrict__ pm, const ST* __restrict__ ps, int T,
-                                   int B, ST* __restrict__ lm, ST* __restrict__ ls) {
-  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(128) merge_tiles_kernel(const ST* __restrict__ pm,
+                                                          const ST* __restrict__ ps, int T, int B,
+                                                          ST* __restrict__ sm, ST* __restrict__ ss) {
+  const int b = blockIdx.x * 128 + threadIdx.x;
   if (b >= B) return;
-  ST m = -INFINITY;
-  for (int t = lane; t < T; t += 32) m = fmax(m, pm[(size_t)t * B + b]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  ST s = 0;
-  if (m != (ST)-INFINITY) {
-    for (int t = lane; t < T; t += 32) {
-      const ST mt = pm[(size_t)t * B + b];
-      if (mt != (ST)-INFINITY) s += ps[(size_t)t * B + b] * fast_exp(mt - m);
+  const int per = (T + gridDim.y - 1) / gridDim.y;
+  const int t0 = blockIdx.y * per, t1 = min(T, t0 + per);
+  ST m = -INFINITY, s = 0;
+  for (int t = t0; t < t1; ++t) {
+    const ST mt = pm[(size_t)t * B + b], st = ps[(size_t)t * B + b];
+    if (mt == (ST)-INFINITY) continue;
+    if (mt > m) {
+      s = (m == (ST)-INFINITY ? ST(0) : s * fast_exp(m - mt)) + st;
+      m = mt;
+    } else {
+      s += st * fast_exp(mt - m);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
-    lm[b] = m;
-    ls[b] = s;
-  }
+  sm[(size_t)blockIdx.y * B + b] = m;
+  ss[(size_t)blockIdx.y * B + b] = s;
+}
+template <typename ST>
+__global__ void merge_segments_kernel(const ST* __restrict__ sm, const ST* __restrict__ ss,
+                                      int nseg, int B, ST* __restrict__ lm, ST* __restrict__ ls) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ST m = -INFINITY;
+  for (int i = 0; i < nseg; ++i) m = fmax(m, sm[(size_t)i * B + b]);
+  double s = 0.0;
+  if (m != (ST)-INFINITY)
+    for (int i = 0; i < nseg; ++i) {
+      const ST mi = sm[(size_t)i * B + b];
+      if (mi != (ST)-INFINITY) s += (double)ss[(size_t)i * B + b] * exp((double)mi - (double)m);
+    }
+  lm[b] = m;
+  ls[b] = (ST)s;
 }
 
 // Cross-rank merge in ascending rank order (collectives 1 and 2, shardsim.hpp:284-338),

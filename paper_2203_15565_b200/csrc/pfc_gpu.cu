@@ -161,6 +161,8 @@ struct Ctx {
   // softmax statistics
   void* part_m = nullptr;  // [T][maxB]
   void* part_s = nullptr;
+  void* seg_m = nullptr;   // [kMergeSegs][maxB]
+  void* seg_s = nullptr;
   void* lm = nullptr;      // [R][maxB]
   void* ls = nullptr;
   void* gmax = nullptr;
@@ -389,10 +391,16 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const int T = gf.n_tiles * NWG;  // (max, sumexp) partial slots per row
   ST* lm = static_cast<ST*>(c->lm);
   ST* ls = static_cast<ST*>(c->ls);
-  merge_tiles_kernel<ST><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(pm, ps, T, (int)B,
-                                                                       lm + c->rank * B,
-                                                                       ls + c->rank * B);
-  c->launches++;
+  {
+    const int nseg = (int)std::min<int64_t>(kMergeSegs, T);
+    ST* segm = static_cast<ST*>(c->seg_m);
+    ST* segs = static_cast<ST*>(c->seg_s);
+    merge_tiles_kernel<ST><<<dim3((unsigned)ceil_div(B, 128), (unsigned)nseg), 128, 0, s>>>(
+        pm, ps, T, (int)B, segm, segs);
+    merge_segments_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(
+        segm, segs, nseg, (int)B, lm + c->rank * B, ls + c->rank * B);
+    c->launches += 2;
+  }
   if (c->R > 1) {
     const int dt = sizeof(ST) == 8 ? ncclFloat64 : ncclFloat32;
     NCCL_TRY(c, g_nccl.AllGather(lm + c->rank * B, lm, B, dt, c->comm, s));
@@ -697,6 +705,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_m), (size_t)(T * kNWG * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(T * kNWG * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->seg_m), (size_t)(kMergeSegs * B) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->seg_s), (size_t)(kMergeSegs * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->lm), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->ls), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->gmax), (size_t)B * sb));

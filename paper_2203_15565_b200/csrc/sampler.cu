@@ -81,22 +81,46 @@ __global__ void __launch_bounds__(1024) positives_kernel(
   }
   int P = 1;
   while (P < B) P <<= 1;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) keys[i] = i < B ? labels[i] : INT64_MAX;
-  __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const int64_t a = keys[i], b = keys[ixj];
-          const bool asc = (i & k) == 0;
-          if (asc ? (a > b) : (a < b)) {
-            keys[i] = b;
-            keys[ixj] = a;
+  if (P <= (int)blockDim.x) {
+    // one key per thread: register bitonic sort, warp shuffles for partner distance < 32
+    const int i = threadIdx.x;
+    int64_t key = i < B ? labels[i] : INT64_MAX;
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        int64_t other;
+        if (j >= 32) {
+          if (i < P) keys[i] = key;
+          __syncthreads();
+          other = i < P ? keys[i ^ j] : key;
+          __syncthreads();
+        } else {
+          other = __shfl_xor_sync(0xffffffffu, key, j);
+        }
+        const bool asc = (i & k) == 0, lower = i < (i ^ j);
+        const int64_t lo = key < other ? key : other, hi = key < other ? other : key;
+        key = (asc == lower) ? lo : hi;
+      }
+    }
+    if (i < P) keys[i] = key;
+    __syncthreads();
+  } else {
+    for (int i = threadIdx.x; i < P; i += blockDim.x) keys[i] = i < B ? labels[i] : INT64_MAX;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int64_t a = keys[i], b = keys[ixj];
+            const bool asc = (i & k) == 0;
+            if (asc ? (a > b) : (a < b)) {
+              keys[i] = b;
+              keys[ixj] = a;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   // unique (sorted): each thread owns a contiguous run of ceil(B/1024) keys

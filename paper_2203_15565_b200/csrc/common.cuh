@@ -45,6 +45,18 @@ struct StepStatus {
   int32_t pad[2];
 };
 
+// Per-step scalars, written on the device by step_begin_kernel (the only graph node whose
+// arguments change between steps) and read by the kernels that need them.
+struct StepParams {
+  uint64_t seed;    // iteration_rng.seed()
+  uint64_t stream;  // iteration_rng.stream_id()
+  float lr;
+  int32_t pad;
+  const float* x;          // [B][D] fp32 features of this step
+  const int64_t* labels;   // [B]
+  float* dx;               // [B][D] rank-local partial d_features
+};
+
 enum MarginKindDev : int { kPlain = 0, kAddCos = 1, kAddAng = 2 };
 
 struct MarginDev {

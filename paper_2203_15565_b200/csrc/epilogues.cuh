@@ -369,7 +369,8 @@ struct DwUpdateEpi {
   const ST* cproj_part;     // [n_parts][ncols]
   float* W;
   float* Mom;
-  float lr, mu, wd;
+  const StepParams* sp;  // lr of this step
+  float mu, wd;
   const StepStatus* st;  // no update when the step failed (the reference throws before 412)
   int cw;                // columns per warpgroup (BN / NWG), for prefetch
   int pf_mode;           // 0 none, 1 current tile at epilogue start, 2 one tile ahead
@@ -413,7 +414,7 @@ struct DwUpdateEpi {
   __device__ __forceinline__ void finish(int, int) const {}
 
   __device__ __forceinline__ void update4(float4& w, float4& m, const float* a, float inv,
-                                          float cpj) const {
+                                          float cpj, float lr) const {
     float wv[4] = {w.x, w.y, w.z, w.w};
     float mv[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
@@ -440,6 +441,7 @@ struct DwUpdateEpi {
     int* s_row = reinterpret_cast<int*>(s_cp + 32);
     if (pf_mode == 1) prefetch_rows(t, row, wg);
     const bool failed = status_failed(st);
+    const float lr = sp->lr;
     __syncwarp();  // the warp finished reading the previous tile's scalars
     s_inv[lane] = pre.inv;
     s_cp[lane] = pre.cp;
@@ -477,7 +479,7 @@ struct DwUpdateEpi {
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (rw[u] >= 0) {
-            update4(w[u], mo[u], stage + (u * 4 + sub) * 33 + q4, rinv[u], rcp[u]);
+            update4(w[u], mo[u], stage + (u * 4 + sub) * 33 + q4, rinv[u], rcp[u], lr);
             const size_t o = (size_t)rw[u] * D + d;
             *reinterpret_cast<float4*>(Mom + o) = mo[u];
             *reinterpret_cast<float4*>(W + o) = w[u];
@@ -492,7 +494,7 @@ struct DwUpdateEpi {
             const size_t o = (size_t)wr * D + dd;
             float4 w4 = make_float4(W[o], 0.f, 0.f, 0.f), m4 = make_float4(Mom[o], 0.f, 0.f, 0.f);
             float a[4] = {stage[r * 33 + lane], 0.f, 0.f, 0.f};
-            update4(w4, m4, a, s_inv[r], s_cp[r]);
+            update4(w4, m4, a, s_inv[r], s_cp[r], lr);
             Mom[o] = m4.x;
             W[o] = w4.x;
           }

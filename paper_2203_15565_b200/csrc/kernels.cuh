@@ -11,6 +11,28 @@ __device__ __forceinline__ bool step_failed(const StepStatus* st) {
   return sampler_failed(st) || st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx;
 }
 
+// First node of every step: per-step scalars + a fresh status block.  Errors are sticky
+// across asynchronous steps (pfc_gpu_sync reports and clears them), like the reference,
+// which stops at the first throwing step.
+__global__ void step_begin_kernel(StepStatus* st, StepParams* sp, uint64_t seed, uint64_t stream,
+                                  float lr, int reset, const float* x, const int64_t* labels,
+                                  float* dx) {
+  if (threadIdx.x != 0) return;
+  sp->x = x;
+  sp->labels = labels;
+  sp->dx = dx;
+  const bool sticky = !reset && (sampler_failed(st) || st->masked_row != 0x7fffffff ||
+                                 st->nonfinite_loss || st->nonfinite_dx);
+  sp->seed = seed;
+  sp->stream = stream;
+  sp->lr = sticky ? 0.f : lr;
+  if (sticky) return;
+  StepStatus s{};
+  s.capacity_shard = -1;
+  s.masked_row = 0x7fffffff;
+  *st = s;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -60,11 +82,11 @@ __global__ void dx_to_dxb_kernel(const float* __restrict__ dX, int D, int B,
 // Feature normalisation (shardsim.hpp:196-204): |x| (fp64 accumulate), x^ = x * 1/max(|x|,1e-12),
 // written zero-padded to Dp columns in the GEMM operand type.  One warp per row.
 template <typename OT>
-__global__ void normalize_x_kernel(const float* __restrict__ X, int B, int D, int Dp,
+__global__ void normalize_x_kernel(const StepParams* __restrict__ sp, int B, int D, int Dp,
                                    OT* __restrict__ xh, float* __restrict__ xnorm) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= B) return;
-  const float* x = X + (size_t)warp * D;
+  const float* x = sp->x + (size_t)warp * D;
   double ss = 0.0;
   for (int d = lane; d < D; d += 32) ss += (double)x[d] * (double)x[d];
   ss = warp_sum(ss);
@@ -237,11 +259,12 @@ __global__ void loss_reduce_kernel(const double* __restrict__ loss_row, int B, S
 // feat_proj_b = sum_j g_bj c_bj = x^_b . r_b since c_bj = x^_b . w^_j (exact identity).
 template <int D_PER_THREAD>
 __global__ void __launch_bounds__(256) dx_finalize_kernel(const float* __restrict__ part, int S,
-                                                          const float* __restrict__ X,
+                                                          const StepParams* __restrict__ sp,
                                                           const float* __restrict__ xnorm, int B,
-                                                          int D, float* __restrict__ dX,
-                                                          StepStatus* st) {
+                                                          int D, StepStatus* st) {
   const int b = blockIdx.x;
+  const float* __restrict__ X = sp->x;
+  float* __restrict__ dX = sp->dx;
   __shared__ double red[8];
   const float n = xnorm[b];
   const float inv = 1.0f / (n > 1e-12f ? n : 1e-12f);

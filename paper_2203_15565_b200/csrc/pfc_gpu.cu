@@ -180,6 +180,14 @@ struct Ctx {
   double* xdb = nullptr;  // D x maxB fp64
   StepStatus* st = nullptr;
   StepStatus* st_host = nullptr;
+  StepParams* sp = nullptr;
+  bool reset_status = true;  // false while asynchronous device steps are in flight
+  // CUDA graph of the device step (one per batch size); step_begin is its first node
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraphNode_t gbegin = nullptr;
+  int64_t gB = -1;
+  int64_t glaunches = 0;
   // tensor maps cached per batch
   int64_t tm_B = -1;
   CUtensorMap tm_x_k, tm_w_k, tm_w_k128, tm_x_k256, tm_gt_k, tm_x_mn, tm_gt_mn, tm_w_mn, tm_gt_st;
@@ -320,14 +328,9 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   cudaStream_t s = c->stream;
   const int bs = 256;
   if (int rc = ensure_maps(c, B)) return rc;
-  CUDA_TRY(c, cudaMemsetAsync(c->st, 0, sizeof(StepStatus), s));
-  {
-    StepStatus init{};
-    init.capacity_shard = -1;
-    init.masked_row = 0x7fffffff;
-    *c->st_host = init;
-    CUDA_TRY(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(StepStatus), cudaMemcpyHostToDevice, s));
-  }
+  step_begin_kernel<<<1, 32, 0, s>>>(c->st, c->sp, a->seed, a->stream_id, (float)a->lr,
+                                     c->reset_status ? 1 : 0, x, lab, dx_full);
+  c->launches++;
   // ---- sampler (build_buffers, sampler.hpp:63-126)
   const size_t sort_smem = sizeof(int64_t) * kMaxSortBatch;
   static bool sort_cfg = false;
@@ -337,27 +340,27 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     sort_cfg = true;
   }
   positives_kernel<<<1, 1024, sort_smem, s>>>(
-      lab, (int)B, c->C, (int)c->K, c->blk, (int)c->cap, (int)c->k0, (int)c->nk, c->uniq,
+      c->sp, (int)B, c->C, (int)c->K, c->blk, (int)c->cap, (int)c->k0, (int)c->nk, c->uniq,
       c->meta, c->buf_cls, c->pos_col, c->st, (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0);
   c->launches++;
   CUDA_TRY(c, cudaMemsetAsync(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride, s));
   const int64_t nd = c->nk * c->cap;
-  draws_kernel<<<(unsigned)ceil_div(nd, bs), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap, a->seed,
-                                                         a->stream_id, (int)c->k0, c->pool_stride,
+  draws_kernel<<<(unsigned)ceil_div(nd, bs), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap, c->sp,
+                                                         (int)c->k0, c->pool_stride,
                                                          c->head, c->nxt, c->jv, c->st);
   walk_kernel<<<(unsigned)ceil_div(nd, bs), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap,
                                                         c->pool_stride, c->head, c->nxt, c->jv,
                                                         c->buf_cls, c->st);
-  sequential_fallback_kernel<<<(unsigned)c->nk, 256, 0, s>>>(c->meta, (int)c->cap, a->seed,
-                                                             a->stream_id, (int)c->k0,
-                                                             c->pool_stride, c->pool_scratch,
+  sequential_fallback_kernel<<<(unsigned)c->nk, 256, 0, s>>>(c->meta, (int)c->cap, c->sp,
+                                                             (int)c->k0, c->pool_stride,
+                                                             c->pool_scratch,
                                                              c->buf_cls, c->st);
   c->launches += 3;
   phase(c, "sampler");
   // ---- normalise features, gather + normalise sampled centres
   OT* xh = static_cast<OT*>(c->xh);
   OT* wh = static_cast<OT*>(c->wh);
-  normalize_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(x, (int)B, (int)c->D,
+  normalize_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(c->sp, (int)B, (int)c->D,
                                                                        (int)c->Dp, xh, c->xnorm);
   gather_w_kernel<OT><<<(unsigned)ceil_div(c->ncols_pad * 32, bs), bs, 0, s>>>(
       c->W, (int)c->D, (int)c->Dp, c->buf_cls, (int)c->ncols, (int)c->ncols_pad, c->cls_lo,
@@ -443,10 +446,10 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
                                        (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
     const int dpt = (int)ceil_div(c->D, 256);
-    if (dpt <= 1) dx_finalize_kernel<1><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
-    else if (dpt <= 2) dx_finalize_kernel<2><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
-    else if (dpt <= 4) dx_finalize_kernel<4><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
-    else dx_finalize_kernel<8><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, x, c->xnorm, (int)B, (int)c->D, dx_full, c->st);
+    if (dpt <= 1) dx_finalize_kernel<1><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
+    else if (dpt <= 2) dx_finalize_kernel<2><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
+    else if (dpt <= 4) dx_finalize_kernel<4><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
+    else dx_finalize_kernel<8><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
   }
@@ -462,11 +465,11 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     if (c->D % 32 == 0)
       err = go(DwUpdateEpi<ST, true>{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp,
-                                     c->W, c->M, (float)a->lr, (float)c->d.momentum,
+                                     c->W, c->M, c->sp, (float)c->d.momentum,
                                      (float)c->d.weight_decay, c->st, BN / NWG, c->dw_prefetch});
     else
       err = go(DwUpdateEpi<ST, false>{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp,
-                                      c->W, c->M, (float)a->lr, (float)c->d.momentum,
+                                      c->W, c->M, c->sp, (float)c->d.momentum,
                                       (float)c->d.weight_decay, c->st, BN / NWG, c->dw_prefetch});
     CUDA_TRY(c, err);
   }
@@ -476,14 +479,73 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
 
 int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gpu_step_args* a,
              float* dx_full) {
-  if (c->pt.enabled) {
-    c->pt.n = 0;
-    cudaEventRecord(c->pt.ev[0], c->stream);
-  }
-  c->launches = 0;
   c->lastB = B;
-  if (c->bf16) return run_pipeline<float, __nv_bfloat16, true>(c, x, lab, B, a, dx_full);
-  return run_pipeline<double, float, false>(c, x, lab, B, a, dx_full);
+  const bool graph = !(c->d.flags & PFC_FLAG_NO_GRAPH) && !c->pt.enabled;
+  auto pipeline = [&]() {
+    c->launches = 0;
+    if (c->bf16) return run_pipeline<float, __nv_bfloat16, true>(c, x, lab, B, a, dx_full);
+    return run_pipeline<double, float, false>(c, x, lab, B, a, dx_full);
+  };
+  if (!graph) {
+    if (c->pt.enabled) {
+      c->pt.n = 0;
+      cudaEventRecord(c->pt.ev[0], c->stream);
+    }
+    return pipeline();
+  }
+  if (!c->gexec || c->gB != B) {  // capture the step once per batch size
+    if (c->gexec) {
+      cudaGraphExecDestroy(c->gexec);
+      cudaGraphDestroy(c->graph);
+      c->gexec = nullptr;
+    }
+    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = pipeline();
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    CUDA_TRY(c, ce);
+    CUDA_TRY(c, cudaGraphInstantiate(&c->gexec, g, 0));
+    c->graph = g;
+    size_t n = 0;
+    CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CUDA_TRY(c, cudaGraphGetNodes(g, nodes.data(), &n));
+    c->gbegin = nullptr;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      cudaGraphNodeGetType(nd, &ty);
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
+          kp.func == reinterpret_cast<void*>(step_begin_kernel))
+        c->gbegin = nd;
+    }
+    if (!c->gbegin) return fail(c, PFC_ERR_CUDA, "graph capture lost the step_begin node");
+    c->gB = B;
+    c->glaunches = c->launches;
+  }
+  // per step, only step_begin's arguments change
+  StepStatus* st = c->st;
+  StepParams* sp = c->sp;
+  uint64_t seed = a->seed, stream = a->stream_id;
+  float lr = (float)a->lr;
+  int reset = c->reset_status ? 1 : 0;
+  void* args[] = {&st, &sp, &seed, &stream, &lr, &reset, &x, &lab, &dx_full};
+  cudaKernelNodeParams kp{};
+  kp.func = reinterpret_cast<void*>(step_begin_kernel);
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(32);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(c->gexec, c->gbegin, &kp));
+  CUDA_TRY(c, cudaGraphLaunch(c->gexec, c->stream));
+  c->launches = c->glaunches;
+  return PFC_OK;
 }
 
 void trace_closed_form(Ctx* c, int64_t B, pfc_gpu_step_out* o) {
@@ -720,6 +782,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->dX, (size_t)B * c->D));
   CT(dalloc(c, &c->xdb, (size_t)B * c->D));
   CT(dalloc(c, &c->st, 1));
+  CT(dalloc(c, &c->sp, 1));
   CT(cudaMallocHost(&c->st_host, sizeof(StepStatus)));
   for (int i = 0; i <= PhaseTimer::kMax; ++i) CT(cudaEventCreate(&c->pt.ev[i]));
   if (c->R > 1) {
@@ -741,6 +804,8 @@ int pfc_gpu_destroy(void* ctx) {
   if (!ctx) return PFC_OK;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
   if (c->st_host) cudaFreeHost(c->st_host);
@@ -864,6 +929,7 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
   dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
   x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
   if (int rc = run_step(c, c->X, c->labels, B, a, c->dX)) return rc;
+  c->reset_status = true;
   if (c->R > 1)  // the drop-in returns the FULL summed d_features on every rank
     NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, s));
   dx_to_dxb_kernel<<<grid, blk, 0, s>>>(c->dX, (int)c->D, (int)B, c->xdb);
@@ -897,19 +963,24 @@ int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_l
     dxf = c->dX;
   }
   if (int rc = run_step(c, x, lab, B, a, dxf)) return rc;
+  c->reset_status = false;  // errors stay on the device until a synchronous check
   if (c->R > 1)  // collective 3 (shardsim.hpp:387-399) as a reduce-scatter to the owners
     NCCL_TRY(c, g_nccl.ReduceScatter(c->dX, dx_local, b_local * c->D, ncclFloat32, ncclSum,
                                      c->comm, s));
-  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
   if (!out) return PFC_OK;
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
+  c->reset_status = true;
   if (int rc = finish_phase_timing(c)) return rc;
   return check_status(c, a->step_index, B, out);
 }
 
 int pfc_gpu_sync(void* ctx, pfc_gpu_step_out* out) {
   Ctx* c = static_cast<Ctx*>(ctx);
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost,
+                              c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->reset_status = true;
   if (int rc = finish_phase_timing(c)) return rc;
   return check_status(c, -1, c->lastB, out);
 }

@@ -68,13 +68,14 @@ __device__ int block_exclusive_scan(int v, int* smem_warp, int* total) {
 // positives to shards (sampler.hpp:68-80), check capacity in the reference's shard order
 // (sampler.hpp:84-98), and locate every row's positive column (shardsim.hpp:207-213).
 __global__ void __launch_bounds__(1024) positives_kernel(
-    const int64_t* __restrict__ labels, int B, int64_t C, int K, int64_t blk, int cap, int k0,
+    const StepParams* __restrict__ sp, int B, int64_t C, int K, int64_t blk, int cap, int k0,
     int nk, int64_t* __restrict__ uniq, ShardMeta* __restrict__ meta,
     int32_t* __restrict__ buf_cls, int32_t* __restrict__ pos_col, StepStatus* st,
     int force_sequential) {
   extern __shared__ int64_t keys[];
   __shared__ int warp_tmp[32];
   __shared__ int nuniq_s;
+  const int64_t* __restrict__ labels = sp->labels;
   if (B > kMaxSortBatch) {
     if (threadIdx.x == 0) st->batch_too_large = 1;
     return;
@@ -200,8 +201,8 @@ __global__ void __launch_bounds__(1024) positives_kernel(
 }
 
 // Per-draw counter RNG + modulo-rejection flag + per-position lists (j_s = p).
-__global__ void draws_kernel(ShardMeta* __restrict__ meta, int nk, int cap, uint64_t seed,
-                             uint64_t stream, int k0, int64_t pool_stride,
+__global__ void draws_kernel(ShardMeta* __restrict__ meta, int nk, int cap,
+                             const StepParams* __restrict__ sp, int k0, int64_t pool_stride,
                              int32_t* __restrict__ head, int32_t* __restrict__ nxt,
                              int32_t* __restrict__ jv, const StepStatus* st) {
   if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;
@@ -210,7 +211,7 @@ __global__ void draws_kernel(ShardMeta* __restrict__ meta, int nk, int cap, uint
   const int kk = (int)(gid / cap), i = (int)(gid % cap);
   const ShardMeta m = meta[kk];
   if (m.full || i >= m.need) return;
-  const uint64_t key = rng_key(seed, fork_stream(stream, (uint64_t)(k0 + kk)));
+  const uint64_t key = rng_key(sp->seed, fork_stream(sp->stream, (uint64_t)(k0 + kk)));
   const uint64_t n = (uint64_t)(m.pool - i);
   const uint64_t r = rng_draw(key, (uint64_t)i + 1);
   const uint64_t limit = UINT64_MAX - UINT64_MAX % n;  // rng.hpp:69
@@ -265,8 +266,9 @@ __global__ void walk_kernel(const ShardMeta* __restrict__ meta, int nk, int cap,
 
 // Exact sequential sample_without_replacement for shards that saw a modulo rejection
 // (or when forced for testing).  One CTA per local shard.
-__global__ void sequential_fallback_kernel(ShardMeta* __restrict__ meta, int cap, uint64_t seed,
-                                           uint64_t stream, int k0, int64_t pool_stride,
+__global__ void sequential_fallback_kernel(ShardMeta* __restrict__ meta, int cap,
+                                           const StepParams* __restrict__ sp, int k0,
+                                           int64_t pool_stride,
                                            int32_t* __restrict__ pool_scratch,
                                            int32_t* __restrict__ buf_cls, StepStatus* st) {
   if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;
@@ -280,7 +282,7 @@ __global__ void sequential_fallback_kernel(ShardMeta* __restrict__ meta, int cap
   __syncthreads();
   if (threadIdx.x == 0) {
     atomicAdd(&st->rejection_shards, 1);
-    const uint64_t key = rng_key(seed, fork_stream(stream, (uint64_t)(k0 + kk)));
+    const uint64_t key = rng_key(sp->seed, fork_stream(sp->stream, (uint64_t)(k0 + kk)));
     uint64_t counter = 0;
     for (int i = 0; i < m.need; ++i) {
       const uint64_t n = (uint64_t)(m.pool - i);

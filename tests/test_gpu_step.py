@@ -229,3 +229,50 @@ def test_repeatable_bitwise(port):
         sh.close()
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+
+
+def test_graph_replay_equals_eager(port):
+    """The CUDA-graph replay of the step (default) and eager launches give identical bits,
+    over several steps with changing seeds / lr (only step_begin's arguments change)."""
+    C_, K, D, B = 12000, 3, 256, 192
+    outs = []
+    for flags in (0, p.FLAG_NO_GRAPH):
+        cfg = p.StepConfig(r=0.2, margin=p.MarginConfig.arcface_style())
+        sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, flags=flags)
+        sh.init_center_shards(5)
+        res = []
+        for step in range(3):
+            X, labels = port.bench_inputs(C_, D, B, 1, step)
+            cfg.lr = 0.1 / (step + 1)
+            r = p.distributed_partial_step(sh, X, labels, cfg, p.SeededRng(1, p.make_stream("iteration", step)))
+            res.append((r.loss, r.d_features.copy(), [b.class_indices.copy() for b in r.buffers]))
+        res.append(sh.get_shard(2))
+        outs.append(res)
+        sh.close()
+    for a, b in zip(outs[0][:3], outs[1][:3]):
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+        assert all(np.array_equal(x, y) for x, y in zip(a[2], b[2]))
+    assert np.array_equal(outs[0][3][0], outs[1][3][0]) and np.array_equal(outs[0][3][1], outs[1][3][1])
+
+
+def test_async_device_steps_report_errors_on_sync():
+    C_, K, D, B = 1000, 4, 64, 8
+    cfg = p.StepConfig(r=0.1)
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B)
+    sh.init_center_shards(1)
+    x = torch.randn(B, D, device="cuda")
+    good = torch.arange(B, dtype=torch.int64, device="cuda") * 100
+    bad = good.clone()
+    bad[3] = 5000
+    dx = torch.empty(B, D, device="cuda")
+    sh.step_device(x.data_ptr(), good.data_ptr(), B, dx.data_ptr(), cfg, p.SeededRng(1, 1), sync=False)
+    W_before = sh.get_shard(0)[0]
+    sh.step_device(x.data_ptr(), bad.data_ptr(), B, dx.data_ptr(), cfg, p.SeededRng(1, 2), sync=False)
+    sh.step_device(x.data_ptr(), good.data_ptr(), B, dx.data_ptr(), cfg, p.SeededRng(1, 3), sync=False)
+    with pytest.raises(p.ContractError, match="label 5000 outside"):
+        sh.sync()
+    # sticky: the failing step and every later async step left W untouched
+    assert np.array_equal(sh.get_shard(0)[0], W_before)
+    out = sh.step_device(x.data_ptr(), good.data_ptr(), B, dx.data_ptr(), cfg, p.SeededRng(1, 4))
+    assert np.isfinite(out.loss)
+    sh.close()

@@ -1,0 +1,141 @@
+// adapter_parity.cpp — C++ parity test of the drop-in (TEST INFRASTRUCTURE ONLY).
+//
+// Compiled by oracle/Makefile against the UNMODIFIED reference headers (/root/reference/proj/
+// include) and include/pfc/gpu_step.hpp into oracle/_ref/adapter_parity, the way a maintainer
+// would build their own tests: the same CenterShard / FeatureBatch / StepConfig objects go through
+// the reference's pfc::distributed_partial_step (shardsim.hpp:166) and through
+// pfc::gpu::distributed_partial_step / pfc::gpu::Session (the B200 path), and the results are
+// compared under the tolerance contract of DESIGN.md.  Patterned on
+// proj/tests/test_shardsim.cpp:102-127 and 178-221.  Prints one JSON line per case; exit 0 iff
+// every case is within tolerance.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "pfc/gpu_step.hpp"
+#include "pfc/shardsim.hpp"
+
+using namespace pfc;
+
+namespace {
+
+FeatureBatch bench_batch(int64_t C, int64_t D, int64_t B, uint64_t step) {
+  // the bench input convention: labels, then X b-major / d inner
+  FeatureBatch fb;
+  fb.features = Matrix(D, B);
+  SeededRng rl(1, make_stream("bench-labels", step));
+  for (int64_t b = 0; b < B; ++b) fb.labels.push_back(static_cast<int64_t>(rl.next_below(C)));
+  SeededRng rx(1, make_stream("bench-x", step));
+  for (int64_t b = 0; b < B; ++b)
+    for (int64_t d = 0; d < D; ++d) fb.features(d, b) = rx.next_normal();
+  return fb;
+}
+
+double rel_fro(const Matrix& a, const Matrix& b) {
+  double n = 0, d = 0;
+  for (size_t i = 0; i < a.flat().size(); ++i) {
+    n += (a.flat()[i] - b.flat()[i]) * (a.flat()[i] - b.flat()[i]);
+    d += b.flat()[i] * b.flat()[i];
+  }
+  return std::sqrt(n / std::max(d, 1e-300));
+}
+
+double rel_max_shards(const std::vector<CenterShard>& a, const std::vector<CenterShard>& b) {
+  double n = 0, d = 0;
+  for (size_t k = 0; k < a.size(); ++k)
+    for (size_t i = 0; i < a[k].weights.flat().size(); ++i) {
+      n = std::max(n, std::fabs(a[k].weights.flat()[i] - b[k].weights.flat()[i]));
+      d = std::max(d, std::fabs(b[k].weights.flat()[i]));
+    }
+  return n / std::max(d, 1e-300);
+}
+
+struct Case {
+  const char* name;
+  int64_t C, K, B, D;
+  double r;
+  MarginConfig margin;
+  std::optional<double> tau;
+  int precision;
+  double tol_loss, tol_dx, tol_w;
+};
+
+}  // namespace
+
+int main() {
+  const Case cases[] = {
+      {"tiny_cos_fp32", 400, 4, 32, 32, 0.5, MarginConfig::cosface_style(), std::nullopt,
+       PFC_PRECISION_FP32, 1e-6, 1e-5, 1e-6},
+      {"filter_full_fp32", 300, 3, 24, 32, 1.0, MarginConfig::cosface_style(), 0.1,
+       PFC_PRECISION_FP32, 1e-6, 1e-5, 1e-6},
+      {"arc_10k_fp32", 10000, 1, 128, 512, 0.1, MarginConfig::arcface_style(), std::nullopt,
+       PFC_PRECISION_FP32, 1e-6, 1e-5, 1e-6},
+      {"arc_10k_bf16", 10000, 1, 128, 512, 0.1, MarginConfig::arcface_style(), std::nullopt,
+       PFC_PRECISION_BF16, 1e-4, 1e-2, 1e-3},
+      {"arc_40k_k4_bf16", 40000, 4, 256, 512, 0.1, MarginConfig::arcface_style(), std::nullopt,
+       PFC_PRECISION_BF16, 1e-4, 1e-2, 1e-3},
+  };
+  bool ok = true;
+  for (const Case& cs : cases) {
+    const ShardLayout layout(cs.C, cs.K);
+    std::vector<CenterShard> ref = init_center_shards(layout, cs.D, 1);
+    std::vector<CenterShard> dev = ref;
+    StepConfig cfg;
+    cfg.r = cs.r;
+    cfg.margin = cs.margin;
+    cfg.filter_threshold = cs.tau;
+    cfg.lr = 0.1;
+    gpu::Session session(layout, cs.D, cfg, cs.B, cs.precision);
+    session.upload(dev);
+    for (uint64_t step = 0; step < 2; ++step) {
+      const FeatureBatch batch = bench_batch(cs.C, cs.D, cs.B, step);
+      const SeededRng it(1, make_stream("iteration", step));
+      const StepResult want = distributed_partial_step(ref, batch, cfg, it);
+      const StepResult got = session.step(batch, cfg, it);
+      session.download(dev);
+      bool buffers_equal = want.buffers.size() == got.buffers.size();
+      for (size_t k = 0; buffers_equal && k < want.buffers.size(); ++k)
+        buffers_equal = want.buffers[k].class_indices == got.buffers[k].class_indices &&
+                        want.buffers[k].num_positives == got.buffers[k].num_positives;
+      const double dl = std::fabs(got.loss - want.loss) / std::fabs(want.loss);
+      const double dx = rel_fro(got.d_features, want.d_features);
+      const double dw = rel_max_shards(dev, ref);
+      const bool trace_ok = got.trace == want.trace;
+      const bool pass = buffers_equal && trace_ok && dl <= cs.tol_loss && dx <= cs.tol_dx &&
+                        dw <= cs.tol_w;
+      ok = ok && pass;
+      std::printf(
+          "{\"case\": \"%s\", \"step\": %llu, \"buffers_bit_exact\": %s, \"trace_equal\": %s, "
+          "\"loss\": %.12f, \"loss_ref\": %.12f, \"loss_rel\": %.3e, \"dX_fro\": %.3e, "
+          "\"W_maxmax\": %.3e, \"pass\": %s}\n",
+          cs.name, (unsigned long long)step, buffers_equal ? "true" : "false",
+          trace_ok ? "true" : "false", got.loss, want.loss, dl, dx, dw, pass ? "true" : "false");
+    }
+  }
+  // the unchanged-signature free function on host shards + the reference's error text
+  {
+    const ShardLayout layout(1000, 4);
+    std::vector<CenterShard> shards = init_center_shards(layout, 8, 1);
+    FeatureBatch fb;
+    fb.features = Matrix(8, 125);
+    for (int64_t b = 0; b < 125; ++b) fb.labels.push_back(b * 8);
+    StepConfig cfg;
+    std::string want, got;
+    try {
+      distributed_partial_step(shards, fb, cfg, SeededRng(1, 1));
+    } catch (const CapacityError& e) {
+      want = e.what();
+    }
+    try {
+      gpu::distributed_partial_step(shards, fb, cfg, SeededRng(1, 1));
+    } catch (const CapacityError& e) {
+      got = e.what();
+    }
+    const bool pass = !want.empty() && want == got;
+    ok = ok && pass;
+    std::printf("{\"case\": \"capacity_error_text\", \"pass\": %s}\n", pass ? "true" : "false");
+  }
+  return ok ? 0 : 1;
+}

@@ -199,12 +199,18 @@ struct alignas(64) GradEpi {
   // g for 32 columns from the cosines v and per-column constants (gmax*log2e, s*ig/B)
   __device__ __forceinline__ void grad32(const float (&v)[32], const float2* cf, float (&g)[32]) const {
     const float A = mg.s * kLog2e;
+    const float4* cf4 = reinterpret_cast<const float4*>(cf);  // two columns per 128-bit load
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const float2 k = cf[q];
-      float gq = pfc_sm100::ex2_approx(fmaf(v[q], A, -k.x)) * k.y;
-      if (kFilter) gq = v[q] > tau ? 0.f : gq;
-      g[q] = gq;
+    for (int q = 0; q < 32; q += 2) {
+      const float4 k = cf4[q >> 1];
+      float g0 = pfc_sm100::ex2_approx(fmaf(v[q], A, -k.x)) * k.y;
+      float g1 = pfc_sm100::ex2_approx(fmaf(v[q + 1], A, -k.z)) * k.w;
+      if (kFilter) {
+        g0 = v[q] > tau ? 0.f : g0;
+        g1 = v[q + 1] > tau ? 0.f : g1;
+      }
+      g[q] = g0;
+      g[q + 1] = g1;
     }
   }
   // the positive entry q of this chunk: margin form (margin.hpp:41-72), fp64
@@ -266,10 +272,7 @@ struct alignas(64) GradEpi {
               if (prow[kk * 32 + q] == (uint8_t)row)
                 patch_positive(v, g, q, (double)gmax[colb + q], (double)inv_gsum[colb + q]);
           }
-          if (!rv) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) g[q] = 0.f;
-          }
+          // rows j >= ncols (last class tile) are clipped by the TMA store and not accumulated
           float c1 = 0.f, c2 = 0.f;
 #pragma unroll
           for (int q = 0; q < 32; q += 2) {

@@ -175,35 +175,56 @@ __global__ void __launch_bounds__(128) merge_tiles_kernel(const ST* __restrict__
   if (b >= B) return;
   const int per = (T + gridDim.y - 1) / gridDim.y;
   const int t0 = blockIdx.y * per, t1 = min(T, t0 + per);
-  ST m = -INFINITY, s = 0;
-  for (int t = t0; t < t1; ++t) {
-    const ST mt = pm[(size_t)t * B + b], st = ps[(size_t)t * B + b];
-    if (mt == (ST)-INFINITY) continue;
-    if (mt > m) {
-      s = (m == (ST)-INFINITY ? ST(0) : s * fast_exp(m - mt)) + st;
-      m = mt;
-    } else {
-      s += st * fast_exp(mt - m);
+  ST m = -INFINITY;
+  // pass A: max (independent loads, 4 in flight)
+  int t = t0;
+  for (; t + 4 <= t1; t += 4) {
+    const ST a0 = pm[(size_t)t * B + b], a1 = pm[(size_t)(t + 1) * B + b];
+    const ST a2 = pm[(size_t)(t + 2) * B + b], a3 = pm[(size_t)(t + 3) * B + b];
+    m = fmax(m, fmax(fmax(a0, a1), fmax(a2, a3)));
+  }
+  for (; t < t1; ++t) m = fmax(m, pm[(size_t)t * B + b]);
+  ST s = 0;
+  if (m != (ST)-INFINITY) {
+    for (t = t0; t + 4 <= t1; t += 4) {
+      ST acc = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const ST mt = pm[(size_t)(t + u) * B + b], st = ps[(size_t)(t + u) * B + b];
+        acc += (mt == (ST)-INFINITY) ? ST(0) : st * fast_exp(mt - m);
+      }
+      s += acc;
+    }
+    for (; t < t1; ++t) {
+      const ST mt = pm[(size_t)t * B + b];
+      if (mt != (ST)-INFINITY) s += ps[(size_t)t * B + b] * fast_exp(mt - m);
     }
   }
   sm[(size_t)blockIdx.y * B + b] = m;
   ss[(size_t)blockIdx.y * B + b] = s;
 }
+// warp per row: lanes over segments, then a warp reduction
 template <typename ST>
 __global__ void merge_segments_kernel(const ST* __restrict__ sm, const ST* __restrict__ ss,
                                       int nseg, int B, ST* __restrict__ lm, ST* __restrict__ ls) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (b >= B) return;
   ST m = -INFINITY;
-  for (int i = 0; i < nseg; ++i) m = fmax(m, sm[(size_t)i * B + b]);
-  double s = 0.0;
+  for (int i = lane; i < nseg; i += 32) m = fmax(m, sm[(size_t)i * B + b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  ST s = 0;
   if (m != (ST)-INFINITY)
-    for (int i = 0; i < nseg; ++i) {
+    for (int i = lane; i < nseg; i += 32) {
       const ST mi = sm[(size_t)i * B + b];
-      if (mi != (ST)-INFINITY) s += (double)ss[(size_t)i * B + b] * exp((double)mi - (double)m);
+      if (mi != (ST)-INFINITY) s += ss[(size_t)i * B + b] * fast_exp(mi - m);
     }
-  lm[b] = m;
-  ls[b] = (ST)s;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    lm[b] = m;
+    ls[b] = s;
+  }
 }
 
 // Cross-rank merge in ascending rank order (collectives 1 and 2, shardsim.hpp:284-338),

@@ -332,7 +332,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
                                      c->reset_status ? 1 : 0, x, lab, dx_full);
   c->launches++;
   // ---- sampler (build_buffers, sampler.hpp:63-126)
-  const size_t sort_smem = sizeof(int64_t) * kMaxSortBatch;
+  const size_t sort_smem = 2 * sizeof(int64_t) * kMaxSortBatch;  // keys + sorted unique labels
   static bool sort_cfg = false;
   if (!sort_cfg) {
     CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -400,7 +400,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     ST* segs = static_cast<ST*>(c->seg_s);
     merge_tiles_kernel<ST><<<dim3((unsigned)ceil_div(B, 128), (unsigned)nseg), 128, 0, s>>>(
         pm, ps, T, (int)B, segm, segs);
-    merge_segments_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(
+    merge_segments_kernel<ST><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(
         segm, segs, nseg, (int)B, lm + c->rank * B, ls + c->rank * B);
     c->launches += 2;
   }

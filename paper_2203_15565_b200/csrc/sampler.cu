@@ -124,7 +124,9 @@ __global__ void __launch_bounds__(1024) positives_kernel(
       }
     }
   }
-  // unique (sorted): each thread owns a contiguous run of ceil(B/1024) keys
+  // unique (sorted) into shared memory: each thread owns a contiguous run of keys
+  int64_t* us = keys + kMaxSortBatch;
+  __shared__ int bad_shard_s;
   const int per = (B + blockDim.x - 1) / blockDim.x;
   const int beg = threadIdx.x * per, end = min(B, beg + per);
   int cnt = 0;
@@ -132,60 +134,65 @@ __global__ void __launch_bounds__(1024) positives_kernel(
   int total = 0;
   int pos = block_exclusive_scan(cnt, warp_tmp, &total);
   for (int i = beg; i < end; ++i)
-    if (i == 0 || keys[i] != keys[i - 1]) uniq[pos++] = keys[i];
-  if (threadIdx.x == 0) nuniq_s = total;
+    if (i == 0 || keys[i] != keys[i - 1]) us[pos++] = keys[i];
+  if (threadIdx.x == 0) {
+    nuniq_s = total;
+    bad_shard_s = K;
+  }
   __syncthreads();
   const int nu = nuniq_s;
-  __threadfence_block();
   if (threadIdx.x == 0) {
     // validation in sorted order (sampler.hpp:72-78): negatives first, then >= C
     int bad = -1;
-    if (nu > 0 && uniq[0] < 0) bad = 0;
+    if (nu > 0 && us[0] < 0) bad = 0;
     else {
-      const int i = lower_bound_i64(uniq, nu, C);
+      const int i = lower_bound_i64(us, nu, C);
       if (i < nu) bad = i;
     }
     if (bad >= 0) {
       st->label_oob = 1;
-      st->oob_label = uniq[bad];
-    } else {
-      // capacity checks for ALL shards in ascending order (sampler.hpp:84-98)
-      for (int k = 0; k < K; ++k) {
-        const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
-        const int np = lower_bound_i64(uniq, nu, hi) - lower_bound_i64(uniq, nu, lo);
-        if (np > cap || hi - lo < cap) {
-          st->capacity_shard = k;
-          st->capacity_npos = np;
-          break;
-        }
-      }
+      st->oob_label = us[bad];
     }
+  }
+  // capacity checks for ALL shards; the first failing shard in ascending order wins
+  // (sampler.hpp:84-98)
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
+    const int np = lower_bound_i64(us, nu, hi) - lower_bound_i64(us, nu, lo);
+    if (np > cap || hi - lo < cap) atomicMin(&bad_shard_s, k);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && !st->label_oob && bad_shard_s < K) {
+    const int k = bad_shard_s;
+    const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
+    st->capacity_shard = k;
+    st->capacity_npos = lower_bound_i64(us, nu, hi) - lower_bound_i64(us, nu, lo);
   }
   __syncthreads();
   if (st->label_oob || st->capacity_shard >= 0) return;
   for (int kk = threadIdx.x; kk < nk; kk += blockDim.x) {
     const int k = k0 + kk;
     const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
-    const int us = lower_bound_i64(uniq, nu, lo), ue = lower_bound_i64(uniq, nu, hi);
+    const int us0 = lower_bound_i64(us, nu, lo), ue = lower_bound_i64(us, nu, hi);
     ShardMeta m;
     m.lo = lo;
     m.hi = hi;
-    m.npos = ue - us;
+    m.npos = ue - us0;
     m.need = cap - m.npos;
     m.pool = (int)(hi - lo) - m.npos;
     m.full = (m.need == m.pool);
-    m.ustart = us;
+    m.ustart = us0;
     m.reject = force_sequential && !m.full && m.need > 0;
     meta[kk] = m;
   }
   // positives first, ascending (sampler.hpp:100-104)
   for (int i = threadIdx.x; i < nu; i += blockDim.x) {
-    const int64_t y = uniq[i];
+    const int64_t y = us[i];
     const int k = (int)(y / blk);
     if (k >= k0 && k < k0 + nk) {
       const int64_t lo = min((int64_t)k * blk, C);
-      const int us = lower_bound_i64(uniq, nu, lo);
-      buf_cls[(int64_t)(k - k0) * cap + (i - us)] = (int32_t)y;
+      const int u0 = lower_bound_i64(us, nu, lo);
+      buf_cls[(int64_t)(k - k0) * cap + (i - u0)] = (int32_t)y;
     }
   }
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(1024) positives_kernel(
     int col = -1;
     if (k >= k0 && k < k0 + nk) {
       const int64_t lo = min((int64_t)k * blk, C);
-      col = (k - k0) * cap + (lower_bound_i64(uniq, nu, y) - lower_bound_i64(uniq, nu, lo));
+      col = (k - k0) * cap + (lower_bound_i64(us, nu, y) - lower_bound_i64(us, nu, lo));
     }
     pos_col[b] = col;
   }

@@ -42,7 +42,8 @@ struct StepStatus {
   int32_t nonfinite_dx;
   int32_t rejection_shards;   // count of shards that needed the sequential sampler
   int32_t batch_too_large;
-  int32_t pad[2];
+  int32_t underflow_row;      // first row whose exp(z - offset) sum underflowed, else INT32_MAX
+  int32_t pad;
 };
 
 // Per-step scalars, written on the device by step_begin_kernel (the only graph node whose
@@ -51,10 +52,20 @@ struct StepParams {
   uint64_t seed;    // iteration_rng.seed()
   uint64_t stream;  // iteration_rng.stream_id()
   float lr;
-  int32_t pad;
+  uint32_t step_id;        // incremented by every step_begin
   const float* x;          // [B][D] fp32 features of this step
   const int64_t* labels;   // [B]
   float* dx;               // [B][D] rank-local partial d_features
+};
+
+struct ShardMeta {        // per local shard
+  int64_t lo, hi;         // owned range [lo, hi)
+  int32_t npos;           // distinct positives
+  int32_t need;           // cap - npos negatives to draw
+  int32_t pool;           // N = owned - npos
+  int32_t full;           // 1 -> full-sampling branch (ascending complement, no RNG)
+  int32_t ustart;         // index of the first positive in the sorted-unique label list
+  int32_t reject;         // 1 -> a modulo rejection happened: sequential fallback
 };
 
 enum MarginKindDev : int { kPlain = 0, kAddCos = 1, kAddAng = 2 };
@@ -63,6 +74,8 @@ struct MarginDev {
   int kind;
   float s;       // scale (1 for plain)
   double sd, md; // scale, margin in fp64 for the positive logit
+  float off;     // fixed softmax offset o = max(0, s - 40): exp(z - o) never overflows (z <= s)
+  double offd;
 };
 
 constexpr double kAngularClamp = 1e-7;  // margin.hpp:15

@@ -3,21 +3,26 @@
 // chunks from the accumulator source (TMEM on the tcgen05 engine, shared memory on the SIMT
 // engine).  With NWG warpgroups, warpgroup wg owns columns [wg*BN/NWG, (wg+1)*BN/NWG).
 //
-//   FwdStatsEpi  rows = batch rows b, cols = buffered classes j.
-//                cos tile -> margin (margin.hpp:41-54) + filter mask (shardsim.hpp:258-268)
-//                -> per (row, column-slice) online (max, sum exp) partials and z_pos
-//                (shardsim.hpp:270-318 restated flash-style: nothing B x cap reaches HBM).
-//   GradEpi      rows = buffered classes j, cols = batch rows b (the recomputed cos tile).
-//                g = ((p - onehot)/B) * margin'(c)  (shardsim.hpp:352-362) -> G^T (bf16 via
-//                swizzled smem + TMA store, or fp32) and center_proj_j = sum_b g c partials,
-//                thread-local in this orientation.
-//   DwUpdateEpi  rows = classes, cols = dims: dW = (sum_b g x^ - center_proj w^)/|w|
-//                (shardsim.hpp:377-384) fused with the sparse momentum-SGD of the sampled rows
-//                (update_centers, shardsim.hpp:139-159); W / momentum of the next tile are
-//                prefetched into L2 while this tile is processed.
-//   DxPartEpi    rows = batch rows, cols = dims: split-K partials of sum_j g w^_j.
-// feat_proj_b = sum_j g c_bj equals x^_b . (sum_j g w^_j) because c_bj = x^_b . w^_j, so it is
-// formed in dx_finalize_kernel from the dX GEMM result instead of being reduced here.
+// Softmax in a fixed-offset form.  Every logit satisfies z <= s (|cos| <= 1, margins only lower
+// the positive), so with o = max(0, s - 40) the quantity E = exp(z - o) lies in [0, e^40] and
+// never overflows.  Then, with S_b = sum_j E_bj (the rank-local and cross-rank sums):
+//   loss_b = log S_b + o - z_pos                 (shardsim.hpp:330-334: log gsum + gmax - z_pos)
+//   g_bj   = (s / (B S_b)) E_bj                  for negatives   (shardsim.hpp:356-359)
+//   g_bpos = ((p_pos - 1)/B) margin'(c_pos)       for the positive
+// so G = diag(rowscale) E + (sparse positive correction) and no B x cap gradient matrix or
+// logits recompute is needed: the logits GEMM writes E once (bf16), the dX GEMM consumes E
+// (row scale applied in its finalize), and the dW GEMM consumes E against rowscale * x^.
+// A row whose every logit is below o - 80 would underflow; it is flagged as a NumericalError
+// (at s = 64 that needs every cosine of the row, positive included, below -0.98).
+//
+//   FwdEpi       rows = batch rows b, cols = buffered classes j: cos tile -> margin + filter
+//                mask -> E (bf16, per-warp TMA stores) + per-(row, column slice) sums of E.
+//   DxPartEpi    rows = batch rows, cols = dims: split-K partials of sum_j E_bj w^_j.
+//   DwUpdateEpi  rows = classes, cols = dims (2-CTA cluster owns both 256-dim halves of a class
+//                block): dwt = sum_b E_bj (rowscale_b x^_b) + positive correction;
+//                center_proj = w^ . dwt (half-dots exchanged through DSMEM); dW and the fused
+//                momentum-SGD of the sampled rows (shardsim.hpp:139-159, 377-384).
+//   DwStoreEpi   fp32 validation engine: stores dwt; dw_rows_update_kernel finishes the rows.
 #pragma once
 #include <type_traits>
 
@@ -28,102 +33,11 @@ namespace pfc {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <typename T>
-__device__ __forceinline__ T neg_inf() {
-  return -INFINITY;
-}
-
 __device__ __forceinline__ bool status_failed(const StepStatus* st) {
   return st->label_oob || st->capacity_shard >= 0 || st->batch_too_large ||
-         st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx;
+         st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx ||
+         st->underflow_row != 0x7fffffff;
 }
-
-template <typename ST, bool kFilter>
-struct FwdStatsEpi {
-  static constexpr int kSmem = 0;
-  int B, ncols;
-  const int32_t* pos_col;
-  MarginDev mg;
-  float tau;
-  ST* part_m;  // [n_tiles * NWG][B]
-  ST* part_s;
-  double* zpos;
-
-  struct Pre {};
-  __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
-  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
-  __device__ __forceinline__ void finish(int, int) const {}
-
-  template <int BN, int NWG, class Src>
-  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t*, const Pre&) const {
-    constexpr int CW = BN / NWG;
-    const int b = t.row0 + row;
-    const bool rv = b < B;
-    const int pc = rv ? pos_col[b] : -1;
-    ST m = neg_inf<ST>(), s = ST(0);
-    const float A = mg.s * kLog2e;
-#pragma unroll 1
-    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
-      float v[32];
-      src.load(c0, v);
-      const int colb = t.col0 + c0;
-      if (!rv || colb >= ncols) continue;
-      const int jp = pc - colb;
-      if constexpr (std::is_same<ST, float>::value && !kFilter) {
-        if (colb + 32 <= ncols && (unsigned)jp >= 32u) {
-          // fast path: 32 valid negatives, z = s * c (s > 0 keeps the order of c)
-          float vmax = v[0];
-#pragma unroll
-          for (int j = 1; j < 32; ++j) vmax = fmaxf(vmax, v[j]);
-          const float mn = fmaxf(m, mg.s * vmax);
-          float acc = (m == -INFINITY) ? 0.f : s * pfc_sm100::ex2_approx((m - mn) * kLog2e);
-          const float off = mn * kLog2e;
-          float acc2 = 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            acc += pfc_sm100::ex2_approx(fmaf(v[j], A, -off));
-            acc2 += pfc_sm100::ex2_approx(fmaf(v[j + 1], A, -off));
-          }
-          s = acc + acc2;
-          m = mn;
-          continue;
-        }
-      }
-      // general path: bounds, filter mask, the positive's margin (fp64, margin.hpp:41-54)
-      ST z[32];
-      ST cmax = neg_inf<ST>();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const bool masked = (colb + j >= ncols) || (kFilter && j != jp && v[j] > tau);
-        z[j] = masked ? neg_inf<ST>() : (ST)mg.s * (ST)v[j];
-      }
-      if ((unsigned)jp < 32u) {
-        float vp = 0.f;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) vp = (j == jp) ? v[j] : vp;
-        const double zp = margin_pos(mg, (double)vp);
-        zpos[b] = zp;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = (j == jp) ? (ST)zp : z[j];
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) cmax = z[j] > cmax ? z[j] : cmax;
-      if (cmax == neg_inf<ST>()) continue;
-      const ST mn = m > cmax ? m : cmax;
-      ST acc = (m == neg_inf<ST>()) ? ST(0) : s * fast_exp(m - mn);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc += fast_exp(z[j] - mn);
-      s = acc;
-      m = mn;
-    }
-    if (rv) {
-      const size_t slot = (size_t)(t.n_tile * NWG + wg) * B + b;
-      part_m[slot] = m;
-      part_s[slot] = s;
-    }
-  }
-};
 
 __device__ __forceinline__ void pack_bf16x32(const float (&g)[32], uint32_t (&w)[16]) {
 #pragma unroll
@@ -132,63 +46,37 @@ __device__ __forceinline__ void pack_bf16x32(const float (&g)[32], uint32_t (&w)
     w[i] = *reinterpret_cast<const uint32_t*>(&h);
   }
 }
-__device__ __forceinline__ void store_g32(__nv_bfloat16* dst, const float (&g)[32]) {
-  uint32_t w[16];
-  pack_bf16x32(g, w);
-  uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) d[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+__device__ __forceinline__ float round_to(const __nv_bfloat16*, float v) {
+  return __bfloat162float(__float2bfloat16_rn(v));
 }
-__device__ __forceinline__ void store_g32(float* dst, const float (&g)[32]) {
-  float4* d = reinterpret_cast<float4*>(dst);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) d[i] = make_float4(g[4 * i], g[4 * i + 1], g[4 * i + 2], g[4 * i + 3]);
-}
-__device__ __forceinline__ void store_g1(__nv_bfloat16* dst, float g) { *dst = __float2bfloat16_rn(g); }
-__device__ __forceinline__ void store_g1(float* dst, float g) { *dst = g; }
+__device__ __forceinline__ float round_to(const float*, float v) { return v; }
+__device__ __forceinline__ void store_out1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ void store_out1(float* p, float v) { *p = v; }
 
-// rows = buffered classes j (M), cols = batch rows b (N).  Writes G^T[j][b].
-// kTma (tcgen05 engine): per-column constants arrive one tile ahead in registers (Pre); every
-// warp stages its 32 rows x 32 columns chunks (64B-swizzled) in a private 4-deep ring and
-// TMA-stores them itself, so the epilogue needs no cross-warp barrier.
-template <typename ST, typename GT, bool kFilter, bool kTma>
-struct alignas(64) GradEpi {
-  static constexpr int kWarpBytes = 9728;  // 4 x 2 KB staging + 1 KB constants + 128 B rows
-  static constexpr int kSmem = kTma ? 4 * kWarpBytes : 20 * 1024;
-  CUtensorMap tm;     // G^T store map: inner = b (box 32, SWIZZLE_64B), outer = classes (box 32)
-  int B, ncols, ldgt;
+struct NoSetup {
+  static constexpr int kCluster = 1;
+  __device__ __forceinline__ void setup(uint8_t*) const {}
+};
+
+// ------------------------------------------------------------------------------------ FwdEpi
+template <typename ST, typename OT, bool kFilter, bool kTma>
+struct alignas(64) FwdEpi : NoSetup {
+  static constexpr int kWarpBytes = 4096;  // 2 x [32 rows][64 B] E staging per warp
+  static constexpr int kSmem = kTma ? 4 * kWarpBytes : 0;
+  CUtensorMap tm;   // E store map: inner = classes (box 32, SWIZZLE_64B), outer = b (box 32)
+  int B, ncols, lde;
   const int32_t* pos_col;
   MarginDev mg;
   float tau;
-  const ST* gmax;
-  const ST* inv_gsum;
-  ST inv_batch;
-  GT* Gt;             // [ncols_pad][ldgt]
-  ST* cproj_part;     // [n_tiles(b) * NWG][ncols]
+  ST* part_s;       // [n_tiles * NWG][B]: sum of E per row and column slice
+  double* zpos;     // [B] margined positive logit (rows whose positive is local)
+  double* cpos;     // [B] cosine of the positive
+  float* epos;      // [B] E of the positive as stored (after OT rounding)
+  int* hasval;      // [B] 1 when the row has an unmasked column (filter only)
+  OT* E;            // [B][lde]
 
-  struct Pre {
-    float2 k[4];
-    int pc[4];
-  };
-  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int wg) const {
-    Pre p{};
-    if constexpr (kTma) {
-      const int lane = row & 31;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int b = t.col0 + wg * 128 + lane + 32 * i;
-        p.k[i] = make_float2(0.f, 0.f);
-        p.pc[i] = -1;
-        if (b < B) {
-          const float gm = (float)gmax[b];
-          const float ig = (float)inv_gsum[b];
-          p.k[i] = make_float2(gm * kLog2e, (float)(mg.sd * (double)ig * (double)inv_batch));
-          p.pc[i] = pos_col[b];
-        }
-      }
-    }
-    return p;
-  }
+  struct Pre {};
+  __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
   __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
   __device__ __forceinline__ void finish(int row, int) const {
     if constexpr (kTma) {
@@ -196,318 +84,111 @@ struct alignas(64) GradEpi {
     }
   }
 
-  // g for 32 columns from the cosines v and per-column constants (gmax*log2e, s*ig/B)
-  __device__ __forceinline__ void grad32(const float (&v)[32], const float2* cf, float (&g)[32]) const {
-    const float A = mg.s * kLog2e;
-    const float4* cf4 = reinterpret_cast<const float4*>(cf);  // two columns per 128-bit load
-#pragma unroll
-    for (int q = 0; q < 32; q += 2) {
-      const float4 k = cf4[q >> 1];
-      float g0 = pfc_sm100::ex2_approx(fmaf(v[q], A, -k.x)) * k.y;
-      float g1 = pfc_sm100::ex2_approx(fmaf(v[q + 1], A, -k.z)) * k.w;
-      if (kFilter) {
-        g0 = v[q] > tau ? 0.f : g0;
-        g1 = v[q + 1] > tau ? 0.f : g1;
-      }
-      g[q] = g0;
-      g[q + 1] = g1;
-    }
-  }
-  // the positive entry q of this chunk: margin form (margin.hpp:41-72), fp64
-  __device__ __forceinline__ void patch_positive(const float (&v)[32], float (&g)[32], int q,
-                                                 double gm, double ig) const {
-    float vq = 0.f;
-#pragma unroll
-    for (int u = 0; u < 32; ++u) vq = (u == q) ? v[u] : vq;
-    const double z = margin_pos(mg, (double)vq);
-    const double p = exp(z - gm) * ig;
-    const double gq = (p - 1.0) * (double)inv_batch * margin_deriv_pos(mg, (double)vq);
-#pragma unroll
-    for (int u = 0; u < 32; ++u) g[u] = (u == q) ? (float)gq : g[u];
-  }
-
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t* smem, const Pre& pre) const {
+                                      uint8_t* smem, const Pre&) const {
     constexpr int CW = BN / NWG;
-    const int cb = wg * CW;
-    const int j = t.row0 + row;
-    const bool rv = j < ncols;
-    ST cp = ST(0);
-    if constexpr (kTma) {
-      static_assert(CW == 128, "warp-private staging assumes 128 columns per warpgroup");
-      const int wig = row >> 5, lane = row & 31;
-      uint8_t* ws = smem + wig * kWarpBytes;
-      uint8_t* stage = ws;                                   // 4 x [32 rows][64 B]
-      float2* cf = reinterpret_cast<float2*>(ws + 8192);     // [128]
-      uint8_t* prow = ws + 9216;                             // [128]
-      __syncwarp();  // lanes finished reading the previous tile's constants
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        cf[lane + 32 * i] = pre.k[i];
-        const int pr = pre.pc[i] - t.row0;
-        prow[lane + 32 * i] = (uint8_t)((unsigned)pr < 128u ? pr : 0xFF);
-      }
-      __syncwarp();
-      const uint32_t rowx4 = 0x01010101u * (uint32_t)row;
-#pragma unroll 1
-      for (int kk = 0; kk < CW / 32; ++kk) {
-        const int c0 = cb + kk * 32;
-        float v[32];
-        src.load(c0, v);
-        const int colb = t.col0 + c0;
-        uint8_t* sb = stage + kk * 2048;
-        if (colb < B) {  // uniform
-          float g[32];
-          grad32(v, cf + kk * 32, g);
-          const uint4* pw = reinterpret_cast<const uint4*>(prow + kk * 32);
-          const uint4 p0 = pw[0], p1 = pw[1];
-          const uint32_t hit = __vcmpeq4(p0.x, rowx4) | __vcmpeq4(p0.y, rowx4) |
-                               __vcmpeq4(p0.z, rowx4) | __vcmpeq4(p0.w, rowx4) |
-                               __vcmpeq4(p1.x, rowx4) | __vcmpeq4(p1.y, rowx4) |
-                               __vcmpeq4(p1.z, rowx4) | __vcmpeq4(p1.w, rowx4);
-          if (hit) {
-#pragma unroll 1
-            for (int q = 0; q < 32; ++q)
-              if (prow[kk * 32 + q] == (uint8_t)row)
-                patch_positive(v, g, q, (double)gmax[colb + q], (double)inv_gsum[colb + q]);
-          }
-          // rows j >= ncols (last class tile) are clipped by the TMA store and not accumulated
-          float c1 = 0.f, c2 = 0.f;
-#pragma unroll
-          for (int q = 0; q < 32; q += 2) {
-            c1 = fmaf(g[q], v[q], c1);
-            c2 = fmaf(g[q + 1], v[q + 1], c2);
-          }
-          cp += (ST)(c1 + c2);
-          uint32_t w[16];
-          pack_bf16x32(g, w);
-          if (lane == 0) pfc_sm100::bulk_wait_read<3>();  // this buffer's store, 4 groups ago
-          __syncwarp();
-          const int sw = (lane >> 1) & 3;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq)
-            *reinterpret_cast<uint4*>(sb + lane * 64 + ((qq ^ sw) << 4)) =
-                make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
-          pfc_sm100::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) pfc_sm100::tma_store_2d(&tm, sb, colb, t.row0 + wig * 32);
-        }
-        if (lane == 0) pfc_sm100::bulk_commit();  // one group per chunk (possibly empty)
-      }
-    } else {
-      // SIMT engine (fp32 validation): block-wide constants, plain stores
-      const uint32_t bar = 1 + wg;
-      float2* cf = reinterpret_cast<float2*>(smem);
-      ST* cg = reinterpret_cast<ST*>(cf + CW);
-      ST* ci = cg + CW;
-      int* pcs = reinterpret_cast<int*>(ci + CW);
-      pfc_sm100::named_bar_sync(bar, 128);
-      for (int i = row; i < CW; i += 128) {
-        const int b = t.col0 + cb + i;
-        ST gm = ST(0), ig = ST(0);
-        int pc = -1;
-        if (b < B) {
-          gm = gmax[b];
-          ig = inv_gsum[b];
-          pc = pos_col[b];
-        }
-        cf[i] = make_float2((float)gm * kLog2e, (float)(mg.sd * (double)ig * (double)inv_batch));
-        cg[i] = gm;
-        ci[i] = ig;
-        pcs[i] = pc;
-      }
-      pfc_sm100::named_bar_sync(bar, 128);
-#pragma unroll 1
-      for (int c0 = cb; c0 < cb + CW; c0 += 32) {
-        float v[32];
-        src.load(c0, v);
-        const int colb = t.col0 + c0;
-        if (colb >= B) continue;
-        const int lc = c0 - cb;
-        float g[32];
-        if constexpr (std::is_same<ST, float>::value) {
-          grad32(v, cf + lc, g);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            double gq = 0.0;
-            if (colb + q < B && !(kFilter && v[q] > tau)) {
-              const double p = exp((double)mg.s * (double)v[q] - (double)cg[lc + q]) * (double)ci[lc + q];
-              gq = p * (double)inv_batch * mg.sd;
-            }
-            g[q] = (float)gq;
-          }
-        }
-        for (int q = 0; q < 32; ++q)
-          if (pcs[lc + q] == j) patch_positive(v, g, q, (double)cg[lc + q], (double)ci[lc + q]);
-        if (!rv) {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) g[q] = 0.f;
-        }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) cp += (ST)g[q] * (ST)v[q];
-        GT* dst = Gt + (size_t)j * ldgt + colb;
-        if (colb + 32 <= B) {
-          store_g32(dst, g);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (colb + q < B) store_g1(dst + q, g[q]);
-        }
-      }
-    }
-    if (rv) cproj_part[(size_t)(t.n_tile * NWG + wg) * ncols + j] = cp;
-  }
-};
-
-template <typename ST, bool kVecD>
-struct DwUpdateEpi {
-  // per warp: transposed 32 x 32 chunk (stride 33) + 3 x 32 row scalars
-  static constexpr int kWarpFloats = 32 * 33 + 3 * 32;
-  static constexpr int kSmem = 4 * kWarpFloats * 4;
-  int ncols, D, n_parts;
-  const float* wnorm;       // [ncols]
-  const int32_t* lrow;      // [ncols] local row of W
-  const ST* cproj_part;     // [n_parts][ncols]
-  float* W;
-  float* Mom;
-  const StepParams* sp;  // lr of this step
-  float mu, wd;
-  const StepStatus* st;  // no update when the step failed (the reference throws before 412)
-  int cw;                // columns per warpgroup (BN / NWG), for prefetch
-  int pf_mode;           // 0 none, 1 current tile at epilogue start, 2 one tile ahead
-
-  struct Pre {
-    float inv, cp;
-    int r;
-  };
-  // the tile's per-row scalars: 1/|w|, center_proj (sum of partials), local W row
-  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int) const {
-    Pre p{0.f, 0.f, -1};
-    const int c = t.row0 + row;
-    if (c < ncols) {
-      const float n = wnorm[c];
-      p.inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
-      ST acc = ST(0);
-      for (int q = 0; q < n_parts; ++q) acc += cproj_part[(size_t)q * ncols + c];
-      p.cp = (float)acc;
-      p.r = lrow[c];
-    }
-    return p;
-  }
-  __device__ __forceinline__ void prefetch(const TileInfo& t, int row, int wg) const {
-    if (pf_mode == 2) prefetch_rows(t, row, wg);
-  }
-  __device__ __forceinline__ void prefetch_rows(const TileInfo& t, int row, int wg) const {
-    const int c = t.row0 + row;
-    if (c >= ncols) return;
-    const int r = lrow[c];
-    if (r < 0) return;
-    const int d0 = t.col0 + wg * cw;
-    if (d0 >= D) return;
-    const int dn = min(cw, D - d0);
-    const char* w = reinterpret_cast<const char*>(W + (size_t)r * D + d0);
-    const char* m = reinterpret_cast<const char*>(Mom + (size_t)r * D + d0);
-    for (int off = 0; off < dn * 4; off += 128) {
-      pfc_sm100::prefetch_l2(w + off);
-      pfc_sm100::prefetch_l2(m + off);
-    }
-  }
-  __device__ __forceinline__ void finish(int, int) const {}
-
-  __device__ __forceinline__ void update4(float4& w, float4& m, const float* a, float inv,
-                                          float cpj, float lr) const {
-    float wv[4] = {w.x, w.y, w.z, w.w};
-    float mv[4] = {m.x, m.y, m.z, m.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float dw = (a[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382
-      const float g = dw + wd * wv[e];                      // shardsim.hpp:152-153
-      const float vv = mu * mv[e] + g;                      // shardsim.hpp:154
-      mv[e] = vv;
-      wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
-    }
-    w = make_float4(wv[0], wv[1], wv[2], wv[3]);
-    m = make_float4(mv[0], mv[1], mv[2], mv[3]);
-  }
-
-  template <int BN, int NWG, class Src>
-  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t* smem, const Pre& pre) const {
-    constexpr int CW = BN / NWG;
+    const int b = t.row0 + row;
+    const bool rv = b < B;
+    const int pc = rv ? pos_col[b] : -1;
+    const float A = mg.s * kLog2e, O = mg.off * kLog2e;
     const int wig = row >> 5, lane = row & 31;
-    float* ws = reinterpret_cast<float*>(smem) + wig * kWarpFloats;
-    float* stage = ws;                 // [32][33]: row-of-warp x dim
-    float* s_inv = ws + 32 * 33;
-    float* s_cp = s_inv + 32;
-    int* s_row = reinterpret_cast<int*>(s_cp + 32);
-    if (pf_mode == 1) prefetch_rows(t, row, wg);
-    const bool failed = status_failed(st);
-    const float lr = sp->lr;
-    __syncwarp();  // the warp finished reading the previous tile's scalars
-    s_inv[lane] = pre.inv;
-    s_cp[lane] = pre.cp;
-    s_row[lane] = failed ? -1 : pre.r;
-    __syncwarp();
-    const int sub = lane >> 3, q4 = (lane & 7) * 4;  // 4 rows x 8 lanes x float4 per warp op
-    int rw[8];
-    float rinv[8], rcp[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = u * 4 + sub;
-      rw[u] = s_row[r];
-      rinv[u] = s_inv[r];
-      rcp[u] = s_cp[r];
-    }
+    uint8_t* stage = smem + wig * kWarpBytes;
+    ST sum = ST(0);
+    bool any = false;
+    int kk = 0;
 #pragma unroll 1
-    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32, ++kk) {
       float v[32];
       src.load(c0, v);
-      const int d = t.col0 + c0 + q4;
-      if (kVecD && t.col0 + c0 >= D) continue;  // uniform
-      __syncwarp();
+      const int colb = t.col0 + c0;
+      if (colb >= ncols) {  // uniform: past the buffer (an empty group keeps the TMA ring even)
+        if (kTma && lane == 0) pfc_sm100::bulk_commit();
+        continue;
+      }
+      float e[32];
+      const int jp = pc - colb;
+      bool done = false;
+      if constexpr (std::is_same<ST, float>::value && !kFilter) {
+        if (colb + 32 <= ncols && (unsigned)jp >= 32u) {  // 32 valid negatives
+          float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
-      __syncwarp();
-      if constexpr (kVecD) {
-        float4 w[8], mo[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (rw[u] >= 0) {
-            const size_t o = (size_t)rw[u] * D + d;
-            w[u] = *reinterpret_cast<const float4*>(W + o);
-            mo[u] = *reinterpret_cast<const float4*>(Mom + o);
+          for (int q = 0; q < 32; q += 2) {
+            e[q] = pfc_sm100::ex2_approx(fmaf(v[q], A, -O));
+            e[q + 1] = pfc_sm100::ex2_approx(fmaf(v[q + 1], A, -O));
+            s1 += e[q];
+            s2 += e[q + 1];
           }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (rw[u] >= 0) {
-            update4(w[u], mo[u], stage + (u * 4 + sub) * 33 + q4, rinv[u], rcp[u], lr);
-            const size_t o = (size_t)rw[u] * D + d;
-            *reinterpret_cast<float4*>(Mom + o) = mo[u];
-            *reinterpret_cast<float4*>(W + o) = w[u];
-          }
-      } else {
-        // generic D: scalar lanes over the chunk's 32 dims, one row per iteration
-        const int dd = t.col0 + c0 + lane;
-        if (dd < D) {
-          for (int r = 0; r < 32; ++r) {
-            const int wr = s_row[r];
-            if (wr < 0) continue;
-            const size_t o = (size_t)wr * D + dd;
-            float4 w4 = make_float4(W[o], 0.f, 0.f, 0.f), m4 = make_float4(Mom[o], 0.f, 0.f, 0.f);
-            float a[4] = {stage[r * 33 + lane], 0.f, 0.f, 0.f};
-            update4(w4, m4, a, s_inv[r], s_cp[r], lr);
-            Mom[o] = m4.x;
-            W[o] = w4.x;
-          }
+          sum += s1 + s2;
+          any = true;
+          done = true;
         }
       }
+      if (!done) {
+        // bounds, filter mask (shardsim.hpp:258-268), the positive's margin (margin.hpp:41-54)
+        ST acc = ST(0);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const bool masked = (colb + q >= ncols) || (kFilter && q != jp && v[q] > tau);
+          ST eq;
+          if constexpr (std::is_same<ST, float>::value)
+            eq = pfc_sm100::ex2_approx(fmaf(v[q], A, -O));
+          else
+            eq = exp((double)mg.s * (double)v[q] - mg.offd);
+          eq = masked ? ST(0) : eq;
+          any = any || !masked;
+          e[q] = (float)eq;
+          if (q != jp) acc += eq;
+        }
+        if ((unsigned)jp < 32u) {
+          float vp = 0.f;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) vp = (q == jp) ? v[q] : vp;
+          const double zp = margin_pos(mg, (double)vp);
+          const double ep = exp(zp - mg.offd);
+          const float eps = round_to(E, (float)ep);
+          zpos[b] = zp;
+          cpos[b] = (double)vp;
+          epos[b] = eps;
+          acc += (ST)ep;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) e[q] = (q == jp) ? (float)ep : e[q];
+        }
+        sum += acc;
+      }
+      if constexpr (kTma) {
+        uint8_t* sb = stage + (kk & 1) * 2048;
+        uint32_t w[16];
+        pack_bf16x32(e, w);
+        if (lane == 0) pfc_sm100::bulk_wait_read<1>();  // this buffer's store, 2 groups ago
+        __syncwarp();
+        const int sw = (lane >> 1) & 3;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+          *reinterpret_cast<uint4*>(sb + lane * 64 + ((qq ^ sw) << 4)) =
+              make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
+        pfc_sm100::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          pfc_sm100::tma_store_2d(&tm, sb, colb, t.row0 + wig * 32);
+          pfc_sm100::bulk_commit();
+        }
+      } else if (rv) {
+        OT* dst = E + (size_t)b * lde + colb;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (colb + q < ncols) store_out1(dst + q, e[q]);
+      }
+    }
+    if (rv) {
+      part_s[(size_t)(t.n_tile * NWG + wg) * B + b] = sum;
+      if (kFilter && any) hasval[b] = 1;
     }
   }
 };
 
-struct DxPartEpi {
+// --------------------------------------------------------------------------------- DxPartEpi
+struct DxPartEpi : NoSetup {
   static constexpr int kSmem = 0;
   int B, D;
   float* part;  // [splits][B][D]
@@ -536,6 +217,224 @@ struct DxPartEpi {
         for (int j = 0; j < 32; ++j)
           if (d0 + j < D) dst[j] = v[j];
       }
+    }
+  }
+};
+
+// ------------------------------------------------------------------------------- DwUpdateEpi
+// Both warpgroups of a CTA cover its 256-dim half of the class block (128 dims each); with
+// kPair the two CTAs of a cluster own the two halves (D = 512) and swap half-dots.
+template <bool kPair>
+struct DwUpdateEpi {
+  static constexpr int kCluster = kPair ? 2 : 1;
+  static constexpr int kWarpFloats = 32 * 33 + 4 * 32;  // stage + inv/row/pslot/cproj
+  static constexpr int kWarpBytes = kWarpFloats * 4;
+  static constexpr int kSharedBytes = 3072 + 16;        // dotp[2][128], hloc/hrem[2][128], mbar
+  static constexpr int kSmem = ((4 * kWarpBytes + kSharedBytes + 1023) / 1024) * 1024;
+  int ncols, D;
+  const float* wnorm;       // [ncols]
+  const int32_t* lrow;      // [ncols] local row of W
+  const int32_t* pslot;     // [ncols] positive-correction slot or -1
+  const float* poscorr;     // [slots][D]: sum over rows with this label of delta_b x^_b
+  float* W;
+  float* Mom;
+  const StepParams* sp;     // lr of this step
+  float mu, wd;
+  const StepStatus* st;     // no update when the step failed (the reference throws before 412)
+
+  struct Pre {
+    float inv;
+    int r, ps;
+  };
+  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int) const {
+    Pre p{0.f, -1, -1};
+    const int c = t.row0 + row;
+    if (c < ncols) {
+      const float n = wnorm[c];
+      p.inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
+      p.r = lrow[c];
+      p.ps = pslot[c];
+    }
+    return p;
+  }
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void finish(int, int) const {}
+
+  // CTA-shared area (inside warpgroup 0's scratch, after its 4 warp areas)
+  __device__ __forceinline__ static uint8_t* shared_area(uint8_t* wg0) { return wg0 + 4 * kWarpBytes; }
+  __device__ __forceinline__ void setup(uint8_t* epi_base) const {
+    if constexpr (kPair) {
+      uint64_t* mbar = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 3072);
+      pfc_sm100::mbar_init(mbar, 128);
+    }
+  }
+
+  __device__ __forceinline__ void load_rows(const int (&rw)[8], int d, float4 (&w)[8]) const {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      w[u] = rw[u] >= 0 ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+
+  template <int BN, int NWG, class Src>
+  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
+                                      uint8_t* smem, const Pre& pre) const {
+    static_assert(NWG == 2 && BN == 256, "DwUpdateEpi: 2 warpgroups x 128 dims");
+    constexpr int CW = BN / NWG;
+    const int wig = row >> 5, lane = row & 31;
+    uint8_t* wg0 = smem - wg * kSmem;
+    float* ws = reinterpret_cast<float*>(smem + wig * kWarpBytes);
+    float* stage = ws;                 // [32][33]: warp row x dim
+    float* s_inv = ws + 32 * 33;
+    int* s_row = reinterpret_cast<int*>(s_inv + 32);
+    int* s_ps = s_row + 32;
+    float* s_cp = reinterpret_cast<float*>(s_ps + 32);
+    float* dotp = reinterpret_cast<float*>(shared_area(wg0));  // [2 wg][128]
+    float* hloc = dotp + 256;                                  // [2 parity][128] own half
+    float* hrem = hloc + 256;                                  // [2 parity][128] partner half
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(shared_area(wg0) + 3072);
+    const bool failed = status_failed(st);
+    const float lr = sp->lr;
+    __syncwarp();  // the warp finished with the previous tile's scalars
+    s_inv[lane] = pre.inv;
+    s_row[lane] = failed ? -1 : pre.r;
+    s_ps[lane] = pre.ps;
+    __syncwarp();
+    const int sub = lane >> 3, q4 = (lane & 7) * 4;  // 4 rows x 8 lanes x float4 per warp op
+    int rw[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) rw[u] = s_row[u * 4 + sub];
+    // ---- pass 1: partial dots w . dwt over this warpgroup's 128 dims
+    float dot[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dot[u] = 0.f;
+#pragma unroll 1
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
+      const int d = t.col0 + c0 + q4;
+      float4 w[8];
+      if (d < D) load_rows(rw, d, w);
+      float v[32];
+      src.load(c0, v);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
+      __syncwarp();
+      if (d >= D) continue;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (rw[u] < 0) continue;
+        const float* a = stage + (u * 4 + sub) * 33 + q4;
+        float a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3];
+        const int rp = s_ps[u * 4 + sub];
+        if (rp >= 0) {
+          const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)rp * D + d);
+          a0 += pc.x; a1 += pc.y; a2 += pc.z; a3 += pc.w;
+        }
+        dot[u] += a0 * w[u].x + a1 * w[u].y + a2 * w[u].z + a3 * w[u].w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 1);
+      dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 2);
+      dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 4);
+    }
+    __syncwarp();
+    if ((lane & 7) == 0) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s_cp[u * 4 + sub] = dot[u];
+    }
+    __syncwarp();
+    dotp[wg * 128 + row] = s_cp[lane];
+    pfc_sm100::named_bar_sync(3, 256);  // both warpgroups' halves of this CTA's 256 dims
+    float half = dotp[row] + dotp[128 + row];
+    const int par = t.iter & 1;
+    if constexpr (kPair) {
+      if (wg == 0) {
+        hloc[par * 128 + row] = half;
+        const uint32_t prank = pfc_sm100::cluster_ctarank() ^ 1u;
+        pfc_sm100::st_cluster_f32(
+            pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hrem + par * 128 + row), prank), half);
+        pfc_sm100::mbar_arrive_cluster(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(mbar), prank));
+      }
+      pfc_sm100::mbar_wait_cluster(mbar, (uint32_t)par);
+      pfc_sm100::named_bar_sync(3, 256);  // hloc written by warpgroup 0 is visible
+      half = hloc[par * 128 + row] + hrem[par * 128 + row];
+    }
+    __syncwarp();
+    s_cp[lane] = half * pre.inv;  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
+    __syncwarp();
+    // ---- pass 2: dW and the momentum-SGD update of the sampled rows
+#pragma unroll 1
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
+      const int d = t.col0 + c0 + q4;
+      float4 w[8], mo[8];
+      if (d < D) {
+        load_rows(rw, d, w);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          mo[u] = rw[u] >= 0 ? *reinterpret_cast<const float4*>(Mom + (size_t)rw[u] * D + d)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float v[32];
+      src.load(c0, v);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
+      __syncwarp();
+      if (d >= D) continue;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (rw[u] < 0) continue;
+        const float* a = stage + (u * 4 + sub) * 33 + q4;
+        float av[4] = {a[0], a[1], a[2], a[3]};
+        const int rp = s_ps[u * 4 + sub];
+        if (rp >= 0) {
+          const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)rp * D + d);
+          av[0] += pc.x; av[1] += pc.y; av[2] += pc.z; av[3] += pc.w;
+        }
+        float wv[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+        float mv[4] = {mo[u].x, mo[u].y, mo[u].z, mo[u].w};
+        const float inv = s_inv[u * 4 + sub], cpj = s_cp[u * 4 + sub];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float dw = (av[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382
+          const float g = dw + wd * wv[e];                      // shardsim.hpp:152-153
+          const float vv = mu * mv[e] + g;                      // shardsim.hpp:154
+          mv[e] = vv;
+          wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
+        }
+        const size_t o = (size_t)rw[u] * D + d;
+        *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+        *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+      }
+    }
+  }
+};
+
+// -------------------------------------------------------------------- DwStoreEpi (SIMT path)
+struct DwStoreEpi : NoSetup {
+  static constexpr int kSmem = 0;
+  int ncols, D;
+  float* dwt;  // [ncols][D]
+  struct Pre {};
+  __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void finish(int, int) const {}
+  template <int BN, int NWG, class Src>
+  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
+                                      uint8_t*, const Pre&) const {
+    constexpr int CW = BN / NWG;
+    const int j = t.row0 + row;
+#pragma unroll 1
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
+      float v[32];
+      src.load(c0, v);
+      const int d0 = t.col0 + c0;
+      if (j >= ncols || d0 >= D) continue;
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (d0 + q < D) dwt[(size_t)j * D + d0 + q] = v[q];
     }
   }
 };

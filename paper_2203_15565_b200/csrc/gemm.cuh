@@ -22,6 +22,7 @@ struct TileInfo {
   int m_tile, n_tile, split;
   int row0, col0;
   int kb0, kb1;
+  int iter;  // this CTA's tile counter (0, 1, 2, ...)
 };
 
 struct GemmGeom {
@@ -46,6 +47,7 @@ struct GemmGeom {
     ti.col0 = ti.n_tile * BN;
     ti.kb0 = ti.split * kb_per_split;
     ti.kb1 = ti.kb0 + kb_per_split < kb_total ? ti.kb0 + kb_per_split : kb_total;
+    ti.iter = 0;
     return ti;
   }
 };
@@ -123,12 +125,14 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 128 * NWG);
     }
+    epi.setup(epi_smem);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (Epi::kCluster > 1) cluster_sync_all();  // partner barriers initialised
   const uint32_t tmem_base = *tmem_slot;
   const int total = g.total();
 
@@ -201,7 +205,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     typename Epi::Pre pre{};
     if ((int)blockIdx.x < total) pre = epi.preload(g.tile(blockIdx.x), row, wg);
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-      const TileInfo ti = g.tile(t);
+      TileInfo ti = g.tile(t);
+      ti.iter = (int)it;
       const uint32_t as = it & 1, aph = (it >> 1) & 1;
       if (it == 0) epi.prefetch(ti, row, wg);
       typename Epi::Pre pre_next{};
@@ -221,6 +226,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     epi.finish(row, wg);
   }
   __syncthreads();
+  if constexpr (Epi::kCluster > 1) cluster_sync_all();  // no CTA leaves while its partner writes
   if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
 #endif
 }
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(128)
   float* sAcc = sB + KC * BN;                       // [128][65]
   uint8_t* epi_smem = reinterpret_cast<uint8_t*>(sAcc + 128 * 65);
   const int tid = threadIdx.x;
-  const TileInfo ti = g.tile(blockIdx.x);
+  TileInfo ti = g.tile(blockIdx.x);
   float acc[BN];
 #pragma unroll
   for (int j = 0; j < BN; ++j) acc[j] = 0.f;

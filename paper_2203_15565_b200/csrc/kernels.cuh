@@ -22,14 +22,17 @@ __global__ void step_begin_kernel(StepStatus* st, StepParams* sp, uint64_t seed,
   sp->labels = labels;
   sp->dx = dx;
   const bool sticky = !reset && (sampler_failed(st) || st->masked_row != 0x7fffffff ||
-                                 st->nonfinite_loss || st->nonfinite_dx);
+                                 st->nonfinite_loss || st->nonfinite_dx ||
+                                 st->underflow_row != 0x7fffffff);
   sp->seed = seed;
   sp->stream = stream;
+  sp->step_id += 1;
   sp->lr = sticky ? 0.f : lr;
   if (sticky) return;
   StepStatus s{};
   s.capacity_shard = -1;
   s.masked_row = 0x7fffffff;
+  s.underflow_row = 0x7fffffff;
   *st = s;
 }
 
@@ -104,9 +107,10 @@ __global__ void gather_w_kernel(const float* __restrict__ W, int D, int Dp,
                                 const int32_t* __restrict__ buf_cls, int ncols, int ncols_pad,
                                 int64_t cls_lo, int64_t rows, OT* __restrict__ wh,
                                 float* __restrict__ wnorm, int32_t* __restrict__ lrow,
-                                const StepStatus* st) {
+                                int32_t* __restrict__ pslot, const StepStatus* st) {
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c >= ncols_pad) return;
+  if (lane == 0 && c < ncols) pslot[c] = -1;
   OT* o = wh + (size_t)c * Dp;
   int64_t r = -1;
   if (c < ncols && !sampler_failed(st)) {
@@ -163,97 +167,140 @@ __global__ void gather_w_kernel(const float* __restrict__ W, int D, int Dp,
   }
 }
 
-// Merge the per-column-tile (max, sumexp) partials of each row into one (max, sum) pair.
-// Pass 1: grid (rows/128, segments); thread = row b, coalesced over b, loops its segment of
-// tiles.  Pass 2: thread = row, folds the segments in order.
+// Sum the per-(column slice) sums of E = exp(z - o) of each row, in a fixed order.
+// Pass 1: grid (rows/128, segments), thread = row (coalesced over b); pass 2: thread = row.
 constexpr int kMergeSegs = 64;
 template <typename ST>
-__global__ void __launch_bounds__(128) merge_tiles_kernel(const ST* __restrict__ pm,
-                                                          const ST* __restrict__ ps, int T, int B,
-                                                          ST* __restrict__ sm, ST* __restrict__ ss) {
+__global__ void __launch_bounds__(128) sum_slices_kernel(const ST* __restrict__ ps, int T, int B,
+                                                         ST* __restrict__ seg) {
   const int b = blockIdx.x * 128 + threadIdx.x;
   if (b >= B) return;
   const int per = (T + gridDim.y - 1) / gridDim.y;
   const int t0 = blockIdx.y * per, t1 = min(T, t0 + per);
-  ST m = -INFINITY;
-  // pass A: max (independent loads, 4 in flight)
+  ST s0 = 0, s1 = 0, s2 = 0, s3 = 0;
   int t = t0;
   for (; t + 4 <= t1; t += 4) {
-    const ST a0 = pm[(size_t)t * B + b], a1 = pm[(size_t)(t + 1) * B + b];
-    const ST a2 = pm[(size_t)(t + 2) * B + b], a3 = pm[(size_t)(t + 3) * B + b];
-    m = fmax(m, fmax(fmax(a0, a1), fmax(a2, a3)));
+    s0 += ps[(size_t)t * B + b];
+    s1 += ps[(size_t)(t + 1) * B + b];
+    s2 += ps[(size_t)(t + 2) * B + b];
+    s3 += ps[(size_t)(t + 3) * B + b];
   }
-  for (; t < t1; ++t) m = fmax(m, pm[(size_t)t * B + b]);
-  ST s = 0;
-  if (m != (ST)-INFINITY) {
-    for (t = t0; t + 4 <= t1; t += 4) {
-      ST acc = 0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const ST mt = pm[(size_t)(t + u) * B + b], st = ps[(size_t)(t + u) * B + b];
-        acc += (mt == (ST)-INFINITY) ? ST(0) : st * fast_exp(mt - m);
-      }
-      s += acc;
-    }
-    for (; t < t1; ++t) {
-      const ST mt = pm[(size_t)t * B + b];
-      if (mt != (ST)-INFINITY) s += ps[(size_t)t * B + b] * fast_exp(mt - m);
-    }
-  }
-  sm[(size_t)blockIdx.y * B + b] = m;
-  ss[(size_t)blockIdx.y * B + b] = s;
+  for (; t < t1; ++t) s0 += ps[(size_t)t * B + b];
+  seg[(size_t)blockIdx.y * B + b] = (s0 + s1) + (s2 + s3);
 }
-// warp per row: lanes over segments, then a warp reduction
 template <typename ST>
-__global__ void merge_segments_kernel(const ST* __restrict__ sm, const ST* __restrict__ ss,
-                                      int nseg, int B, ST* __restrict__ lm, ST* __restrict__ ls) {
-  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__global__ void sum_segments_kernel(const ST* __restrict__ seg, int nseg, int B,
+                                    ST* __restrict__ ls) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  ST m = -INFINITY;
-  for (int i = lane; i < nseg; i += 32) m = fmax(m, sm[(size_t)i * B + b]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  ST s = 0;
-  if (m != (ST)-INFINITY)
-    for (int i = lane; i < nseg; i += 32) {
-      const ST mi = sm[(size_t)i * B + b];
-      if (mi != (ST)-INFINITY) s += ss[(size_t)i * B + b] * fast_exp(mi - m);
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
-    lm[b] = m;
-    ls[b] = s;
-  }
+  double s = 0.0;
+  for (int i = 0; i < nseg; ++i) s += (double)seg[(size_t)i * B + b];
+  ls[b] = (ST)s;
 }
 
-// Cross-rank merge in ascending rank order (collectives 1 and 2, shardsim.hpp:284-338),
-// per-row loss terms, and the "all columns masked" contract check.
+// Cross-rank sum in ascending rank order (collectives 1 + 2, shardsim.hpp:284-338), the loss
+// terms, the row scale of G and the positive's correction:
+//   S = sum_r ls[r];  loss_b = log S + o - z_pos;  rowscale = s / (B S)
+//   delta_b = ((p_pos - 1)/B) margin'(c_pos) - rowscale * E_pos(stored)   (owner rank only)
 template <typename ST>
-__global__ void merge_ranks_kernel(const ST* __restrict__ lm, const ST* __restrict__ ls, int R,
-                                   int B, const double* __restrict__ zpos, ST* __restrict__ gmax,
-                                   ST* __restrict__ inv_gsum, double* __restrict__ loss_row,
-                                   StepStatus* st) {
+__global__ void finalize_stats_kernel(const ST* __restrict__ ls, int R, int B,
+                                      const double* __restrict__ zpos,
+                                      const double* __restrict__ cpos,
+                                      const float* __restrict__ epos,
+                                      const int32_t* __restrict__ pos_col,
+                                      const int* __restrict__ hasval, int has_filter,
+                                      MarginDev mg, ST* __restrict__ rowscale,
+                                      ST* __restrict__ delta, double* __restrict__ loss_row,
+                                      StepStatus* st) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   if (sampler_failed(st)) return;
-  ST m = -INFINITY;
-  for (int r = 0; r < R; ++r) m = fmax(m, lm[(size_t)r * B + b]);
-  if (!(m > (ST)-INFINITY)) {
+  rowscale[b] = 0;
+  delta[b] = 0;
+  loss_row[b] = 0;
+  if (has_filter && hasval[b] == 0) {  // every buffer column masked (shardsim.hpp:294-297)
     atomicMin(&st->masked_row, b);
-    gmax[b] = 0;
-    inv_gsum[b] = 0;
-    loss_row[b] = 0;
     return;
   }
-  double s = 0.0;
-  for (int r = 0; r < R; ++r) {
-    const ST mr = lm[(size_t)r * B + b];
-    if (mr != (ST)-INFINITY) s += (double)ls[(size_t)r * B + b] * exp((double)mr - (double)m);
+  double S = 0.0;
+  for (int r = 0; r < R; ++r) S += (double)ls[(size_t)r * B + b];
+  if (!(S > 1e-30) || !isfinite(S)) {
+    atomicMin(&st->underflow_row, b);
+    return;
   }
-  gmax[b] = m;
-  inv_gsum[b] = (ST)(1.0 / s);
-  loss_row[b] = log(s) + (double)m - zpos[b];
+  const double invB = 1.0 / (double)B;
+  const double rs = mg.sd * invB / S;
+  rowscale[b] = (ST)rs;
+  loss_row[b] = log(S) + mg.offd - zpos[b];
+  if (pos_col[b] >= 0) {
+    const double p = exp(zpos[b] - mg.offd) / S;
+    const double g = (p - 1.0) * invB * margin_deriv_pos(mg, cpos[b]);
+    delta[b] = (ST)(g - (double)(ST)rs * (double)epos[b]);
+  }
+}
+
+// rowscale_b * x^_b in the GEMM operand type: the dW GEMM's B operand (G = diag(rowscale) E).
+template <typename ST, typename OT>
+__global__ void xs_kernel(const StepParams* __restrict__ sp, const float* __restrict__ xnorm,
+                          const ST* __restrict__ rowscale, int B, int D, int Dp,
+                          OT* __restrict__ xs) {
+  const int b = blockIdx.x;
+  const float* x = sp->x + (size_t)b * D;
+  const float n = xnorm[b];
+  const float inv = (float)(1.0 / (double)(n > 1e-12f ? n : 1e-12f));
+  const ST rs = rowscale[b];
+  OT* o = xs + (size_t)b * Dp;
+  for (int d = threadIdx.x; d < Dp; d += blockDim.x)
+    store_out(o + d, d < D ? (float)(rs * (ST)(x[d] * inv)) : 0.f);
+}
+
+// Positive corrections of dwt: poscorr[slot(j)] = sum over rows b with pos_col[b] == j (in
+// ascending b) of delta_b x^_b; pslot[j] = slot for this step's positive columns.
+__global__ void __launch_bounds__(256) poscorr_kernel(
+    const ShardMeta* __restrict__ meta, int cap, int pmax, const int32_t* __restrict__ pos_col,
+    int B, const StepParams* __restrict__ sp, const float* __restrict__ xnorm, int D,
+    const float* __restrict__ delta_f, const double* __restrict__ delta_d,
+    float* __restrict__ poscorr, int32_t* __restrict__ pslot, const StepStatus* st) {
+  const int kk = blockIdx.y, i = blockIdx.x;
+  if (sampler_failed(st)) return;
+  if (i >= meta[kk].npos) return;
+  const int col = kk * cap + i, slot = kk * pmax + i;
+  __shared__ int rows[256];
+  __shared__ int nrows;
+  __shared__ int warp_cnt[8];
+  if (threadIdx.x == 0) nrows = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < B; b0 += 256) {  // ordered compaction of matching rows
+    const int b = b0 + threadIdx.x;
+    const bool hit = b < B && pos_col[b] == col;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) warp_cnt[w] = __popc(m);
+    __syncthreads();
+    int before = nrows;
+    for (int q = 0; q < w; ++q) before += warp_cnt[q];
+    if (hit && before + __popc(m & ((1u << lane) - 1)) < 256) rows[before + __popc(m & ((1u << lane) - 1))] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = nrows;
+      for (int q = 0; q < 8; ++q) tot += warp_cnt[q];
+      nrows = min(tot, 256);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pslot[col] = slot;
+  const int nr = nrows;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+    for (int q = 0; q < nr; ++q) {
+      const int b = rows[q];
+      const float n = xnorm[b];
+      const float xh = sp->x[(size_t)b * D + d] * (1.0f / (n > 1e-12f ? n : 1e-12f));
+      const float dl = delta_f ? delta_f[b] : (float)delta_d[b];
+      acc += dl * xh;
+    }
+    poscorr[(size_t)slot * D + d] = acc;
+  }
 }
 
 // loss = mean_b loss_row[b] in a fixed order (one CTA, deterministic).
@@ -268,7 +315,8 @@ __global__ void loss_reduce_kernel(const double* __restrict__ loss_row, int B, S
     double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     v = warp_sum(v);
     if (threadIdx.x == 0) {
-      if (sampler_failed(st) || st->masked_row != 0x7fffffff) return;
+      if (sampler_failed(st) || st->masked_row != 0x7fffffff || st->underflow_row != 0x7fffffff)
+        return;
       const double loss = v / (double)B;
       st->loss = loss;
       if (!isfinite(loss)) st->nonfinite_loss = 1;
@@ -276,19 +324,35 @@ __global__ void loss_reduce_kernel(const double* __restrict__ loss_row, int B, S
   }
 }
 
-// dX = (r - feat_proj * x^) / max(|x|, 1e-12)  (shardsim.hpp:371-375), r = sum_split part.
-// feat_proj_b = sum_j g_bj c_bj = x^_b . r_b since c_bj = x^_b . w^_j (exact identity).
-template <int D_PER_THREAD>
-__global__ void __launch_bounds__(256) dx_finalize_kernel(const float* __restrict__ part, int S,
-                                                          const StepParams* __restrict__ sp,
-                                                          const float* __restrict__ xnorm, int B,
-                                                          int D, StepStatus* st) {
+// dX = (r - feat_proj * x^) / max(|x|, 1e-12)  (shardsim.hpp:371-375) with
+//   r = rowscale_b * sum_split part + delta_b w^_pos(b)    (G = diag(rowscale) E + positive)
+//   feat_proj_b = sum_j g_bj c_bj = x^_b . r_b              (c_bj = x^_b . w^_j, exact identity)
+template <int D_PER_THREAD, typename ST>
+__global__ void __launch_bounds__(256) dx_finalize_kernel(
+    const float* __restrict__ part, int S, const StepParams* __restrict__ sp,
+    const float* __restrict__ xnorm, const ST* __restrict__ rowscale,
+    const ST* __restrict__ delta, const int32_t* __restrict__ pos_col,
+    const int32_t* __restrict__ lrow, const float* __restrict__ wnorm,
+    const float* __restrict__ W, int B, int D, StepStatus* st) {
   const int b = blockIdx.x;
+  __shared__ double red[8];
   const float* __restrict__ X = sp->x;
   float* __restrict__ dX = sp->dx;
-  __shared__ double red[8];
   const float n = xnorm[b];
   const float inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
+  const float rs = (float)rowscale[b];
+  const float dl = (float)delta[b];
+  const int pc = pos_col[b];
+  const float* wpos = nullptr;
+  float winv = 0.f;
+  if (pc >= 0 && dl != 0.f) {
+    const int r = lrow[pc];
+    if (r >= 0) {
+      wpos = W + (size_t)r * D;
+      const float wn = wnorm[pc];
+      winv = 1.0f / (wn > 1e-12f ? wn : 1e-12f);
+    }
+  }
   float r[D_PER_THREAD], xh[D_PER_THREAD];
   double dot = 0.0;
 #pragma unroll
@@ -298,6 +362,8 @@ __global__ void __launch_bounds__(256) dx_finalize_kernel(const float* __restric
     xh[i] = 0.f;
     if (d < D) {
       for (int s = 0; s < S; ++s) acc += part[((size_t)s * B + b) * D + d];
+      acc *= rs;
+      if (wpos) acc += dl * (wpos[d] * winv);
       xh[i] = X[(size_t)b * D + d] * inv;
     }
     r[i] = acc;
@@ -320,6 +386,48 @@ __global__ void __launch_bounds__(256) dx_finalize_kernel(const float* __restric
     }
   }
   if (bad && !sampler_failed(st)) st->nonfinite_dx = 1;
+}
+
+// fp32 validation path: finish the sampled rows from the stored dwt (warp per class):
+// center_proj = w^ . dwt, dW = (dwt - center_proj w^)/|w|, momentum-SGD (shardsim.hpp:139-159).
+__global__ void dw_rows_update_kernel(const float* __restrict__ dwt, const int32_t* __restrict__ lrow,
+                                      const float* __restrict__ wnorm,
+                                      const int32_t* __restrict__ pslot,
+                                      const float* __restrict__ poscorr, int ncols, int D,
+                                      float* __restrict__ W, float* __restrict__ Mom,
+                                      const StepParams* __restrict__ sp, float mu, float wd,
+                                      const StepStatus* st) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (c >= ncols) return;
+  if (sampler_failed(st) || st->masked_row != 0x7fffffff || st->nonfinite_loss ||
+      st->nonfinite_dx || st->underflow_row != 0x7fffffff)
+    return;
+  const int r = lrow[c];
+  if (r < 0) return;
+  const int ps = pslot[c];
+  const float n = wnorm[c];
+  const double inv = 1.0 / (double)(n > 1e-12f ? n : 1e-12f);
+  float* w = W + (size_t)r * D;
+  float* m = Mom + (size_t)r * D;
+  double dot = 0.0;
+  for (int d = lane; d < D; d += 32) {
+    double a = dwt[(size_t)c * D + d];
+    if (ps >= 0) a += poscorr[(size_t)ps * D + d];
+    dot += a * (double)w[d];
+  }
+  dot = warp_sum(dot);
+  const double cp = dot * inv;
+  const float lr = sp->lr;
+  for (int d = lane; d < D; d += 32) {
+    double a = dwt[(size_t)c * D + d];
+    if (ps >= 0) a += poscorr[(size_t)ps * D + d];
+    const float wv = w[d];
+    const float dw = (float)((a - cp * ((double)wv * inv)) * inv);
+    const float g = dw + wd * wv;
+    const float vv = mu * m[d] + g;
+    m[d] = vv;
+    w[d] = wv - lr * vv;
+  }
 }
 
 // SeededRng::next_normal (rng.hpp:77-81) from its two draws.

@@ -5,11 +5,11 @@
 //   [NCCL all-gather labels, X]  (world > 1)
 //   sampler (bit-exact build_buffers)                 sampler.cu
 //   normalise X, gather+normalise sampled W rows      kernels.cuh
-//   logits GEMM + margin + online softmax partials    tcgen05 GEMM, FwdStatsEpi
-//   merge partials [NCCL all-gather of (max,sum), all-reduce z_pos]  -> loss
-//   recompute logits GEMM -> G, feat/center proj      tcgen05 GEMM, GradEpi
-//   dX = G W^ (split-K) + correction [NCCL reduce-scatter]   tcgen05 GEMM, DxPartEpi
-//   dW = G^T X^ -> fused sparse momentum-SGD          tcgen05 GEMM, DwUpdateEpi
+//   logits GEMM + margin -> E = exp(z - o) + row sums  tcgen05 GEMM, FwdEpi
+//   row sums [NCCL all-gather, all-reduce z_pos] -> loss, rowscale, positive correction
+//   dX = rowscale E W^ (split-K) + corrections [NCCL reduce-scatter]  tcgen05 GEMM, DxPartEpi
+//   dW = E^T (rowscale X^) -> center_proj (2-CTA DSMEM) -> fused sparse momentum-SGD
+//                                                      tcgen05 GEMM, DwUpdateEpi
 //
 // mirroring pfc::distributed_partial_step (proj/include/pfc/shardsim.hpp:166-420).
 #include <cuda.h>
@@ -41,7 +41,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct {
   char internal[128];
 } ncclUniqueId;
-enum { ncclInt8 = 0, ncclInt64 = 4, ncclFloat32 = 7, ncclFloat64 = 8 };
+enum { ncclInt8 = 0, ncclInt32 = 2, ncclInt64 = 4, ncclFloat32 = 7, ncclFloat64 = 8 };
 enum { ncclSum = 0 };
 struct Nccl {
   void* h = nullptr;
@@ -158,20 +158,24 @@ struct Ctx {
   void* wh = nullptr;  // [ncols_pad][Dp]
   float* wnorm = nullptr;
   int32_t* lrow = nullptr;
-  // softmax statistics
-  void* part_m = nullptr;  // [T][maxB]
-  void* part_s = nullptr;
-  void* seg_m = nullptr;   // [kMergeSegs][maxB]
-  void* seg_s = nullptr;
-  void* lm = nullptr;      // [R][maxB]
-  void* ls = nullptr;
-  void* gmax = nullptr;
-  void* inv_gsum = nullptr;
+  // softmax statistics (fixed-offset form, see epilogues.cuh)
+  void* part_s = nullptr;  // [T * NWG][maxB] sums of E per column slice
+  void* seg_s = nullptr;   // [kMergeSegs][maxB]
+  void* ls = nullptr;      // [R][maxB] rank-local sums
+  void* rowscale = nullptr;
+  void* delta = nullptr;
   double* zpos = nullptr;
+  double* cpos = nullptr;
+  float* epos = nullptr;
+  int* hasval = nullptr;
   double* loss_row = nullptr;
   // backward
-  void* G = nullptr;       // G^T [ncols_pad][ldg] (ldg = maxB rounded to 8)
-  void* cproj = nullptr;   // [mt][ncols]
+  void* G = nullptr;       // E [maxB][lde]: exp(z - o) (bf16 / fp32)
+  void* xs = nullptr;      // [maxB][Dp] rowscale * x^
+  float* poscorr = nullptr;  // [nk * pmax][D]
+  int32_t* pslot = nullptr;  // [ncols]
+  float* dwt = nullptr;      // fp32 validation path: [ncols][D]
+  int64_t pmax = 1;
   float* dx_part = nullptr;  // [S][maxB][D]
   float* dX = nullptr;       // [maxB][D]
   int max_splits = 1;
@@ -190,7 +194,7 @@ struct Ctx {
   int64_t glaunches = 0;
   // tensor maps cached per batch
   int64_t tm_B = -1;
-  CUtensorMap tm_x_k, tm_w_k, tm_w_k128, tm_x_k256, tm_gt_k, tm_x_mn, tm_gt_mn, tm_w_mn, tm_gt_st;
+  CUtensorMap tm_x_k, tm_w_k, tm_e_st, tm_e_k, tm_w_mn, tm_e_mn, tm_xs_mn;
   // nccl
   ncclComm_t comm = nullptr;
   // bookkeeping
@@ -260,11 +264,31 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
     configured = true;
   }
   const int total = g.total();
-  const int grid = total < c->num_sms ? total : c->num_sms;
+  int grid = total < c->num_sms ? total : c->num_sms;
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, 128 + 128 * NWG, smem, c->stream>>>(ta, tb, g, epi);
-  c->launches++;
-  return cudaGetLastError();
+  if constexpr (Epi::kCluster > 1) {
+    // 2-CTA clusters: CTAs (2i, 2i+1) own the two dim halves of the same class blocks
+    grid = (c->num_sms / 2) * 2;
+    if (grid > total) grid = total;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(128 + 128 * NWG);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = Epi::kCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    c->launches++;
+    return cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epi);
+  } else {
+    kern<<<grid, 128 + 128 * NWG, smem, c->stream>>>(ta, tb, g, epi);
+    c->launches++;
+    return cudaGetLastError();
+  }
 }
 
 template <bool A_MN, bool B_MN, class Epi>
@@ -287,20 +311,18 @@ cudaError_t launch_simt(Ctx* c, const float* A, int lda, const float* Bm, int ld
 int ensure_maps(Ctx* c, int64_t B) {
   if (!c->bf16 || c->tm_B == B) return PFC_OK;
   bool ok = true;
-  // logits GEMM (M = b, N = classes): A = X^ [B][Dp], B = W^ [ncols][Dp], both K-major
+  // logits GEMM (M = b, N = classes): A = X^ [B][Dp], B = W^ [ncols][Dp], both K-major;
+  // its epilogue stores E [B][ncols] (per-warp box 32 classes x 32 rows, 64B swizzle)
   ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128);
   ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kBN);
-  // G GEMM (M = classes, N = b): A = W^ K-major, B = X^ K-major
-  ok &= make_map(&c->tm_w_k128, c->wh, c->Dp, c->ncols, c->Dp, 128);
-  ok &= make_map(&c->tm_x_k256, c->xh, c->Dp, B, c->Dp, kBN);
-  // dW GEMM (M = classes, N = d, K = b): A = G^T [ncols][ldg] K-major; B = X^ MN-major
-  ok &= make_map(&c->tm_gt_k, c->G, B, c->ncols, c->ldg, 128);
-  ok &= make_map(&c->tm_x_mn, c->xh, c->Dp, B, c->Dp, 64);
-  // dX GEMM (M = b, N = d, K = classes): A = G^T read MN-major (b contiguous); B = W^ MN-major
-  ok &= make_map(&c->tm_gt_mn, c->G, B, c->ncols, c->ldg, 64);
+  ok &= make_map(&c->tm_e_st, c->G, c->ncols, B, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  // dX GEMM (M = b, N = d, K = classes): A = E K-major; B = W^ MN-major (d contiguous)
+  ok &= make_map(&c->tm_e_k, c->G, c->ncols, B, c->ldg, 128);
   ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, 64);
-  // G GEMM epilogue store of G^T (per-warp box 32 b x 32 classes, 64B swizzle)
-  ok &= make_map(&c->tm_gt_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  // dW GEMM (M = classes, N = d, K = b): A = E read MN-major (classes contiguous);
+  // B = rowscale * x^ MN-major
+  ok &= make_map(&c->tm_e_mn, c->G, c->ncols, B, c->ldg, 64);
+  ok &= make_map(&c->tm_xs_mn, c->xs, c->Dp, B, c->Dp, 64);
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
   return PFC_OK;
@@ -364,19 +386,20 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
                                                                        (int)c->Dp, xh, c->xnorm);
   gather_w_kernel<OT><<<(unsigned)ceil_div(c->ncols_pad * 32, bs), bs, 0, s>>>(
       c->W, (int)c->D, (int)c->Dp, c->buf_cls, (int)c->ncols, (int)c->ncols_pad, c->cls_lo,
-      c->rows, wh, c->wnorm, c->lrow, c->st);
+      c->rows, wh, c->wnorm, c->lrow, c->pslot, c->st);
   c->launches += 2;
   CUDA_TRY(c, cudaGetLastError());
   phase(c, "gather");
   CUDA_TRY(c, cudaMemsetAsync(c->zpos, 0, sizeof(double) * B, s));
+  if (c->d.has_filter) CUDA_TRY(c, cudaMemsetAsync(c->hasval, 0, sizeof(int) * B, s));
 
   constexpr int BN = kUmma ? kBN : kSimtBN;
   constexpr int NWG = kUmma ? kNWG : 1;
-  ST* pm = static_cast<ST*>(c->part_m);
   ST* ps = static_cast<ST*>(c->part_s);
+  OT* E = static_cast<OT*>(c->G);
   const float tau = (float)c->d.filter_threshold;
   const bool filt = c->d.has_filter != 0;
-  // ---- logits GEMM + margin + online softmax partials (shardsim.hpp:249-318)
+  // ---- logits GEMM + margin + E = exp(z - o) and its per-slice row sums (shardsim.hpp:249-318)
   const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, BN, 1, 0);
   {
     cudaError_t err;
@@ -385,92 +408,101 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
       else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
                                             (const float*)c->wh, (int)c->Dp, gf, e);
     };
-    if (filt) err = go(FwdStatsEpi<ST, true>{(int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, ps, c->zpos});
-    else err = go(FwdStatsEpi<ST, false>{(int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, ps, c->zpos});
+    if (filt)
+      err = go(FwdEpi<ST, OT, true, kUmma>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
+                                           c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E});
+    else
+      err = go(FwdEpi<ST, OT, false, kUmma>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
+                                            c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E});
     CUDA_TRY(c, err);
   }
   phase(c, "logits_gemm");
-  // ---- softmax statistics: tiles -> rank-local, then across ranks (collectives 1 + 2)
-  const int T = gf.n_tiles * NWG;  // (max, sumexp) partial slots per row
-  ST* lm = static_cast<ST*>(c->lm);
+  // ---- softmax statistics: slices -> rank-local sum -> ranks (collectives 1 + 2) -> loss
+  const int T = gf.n_tiles * NWG;
   ST* ls = static_cast<ST*>(c->ls);
   {
     const int nseg = (int)std::min<int64_t>(kMergeSegs, T);
-    ST* segm = static_cast<ST*>(c->seg_m);
-    ST* segs = static_cast<ST*>(c->seg_s);
-    merge_tiles_kernel<ST><<<dim3((unsigned)ceil_div(B, 128), (unsigned)nseg), 128, 0, s>>>(
-        pm, ps, T, (int)B, segm, segs);
-    merge_segments_kernel<ST><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(
-        segm, segs, nseg, (int)B, lm + c->rank * B, ls + c->rank * B);
+    ST* seg = static_cast<ST*>(c->seg_s);
+    sum_slices_kernel<ST><<<dim3((unsigned)ceil_div(B, 128), (unsigned)nseg), 128, 0, s>>>(
+        ps, T, (int)B, seg);
+    sum_segments_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(seg, nseg, (int)B,
+                                                                     ls + c->rank * B);
     c->launches += 2;
   }
   if (c->R > 1) {
     const int dt = sizeof(ST) == 8 ? ncclFloat64 : ncclFloat32;
-    NCCL_TRY(c, g_nccl.AllGather(lm + c->rank * B, lm, B, dt, c->comm, s));
     NCCL_TRY(c, g_nccl.AllGather(ls + c->rank * B, ls, B, dt, c->comm, s));
     NCCL_TRY(c, g_nccl.AllReduce(c->zpos, c->zpos, B, ncclFloat64, ncclSum, c->comm, s));
+    if (filt) NCCL_TRY(c, g_nccl.AllReduce(c->hasval, c->hasval, B, ncclInt32, ncclSum, c->comm, s));
   }
-  ST* gm = static_cast<ST*>(c->gmax);
-  ST* ig = static_cast<ST*>(c->inv_gsum);
-  merge_ranks_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(lm, ls, c->R, (int)B, c->zpos,
-                                                                  gm, ig, c->loss_row, c->st);
+  ST* rsc = static_cast<ST*>(c->rowscale);
+  ST* dlt = static_cast<ST*>(c->delta);
+  finalize_stats_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(
+      ls, c->R, (int)B, c->zpos, c->cpos, c->epos, c->pos_col, c->hasval, filt ? 1 : 0, c->mg,
+      rsc, dlt, c->loss_row, c->st);
   loss_reduce_kernel<<<1, 1024, 0, s>>>(c->loss_row, (int)B, c->st);
-  c->launches += 2;
+  xs_kernel<ST, OT><<<(unsigned)B, 128, 0, s>>>(c->sp, c->xnorm, rsc, (int)B, (int)c->D,
+                                                (int)c->Dp, static_cast<OT*>(c->xs));
+  poscorr_kernel<<<dim3((unsigned)c->pmax, (unsigned)c->nk), 256, 0, s>>>(
+      c->meta, (int)c->cap, (int)c->pmax, c->pos_col, (int)B, c->sp, c->xnorm, (int)c->D,
+      std::is_same<ST, float>::value ? reinterpret_cast<const float*>(dlt) : nullptr,
+      std::is_same<ST, double>::value ? reinterpret_cast<const double*>(dlt) : nullptr,
+      c->poscorr, c->pslot, c->st);
+  c->launches += 4;
   CUDA_TRY(c, cudaGetLastError());
   phase(c, "softmax_stats");
-  // ---- G^T = dL/dcos (recomputed logits, M = classes, N = b) + center_proj partials
-  ST* cp = static_cast<ST*>(c->cproj);
-  const GemmGeom gg = make_geom((int)c->ncols, (int)B, (int)c->Dp, BN, 1, 1);
-  {
-    cudaError_t err;
-    auto go = [&](auto e) {
-      if constexpr (kUmma) return launch_umma<kBN, 3, kNWG, false, false>(c, c->tm_w_k128, c->tm_x_k256, gg, e);
-      else return launch_simt<false, false>(c, (const float*)c->wh, (int)c->Dp,
-                                            (const float*)c->xh, (int)c->Dp, gg, e);
-    };
-    OT* Gt = static_cast<OT*>(c->G);
-    const ST invB = (ST)(1.0 / (double)B);
-    if (filt) err = go(GradEpi<ST, OT, true, kUmma>{c->tm_gt_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
-    else err = go(GradEpi<ST, OT, false, kUmma>{c->tm_gt_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col, c->mg, tau, gm, ig, invB, Gt, cp});
-    CUDA_TRY(c, err);
-  }
-  phase(c, "grad_gemm");
-  // ---- dX = sum_j g_bj w^_j (split-K), then tangent projection / |x| (shardsim.hpp:363-376)
+  // ---- dX = rowscale * E W^ + delta w^_pos (split-K), tangent projection (shardsim.hpp:363-376)
   {
     const int S = dx_splits(c, B);
     const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0);
-    DxPartEpi e{(int)B, (int)c->D, c->dx_part};
+    DxPartEpi e{{}, (int)B, (int)c->D, c->dx_part};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, true, true>(c, c->tm_gt_mn, c->tm_w_mn, gx, e);
-    else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
-                                       (int)c->Dp, gx, e);
+    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, false, true>(c, c->tm_e_k, c->tm_w_mn, gx, e);
+    else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
+                                        (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
     const int dpt = (int)ceil_div(c->D, 256);
-    if (dpt <= 1) dx_finalize_kernel<1><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
-    else if (dpt <= 2) dx_finalize_kernel<2><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
-    else if (dpt <= 4) dx_finalize_kernel<4><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
-    else dx_finalize_kernel<8><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, (int)B, (int)c->D, c->st);
+#define PFC_FIN(N)                                                                               \
+  dx_finalize_kernel<N, ST><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, \
+                                                        rsc, dlt, c->pos_col, c->lrow, c->wnorm, \
+                                                        c->W, (int)B, (int)c->D, c->st)
+    if (dpt <= 1) PFC_FIN(1);
+    else if (dpt <= 2) PFC_FIN(2);
+    else if (dpt <= 4) PFC_FIN(4);
+    else PFC_FIN(8);
+#undef PFC_FIN
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
   }
   phase(c, "dx_gemm");
-  // ---- dW = sum_b g_bj x^_b, corrected, fused momentum-SGD on sampled rows (shardsim.hpp:377-417)
+  // ---- dwt = E^T (rowscale x^) + positive corrections; center_proj; fused momentum-SGD
   {
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
-    auto go = [&](auto e) {
-      if constexpr (kUmma) return launch_umma<kBN, 3, kNWG, false, true>(c, c->tm_gt_k, c->tm_x_mn, gw, e);
-      else return launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xh,
-                                           (int)c->Dp, gw, e);
-    };
     cudaError_t err;
-    if (c->D % 32 == 0)
-      err = go(DwUpdateEpi<ST, true>{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp,
-                                     c->W, c->M, c->sp, (float)c->d.momentum,
-                                     (float)c->d.weight_decay, c->st, BN / NWG, c->dw_prefetch});
-    else
-      err = go(DwUpdateEpi<ST, false>{(int)c->ncols, (int)c->D, gg.n_tiles * NWG, c->wnorm, c->lrow, cp,
-                                      c->W, c->M, c->sp, (float)c->d.momentum,
-                                      (float)c->d.weight_decay, c->st, BN / NWG, c->dw_prefetch});
+    if constexpr (kUmma) {
+      if (gw.n_tiles == 2)
+        err = launch_umma<kBN, 3, kNWG, true, true>(
+            c, c->tm_e_mn, c->tm_xs_mn, gw,
+            DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
+                              c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
+                              c->st});
+      else
+        err = launch_umma<kBN, 3, kNWG, true, true>(
+            c, c->tm_e_mn, c->tm_xs_mn, gw,
+            DwUpdateEpi<false>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
+                               c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
+                               c->st});
+    } else {
+      err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xs,
+                                    (int)c->Dp, gw, DwStoreEpi{{}, (int)c->ncols, (int)c->D, c->dwt});
+      if (err == cudaSuccess) {
+        dw_rows_update_kernel<<<(unsigned)ceil_div(c->ncols * 32, bs), bs, 0, s>>>(
+            c->dwt, c->lrow, c->wnorm, c->pslot, c->poscorr, (int)c->ncols, (int)c->D, c->W, c->M,
+            c->sp, (float)c->d.momentum, (float)c->d.weight_decay, c->st);
+        c->launches++;
+        err = cudaGetLastError();
+      }
+    }
     CUDA_TRY(c, err);
   }
   phase(c, "dw_update_gemm");
@@ -583,6 +615,11 @@ int check_status(Ctx* c, int64_t step_index, int64_t B, pfc_gpu_step_out* out) {
   if (st.masked_row != 0x7fffffff)
     return fail(c, PFC_ERR_CONTRACT,
                 "distributed_partial_step: all buffer columns masked for row %d", st.masked_row);
+  if (st.underflow_row != 0x7fffffff)
+    return fail(c, PFC_ERR_NUMERICAL,
+                "pfc_gpu: row %d: every logit is below the fixed softmax offset range "
+                "(exp(z - max(0, s - 40)) underflows); use PFC_PRECISION_FP32 semantics",
+                st.underflow_row);
   if (st.nonfinite_loss)
     return fail(c, PFC_ERR_NUMERICAL, "distributed_partial_step: non-finite loss at step %lld",
                 (long long)step_index);
@@ -659,6 +696,10 @@ int validate_desc(const pfc_gpu_desc* d) {
       d->num_shards % d->world_size != 0)
     return fail(nullptr, PFC_ERR_CONTRACT,
                 "pfc_gpu_create: world_size must divide num_shards and 0 <= rank < world_size");
+  if (d->precision == PFC_PRECISION_BF16 && (d->dim % 4 != 0 || d->dim > 512))
+    return fail(nullptr, PFC_ERR_CONFIG,
+                "pfc_gpu: the bf16 tcgen05 path needs dim %% 4 == 0 and dim <= 512 "
+                "(use PFC_PRECISION_FP32 otherwise)");
   if (d->num_classes >= (int64_t)INT32_MAX)
     return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: num_classes must be < 2^31");
   return PFC_OK;
@@ -711,7 +752,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->rows = c->cls_hi - c->cls_lo;
   c->ncols = c->nk * c->cap;
   c->ncols_pad = round_up(std::max<int64_t>(c->ncols, 1), 256);
-  c->ldg = round_up(desc->max_batch, 8);  // G^T row stride
+  c->ldg = round_up(std::max<int64_t>(c->ncols, 1), 8);  // E row stride
   c->pool_stride = std::max<int64_t>(c->blk, 1);
   c->maxB = desc->max_batch;
   if (const char* e = getenv("PFC_DW_PREFETCH")) c->dw_prefetch = atoi(e);
@@ -719,6 +760,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->mg.s = (float)desc->margin_scale;
   c->mg.sd = desc->margin_scale;
   c->mg.md = desc->margin_m;
+  c->mg.offd = std::max(0.0, desc->margin_scale - 40.0);  // E = exp(z - o) <= e^40
+  c->mg.off = (float)c->mg.offd;
   int64_t B = c->maxB;
   auto bail = [&](int rc) {
     g_create_error = c->err;
@@ -765,19 +808,22 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->wh), (size_t)c->ncols_pad * c->Dp * ob));
   CT(dalloc(c, &c->wnorm, (size_t)c->ncols_pad));
   CT(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_m), (size_t)(T * kNWG * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(T * kNWG * B) * sb));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->seg_m), (size_t)(kMergeSegs * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->seg_s), (size_t)(kMergeSegs * B) * sb));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->lm), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->ls), (size_t)(c->R * B) * sb));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->gmax), (size_t)B * sb));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->inv_gsum), (size_t)B * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->rowscale), (size_t)B * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->delta), (size_t)B * sb));
   CT(dalloc(c, &c->zpos, (size_t)B));
+  CT(dalloc(c, &c->cpos, (size_t)B));
+  CT(dalloc(c, &c->epos, (size_t)B));
+  CT(dalloc(c, &c->hasval, (size_t)B));
   CT(dalloc(c, &c->loss_row, (size_t)B));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->cproj),
-            (size_t)(ceil_div(B, BN) * kNWG * std::max<int64_t>(c->ncols, 1)) * sb));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)B * c->ldg * ob));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->xs), (size_t)B * c->Dp * ob));
+  c->pmax = std::max<int64_t>(1, std::min<int64_t>(c->cap, B));
+  CT(dalloc(c, &c->poscorr, (size_t)(c->nk * c->pmax * c->D)));
+  CT(dalloc(c, &c->pslot, (size_t)std::max<int64_t>(c->ncols, 1)));
+  if (!c->bf16) CT(dalloc(c, &c->dwt, (size_t)std::max<int64_t>(c->ncols, 1) * c->D));
   CT(dalloc(c, &c->dx_part, (size_t)c->max_splits * B * c->D));
   CT(dalloc(c, &c->dX, (size_t)B * c->D));
   CT(dalloc(c, &c->xdb, (size_t)B * c->D));

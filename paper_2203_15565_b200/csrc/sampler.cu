@@ -18,16 +18,6 @@ namespace pfc {
 
 constexpr int kMaxSortBatch = 8192;
 
-struct ShardMeta {        // per local shard
-  int64_t lo, hi;         // owned range [lo, hi)
-  int32_t npos;           // distinct positives
-  int32_t need;           // cap - npos negatives to draw
-  int32_t pool;           // N = owned - npos
-  int32_t full;           // 1 -> full-sampling branch (ascending complement, no RNG)
-  int32_t ustart;         // index of the first positive in the sorted-unique label list
-  int32_t reject;         // 1 -> a modulo rejection happened: sequential fallback
-};
-
 __device__ __forceinline__ int lower_bound_i64(const int64_t* a, int n, int64_t v) {
   int lo = 0, hi = n;
   while (lo < hi) {

@@ -304,15 +304,22 @@ struct DwUpdateEpi {
     int rw[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) rw[u] = s_row[u * 4 + sub];
-    // ---- pass 1: partial dots w . dwt over this warpgroup's 128 dims
+    // ---- pass 1: partial dots w . dwt over this warpgroup's 128 dims (W one chunk ahead)
     float dot[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) dot[u] = 0.f;
+    float4 wn[8];
+    {
+      const int d = t.col0 + wg * CW + q4;
+      if (d < D) load_rows(rw, d, wn);
+    }
 #pragma unroll 1
     for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
       const int d = t.col0 + c0 + q4;
       float4 w[8];
-      if (d < D) load_rows(rw, d, w);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u] = wn[u];
+      if (c0 + 32 < (wg + 1) * CW && d + 32 < D) load_rows(rw, d + 32, wn);
       float v[32];
       src.load(c0, v);
       __syncwarp();

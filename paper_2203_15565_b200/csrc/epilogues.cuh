@@ -63,8 +63,8 @@ template <typename ST, typename OT, bool kFilter, bool kTma>
 struct alignas(64) FwdEpi : NoSetup {
   static constexpr int kWarpBytes = 4096;  // 2 x [32 rows][64 B] E staging per warp
   static constexpr int kSmem = kTma ? 4 * kWarpBytes : 0;
-  CUtensorMap tm;   // E store map: inner = classes (box 32, SWIZZLE_64B), outer = b (box 32)
-  int B, ncols, lde;
+  CUtensorMap tm;   // E^T store map: inner = b (box 32, SWIZZLE_64B), outer = classes (box 32)
+  int B, ncols, lde;  // lde = row stride of E^T (>= B)
   const int32_t* pos_col;
   MarginDev mg;
   float tau;
@@ -73,7 +73,7 @@ struct alignas(64) FwdEpi : NoSetup {
   double* cpos;     // [B] cosine of the positive
   float* epos;      // [B] E of the positive as stored (after OT rounding)
   int* hasval;      // [B] 1 when the row has an unmasked column (filter only)
-  OT* E;            // [B][lde]
+  OT* E;            // E^T [ncols][lde]: class-major, so the dW GEMM streams whole class blocks
 
   struct Pre {};
   __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
@@ -157,27 +157,29 @@ struct alignas(64) FwdEpi : NoSetup {
         sum += acc;
       }
       if constexpr (kTma) {
+        // transposed staging: E^T chunk [32 classes][32 rows b] (64 B per class, 64B swizzle)
         uint8_t* sb = stage + (kk & 1) * 2048;
-        uint32_t w[16];
-        pack_bf16x32(e, w);
         if (lane == 0) pfc_sm100::bulk_wait_read<1>();  // this buffer's store, 2 groups ago
         __syncwarp();
-        const int sw = (lane >> 1) & 3;
+        const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq)
-          *reinterpret_cast<uint4*>(sb + lane * 64 + ((qq ^ sw) << 4)) =
-              make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
+        for (int q = 0; q < 32; ++q) {
+          // element (class q, row lane) at byte q*64 + lane*2, 16-byte chunk swizzled by q
+          const int chunk = (lane >> 3) ^ ((q >> 1) & 3);
+          *reinterpret_cast<__nv_bfloat16*>(sb + q * 64 + chunk * 16 + (lane & 7) * 2) =
+              rv ? __float2bfloat16_rn(e[q]) : zero;
+        }
         pfc_sm100::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          pfc_sm100::tma_store_2d(&tm, sb, colb, t.row0 + wig * 32);
+          pfc_sm100::tma_store_2d(&tm, sb, t.row0 + wig * 32, colb);
           pfc_sm100::bulk_commit();
         }
       } else if (rv) {
-        OT* dst = E + (size_t)b * lde + colb;
+        // E^T[class][b] (fp32 validation engine)
 #pragma unroll
         for (int q = 0; q < 32; ++q)
-          if (colb + q < ncols) store_out1(dst + q, e[q]);
+          if (colb + q < ncols) store_out1(E + (size_t)(colb + q) * lde + b, e[q]);
       }
     }
     if (rv) {
@@ -241,6 +243,7 @@ struct DwUpdateEpi {
   const StepParams* sp;     // lr of this step
   float mu, wd;
   const StepStatus* st;     // no update when the step failed (the reference throws before 412)
+  int skip_dot;             // timing experiment only
 
   struct Pre {
     float inv;
@@ -306,6 +309,7 @@ struct DwUpdateEpi {
     for (int u = 0; u < 8; ++u) rw[u] = s_row[u * 4 + sub];
     // ---- pass 1: partial dots w . dwt over this warpgroup's 128 dims (W one chunk ahead)
     float dot[8];
+    if (!skip_dot) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) dot[u] = 0.f;
     float4 wn[8];
@@ -339,6 +343,10 @@ struct DwUpdateEpi {
         }
         dot[u] += a0 * w[u].x + a1 * w[u].y + a2 * w[u].z + a3 * w[u].w;
       }
+    }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dot[u] = 0.f;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {

@@ -170,7 +170,7 @@ struct Ctx {
   int* hasval = nullptr;
   double* loss_row = nullptr;
   // backward
-  void* G = nullptr;       // E [maxB][lde]: exp(z - o) (bf16 / fp32)
+  void* G = nullptr;       // E^T [ncols_pad][ldg]: exp(z - o) (bf16 / fp32), class-major
   void* xs = nullptr;      // [maxB][Dp] rowscale * x^
   float* poscorr = nullptr;  // [nk * pmax][D]
   int32_t* pslot = nullptr;  // [ncols]
@@ -312,16 +312,16 @@ int ensure_maps(Ctx* c, int64_t B) {
   if (!c->bf16 || c->tm_B == B) return PFC_OK;
   bool ok = true;
   // logits GEMM (M = b, N = classes): A = X^ [B][Dp], B = W^ [ncols][Dp], both K-major;
-  // its epilogue stores E [B][ncols] (per-warp box 32 classes x 32 rows, 64B swizzle)
+  // its epilogue stores E^T [ncols][ldg] (per-warp box 32 b x 32 classes, 64B swizzle)
   ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128);
   ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kBN);
-  ok &= make_map(&c->tm_e_st, c->G, c->ncols, B, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
-  // dX GEMM (M = b, N = d, K = classes): A = E K-major; B = W^ MN-major (d contiguous)
-  ok &= make_map(&c->tm_e_k, c->G, c->ncols, B, c->ldg, 128);
+  ok &= make_map(&c->tm_e_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  // dX GEMM (M = b, N = d, K = classes): A = E^T read MN-major (b contiguous); B = W^ MN-major
+  ok &= make_map(&c->tm_e_mn, c->G, B, c->ncols, c->ldg, 64);
   ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, 64);
-  // dW GEMM (M = classes, N = d, K = b): A = E read MN-major (classes contiguous);
+  // dW GEMM (M = classes, N = d, K = b): A = E^T K-major (whole class blocks contiguous);
   // B = rowscale * x^ MN-major
-  ok &= make_map(&c->tm_e_mn, c->G, c->ncols, B, c->ldg, 64);
+  ok &= make_map(&c->tm_e_k, c->G, B, c->ncols, c->ldg, 128);
   ok &= make_map(&c->tm_xs_mn, c->xs, c->Dp, B, c->Dp, 64);
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
@@ -457,9 +457,9 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0);
     DxPartEpi e{{}, (int)B, (int)c->D, c->dx_part};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, false, true>(c, c->tm_e_k, c->tm_w_mn, gx, e);
-    else err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
-                                        (int)c->Dp, gx, e);
+    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, true, true>(c, c->tm_e_mn, c->tm_w_mn, gx, e);
+    else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
+                                       (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
     const int dpt = (int)ceil_div(c->D, 256);
 #define PFC_FIN(N)                                                                               \
@@ -480,21 +480,22 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
     cudaError_t err;
     if constexpr (kUmma) {
-      if (gw.n_tiles == 2)
-        err = launch_umma<kBN, 3, kNWG, true, true>(
-            c, c->tm_e_mn, c->tm_xs_mn, gw,
+      static const bool nopair = getenv("PFC_DEBUG_DW_NOPAIR") != nullptr;  // timing experiment only
+      if (gw.n_tiles == 2 && !nopair)
+        err = launch_umma<kBN, 3, kNWG, false, true>(
+            c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                               c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                              c->st});
+                              c->st, getenv("PFC_DEBUG_DW_NODOT") ? 1 : 0});
       else
-        err = launch_umma<kBN, 3, kNWG, true, true>(
-            c, c->tm_e_mn, c->tm_xs_mn, gw,
+        err = launch_umma<kBN, 3, kNWG, false, true>(
+            c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<false>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                                c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                               c->st});
+                               c->st, getenv("PFC_DEBUG_DW_NODOT") ? 1 : 0});
     } else {
-      err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xs,
-                                    (int)c->Dp, gw, DwStoreEpi{{}, (int)c->ncols, (int)c->D, c->dwt});
+      err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xs,
+                                     (int)c->Dp, gw, DwStoreEpi{{}, (int)c->ncols, (int)c->D, c->dwt});
       if (err == cudaSuccess) {
         dw_rows_update_kernel<<<(unsigned)ceil_div(c->ncols * 32, bs), bs, 0, s>>>(
             c->dwt, c->lrow, c->wnorm, c->pslot, c->poscorr, (int)c->ncols, (int)c->D, c->W, c->M,
@@ -752,7 +753,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->rows = c->cls_hi - c->cls_lo;
   c->ncols = c->nk * c->cap;
   c->ncols_pad = round_up(std::max<int64_t>(c->ncols, 1), 256);
-  c->ldg = round_up(std::max<int64_t>(c->ncols, 1), 8);  // E row stride
+  c->ldg = round_up(desc->max_batch, 8);  // E^T row stride
   c->pool_stride = std::max<int64_t>(c->blk, 1);
   c->maxB = desc->max_batch;
   if (const char* e = getenv("PFC_DW_PREFETCH")) c->dw_prefetch = atoi(e);
@@ -818,7 +819,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->epos, (size_t)B));
   CT(dalloc(c, &c->hasval, (size_t)B));
   CT(dalloc(c, &c->loss_row, (size_t)B));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)B * c->ldg * ob));
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->xs), (size_t)B * c->Dp * ob));
   c->pmax = std::max<int64_t>(1, std::min<int64_t>(c->cap, B));
   CT(dalloc(c, &c->poscorr, (size_t)(c->nk * c->pmax * c->D)));

@@ -224,14 +224,17 @@ struct DxPartEpi : NoSetup {
 };
 
 // ------------------------------------------------------------------------------- DwUpdateEpi
-// Both warpgroups of a CTA cover its 256-dim half of the class block (128 dims each); with
-// kPair the two CTAs of a cluster own the two halves (D = 512) and swap half-dots.
+// Each CTA owns a 256-dim half of a 128-class block; warp k of warpgroup g owns the 16 rows
+// 32k + 16g .. +15 over all 256 dims, so the CTA-local half-dot of a row is warp-local.  With
+// kPair (D = 512) the two CTAs of a 2-CTA cluster own the two halves and swap half-dots warp
+// by warp through DSMEM (per-warp mbarriers, no CTA-wide barrier).
 template <bool kPair>
 struct DwUpdateEpi {
   static constexpr int kCluster = kPair ? 2 : 1;
   static constexpr int kWarpFloats = 32 * 33 + 4 * 32;  // stage + inv/row/pslot/cproj
   static constexpr int kWarpBytes = kWarpFloats * 4;
-  static constexpr int kSharedBytes = 3072 + 16;        // dotp[2][128], hloc/hrem[2][128], mbar
+  // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][4 k][32 rows] + 4 mbarriers
+  static constexpr int kSharedBytes = 2 * 4 * 32 * 4 + 4 * 8;
   static constexpr int kSmem = ((4 * kWarpBytes + kSharedBytes + 1023) / 1024) * 1024;
   int ncols, D;
   const float* wnorm;       // [ncols]
@@ -243,7 +246,6 @@ struct DwUpdateEpi {
   const StepParams* sp;     // lr of this step
   float mu, wd;
   const StepStatus* st;     // no update when the step failed (the reference throws before 412)
-  int skip_dot;             // timing experiment only
 
   struct Pre {
     float inv;
@@ -263,39 +265,28 @@ struct DwUpdateEpi {
   __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
   __device__ __forceinline__ void finish(int, int) const {}
 
-  // CTA-shared area (inside warpgroup 0's scratch, after its 4 warp areas)
   __device__ __forceinline__ static uint8_t* shared_area(uint8_t* wg0) { return wg0 + 4 * kWarpBytes; }
   __device__ __forceinline__ void setup(uint8_t* epi_base) const {
     if constexpr (kPair) {
-      uint64_t* mbar = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 3072);
-      pfc_sm100::mbar_init(mbar, 128);
+      uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 1024);
+      for (int k = 0; k < 4; ++k) pfc_sm100::mbar_init(&mb[k], 8);  // 4 writer lanes x 2 WGs
     }
-  }
-
-  __device__ __forceinline__ void load_rows(const int (&rw)[8], int d, float4 (&w)[8]) const {
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      w[u] = rw[u] >= 0 ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
                                       uint8_t* smem, const Pre& pre) const {
-    static_assert(NWG == 2 && BN == 256, "DwUpdateEpi: 2 warpgroups x 128 dims");
-    constexpr int CW = BN / NWG;
-    const int wig = row >> 5, lane = row & 31;
+    static_assert(NWG == 2 && BN == 256, "DwUpdateEpi: 2 warpgroups, 256-dim tiles");
+    const int wk = row >> 5, lane = row & 31;
     uint8_t* wg0 = smem - wg * kSmem;
-    float* ws = reinterpret_cast<float*>(smem + wig * kWarpBytes);
-    float* stage = ws;                 // [32][33]: warp row x dim
+    float* ws = reinterpret_cast<float*>(smem + wk * kWarpBytes);
+    float* stage = ws;                 // [32 lanes][33]
     float* s_inv = ws + 32 * 33;
     int* s_row = reinterpret_cast<int*>(s_inv + 32);
     int* s_ps = s_row + 32;
     float* s_cp = reinterpret_cast<float*>(s_ps + 32);
-    float* dotp = reinterpret_cast<float*>(shared_area(wg0));  // [2 wg][128]
-    float* hloc = dotp + 256;                                  // [2 parity][128] own half
-    float* hrem = hloc + 256;                                  // [2 parity][128] partner half
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(shared_area(wg0) + 3072);
+    float* hrem = reinterpret_cast<float*>(shared_area(wg0));           // [2][4][32]
+    uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + 1024); // [4]
     const bool failed = status_failed(st);
     const float lr = sp->lr;
     __syncwarp();  // the warp finished with the previous tile's scalars
@@ -303,40 +294,39 @@ struct DwUpdateEpi {
     s_row[lane] = failed ? -1 : pre.r;
     s_ps[lane] = pre.ps;
     __syncwarp();
-    const int sub = lane >> 3, q4 = (lane & 7) * 4;  // 4 rows x 8 lanes x float4 per warp op
-    int rw[8];
+    // this warp's 16 rows: lanes 16wg .. 16wg+15 of its TMEM quadrant; 4 rows x 8 lanes/op
+    const int sub = lane >> 3, q4 = (lane & 7) * 4;
+    int rl[4], rw[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) rw[u] = s_row[u * 4 + sub];
-    // ---- pass 1: partial dots w . dwt over this warpgroup's 128 dims (W one chunk ahead)
-    float dot[8];
-    if (!skip_dot) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) dot[u] = 0.f;
-    float4 wn[8];
-    {
-      const int d = t.col0 + wg * CW + q4;
-      if (d < D) load_rows(rw, d, wn);
+    for (int u = 0; u < 4; ++u) {
+      rl[u] = 16 * wg + u * 4 + sub;
+      rw[u] = s_row[rl[u]];
     }
+    // ---- pass 1: half-dot w . dwt over this CTA's 256 dims
+    float dot[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
-    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
+    for (int c0 = 0; c0 < BN; c0 += 32) {
       const int d = t.col0 + c0 + q4;
-      float4 w[8];
+      float4 w[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) w[u] = wn[u];
-      if (c0 + 32 < (wg + 1) * CW && d + 32 < D) load_rows(rw, d + 32, wn);
+      for (int u = 0; u < 4; ++u)
+        w[u] = (rw[u] >= 0 && d < D) ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
       float v[32];
       src.load(c0, v);
       __syncwarp();
+      if ((lane >> 4) == wg) {
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
+        for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
+      }
       __syncwarp();
       if (d >= D) continue;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         if (rw[u] < 0) continue;
-        const float* a = stage + (u * 4 + sub) * 33 + q4;
+        const float* a = stage + rl[u] * 33 + q4;
         float a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3];
-        const int rp = s_ps[u * 4 + sub];
+        const int rp = s_ps[rl[u]];
         if (rp >= 0) {
           const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)rp * D + d);
           a0 += pc.x; a1 += pc.y; a2 += pc.z; a3 += pc.w;
@@ -344,73 +334,66 @@ struct DwUpdateEpi {
         dot[u] += a0 * w[u].x + a1 * w[u].y + a2 * w[u].z + a3 * w[u].w;
       }
     }
-    } else {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) dot[u] = 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 1);
       dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 2);
       dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 4);
     }
-    __syncwarp();
-    if ((lane & 7) == 0) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s_cp[u * 4 + sub] = dot[u];
-    }
-    __syncwarp();
-    dotp[wg * 128 + row] = s_cp[lane];
-    pfc_sm100::named_bar_sync(3, 256);  // both warpgroups' halves of this CTA's 256 dims
-    float half = dotp[row] + dotp[128 + row];
-    const int par = t.iter & 1;
     if constexpr (kPair) {
-      if (wg == 0) {
-        hloc[par * 128 + row] = half;
+      const int par = t.iter & 1;
+      if ((lane & 7) == 0) {
         const uint32_t prank = pfc_sm100::cluster_ctarank() ^ 1u;
-        pfc_sm100::st_cluster_f32(
-            pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hrem + par * 128 + row), prank), half);
-        pfc_sm100::mbar_arrive_cluster(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(mbar), prank));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          pfc_sm100::st_cluster_f32(
+              pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hrem + (par * 4 + wk) * 32 + rl[u]), prank),
+              dot[u]);
+        pfc_sm100::mbar_arrive_cluster(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[wk]), prank));
       }
-      pfc_sm100::mbar_wait_cluster(mbar, (uint32_t)par);
-      pfc_sm100::named_bar_sync(3, 256);  // hloc written by warpgroup 0 is visible
-      half = hloc[par * 128 + row] + hrem[par * 128 + row];
+      pfc_sm100::mbar_wait_cluster(&mb[wk], (uint32_t)par);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dot[u] += hrem[(par * 4 + wk) * 32 + rl[u]];
     }
-    __syncwarp();
-    s_cp[lane] = half * pre.inv;  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
-    __syncwarp();
+    float rcp[4], rinv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      rinv[u] = s_inv[rl[u]];
+      rcp[u] = dot[u] * rinv[u];  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
+    }
     // ---- pass 2: dW and the momentum-SGD update of the sampled rows
 #pragma unroll 1
-    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
+    for (int c0 = 0; c0 < BN; c0 += 32) {
       const int d = t.col0 + c0 + q4;
-      float4 w[8], mo[8];
-      if (d < D) {
-        load_rows(rw, d, w);
+      float4 w[4], mo[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          mo[u] = rw[u] >= 0 ? *reinterpret_cast<const float4*>(Mom + (size_t)rw[u] * D + d)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = rw[u] >= 0 && d < D;
+        w[u] = ok ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
+        mo[u] = ok ? *reinterpret_cast<const float4*>(Mom + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       float v[32];
       src.load(c0, v);
       __syncwarp();
+      if ((lane >> 4) == wg) {
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
+        for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
+      }
       __syncwarp();
       if (d >= D) continue;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         if (rw[u] < 0) continue;
-        const float* a = stage + (u * 4 + sub) * 33 + q4;
+        const float* a = stage + rl[u] * 33 + q4;
         float av[4] = {a[0], a[1], a[2], a[3]};
-        const int rp = s_ps[u * 4 + sub];
+        const int rp = s_ps[rl[u]];
         if (rp >= 0) {
           const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)rp * D + d);
           av[0] += pc.x; av[1] += pc.y; av[2] += pc.z; av[3] += pc.w;
         }
         float wv[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
         float mv[4] = {mo[u].x, mo[u].y, mo[u].z, mo[u].w};
-        const float inv = s_inv[u * 4 + sub], cpj = s_cp[u * 4 + sub];
+        const float inv = rinv[u], cpj = rcp[u];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float dw = (av[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382

@@ -480,8 +480,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
     cudaError_t err;
     if constexpr (kUmma) {
-      static const bool nopair = getenv("PFC_DEBUG_DW_NOPAIR") != nullptr;  // timing experiment only
-      if (gw.n_tiles == 2 && !nopair)
+      if (gw.n_tiles == 2)
         err = launch_umma<kBN, 3, kNWG, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,

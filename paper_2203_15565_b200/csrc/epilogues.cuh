@@ -77,7 +77,7 @@ struct alignas(64) FwdEpi : NoSetup {
 
   struct Pre {};
   __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
-  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
   __device__ __forceinline__ void finish(int row, int) const {
     if constexpr (kTma) {
       if ((row & 31) == 0) pfc_sm100::bulk_wait_all();
@@ -196,7 +196,7 @@ struct DxPartEpi : NoSetup {
   float* part;  // [splits][B][D]
   struct Pre {};
   __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
-  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
   __device__ __forceinline__ void finish(int, int) const {}
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
@@ -231,7 +231,7 @@ struct DxPartEpi : NoSetup {
 template <bool kPair>
 struct DwUpdateEpi {
   static constexpr int kCluster = kPair ? 2 : 1;
-  static constexpr int kWarpFloats = 32 * 33 + 4 * 32;  // stage + inv/row/pslot/cproj
+  static constexpr int kWarpFloats = 32 * 33 + 3 * 32;  // stage + inv/row/pslot
   static constexpr int kWarpBytes = kWarpFloats * 4;
   // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][4 k][32 rows] + 4 mbarriers
   static constexpr int kSharedBytes = 2 * 4 * 32 * 4 + 4 * 8;
@@ -246,6 +246,7 @@ struct DwUpdateEpi {
   const StepParams* sp;     // lr of this step
   float mu, wd;
   const StepStatus* st;     // no update when the step failed (the reference throws before 412)
+  int failed_hint;          // 1: skip the L2 prefetch (set by the host for A/B timing)
 
   struct Pre {
     float inv;
@@ -262,7 +263,15 @@ struct DwUpdateEpi {
     }
     return p;
   }
-  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  // bulk L2 prefetch of the W (warpgroup 0) / momentum (warpgroup 1) row segment the tile
+  // updates, one tile ahead: the update loops then hit L2 instead of waiting on HBM
+  __device__ __forceinline__ void prefetch(const TileInfo& t, int, int wg, const Pre& p) const {
+    if (p.r < 0 || failed_hint) return;
+    const int n = min(256, D - t.col0);
+    if (n <= 0) return;
+    const float* base = (wg == 0 ? W : Mom) + (size_t)p.r * D + t.col0;
+    pfc_sm100::prefetch_l2_bulk(base, (uint32_t)n * 4u);
+  }
   __device__ __forceinline__ void finish(int, int) const {}
 
   __device__ __forceinline__ static uint8_t* shared_area(uint8_t* wg0) { return wg0 + 4 * kWarpBytes; }
@@ -284,7 +293,6 @@ struct DwUpdateEpi {
     float* s_inv = ws + 32 * 33;
     int* s_row = reinterpret_cast<int*>(s_inv + 32);
     int* s_ps = s_row + 32;
-    float* s_cp = reinterpret_cast<float*>(s_ps + 32);
     float* hrem = reinterpret_cast<float*>(shared_area(wg0));           // [2][4][32]
     uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + 1024); // [4]
     const bool failed = status_failed(st);
@@ -417,7 +425,7 @@ struct DwStoreEpi : NoSetup {
   float* dwt;  // [ncols][D]
   struct Pre {};
   __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
-  __device__ __forceinline__ void prefetch(const TileInfo&, int, int) const {}
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
   __device__ __forceinline__ void finish(int, int) const {}
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,

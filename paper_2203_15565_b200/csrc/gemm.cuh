@@ -200,28 +200,29 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     const int row = ((warp & 3) << 5) | lane;
     uint8_t* wsm = epi_smem + wg * Epi::kSmem;
     uint32_t it = 0;
-    // per-tile operands of the epilogue are loaded one tile ahead (registers), so their
-    // global-memory latency hides behind the current tile
-    typename Epi::Pre pre{};
+    // per-tile operands of the epilogue are loaded two tiles ahead (registers), so their
+    // global-memory latency hides behind the current tile; epi.prefetch(next tile) runs on values
+    // that have already arrived (e.g. bulk L2 prefetch of the rows the next tile updates)
+    typename Epi::Pre pre{}, pre_n{};
+    const int stride = (int)gridDim.x;
     if ((int)blockIdx.x < total) pre = epi.preload(g.tile(blockIdx.x), row, wg);
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    if ((int)blockIdx.x + stride < total) pre_n = epi.preload(g.tile(blockIdx.x + stride), row, wg);
+    if ((int)blockIdx.x < total) epi.prefetch(g.tile(blockIdx.x), row, wg, pre);
+    for (int t = blockIdx.x; t < total; t += stride, ++it) {
       TileInfo ti = g.tile(t);
       ti.iter = (int)it;
       const uint32_t as = it & 1, aph = (it >> 1) & 1;
-      if (it == 0) epi.prefetch(ti, row, wg);
-      typename Epi::Pre pre_next{};
-      if (t + (int)gridDim.x < total) {
-        const TileInfo tn = g.tile(t + gridDim.x);
-        epi.prefetch(tn, row, wg);
-        pre_next = epi.preload(tn, row, wg);
-      }
+      if (t + stride < total) epi.prefetch(g.tile(t + stride), row, wg, pre_n);
+      typename Epi::Pre pre_n2{};
+      if (t + 2 * stride < total) pre_n2 = epi.preload(g.tile(t + 2 * stride), row, wg);
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const TmemSrc src{tmem_base + as * BN + ((uint32_t)((warp & 3) * 32) << 16)};
       epi.template run<BN, NWG>(ti, src, row, wg, wsm, pre);
       tc_fence_before();
       mbar_arrive(&tempty[as]);
-      pre = pre_next;
+      pre = pre_n;
+      pre_n = pre_n2;
     }
     epi.finish(row, wg);
   }

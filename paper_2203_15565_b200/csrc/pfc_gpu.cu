@@ -179,7 +179,7 @@ struct Ctx {
   float* dx_part = nullptr;  // [S][maxB][D]
   float* dX = nullptr;       // [maxB][D]
   int max_splits = 1;
-  int dw_prefetch = 0;  // DwUpdateEpi L2 prefetch policy (PFC_DW_PREFETCH=0/1/2)
+  int dw_prefetch = 1;  // DwUpdateEpi bulk L2 prefetch of the next tile's rows (PFC_DW_PREFETCH=0 off)
   // host-path scratch
   double* xdb = nullptr;  // D x maxB fp64
   StepStatus* st = nullptr;
@@ -485,13 +485,13 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                               c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                              c->st, getenv("PFC_DEBUG_DW_NODOT") ? 1 : 0});
+                              c->st, c->dw_prefetch ? 0 : 1});
       else
         err = launch_umma<kBN, 3, kNWG, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<false>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                                c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                               c->st, getenv("PFC_DEBUG_DW_NODOT") ? 1 : 0});
+                               c->st, c->dw_prefetch ? 0 : 1});
     } else {
       err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xs,
                                      (int)c->Dp, gw, DwStoreEpi{{}, (int)c->ncols, (int)c->D, c->dwt});

@@ -1,0 +1,120 @@
+// Microbenchmark: gathered-row momentum-SGD update (the dW epilogue's HBM pattern) at different
+// access granularities.  200k random rows of a [2M][512] fp32 table (W and momentum), plus a
+// dense [200k][512] fp32 "dwt" source.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <random>
+#include <cuda_runtime.h>
+
+constexpr int D = 512;
+// (a) epilogue pattern: warp = 32 rows x 128 dims; per step 8 lanes x float4 per row, 4 rows/op
+template <int RPI>
+__global__ void upd_a(float* W, float* M, const float* src, const int* rows, int n, float lr) {
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  constexpr int LPR = 32 / RPI;          // lanes per row
+  const int sub = lane / LPR, q = (lane % LPR) * 4;
+  for (int blk = warp; blk < n / 32 * (D / 128); blk += nw) {
+    const int r0 = (blk / (D / 128)) * 32, d0 = (blk % (D / 128)) * 128;
+    for (int c = 0; c < 128; c += LPR * 4) {
+#pragma unroll
+      for (int u = 0; u < 32 / RPI; ++u) {
+        const int rr = r0 + u * RPI + sub;
+        const int r = rows[rr];
+        const size_t o = (size_t)r * D + d0 + c + q;
+        float4 w = *reinterpret_cast<float4*>(W + o), m = *reinterpret_cast<float4*>(M + o);
+        const float4 a = *reinterpret_cast<const float4*>(src + (size_t)rr * D + d0 + c + q);
+        m.x = 0.9f * m.x + a.x; m.y = 0.9f * m.y + a.y; m.z = 0.9f * m.z + a.z; m.w = 0.9f * m.w + a.w;
+        w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
+        *reinterpret_cast<float4*>(W + o) = w;
+        *reinterpret_cast<float4*>(M + o) = m;
+      }
+    }
+  }
+}
+
+// (b) loads grouped ahead of all stores: U row groups x (W, M, src) float4 in flight per lane
+template <int U>
+__global__ void upd_b(float* __restrict__ W, float* __restrict__ M, const float* __restrict__ src,
+                      const int* __restrict__ rows, int n, float lr) {
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int sub = lane >> 3, q = (lane & 7) * 4;  // 4 rows x 128 B per op
+  constexpr int RB = 4 * U;                       // rows per block step
+  for (int blk = warp; blk < n / RB * (D / 32); blk += nw) {
+    const int r0 = (blk / (D / 32)) * RB, d = (blk % (D / 32)) * 32 + q;
+    float4 w[U], m[U], a[U];
+    size_t o[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int rr = r0 + u * 4 + sub;
+      o[u] = (size_t)__ldg(rows + rr) * D + d;
+      w[u] = *reinterpret_cast<const float4*>(W + o[u]);
+      m[u] = *reinterpret_cast<const float4*>(M + o[u]);
+      a[u] = __ldg(reinterpret_cast<const float4*>(src + (size_t)rr * D + d));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      m[u].x = 0.9f * m[u].x + a[u].x; m[u].y = 0.9f * m[u].y + a[u].y;
+      m[u].z = 0.9f * m[u].z + a[u].z; m[u].w = 0.9f * m[u].w + a[u].w;
+      w[u].x -= lr * m[u].x; w[u].y -= lr * m[u].y; w[u].z -= lr * m[u].z; w[u].w -= lr * m[u].w;
+      *reinterpret_cast<float4*>(W + o[u]) = w[u];
+      *reinterpret_cast<float4*>(M + o[u]) = m[u];
+    }
+  }
+}
+
+int main() {
+  const int C = 2000000, n = 200000;
+  float *W, *M, *src;
+  int* rows;
+  cudaMalloc(&W, (size_t)C * D * 4);
+  cudaMalloc(&M, (size_t)C * D * 4);
+  cudaMalloc(&src, (size_t)n * D * 4);
+  cudaMalloc(&rows, n * 4);
+  cudaMemset(W, 0, (size_t)C * D * 4);
+  cudaMemset(M, 0, (size_t)C * D * 4);
+  cudaMemset(src, 0, (size_t)n * D * 4);
+  std::vector<int> h(C);
+  for (int i = 0; i < C; ++i) h[i] = i;
+  std::mt19937 g(1);
+  std::shuffle(h.begin(), h.end(), g);
+  h.resize(n);
+  for (int sorted = 0; sorted < 2; ++sorted) {
+    std::vector<int> hh = h;
+    if (sorted) std::sort(hh.begin(), hh.end());
+    cudaMemcpy(rows, hh.data(), n * 4, cudaMemcpyHostToDevice);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double bytes = (double)n * D * 4 * 5;
+    auto run = [&](const char* name, auto kern, int blocks, int threads) {
+      for (int i = 0; i < 3; ++i) kern<<<blocks, threads>>>(W, M, src, rows, n, 0.1f);
+      cudaEventRecord(e0);
+      for (int i = 0; i < 10; ++i) kern<<<blocks, threads>>>(W, M, src, rows, n, 0.1f);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= 10;
+      printf("%s sorted=%d blocks=%d threads=%d: %.1f us  %.0f GB/s\n", name, sorted, blocks, threads,
+             ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+    };
+    for (int th : {512}) {
+      run("rows/op=4 (128B/row)", upd_a<4>, 148 * (2048 / th), th);
+      run("rows/op=2 (256B/row)", upd_a<2>, 148 * (2048 / th), th);
+      run("rows/op=1 (512B/row)", upd_a<1>, 148 * (2048 / th), th);
+    }
+    run("rows/op=4 8warps/SM", upd_a<4>, 148, 256);
+    run("rows/op=1 8warps/SM", upd_a<1>, 148, 256);
+    run("grouped U=2 8warps/SM", upd_b<2>, 148, 256);
+    run("grouped U=4 8warps/SM", upd_b<4>, 148, 256);
+    run("grouped U=8 8warps/SM", upd_b<8>, 148, 256);
+    run("grouped U=4 16warps/SM", upd_b<4>, 148, 512);
+    run("grouped U=8 16warps/SM", upd_b<8>, 148, 512);
+    run("grouped U=4 64warps/SM", upd_b<4>, 148 * 4, 512);
+  }
+  printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+}

@@ -224,18 +224,21 @@ struct DxPartEpi : NoSetup {
 };
 
 // ------------------------------------------------------------------------------- DwUpdateEpi
-// Each CTA owns a 256-dim half of a 128-class block; warp k of warpgroup g owns the 16 rows
-// 32k + 16g .. +15 over all 256 dims, so the CTA-local half-dot of a row is warp-local.  With
-// kPair (D = 512) the two CTAs of a 2-CTA cluster own the two halves and swap half-dots warp
-// by warp through DSMEM (per-warp mbarriers, no CTA-wide barrier).
+// Four epilogue warpgroups (16 warps): the update is a latency-bound gathered-row stream (W and
+// momentum read + write), and bytes in flight per SM, i.e. warps x loads per warp, set its speed
+// (profiles/micro/rowupd.cu: 8 warps/SM reach 4.7 TB/s, 16 warps 6.2 TB/s).  Each CTA owns a
+// 256-dim half of a 128-class block; warp (g, q) owns the 8 rows 32q + 8g .. +7 of TMEM lane
+// quadrant q over all 256 dims, so a row's CTA-local half-dot is warp-local.  With kPair
+// (D = 512) the two CTAs of a 2-CTA cluster own the two halves and swap half-dots warp by warp
+// through DSMEM (one mbarrier per warp and tile parity).
 template <bool kPair>
 struct DwUpdateEpi {
   static constexpr int kCluster = kPair ? 2 : 1;
-  static constexpr int kWarpFloats = 32 * 33 + 3 * 32;  // stage + inv/row/pslot
+  static constexpr int kWarpFloats = 8 * 33 + 3 * 8;  // stage [8 rows][33] + inv/row/pslot
   static constexpr int kWarpBytes = kWarpFloats * 4;
-  // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][4 k][32 rows] + 4 mbarriers
-  static constexpr int kSharedBytes = 2 * 4 * 32 * 4 + 4 * 8;
-  static constexpr int kSmem = ((4 * kWarpBytes + kSharedBytes + 1023) / 1024) * 1024;
+  // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][128 rows] + mbarriers [2][16 warps]
+  static constexpr int kSharedBytes = 2 * 128 * 4 + 2 * 16 * 8;
+  static constexpr int kSmem = ((4 * kWarpBytes + kSharedBytes + 127) / 128) * 128;
   int ncols, D;
   const float* wnorm;       // [ncols]
   const int32_t* lrow;      // [ncols] local row of W
@@ -246,16 +249,16 @@ struct DwUpdateEpi {
   const StepParams* sp;     // lr of this step
   float mu, wd;
   const StepStatus* st;     // no update when the step failed (the reference throws before 412)
-  int failed_hint;          // 1: skip the L2 prefetch (set by the host for A/B timing)
 
   struct Pre {
     float inv;
     int r, ps;
   };
-  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int) const {
+  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int wg) const {
     Pre p{0.f, -1, -1};
-    const int c = t.row0 + row;
-    if (c < ncols) {
+    const int lane = row & 31;
+    const int c = t.row0 + (row & ~31) + lane;
+    if ((lane >> 3) == wg && c < ncols) {  // only this warp's 8 rows
       const float n = wnorm[c];
       p.inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
       p.r = lrow[c];
@@ -263,156 +266,164 @@ struct DwUpdateEpi {
     }
     return p;
   }
-  // bulk L2 prefetch of the W (warpgroup 0) / momentum (warpgroup 1) row segment the tile
-  // updates, one tile ahead: the update loops then hit L2 instead of waiting on HBM
-  __device__ __forceinline__ void prefetch(const TileInfo& t, int, int wg, const Pre& p) const {
-    if (p.r < 0 || failed_hint) return;
-    const int n = min(256, D - t.col0);
-    if (n <= 0) return;
-    const float* base = (wg == 0 ? W : Mom) + (size_t)p.r * D + t.col0;
-    pfc_sm100::prefetch_l2_bulk(base, (uint32_t)n * 4u);
-  }
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
   __device__ __forceinline__ void finish(int, int) const {}
 
   __device__ __forceinline__ static uint8_t* shared_area(uint8_t* wg0) { return wg0 + 4 * kWarpBytes; }
   __device__ __forceinline__ void setup(uint8_t* epi_base) const {
     if constexpr (kPair) {
-      uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 1024);
-      for (int k = 0; k < 4; ++k) pfc_sm100::mbar_init(&mb[k], 8);  // 4 writer lanes x 2 WGs
+      uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 2 * 128 * 4);
+      for (int k = 0; k < 32; ++k) pfc_sm100::mbar_init(&mb[k], 4);  // 4 writer lanes per warp
     }
   }
 
   template <int BN, int NWG, class Src>
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
                                       uint8_t* smem, const Pre& pre) const {
-    static_assert(NWG == 2 && BN == 256, "DwUpdateEpi: 2 warpgroups, 256-dim tiles");
-    const int wk = row >> 5, lane = row & 31;
+    static_assert(NWG == 4 && BN == 256, "DwUpdateEpi: 4 warpgroups, 256-dim tiles");
+    constexpr int NC = BN / 32;  // 32-dim chunks
+    const int q = row >> 5, lane = row & 31;
     uint8_t* wg0 = smem - wg * kSmem;
-    float* ws = reinterpret_cast<float*>(smem + wk * kWarpBytes);
-    float* stage = ws;                 // [32 lanes][33]
-    float* s_inv = ws + 32 * 33;
-    int* s_row = reinterpret_cast<int*>(s_inv + 32);
-    int* s_ps = s_row + 32;
-    float* hrem = reinterpret_cast<float*>(shared_area(wg0));           // [2][4][32]
-    uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + 1024); // [4]
+    float* ws = reinterpret_cast<float*>(smem + q * kWarpBytes);
+    float* stage = ws;               // [8 rows][33]
+    float* s_inv = ws + 8 * 33;
+    int* s_row = reinterpret_cast<int*>(s_inv + 8);
+    int* s_ps = s_row + 8;
+    float* hrem = reinterpret_cast<float*>(shared_area(wg0));                   // [2][128]
+    uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + 2 * 128 * 4);  // [2][16]
     const bool failed = status_failed(st);
     const float lr = sp->lr;
+    const bool mine = (lane >> 3) == wg;  // this lane's TMEM row is one of the warp's 8
+    const int li = lane & 7;
     __syncwarp();  // the warp finished with the previous tile's scalars
-    s_inv[lane] = pre.inv;
-    s_row[lane] = failed ? -1 : pre.r;
-    s_ps[lane] = pre.ps;
+    if (mine) {
+      s_inv[li] = pre.inv;
+      s_row[li] = failed ? -1 : pre.r;
+      s_ps[li] = pre.ps;
+    }
     __syncwarp();
-    // this warp's 16 rows: lanes 16wg .. 16wg+15 of its TMEM quadrant; 4 rows x 8 lanes/op
+    // lanes run along dims: 8 lanes x float4 per row, rows u*4 + sub (u = 0, 1)
     const int sub = lane >> 3, q4 = (lane & 7) * 4;
-    int rl[4], rw[4];
+    int rw[2], ps[2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      rl[u] = 16 * wg + u * 4 + sub;
-      rw[u] = s_row[rl[u]];
+    for (int u = 0; u < 2; ++u) {
+      rw[u] = s_row[u * 4 + sub];
+      ps[u] = s_ps[u * 4 + sub];
     }
-    // ---- pass 1: half-dot w . dwt over this CTA's 256 dims
-    float dot[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      const int d = t.col0 + c0 + q4;
-      float4 w[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        w[u] = (rw[u] >= 0 && d < D) ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d)
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-      float v[32];
-      src.load(c0, v);
+    const int dbase = t.col0 + q4;
+    auto stage_chunk = [&](int c0) {
       __syncwarp();
-      if ((lane >> 4) == wg) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
-      }
-      __syncwarp();
-      if (d >= D) continue;
+      for (int h = 0; h < 2; ++h) {
+        float v[16];
+        src.load16(c0 + 16 * h, v);
+        if (mine) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (rw[u] < 0) continue;
-        const float* a = stage + rl[u] * 33 + q4;
-        float a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3];
-        const int rp = s_ps[rl[u]];
-        if (rp >= 0) {
-          const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)rp * D + d);
-          a0 += pc.x; a1 += pc.y; a2 += pc.z; a3 += pc.w;
+          for (int j = 0; j < 16; ++j) stage[li * 33 + 16 * h + j] = v[j];
         }
-        dot[u] += a0 * w[u].x + a1 * w[u].y + a2 * w[u].z + a3 * w[u].w;
+      }
+      __syncwarp();
+    };
+    auto dwt4 = [&](int u, int d) {
+      const float* a = stage + (u * 4 + sub) * 33 + q4;
+      float4 r = make_float4(a[0], a[1], a[2], a[3]);
+      if (ps[u] >= 0) {
+        const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)ps[u] * D + d);
+        r.x += pc.x; r.y += pc.y; r.z += pc.z; r.w += pc.w;
+      }
+      return r;
+    };
+    // ---- pass 1: half-dot w . dwt over this CTA's dims; W loads 4 chunks at a time
+    float dot[2] = {0.f, 0.f};
+#pragma unroll 1
+    for (int cb = 0; cb < NC; cb += 4) {
+      float4 w[4][2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int d = dbase + (cb + k) * 32;
+          w[k][u] = (rw[u] >= 0 && d < D) ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int d = dbase + (cb + k) * 32;
+        stage_chunk((cb + k) * 32);
+        if (d < D) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float4 a = dwt4(u, d);
+            dot[u] += a.x * w[k][u].x + a.y * w[k][u].y + a.z * w[k][u].z + a.w * w[k][u].w;
+          }
+        }
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 2; ++u) {
       dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 1);
       dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 2);
       dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 4);
     }
     if constexpr (kPair) {
-      const int par = t.iter & 1;
+      const int it = t.iter, par = it & 1, e = wg * 4 + q;
+      float* hr = hrem + par * 128 + q * 32 + wg * 8;  // this warp's 8 rows
       if ((lane & 7) == 0) {
         const uint32_t prank = pfc_sm100::cluster_ctarank() ^ 1u;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          pfc_sm100::st_cluster_f32(
-              pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hrem + (par * 4 + wk) * 32 + rl[u]), prank),
-              dot[u]);
-        pfc_sm100::mbar_arrive_cluster(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[wk]), prank));
+        for (int u = 0; u < 2; ++u)
+          pfc_sm100::st_cluster_f32(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hr + u * 4 + sub), prank),
+                                    dot[u]);
+        pfc_sm100::mbar_arrive_cluster(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[par * 16 + e]), prank));
       }
-      pfc_sm100::mbar_wait_cluster(&mb[wk], (uint32_t)par);
+      pfc_sm100::mbar_wait_cluster(&mb[par * 16 + e], (uint32_t)((it >> 1) & 1));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dot[u] += hrem[(par * 4 + wk) * 32 + rl[u]];
+      for (int u = 0; u < 2; ++u) dot[u] += hr[u * 4 + sub];
     }
-    float rcp[4], rinv[4];
+    float rcp[2], rinv[2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      rinv[u] = s_inv[rl[u]];
+    for (int u = 0; u < 2; ++u) {
+      rinv[u] = s_inv[u * 4 + sub];
       rcp[u] = dot[u] * rinv[u];  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
     }
-    // ---- pass 2: dW and the momentum-SGD update of the sampled rows
+    // ---- pass 2: dW and the momentum-SGD update; W + momentum loads 2 chunks at a time
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      const int d = t.col0 + c0 + q4;
-      float4 w[4], mo[4];
+    for (int cb = 0; cb < NC; cb += 2) {
+      float4 w[2][2], mo[2][2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool ok = rw[u] >= 0 && d < D;
-        w[u] = ok ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
-        mo[u] = ok ? *reinterpret_cast<const float4*>(Mom + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      float v[32];
-      src.load(c0, v);
-      __syncwarp();
-      if ((lane >> 4) == wg) {
+      for (int k = 0; k < 2; ++k)
 #pragma unroll
-        for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = v[q];
-      }
-      __syncwarp();
-      if (d >= D) continue;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (rw[u] < 0) continue;
-        const float* a = stage + rl[u] * 33 + q4;
-        float av[4] = {a[0], a[1], a[2], a[3]};
-        const int rp = s_ps[rl[u]];
-        if (rp >= 0) {
-          const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)rp * D + d);
-          av[0] += pc.x; av[1] += pc.y; av[2] += pc.z; av[3] += pc.w;
+        for (int u = 0; u < 2; ++u) {
+          const int d = dbase + (cb + k) * 32;
+          const bool ok = rw[u] >= 0 && d < D;
+          w[k][u] = ok ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
+          mo[k][u] = ok ? *reinterpret_cast<const float4*>(Mom + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        float wv[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-        float mv[4] = {mo[u].x, mo[u].y, mo[u].z, mo[u].w};
-        const float inv = rinv[u], cpj = rcp[u];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float dw = (av[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382
-          const float g = dw + wd * wv[e];                      // shardsim.hpp:152-153
-          const float vv = mu * mv[e] + g;                      // shardsim.hpp:154
-          mv[e] = vv;
-          wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
+      for (int k = 0; k < 2; ++k) {
+        const int d = dbase + (cb + k) * 32;
+        stage_chunk((cb + k) * 32);
+        if (d >= D) continue;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (rw[u] < 0) continue;
+          const float4 a4 = dwt4(u, d);
+          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+          float wv[4] = {w[k][u].x, w[k][u].y, w[k][u].z, w[k][u].w};
+          float mv[4] = {mo[k][u].x, mo[k][u].y, mo[k][u].z, mo[k][u].w};
+          const float inv = rinv[u], cpj = rcp[u];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float dw = (av[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382
+            const float g = dw + wd * wv[e];                      // shardsim.hpp:152-153
+            const float vv = mu * mv[e] + g;                      // shardsim.hpp:154
+            mv[e] = vv;
+            wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
+          }
+          const size_t o = (size_t)rw[u] * D + d;
+          *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+          *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
         }
-        const size_t o = (size_t)rw[u] * D + d;
-        *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-        *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
       }
     }
   }

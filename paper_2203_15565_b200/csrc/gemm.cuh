@@ -83,6 +83,9 @@ struct TmemSrc {
   __device__ __forceinline__ void load(int c0, float (&v)[32]) const {
     pfc_sm100::tmem_ld32(taddr + (uint32_t)c0, v);
   }
+  __device__ __forceinline__ void load16(int c0, float (&v)[16]) const {
+    pfc_sm100::tmem_ld16(taddr + (uint32_t)c0, v);
+  }
 };
 
 template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi>

@@ -481,17 +481,17 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     if constexpr (kUmma) {
       if (gw.n_tiles == 2)
-        err = launch_umma<kBN, 3, kNWG, false, true>(
+        err = launch_umma<kBN, 3, 4, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                               c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                              c->st, c->dw_prefetch ? 0 : 1});
+                              c->st});
       else
-        err = launch_umma<kBN, 3, kNWG, false, true>(
+        err = launch_umma<kBN, 3, 4, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<false>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                                c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                               c->st, c->dw_prefetch ? 0 : 1});
+                               c->st});
     } else {
       err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xs,
                                      (int)c->Dp, gw, DwStoreEpi{{}, (int)c->ncols, (int)c->D, c->dwt});

@@ -3,8 +3,9 @@
 //  * umma_gemm_kernel: persistent, warp-specialised tcgen05 GEMM for sm_100a.
 //      warp 0      : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier complete_tx)
 //      warp 1      : single-thread tcgen05.mma issuer (kind::f16, bf16 in, fp32 accum in TMEM)
-//      warp 2      : TMEM allocator (2 x BN columns: double-buffered accumulators)
-//      warps 4..7  : epilogue (tcgen05.ld 32x32b -> registers -> fused epilogue functor)
+//                    and TMEM allocator (2 x BN columns: double-buffered accumulators)
+//      warps 2..   : NWG epilogue warpgroups; warp w reads TMEM lane quadrant w % 4
+//                    (tcgen05.ld 32x32b -> registers -> fused epilogue functor)
 //    Tile = 128 x BN, BK = 64, STAGES-deep smem ring.  A and B may each be K-major or
 //    MN-major (UMMA descriptor transpose bits), so one gathered centre block and one
 //    normalised feature block serve all three GEMMs of the step without transposes.
@@ -88,8 +89,11 @@ struct TmemSrc {
   }
 };
 
+#ifndef PFC_CTRL_WARPS
+#define PFC_CTRL_WARPS 2
+#endif
 template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi>
-__global__ void __launch_bounds__(128 + 128 * NWG, 1)
+__global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, const GemmGeom g,
                      const __grid_constant__ Epi epi) {
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     epi.setup(epi_smem);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -196,10 +200,10 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         umma_commit(&tfull[as]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= PFC_CTRL_WARPS) {
     // epilogue warpgroups: warp w reads TMEM lanes 32*(w%4).. (row = accumulator row);
     // warpgroup wg takes columns [wg*BN/NWG, (wg+1)*BN/NWG) of every tile.
-    const int wg = (warp - 4) >> 2;
+    const int wg = (warp - PFC_CTRL_WARPS) >> 2;
     const int row = ((warp & 3) << 5) | lane;
     uint8_t* wsm = epi_smem + wg * Epi::kSmem;
     uint32_t it = 0;
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   }
   __syncthreads();
   if constexpr (Epi::kCluster > 1) cluster_sync_all();  // no CTA leaves while its partner writes
-  if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
+  if (warp == 1) tmem_dealloc(tmem_base, TMEM_COLS);
 #endif
 }
 

@@ -116,7 +116,10 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 constexpr int kBN = 256;  // tcgen05 tile 128 x 256
-constexpr int kNWG = 2;   // epilogue warpgroups per CTA on the tcgen05 engine
+constexpr int kNWG = 2;
+#ifndef PFC_DW_STAGES
+#define PFC_DW_STAGES 3
+#endif   // epilogue warpgroups per CTA on the tcgen05 engine
 constexpr int kSimtBN = 64;
 
 struct PhaseTimer {
@@ -272,7 +275,7 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
     if (grid > total) grid = total;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(128 + 128 * NWG);
+    cfg.blockDim = dim3(32 * PFC_CTRL_WARPS + 128 * NWG);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
@@ -285,7 +288,7 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
     c->launches++;
     return cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epi);
   } else {
-    kern<<<grid, 128 + 128 * NWG, smem, c->stream>>>(ta, tb, g, epi);
+    kern<<<grid, 32 * PFC_CTRL_WARPS + 128 * NWG, smem, c->stream>>>(ta, tb, g, epi);
     c->launches++;
     return cudaGetLastError();
   }
@@ -481,13 +484,13 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     if constexpr (kUmma) {
       if (gw.n_tiles == 2)
-        err = launch_umma<kBN, 3, 4, false, true>(
+        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                               c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
                               c->st});
       else
-        err = launch_umma<kBN, 3, 4, false, true>(
+        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<false>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                                c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,

@@ -1,0 +1,10 @@
+set -u
+cp paper_2203_15565_b200/libpfc_gpu.so /tmp/main.so
+for v in "$@"; do
+  cp paper_2203_15565_b200/$v.so paper_2203_15565_b200/libpfc_gpu.so
+  for rep in 1 2; do
+    timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e > gpurun_out/bench_$v.log 2>&1
+    python -c "import json,sys;d=json.loads(open('gpurun_out/bench_$v.log').read().strip().splitlines()[-1]);print('$v', round(d['value']), round(d['ms_per_step'],4), {k:round(v['ms'],4) for k,v in d['phases_ms'].items()})"
+  done
+done
+cp /tmp/main.so paper_2203_15565_b200/libpfc_gpu.so

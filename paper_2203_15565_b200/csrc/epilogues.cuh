@@ -24,6 +24,7 @@
 //                momentum-SGD of the sampled rows (shardsim.hpp:139-159, 377-384).
 //   DwStoreEpi   fp32 validation engine: stores dwt; dw_rows_update_kernel finishes the rows.
 #pragma once
+#include <utility>
 #include <type_traits>
 
 #include "common.cuh"
@@ -224,17 +225,51 @@ struct DxPartEpi : NoSetup {
 };
 
 // ------------------------------------------------------------------------------- DwUpdateEpi
-// Four epilogue warpgroups (16 warps): the update is a latency-bound gathered-row stream (W and
-// momentum read + write), and bytes in flight per SM, i.e. warps x loads per warp, set its speed
-// (profiles/micro/rowupd.cu: 8 warps/SM reach 4.7 TB/s, 16 warps 6.2 TB/s).  Each CTA owns a
-// 256-dim half of a 128-class block; warp (g, q) owns the 8 rows 32q + 8g .. +7 of TMEM lane
-// quadrant q over all 256 dims, so a row's CTA-local half-dot is warp-local.  With kPair
-// (D = 512) the two CTAs of a 2-CTA cluster own the two halves and swap half-dots warp by warp
-// through DSMEM (one mbarrier per warp and tile parity).
+// Four epilogue warpgroups (16 warps).  The update is a gathered-row stream (W and momentum read
+// + write) whose speed is set by the bytes in flight per SM (profiles/micro/rowupd.cu: 16 warps
+// with 6 KB each in flight reach 6.2 TB/s, 8 warps with 1.5 KB 3.3 TB/s).  Registers cannot hold
+// that much next to the TMEM chunk, so each warp streams its rows through a 6 KB cp.async ring
+// in shared memory: a compile-time greedy schedule keeps it full across both passes of a tile
+// (the update pass's loads are in flight during the dot pass and the half-dot exchange).
+//
+// Each CTA owns a 256-dim half of a 128-class block; warp (g, q) owns the 8 rows 32q + 8g .. +7
+// of TMEM lane quadrant q over all 256 dims, so a row's CTA-local half-dot is warp-local.  With
+// kPair (D = 512) the two CTAs of a 2-CTA cluster own the two halves and swap half-dots warp by
+// warp (st.async into the peer's shared memory, completing its per-warp mbarrier).
+namespace dw_ring {
+constexpr int kNC = 8;                      // 32-dim chunks per 256-dim tile half
+constexpr int kItems = 2 * kNC;             // W chunk c (dot pass), then W + momentum chunk c
+constexpr int kCap = 6;                     // ring capacity in 1 KB sub-slots (8 rows x 128 B)
+__host__ __device__ constexpr int size(int i) { return i < kNC ? 1 : 2; }
+__host__ __device__ constexpr int pos(int i) {                  // first sub-slot of item i
+  int p = 0;
+  for (int j = 0; j < i; ++j) p += size(j);
+  return p % kCap;
+}
+__host__ __device__ constexpr int issued_before(int k) {        // items issued before item k is consumed (greedy)
+  int issued = 0, used = 0;
+  for (int c = 0;; ++c) {
+    while (issued < kItems && used + size(issued) <= kCap) used += size(issued++);
+    if (c == k) return issued;
+    used -= size(c);
+  }
+}
+// compile-time loop: f(std::integral_constant<int, I>) for I in [A, B)
+template <int A, int B, class F>
+__device__ __forceinline__ void static_range(F&& f) {
+  if constexpr (A < B) {
+    f(std::integral_constant<int, A>{});
+    static_range<A + 1, B>(f);
+  }
+}
+}  // namespace dw_ring
+
 template <bool kPair>
 struct DwUpdateEpi {
   static constexpr int kCluster = kPair ? 2 : 1;
-  static constexpr int kWarpFloats = 8 * 33 + 3 * 8;  // stage [8 rows][33] + inv/row/pslot
+  static constexpr int kStageFloats = 8 * 36;             // TMEM chunk of the warp's 8 rows
+  static constexpr int kRingFloats = dw_ring::kCap * 256;  // 6 x 1 KB
+  static constexpr int kWarpFloats = kStageFloats + kRingFloats + 3 * 8;  // + inv/row/pslot
   static constexpr int kWarpBytes = kWarpFloats * 4;
   // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][128 rows] + mbarriers [2][16 warps]
   static constexpr int kSharedBytes = 2 * 128 * 4 + 2 * 16 * 8;
@@ -273,7 +308,7 @@ struct DwUpdateEpi {
   __device__ __forceinline__ void setup(uint8_t* epi_base) const {
     if constexpr (kPair) {
       uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 2 * 128 * 4);
-      for (int k = 0; k < 32; ++k) pfc_sm100::mbar_init(&mb[k], 4);  // 4 writer lanes per warp
+      for (int k = 0; k < 32; ++k) pfc_sm100::mbar_init(&mb[k], 1);  // local arrive + 32 tx bytes
     }
   }
 
@@ -281,12 +316,13 @@ struct DwUpdateEpi {
   __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
                                       uint8_t* smem, const Pre& pre) const {
     static_assert(NWG == 4 && BN == 256, "DwUpdateEpi: 4 warpgroups, 256-dim tiles");
-    constexpr int NC = BN / 32;  // 32-dim chunks
+    using namespace dw_ring;
     const int q = row >> 5, lane = row & 31;
     uint8_t* wg0 = smem - wg * kSmem;
     float* ws = reinterpret_cast<float*>(smem + q * kWarpBytes);
-    float* stage = ws;               // [8 rows][33]
-    float* s_inv = ws + 8 * 33;
+    float* stage = ws;                          // [8 rows][36]
+    float* ring = ws + kStageFloats;            // [6 sub-slots][8 rows][32]
+    float* s_inv = ring + kRingFloats;
     int* s_row = reinterpret_cast<int*>(s_inv + 8);
     int* s_ps = s_row + 8;
     float* hrem = reinterpret_cast<float*>(shared_area(wg0));                   // [2][128]
@@ -311,6 +347,31 @@ struct DwUpdateEpi {
       ps[u] = s_ps[u * 4 + sub];
     }
     const int dbase = t.col0 + q4;
+    const bool anyp = __any_sync(0xffffffffu, ps[0] >= 0 || ps[1] >= 0);  // positives are rare
+    if constexpr (kPair) {  // this tile's exchange: the peer's 8 half-dots arrive as 32 tx bytes
+      if (lane == 0) pfc_sm100::mbar_arrive_expect_tx(&mb[(t.iter & 1) * 16 + wg * 4 + q], 32u);
+    }
+    // this lane's 16-byte piece of row (u*4+sub) in ring sub-slot p
+    const uint32_t ring_s = pfc_sm100::smem_u32(ring);
+    auto slot_off = [&](int p, int u) { return (uint32_t)((p * 256 + (u * 4 + sub) * 32 + q4) * 4); };
+    auto issue = [&](auto ic) {  // item i: W chunk i (i < 8) or W + momentum chunk i - 8
+      constexpr int i = decltype(ic)::value;
+      constexpr int c = i < kNC ? i : i - kNC;
+      constexpr int p = pos(i);
+      const int d = dbase + c * 32;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (rw[u] >= 0 && d < D) {
+          const size_t o = (size_t)rw[u] * D + d;
+          pfc_sm100::cp_async16(ring_s + slot_off(p, u), W + o);
+          if (i >= kNC) pfc_sm100::cp_async16(ring_s + slot_off((p + 1) % kCap, u), Mom + o);
+        }
+      }
+      pfc_sm100::cp_async_commit();
+    };
+    auto ring4 = [&](int p, int u) {
+      return *reinterpret_cast<const float4*>(ring + p * 256 + (u * 4 + sub) * 32 + q4);
+    };
     auto stage_chunk = [&](int c0) {
       __syncwarp();
 #pragma unroll
@@ -319,113 +380,96 @@ struct DwUpdateEpi {
         src.load16(c0 + 16 * h, v);
         if (mine) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) stage[li * 33 + 16 * h + j] = v[j];
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float4*>(stage + li * 36 + 16 * h + 4 * j) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
       }
       __syncwarp();
     };
     auto dwt4 = [&](int u, int d) {
-      const float* a = stage + (u * 4 + sub) * 33 + q4;
-      float4 r = make_float4(a[0], a[1], a[2], a[3]);
-      if (ps[u] >= 0) {
-        const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)ps[u] * D + d);
-        r.x += pc.x; r.y += pc.y; r.z += pc.z; r.w += pc.w;
+      float4 r = *reinterpret_cast<const float4*>(stage + (u * 4 + sub) * 36 + q4);
+      if (anyp) {
+        if (ps[u] >= 0) {
+          const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)ps[u] * D + d);
+          r.x += pc.x; r.y += pc.y; r.z += pc.z; r.w += pc.w;
+        }
       }
       return r;
     };
-    // ---- pass 1: half-dot w . dwt over this CTA's dims; W loads 4 chunks at a time
-    float dot[2] = {0.f, 0.f};
-#pragma unroll 1
-    for (int cb = 0; cb < NC; cb += 4) {
-      float4 w[4][2];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
+
+    static_range<0, issued_before(0)>(issue);
+    float dot[2] = {0.f, 0.f}, rcp[2] = {0.f, 0.f}, rinv[2] = {0.f, 0.f};
+    static_range<0, kItems>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int c = k < kNC ? k : k - kNC;
+      const int d = dbase + c * 32;
+      if constexpr (k == kNC) {
+        // ---- dot pass done: reduce, exchange half-dots with the peer CTA, center_proj
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int d = dbase + (cb + k) * 32;
-          w[k][u] = (rw[u] >= 0 && d < D) ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d)
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 1);
+          dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 2);
+          dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 4);
+        }
+        if constexpr (kPair) {
+          const int it = t.iter, par = it & 1, e = wg * 4 + q;
+          float* hr = hrem + par * 128 + q * 32 + wg * 8;  // this warp's 8 rows
+          if ((lane & 7) == 0) {
+            const uint32_t prank = pfc_sm100::cluster_ctarank() ^ 1u;
+            const uint32_t rbar = pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[par * 16 + e]), prank);
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+              pfc_sm100::st_async_f32(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hr + u * 4 + sub), prank),
+                                      dot[u], rbar);
+          }
+          pfc_sm100::mbar_wait_cluster(&mb[par * 16 + e], (uint32_t)((it >> 1) & 1));
+#pragma unroll
+          for (int u = 0; u < 2; ++u) dot[u] += hr[u * 4 + sub];
         }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int d = dbase + (cb + k) * 32;
-        stage_chunk((cb + k) * 32);
-        if (d < D) {
+        for (int u = 0; u < 2; ++u) {
+          rinv[u] = s_inv[u * 4 + sub];
+          rcp[u] = dot[u] * rinv[u];  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
+        }
+      }
+      pfc_sm100::cp_async_wait<issued_before(k) - k - 1>();  // item k landed (this lane's pieces)
+      stage_chunk(c * 32);
+      if (d < D) {
+        if constexpr (k < kNC) {  // dot pass: half-dot w . dwt over this CTA's dims
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const float4 a = dwt4(u, d);
-            dot[u] += a.x * w[k][u].x + a.y * w[k][u].y + a.z * w[k][u].z + a.w * w[k][u].w;
+            const float4 w = ring4(pos(k), u);
+            dot[u] += a.x * w.x + a.y * w.y + a.z * w.z + a.w * w.w;
+          }
+        } else {  // update pass: dW and the momentum-SGD update of the sampled rows
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (rw[u] < 0) continue;
+            const float4 a4 = dwt4(u, d);
+            const float4 w4 = ring4(pos(k), u), m4 = ring4((pos(k) + 1) % kCap, u);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+            float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+            float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+            const float inv = rinv[u], cpj = rcp[u];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float dw = (av[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382
+              const float g = dw + wd * wv[e];                      // shardsim.hpp:152-153
+              const float vv = mu * mv[e] + g;                      // shardsim.hpp:154
+              mv[e] = vv;
+              wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
+            }
+            const size_t o = (size_t)rw[u] * D + d;
+            *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+            *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
           }
         }
       }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 1);
-      dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 2);
-      dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 4);
-    }
-    if constexpr (kPair) {
-      const int it = t.iter, par = it & 1, e = wg * 4 + q;
-      float* hr = hrem + par * 128 + q * 32 + wg * 8;  // this warp's 8 rows
-      if ((lane & 7) == 0) {
-        const uint32_t prank = pfc_sm100::cluster_ctarank() ^ 1u;
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-          pfc_sm100::st_cluster_f32(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hr + u * 4 + sub), prank),
-                                    dot[u]);
-        pfc_sm100::mbar_arrive_cluster(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[par * 16 + e]), prank));
-      }
-      pfc_sm100::mbar_wait_cluster(&mb[par * 16 + e], (uint32_t)((it >> 1) & 1));
-#pragma unroll
-      for (int u = 0; u < 2; ++u) dot[u] += hr[u * 4 + sub];
-    }
-    float rcp[2], rinv[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      rinv[u] = s_inv[u * 4 + sub];
-      rcp[u] = dot[u] * rinv[u];  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
-    }
-    // ---- pass 2: dW and the momentum-SGD update; W + momentum loads 2 chunks at a time
-#pragma unroll 1
-    for (int cb = 0; cb < NC; cb += 2) {
-      float4 w[2][2], mo[2][2];
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int d = dbase + (cb + k) * 32;
-          const bool ok = rw[u] >= 0 && d < D;
-          w[k][u] = ok ? *reinterpret_cast<const float4*>(W + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
-          mo[k][u] = ok ? *reinterpret_cast<const float4*>(Mom + (size_t)rw[u] * D + d) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int d = dbase + (cb + k) * 32;
-        stage_chunk((cb + k) * 32);
-        if (d >= D) continue;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (rw[u] < 0) continue;
-          const float4 a4 = dwt4(u, d);
-          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-          float wv[4] = {w[k][u].x, w[k][u].y, w[k][u].z, w[k][u].w};
-          float mv[4] = {mo[k][u].x, mo[k][u].y, mo[k][u].z, mo[k][u].w};
-          const float inv = rinv[u], cpj = rcp[u];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float dw = (av[e] - cpj * (wv[e] * inv)) * inv;  // shardsim.hpp:382
-            const float g = dw + wd * wv[e];                      // shardsim.hpp:152-153
-            const float vv = mu * mv[e] + g;                      // shardsim.hpp:154
-            mv[e] = vv;
-            wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
-          }
-          const size_t o = (size_t)rw[u] * D + d;
-          *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-          *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
-        }
-      }
-    }
+      // refill the ring (reads of item k's sub-slots were consumed above: in-order issue)
+      static_range<issued_before(k), issued_before(k + 1)>(issue);
+    });
   }
 };
 

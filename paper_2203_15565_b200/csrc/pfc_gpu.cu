@@ -118,7 +118,7 @@ int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 constexpr int kBN = 256;  // tcgen05 tile 128 x 256
 constexpr int kNWG = 2;
 #ifndef PFC_DW_STAGES
-#define PFC_DW_STAGES 3
+#define PFC_DW_STAGES 2
 #endif   // epilogue warpgroups per CTA on the tcgen05 engine
 constexpr int kSimtBN = 64;
 

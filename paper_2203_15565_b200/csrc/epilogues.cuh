@@ -236,10 +236,13 @@ struct DxPartEpi : NoSetup {
 // of TMEM lane quadrant q over all 256 dims, so a row's CTA-local half-dot is warp-local.  With
 // kPair (D = 512) the two CTAs of a 2-CTA cluster own the two halves and swap half-dots warp by
 // warp (st.async into the peer's shared memory, completing its per-warp mbarrier).
+#ifndef PFC_DW_CAP
+#define PFC_DW_CAP 6
+#endif
 namespace dw_ring {
 constexpr int kNC = 8;                      // 32-dim chunks per 256-dim tile half
 constexpr int kItems = 2 * kNC;             // W chunk c (dot pass), then W + momentum chunk c
-constexpr int kCap = 6;                     // ring capacity in 1 KB sub-slots (8 rows x 128 B)
+constexpr int kCap = PFC_DW_CAP;            // ring capacity in 1 KB sub-slots (8 rows x 128 B)
 __host__ __device__ constexpr int size(int i) { return i < kNC ? 1 : 2; }
 __host__ __device__ constexpr int pos(int i) {                  // first sub-slot of item i
   int p = 0;

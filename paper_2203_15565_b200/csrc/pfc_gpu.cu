@@ -182,7 +182,6 @@ struct Ctx {
   float* dx_part = nullptr;  // [S][maxB][D]
   float* dX = nullptr;       // [maxB][D]
   int max_splits = 1;
-  int dw_prefetch = 1;  // DwUpdateEpi bulk L2 prefetch of the next tile's rows (PFC_DW_PREFETCH=0 off)
   // host-path scratch
   double* xdb = nullptr;  // D x maxB fp64
   StepStatus* st = nullptr;
@@ -758,7 +757,6 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->ldg = round_up(desc->max_batch, 8);  // E^T row stride
   c->pool_stride = std::max<int64_t>(c->blk, 1);
   c->maxB = desc->max_batch;
-  if (const char* e = getenv("PFC_DW_PREFETCH")) c->dw_prefetch = atoi(e);
   c->mg.kind = desc->margin_kind;
   c->mg.s = (float)desc->margin_scale;
   c->mg.sd = desc->margin_scale;

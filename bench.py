@@ -161,7 +161,8 @@ def cpu_reference_time(C_full, K, D, B, r, steps, warmup, target_s=2.0):
             "sample": (f"reference distributed_partial_step at C={C_s} (cap {cap_s}/shard vs "
                        f"{cap_full}), K={K}, B={B}, d={D}, r={r}, ArcFace; median of {steps} steps "
                        f"= {t:.3f} s, scaled x{scale:.1f} (work is linear in cap); "
-                       f"PFC_SIM_THREADS={cores} (reference parallelises over K shards)"),
+                       f"the reference runs one thread per shard: {threads} threads on "
+                       f"{cores} host cores"),
             "step_s_sample": t, "host_cores": cores}
 
 
@@ -188,7 +189,7 @@ def workload_config(args):
             "classes": args.classes, "dim": args.dim, "global_batch": args.batch, "r": args.r,
             "reference_shards": args.shards, "margin": "arcface s=64 m=0.5",
             "parallelism": f"class-sharded x{args.gpus}",
-            "l2": "no flush: per-step working set (W+mom 8.2 GB, W^ 205 MB, G 410 MB) >> 126 MB L2"}
+            "l2": "no flush: per-step working set (W+mom 8.2 GB, W^ 205 MB, E 410 MB) >> 126 MB L2"}
 
 
 def main():

@@ -56,6 +56,7 @@ __device__ __forceinline__ void store_out1(float* p, float v) { *p = v; }
 
 struct NoSetup {
   static constexpr int kCluster = 1;
+  static constexpr bool kNext = false;  // true: run_next() also receives the next tile's Pre
   __device__ __forceinline__ void setup(uint8_t*) const {}
 };
 
@@ -243,20 +244,26 @@ namespace dw_ring {
 constexpr int kNC = 8;                      // 32-dim chunks per 256-dim tile half
 constexpr int kItems = 2 * kNC;             // W chunk c (dot pass), then W + momentum chunk c
 constexpr int kCap = PFC_DW_CAP;            // ring capacity in 1 KB sub-slots (8 rows x 128 B)
-__host__ __device__ constexpr int size(int i) { return i < kNC ? 1 : 2; }
+constexpr int kTileSlots = kNC * 1 + kNC * 2;
+static_assert(kTileSlots % kCap == 0, "ring positions must repeat every tile");
+__host__ __device__ constexpr int size(int i) { return (i % kItems) < kNC ? 1 : 2; }
 __host__ __device__ constexpr int pos(int i) {                  // first sub-slot of item i
   int p = 0;
-  for (int j = 0; j < i; ++j) p += size(j);
+  for (int j = 0; j < i % kItems; ++j) p += size(j);
   return p % kCap;
 }
-__host__ __device__ constexpr int issued_before(int k) {        // items issued before item k is consumed (greedy)
+// Greedy issue over the endless item stream (tile after tile): items issued before item k is
+// consumed, in steady state (the previous tile already issued this tile's first items).
+__host__ __device__ constexpr int issued_before(int k) {
   int issued = 0, used = 0;
   for (int c = 0;; ++c) {
-    while (issued < kItems && used + size(issued) <= kCap) used += size(issued++);
-    if (c == k) return issued;
+    while (issued < 3 * kItems && used + size(issued) <= kCap) used += size(issued++);
+    if (c == kItems + k) return issued - kItems;
     used -= size(c);
   }
 }
+constexpr int kHead = issued_before(0);     // items of a tile in flight when it starts
+static_assert(issued_before(kItems) - kItems == kHead, "periodic steady state");
 // compile-time loop: f(std::integral_constant<int, I>) for I in [A, B)
 template <int A, int B, class F>
 __device__ __forceinline__ void static_range(F&& f) {
@@ -270,9 +277,10 @@ __device__ __forceinline__ void static_range(F&& f) {
 template <bool kPair>
 struct DwUpdateEpi {
   static constexpr int kCluster = kPair ? 2 : 1;
+  static constexpr bool kNext = true;
   static constexpr int kStageFloats = 8 * 36;             // TMEM chunk of the warp's 8 rows
   static constexpr int kRingFloats = dw_ring::kCap * 256;  // 6 x 1 KB
-  static constexpr int kWarpFloats = kStageFloats + kRingFloats + 3 * 8;  // + inv/row/pslot
+  static constexpr int kWarpFloats = kStageFloats + kRingFloats + 2 * 3 * 8;  // + [2][inv|row|pslot]
   static constexpr int kWarpBytes = kWarpFloats * 4;
   // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][128 rows] + mbarriers [2][16 warps]
   static constexpr int kSharedBytes = 2 * 128 * 4 + 2 * 16 * 8;
@@ -315,9 +323,13 @@ struct DwUpdateEpi {
     }
   }
 
+  // The ring runs across tiles: the end of tile i issues tile i+1's first loads (its rows come
+  // from pre_next), so the ring never drains at a tile boundary.  The CTA's dims half (col0) is
+  // the same for all its tiles (the tile stride is a multiple of n_tiles).
   template <int BN, int NWG, class Src>
-  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
-                                      uint8_t* smem, const Pre& pre) const {
+  __device__ __forceinline__ void run_next(const TileInfo& t, const Src& src, int row, int wg,
+                                           uint8_t* smem, const Pre& pre, const Pre& pre_next,
+                                           bool has_next) const {
     static_assert(NWG == 4 && BN == 256, "DwUpdateEpi: 4 warpgroups, 256-dim tiles");
     using namespace dw_ring;
     const int q = row >> 5, lane = row & 31;
@@ -325,9 +337,11 @@ struct DwUpdateEpi {
     float* ws = reinterpret_cast<float*>(smem + q * kWarpBytes);
     float* stage = ws;                          // [8 rows][36]
     float* ring = ws + kStageFloats;            // [6 sub-slots][8 rows][32]
-    float* s_inv = ring + kRingFloats;
+    float* sc = ring + kRingFloats;             // [2 tile parity][inv 8 | row 8 | pslot 8]
+    float* s_inv = sc + (t.iter & 1) * 24;
     int* s_row = reinterpret_cast<int*>(s_inv + 8);
     int* s_ps = s_row + 8;
+    int* s_row_n = reinterpret_cast<int*>(sc + ((t.iter & 1) ^ 1) * 24 + 8);
     float* hrem = reinterpret_cast<float*>(shared_area(wg0));                   // [2][128]
     uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + 2 * 128 * 4);  // [2][16]
     const bool failed = status_failed(st);
@@ -336,18 +350,25 @@ struct DwUpdateEpi {
     const int li = lane & 7;
     __syncwarp();  // the warp finished with the previous tile's scalars
     if (mine) {
-      s_inv[li] = pre.inv;
-      s_row[li] = failed ? -1 : pre.r;
-      s_ps[li] = pre.ps;
+      if (t.iter == 0) {  // later tiles' scalars were stored by the tile before them
+        s_inv[li] = pre.inv;
+        s_row[li] = failed ? -1 : pre.r;
+        s_ps[li] = pre.ps;
+      }
+      float* sn = sc + ((t.iter & 1) ^ 1) * 24;
+      sn[li] = pre_next.inv;
+      reinterpret_cast<int*>(sn)[8 + li] = (failed || !has_next) ? -1 : pre_next.r;
+      reinterpret_cast<int*>(sn)[16 + li] = pre_next.ps;
     }
     __syncwarp();
     // lanes run along dims: 8 lanes x float4 per row, rows u*4 + sub (u = 0, 1)
     const int sub = lane >> 3, q4 = (lane & 7) * 4;
-    int rw[2], ps[2];
+    int rw[2], ps[2], rwn[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       rw[u] = s_row[u * 4 + sub];
       ps[u] = s_ps[u * 4 + sub];
+      rwn[u] = s_row_n[u * 4 + sub];
     }
     const int dbase = t.col0 + q4;
     const bool anyp = __any_sync(0xffffffffu, ps[0] >= 0 || ps[1] >= 0);  // positives are rare
@@ -357,17 +378,21 @@ struct DwUpdateEpi {
     // this lane's 16-byte piece of row (u*4+sub) in ring sub-slot p
     const uint32_t ring_s = pfc_sm100::smem_u32(ring);
     auto slot_off = [&](int p, int u) { return (uint32_t)((p * 256 + (u * 4 + sub) * 32 + q4) * 4); };
-    auto issue = [&](auto ic) {  // item i: W chunk i (i < 8) or W + momentum chunk i - 8
+    // item i of the stream: W chunk c (i % 16 < 8) or W + momentum chunk c of this tile
+    // (i < 16) or of the next one (i >= 16; an empty group when there is none)
+    auto issue = [&](auto ic) {
       constexpr int i = decltype(ic)::value;
-      constexpr int c = i < kNC ? i : i - kNC;
+      constexpr int ii = i % kItems;
+      constexpr int c = ii < kNC ? ii : ii - kNC;
       constexpr int p = pos(i);
       const int d = dbase + c * 32;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        if (rw[u] >= 0 && d < D) {
-          const size_t o = (size_t)rw[u] * D + d;
+        const int r = i < kItems ? rw[u] : rwn[u];
+        if (r >= 0 && d < D) {
+          const size_t o = (size_t)r * D + d;
           pfc_sm100::cp_async16(ring_s + slot_off(p, u), W + o);
-          if (i >= kNC) pfc_sm100::cp_async16(ring_s + slot_off((p + 1) % kCap, u), Mom + o);
+          if (ii >= kNC) pfc_sm100::cp_async16(ring_s + slot_off((p + 1) % kCap, u), Mom + o);
         }
       }
       pfc_sm100::cp_async_commit();
@@ -401,7 +426,7 @@ struct DwUpdateEpi {
       return r;
     };
 
-    static_range<0, issued_before(0)>(issue);
+    if (t.iter == 0) static_range<0, kHead>(issue);  // otherwise issued by the previous tile
     float dot[2] = {0.f, 0.f}, rcp[2] = {0.f, 0.f}, rinv[2] = {0.f, 0.f};
     static_range<0, kItems>([&](auto kc) {
       constexpr int k = decltype(kc)::value;

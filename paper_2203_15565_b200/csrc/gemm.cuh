@@ -225,7 +225,10 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const TmemSrc src{tmem_base + as * BN + ((uint32_t)((warp & 3) * 32) << 16)};
-      epi.template run<BN, NWG>(ti, src, row, wg, wsm, pre);
+      if constexpr (Epi::kNext)  // the epilogue also starts the next tile's loads
+        epi.template run_next<BN, NWG>(ti, src, row, wg, wsm, pre, pre_n, t + stride < total);
+      else
+        epi.template run<BN, NWG>(ti, src, row, wg, wsm, pre);
       tc_fence_before();
       mbar_arrive(&tempty[as]);
       pre = pre_n;

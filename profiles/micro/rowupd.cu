@@ -66,6 +66,43 @@ __global__ void upd_b(float* __restrict__ W, float* __restrict__ M, const float*
   }
 }
 
+// (d) temporal spread: a warp owns G*4 rows x 256 dims; chunk-major order (c outer, row groups
+// inner, 4 row groups per batch of loads): a row's consecutive 128 B chunks are G/4 batches apart
+template <int G>
+__global__ void upd_d(float* __restrict__ W, float* __restrict__ M, const float* __restrict__ src,
+                      const int* __restrict__ rows, int n, float lr) {
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int sub = lane >> 3, q = (lane & 7) * 4;
+  constexpr int RB = 4 * G;
+  for (int blk = warp; blk < n / RB * 2; blk += nw) {
+    const int r0 = (blk >> 1) * RB, h = (blk & 1) * 256;
+    for (int c = 0; c < 8; ++c) {
+      const int d = h + c * 32 + q;
+      for (int g0 = 0; g0 < G; g0 += 4) {
+        float4 w[4], m[4], a[4];
+        size_t o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = r0 + (g0 + u) * 4 + sub;
+          o[u] = (size_t)__ldg(rows + rr) * D + d;
+          w[u] = *reinterpret_cast<const float4*>(W + o[u]);
+          m[u] = *reinterpret_cast<const float4*>(M + o[u]);
+          a[u] = __ldg(reinterpret_cast<const float4*>(src + (size_t)rr * D + d));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          m[u].x = 0.9f * m[u].x + a[u].x; m[u].y = 0.9f * m[u].y + a[u].y;
+          m[u].z = 0.9f * m[u].z + a[u].z; m[u].w = 0.9f * m[u].w + a[u].w;
+          w[u].x -= lr * m[u].x; w[u].y -= lr * m[u].y; w[u].z -= lr * m[u].z; w[u].w -= lr * m[u].w;
+          *reinterpret_cast<float4*>(W + o[u]) = w[u];
+          *reinterpret_cast<float4*>(M + o[u]) = m[u];
+        }
+      }
+    }
+  }
+}
+
 int main() {
   const int C = 2000000, n = 200000;
   float *W, *M, *src;
@@ -82,7 +119,7 @@ int main() {
   std::mt19937 g(1);
   std::shuffle(h.begin(), h.end(), g);
   h.resize(n);
-  for (int sorted = 0; sorted < 2; ++sorted) {
+  for (int sorted = 0; sorted < 1; ++sorted) {
     std::vector<int> hh = h;
     if (sorted) std::sort(hh.begin(), hh.end());
     cudaMemcpy(rows, hh.data(), n * 4, cudaMemcpyHostToDevice);
@@ -115,6 +152,10 @@ int main() {
     run("grouped U=4 16warps/SM", upd_b<4>, 148, 512);
     run("grouped U=8 16warps/SM", upd_b<8>, 148, 512);
     run("grouped U=4 64warps/SM", upd_b<4>, 148 * 4, 512);
+    run("spread G=4 16warps/SM", upd_d<4>, 148, 512);
+    run("spread G=8 16warps/SM", upd_d<8>, 148, 512);
+    run("spread G=32 16warps/SM", upd_d<32>, 148, 512);
+    run("spread G=128 16warps/SM", upd_d<128>, 148, 512);
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }

@@ -163,13 +163,21 @@ struct alignas(64) FwdEpi : NoSetup {
         uint8_t* sb = stage + (kk & 1) * 2048;
         if (lane == 0) pfc_sm100::bulk_wait_read<1>();  // this buffer's store, 2 groups ago
         __syncwarp();
-        const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
+        // element (class q, row b) lives at byte q*64 + b*2, its 16-byte chunk swizzled by q.
+        // Lanes b, b^1 swap halves of their packed (q, q+1) pairs so that each stores one
+        // 4-byte (rows b&~1, b|1) pair: the even lane class q, the odd lane class q+1.
+        const bool odd = lane & 1;
+        const int b0 = lane & ~1;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          // element (class q, row lane) at byte q*64 + lane*2, 16-byte chunk swizzled by q
-          const int chunk = (lane >> 3) ^ ((q >> 1) & 3);
-          *reinterpret_cast<__nv_bfloat16*>(sb + q * 64 + chunk * 16 + (lane & 7) * 2) =
-              rv ? __float2bfloat16_rn(e[q]) : zero;
+        for (int q = 0; q < 32; q += 2) {
+          __nv_bfloat162 own = __floats2bfloat162_rn(rv ? e[q] : 0.f, rv ? e[q + 1] : 0.f);
+          const uint32_t ou = *reinterpret_cast<uint32_t*>(&own);
+          const uint32_t nu = __shfl_xor_sync(0xffffffffu, ou, 1);
+          // even: (own.lo, nb.lo) = class q rows (b, b+1); odd: (nb.hi, own.hi) = class q+1
+          const uint32_t packed = odd ? __byte_perm(nu, ou, 0x7632) : __byte_perm(ou, nu, 0x5410);
+          const int qq = q + (odd ? 1 : 0);
+          const int chunk = (b0 >> 3) ^ ((qq >> 1) & 3);
+          *reinterpret_cast<uint32_t*>(sb + qq * 64 + chunk * 16 + (b0 & 7) * 2) = packed;
         }
         pfc_sm100::fence_proxy_async_smem();
         __syncwarp();

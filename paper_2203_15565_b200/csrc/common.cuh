@@ -43,7 +43,7 @@ struct StepStatus {
   int32_t rejection_shards;   // count of shards that needed the sequential sampler
   int32_t batch_too_large;
   int32_t underflow_row;      // first row whose exp(z - offset) sum underflowed, else INT32_MAX
-  int32_t pad;
+  uint32_t fin_blocks;        // finalize_stats blocks done (last one reduces the loss)
 };
 
 // Per-step scalars, written on the device by step_begin_kernel (the only graph node whose

@@ -202,40 +202,70 @@ __global__ void sum_segments_kernel(const ST* __restrict__ seg, int nseg, int B,
 // terms, the row scale of G and the positive's correction:
 //   S = sum_r ls[r];  loss_b = log S + o - z_pos;  rowscale = s / (B S)
 //   delta_b = ((p_pos - 1)/B) margin'(c_pos) - rowscale * E_pos(stored)   (owner rank only)
+// With one rank (seg != nullptr) the rank-local sum is formed here from the nseg segment sums
+// (same order and rounding as sum_segments_kernel).  The last block to finish reduces loss_row
+// in a fixed order into the step's loss (was loss_reduce_kernel).
 template <typename ST>
-__global__ void finalize_stats_kernel(const ST* __restrict__ ls, int R, int B,
-                                      const double* __restrict__ zpos,
-                                      const double* __restrict__ cpos,
-                                      const float* __restrict__ epos,
-                                      const int32_t* __restrict__ pos_col,
-                                      const int* __restrict__ hasval, int has_filter,
-                                      MarginDev mg, ST* __restrict__ rowscale,
-                                      ST* __restrict__ delta, double* __restrict__ loss_row,
-                                      StepStatus* st) {
+__global__ void __launch_bounds__(256) finalize_stats_kernel(
+    const ST* __restrict__ ls, int R, const ST* __restrict__ seg, int nseg, int B,
+    const double* __restrict__ zpos, const double* __restrict__ cpos,
+    const float* __restrict__ epos, const int32_t* __restrict__ pos_col,
+    const int* __restrict__ hasval, int has_filter, MarginDev mg, ST* __restrict__ rowscale,
+    ST* __restrict__ delta, double* __restrict__ loss_row, StepStatus* st) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  if (sampler_failed(st)) return;
-  rowscale[b] = 0;
-  delta[b] = 0;
-  loss_row[b] = 0;
-  if (has_filter && hasval[b] == 0) {  // every buffer column masked (shardsim.hpp:294-297)
-    atomicMin(&st->masked_row, b);
-    return;
-  }
-  double S = 0.0;
-  for (int r = 0; r < R; ++r) S += (double)ls[(size_t)r * B + b];
-  if (!(S > 1e-30) || !isfinite(S)) {
-    atomicMin(&st->underflow_row, b);
-    return;
-  }
-  const double invB = 1.0 / (double)B;
-  const double rs = mg.sd * invB / S;
-  rowscale[b] = (ST)rs;
-  loss_row[b] = log(S) + mg.offd - zpos[b];
-  if (pos_col[b] >= 0) {
-    const double p = exp(zpos[b] - mg.offd) / S;
-    const double g = (p - 1.0) * invB * margin_deriv_pos(mg, cpos[b]);
-    delta[b] = (ST)(g - (double)(ST)rs * (double)epos[b]);
+  [&] {
+    if (b >= B || sampler_failed(st)) return;
+    rowscale[b] = 0;
+    delta[b] = 0;
+    loss_row[b] = 0;
+    if (has_filter && hasval[b] == 0) {  // every buffer column masked (shardsim.hpp:294-297)
+      atomicMin(&st->masked_row, b);
+      return;
+    }
+    double S = 0.0;
+    if (seg) {
+      double s = 0.0;
+      for (int i = 0; i < nseg; ++i) s += (double)seg[(size_t)i * B + b];
+      S = (double)(ST)s;
+    } else {
+      for (int r = 0; r < R; ++r) S += (double)ls[(size_t)r * B + b];
+    }
+    if (!(S > 1e-30) || !isfinite(S)) {
+      atomicMin(&st->underflow_row, b);
+      return;
+    }
+    const double invB = 1.0 / (double)B;
+    const double rs = mg.sd * invB / S;
+    rowscale[b] = (ST)rs;
+    loss_row[b] = log(S) + mg.offd - zpos[b];
+    if (pos_col[b] >= 0) {
+      const double p = exp(zpos[b] - mg.offd) / S;
+      const double g = (p - 1.0) * invB * margin_deriv_pos(mg, cpos[b]);
+      delta[b] = (ST)(g - (double)(ST)rs * (double)epos[b]);
+    }
+  }();
+  __threadfence();
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&st->fin_blocks, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double red[8];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) acc += ((volatile double*)loss_row)[i];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w];
+    st->fin_blocks = 0;
+    if (sampler_failed(st) || st->masked_row != 0x7fffffff || st->underflow_row != 0x7fffffff)
+      return;
+    const double loss = v / (double)B;
+    st->loss = loss;
+    if (!isfinite(loss)) st->nonfinite_loss = 1;
   }
 }
 
@@ -300,27 +330,6 @@ __global__ void __launch_bounds__(256) poscorr_kernel(
       acc += dl * xh;
     }
     poscorr[(size_t)slot * D + d] = acc;
-  }
-}
-
-// loss = mean_b loss_row[b] in a fixed order (one CTA, deterministic).
-__global__ void loss_reduce_kernel(const double* __restrict__ loss_row, int B, StepStatus* st) {
-  __shared__ double red[32];
-  double acc = 0.0;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) acc += loss_row[b];
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) {
-      if (sampler_failed(st) || st->masked_row != 0x7fffffff || st->underflow_row != 0x7fffffff)
-        return;
-      const double loss = v / (double)B;
-      st->loss = loss;
-      if (!isfinite(loss)) st->nonfinite_loss = 1;
-    }
   }
 }
 

@@ -140,6 +140,8 @@ struct Ctx {
   bool bf16;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t s2 = nullptr;                      // forked stream inside the step
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   MarginDev mg{};
   // state
   float* W = nullptr;
@@ -422,14 +424,15 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- softmax statistics: slices -> rank-local sum -> ranks (collectives 1 + 2) -> loss
   const int T = gf.n_tiles * NWG;
   ST* ls = static_cast<ST*>(c->ls);
-  {
-    const int nseg = (int)std::min<int64_t>(kMergeSegs, T);
-    ST* seg = static_cast<ST*>(c->seg_s);
-    sum_slices_kernel<ST><<<dim3((unsigned)ceil_div(B, 128), (unsigned)nseg), 128, 0, s>>>(
-        ps, T, (int)B, seg);
+  const int nseg = (int)std::min<int64_t>(kMergeSegs, T);
+  ST* seg = static_cast<ST*>(c->seg_s);
+  sum_slices_kernel<ST><<<dim3((unsigned)ceil_div(B, 128), (unsigned)nseg), 128, 0, s>>>(
+      ps, T, (int)B, seg);
+  c->launches++;
+  if (c->R > 1) {  // the rank-local sums are exchanged; with one rank finalize forms them
     sum_segments_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(seg, nseg, (int)B,
                                                                      ls + c->rank * B);
-    c->launches += 2;
+    c->launches++;
   }
   if (c->R > 1) {
     const int dt = sizeof(ST) == 8 ? ncclFloat64 : ncclFloat32;
@@ -439,20 +442,26 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   }
   ST* rsc = static_cast<ST*>(c->rowscale);
   ST* dlt = static_cast<ST*>(c->delta);
-  finalize_stats_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(
-      ls, c->R, (int)B, c->zpos, c->cpos, c->epos, c->pos_col, c->hasval, filt ? 1 : 0, c->mg,
-      rsc, dlt, c->loss_row, c->st);
-  loss_reduce_kernel<<<1, 1024, 0, s>>>(c->loss_row, (int)B, c->st);
-  xs_kernel<ST, OT><<<(unsigned)B, 128, 0, s>>>(c->sp, c->xnorm, rsc, (int)B, (int)c->D,
-                                                (int)c->Dp, static_cast<OT*>(c->xs));
-  poscorr_kernel<<<dim3((unsigned)c->pmax, (unsigned)c->nk), 256, 0, s>>>(
+  finalize_stats_kernel<ST><<<(unsigned)ceil_div(B, 256), 256, 0, s>>>(
+      ls, c->R, c->R > 1 ? nullptr : seg, nseg, (int)B, c->zpos, c->cpos, c->epos, c->pos_col,
+      c->hasval, filt ? 1 : 0, c->mg, rsc, dlt, c->loss_row, c->st);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  phase(c, "softmax_stats");
+  // X^s and the positive corrections feed only the dW GEMM: they run on a forked stream,
+  // concurrently with the dX GEMM (which leaves SMs free: split-K grid of 144 CTAs)
+  CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_fork, 0));
+  xs_kernel<ST, OT><<<(unsigned)B, 128, 0, c->s2>>>(c->sp, c->xnorm, rsc, (int)B, (int)c->D,
+                                                    (int)c->Dp, static_cast<OT*>(c->xs));
+  poscorr_kernel<<<dim3((unsigned)c->pmax, (unsigned)c->nk), 256, 0, c->s2>>>(
       c->meta, (int)c->cap, (int)c->pmax, c->pos_col, (int)B, c->sp, c->xnorm, (int)c->D,
       std::is_same<ST, float>::value ? reinterpret_cast<const float*>(dlt) : nullptr,
       std::is_same<ST, double>::value ? reinterpret_cast<const double*>(dlt) : nullptr,
       c->poscorr, c->pslot, c->st);
-  c->launches += 4;
+  c->launches += 2;
   CUDA_TRY(c, cudaGetLastError());
-  phase(c, "softmax_stats");
+  CUDA_TRY(c, cudaEventRecord(c->ev_join, c->s2));
   // ---- dX = rowscale * E W^ + delta w^_pos (split-K), tangent projection (shardsim.hpp:363-376)
   {
     const int S = dx_splits(c, B);
@@ -477,6 +486,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     CUDA_TRY(c, cudaGetLastError());
   }
   phase(c, "dx_gemm");
+  CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));  // X^s and the positive corrections
   // ---- dwt = E^T (rowscale x^) + positive corrections; center_proj; fused momentum-SGD
   {
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
@@ -787,6 +797,9 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
     CT(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, desc->device));
   }
   CT(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CT(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+  CT(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CT(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   const size_t ob = c->bf16 ? 2 : 4;  // operand bytes
   const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
   const int BN = c->bf16 ? kBN : kSimtBN;
@@ -859,6 +872,9 @@ int pfc_gpu_destroy(void* ctx) {
   for (int i = 0; i <= PhaseTimer::kMax; ++i)
     if (c->pt.ev[i]) cudaEventDestroy(c->pt.ev[i]);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->s2) cudaStreamDestroy(c->s2);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return PFC_OK;
 }

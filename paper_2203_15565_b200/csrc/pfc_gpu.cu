@@ -358,11 +358,13 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
                                      c->reset_status ? 1 : 0, x, lab, dx_full);
   c->launches++;
   // ---- sampler (build_buffers, sampler.hpp:63-126)
-  const size_t sort_smem = 2 * sizeof(int64_t) * kMaxSortBatch;  // keys + sorted unique labels
+  int P2 = 1;
+  while (P2 < B) P2 <<= 1;
+  const size_t sort_smem = 2 * sizeof(int64_t) * (size_t)P2;  // keys + sorted unique labels
   static bool sort_cfg = false;
   if (!sort_cfg) {
     CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sort_smem));
+                                     (int)(2 * sizeof(int64_t) * kMaxSortBatch)));
     sort_cfg = true;
   }
   positives_kernel<<<1, 1024, sort_smem, s>>>(
@@ -371,27 +373,25 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   c->launches++;
   CUDA_TRY(c, cudaMemsetAsync(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride, s));
   const int64_t nd = c->nk * c->cap;
-  draws_kernel<<<(unsigned)ceil_div(nd, bs), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap, c->sp,
-                                                         (int)c->k0, c->pool_stride,
-                                                         c->head, c->nxt, c->jv, c->st);
-  walk_kernel<<<(unsigned)ceil_div(nd, bs), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap,
-                                                        c->pool_stride, c->head, c->nxt, c->jv,
-                                                        c->buf_cls, c->st);
-  sequential_fallback_kernel<<<(unsigned)c->nk, 256, 0, s>>>(c->meta, (int)c->cap, c->sp,
-                                                             (int)c->k0, c->pool_stride,
-                                                             c->pool_scratch,
-                                                             c->buf_cls, c->st);
-  c->launches += 3;
-  phase(c, "sampler");
-  // ---- normalise features, gather + normalise sampled centres
   OT* xh = static_cast<OT*>(c->xh);
+  const int nbd = (int)ceil_div(nd, bs);
+  // draws + (trailing blocks) x^ = x / |x|   (shardsim.hpp:196-232)
+  draws_kernel<OT><<<(unsigned)(nbd + ceil_div(B * 32, bs)), bs, 0, s>>>(
+      c->meta, (int)c->nk, (int)c->cap, c->sp, (int)c->k0, c->pool_stride, c->head, c->nxt,
+      c->jv, c->st, nbd, (int)B, (int)c->D, (int)c->Dp, xh, c->xnorm);
+  // chain walk + (trailing blocks, one per shard) the exact sequential fallback
+  walk_kernel<<<(unsigned)(nbd + c->nk), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap,
+                                                     c->pool_stride, c->head, c->nxt, c->jv,
+                                                     c->buf_cls, c->st, nbd, c->sp, (int)c->k0,
+                                                     c->pool_scratch);
+  c->launches += 2;
+  phase(c, "sampler");
+  // ---- gather + normalise sampled centres
   OT* wh = static_cast<OT*>(c->wh);
-  normalize_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(c->sp, (int)B, (int)c->D,
-                                                                       (int)c->Dp, xh, c->xnorm);
   gather_w_kernel<OT><<<(unsigned)ceil_div(c->ncols_pad * 32, bs), bs, 0, s>>>(
       c->W, (int)c->D, (int)c->Dp, c->buf_cls, (int)c->ncols, (int)c->ncols_pad, c->cls_lo,
       c->rows, wh, c->wnorm, c->lrow, c->pslot, c->st);
-  c->launches += 2;
+  c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   phase(c, "gather");
   CUDA_TRY(c, cudaMemsetAsync(c->zpos, 0, sizeof(double) * B, s));

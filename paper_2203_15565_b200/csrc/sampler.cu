@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(1024) positives_kernel(
     }
   }
   // unique (sorted) into shared memory: each thread owns a contiguous run of keys
-  int64_t* us = keys + kMaxSortBatch;
+  int64_t* us = keys + P;  // dynamic smem = 2 x P keys (P = B rounded up to a power of two)
   __shared__ int bad_shard_s;
   const int per = (B + blockDim.x - 1) / blockDim.x;
   const int beg = threadIdx.x * per, end = min(B, beg + per);
@@ -197,11 +197,19 @@ __global__ void __launch_bounds__(1024) positives_kernel(
   }
 }
 
-// Per-draw counter RNG + modulo-rejection flag + per-position lists (j_s = p).
+// Per-draw counter RNG + modulo-rejection flag + per-position lists (j_s = p).  Blocks past
+// the draws (blockIdx.x >= nblk_draws) normalise the features instead (independent work that
+// shares the launch).
+template <typename OT>
 __global__ void draws_kernel(ShardMeta* __restrict__ meta, int nk, int cap,
                              const StepParams* __restrict__ sp, int k0, int64_t pool_stride,
                              int32_t* __restrict__ head, int32_t* __restrict__ nxt,
-                             int32_t* __restrict__ jv, const StepStatus* st) {
+                             int32_t* __restrict__ jv, const StepStatus* st, int nblk_draws,
+                             int B, int D, int Dp, OT* __restrict__ xh, float* __restrict__ xnorm) {
+  if ((int)blockIdx.x >= nblk_draws) {
+    normalize_x_rows(sp, B, D, Dp, xh, xnorm, (int)blockIdx.x - nblk_draws);
+    return;
+  }
   if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)nk * cap) return;
@@ -230,11 +238,24 @@ __device__ __forceinline__ int64_t pool_value(int64_t lo, const int32_t* pos, in
   return lo + p + a;
 }
 
-__global__ void walk_kernel(const ShardMeta* __restrict__ meta, int nk, int cap,
+__device__ void sequential_fallback(ShardMeta* meta, int cap, const StepParams* sp, int k0,
+                                    int64_t pool_stride, int32_t* pool_scratch, int32_t* buf_cls,
+                                    StepStatus* st, int kk);
+
+// Chain walk of the parallel Fisher-Yates restatement; the last nk blocks run the exact
+// sequential sampler for shards that saw a modulo rejection (disjoint from the walked shards).
+__global__ void walk_kernel(ShardMeta* __restrict__ meta, int nk, int cap,
                             int64_t pool_stride, const int32_t* __restrict__ head,
                             const int32_t* __restrict__ nxt, const int32_t* __restrict__ jv,
-                            int32_t* __restrict__ buf_cls, const StepStatus* st) {
+                            int32_t* __restrict__ buf_cls, StepStatus* st, int nblk_walk,
+                            const StepParams* __restrict__ sp, int k0,
+                            int32_t* __restrict__ pool_scratch) {
   if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;
+  if ((int)blockIdx.x >= nblk_walk) {
+    sequential_fallback(meta, cap, sp, k0, pool_stride, pool_scratch, buf_cls, st,
+                        (int)blockIdx.x - nblk_walk);
+    return;
+  }
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)nk * cap) return;
   const int kk = (int)(gid / cap), i = (int)(gid % cap);
@@ -262,14 +283,10 @@ __global__ void walk_kernel(const ShardMeta* __restrict__ meta, int nk, int cap,
 }
 
 // Exact sequential sample_without_replacement for shards that saw a modulo rejection
-// (or when forced for testing).  One CTA per local shard.
-__global__ void sequential_fallback_kernel(ShardMeta* __restrict__ meta, int cap,
-                                           const StepParams* __restrict__ sp, int k0,
-                                           int64_t pool_stride,
-                                           int32_t* __restrict__ pool_scratch,
-                                           int32_t* __restrict__ buf_cls, StepStatus* st) {
-  if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;
-  const int kk = blockIdx.x;
+// (or when forced for testing).  One CTA per local shard (walk_kernel's trailing blocks).
+__device__ void sequential_fallback(ShardMeta* meta, int cap, const StepParams* sp, int k0,
+                                    int64_t pool_stride, int32_t* pool_scratch, int32_t* buf_cls,
+                                    StepStatus* st, int kk) {
   const ShardMeta m = meta[kk];
   if (!m.reject) return;
   int32_t* row = buf_cls + (int64_t)kk * cap;

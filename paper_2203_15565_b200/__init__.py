@@ -398,14 +398,22 @@ class CenterShards:
 
     # -- steps
     def step_host(self, features_dxb: np.ndarray, labels: np.ndarray, cfg: StepConfig,
-                  iteration_rng: SeededRng) -> StepResult:
+                  iteration_rng: SeededRng, out: np.ndarray | None = None) -> StepResult:
+        """pfc_gpu_step on host arrays.  When features, labels and ``out`` (D x B float64,
+        receives d_features) are all page-locked, the library runs its copies inside the step
+        (upload overlapping the sampler, download overlapping the centre update)."""
         x = np.ascontiguousarray(features_dxb, dtype=np.float64)
         lab = np.ascontiguousarray(labels, dtype=np.int64)
         if x.ndim != 2 or x.shape[1] != lab.shape[0]:
             raise ShapeError("FeatureBatch: label count != feature columns")
         if x.shape[0] != self.dim:
             raise ShapeError(f"pfc_gpu: feature dim {x.shape[0]} != {self.dim}")
-        dx = np.zeros_like(x)
+        if out is None:
+            dx = np.zeros_like(x)
+        else:
+            if out.shape != x.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+                raise ShapeError("pfc_gpu: out must be a contiguous float64 array shaped like the features")
+            dx = out
         out = StepOut()
         args = StepArgs(iteration_rng.seed, iteration_rng.stream_id, cfg.lr, cfg.step_index)
         _check(_lib.pfc_gpu_step(self._h, _ptr(x), _ptr(lab), lab.shape[0], C.byref(args),

@@ -101,6 +101,12 @@ __device__ __forceinline__ void normalize_x_rows(const StepParams* __restrict__ 
   for (int d = lane; d < Dp; d += 32) store_out(o + d, d < D ? x[d] * inv : 0.f);
 }
 
+template <typename OT>
+__global__ void normalize_x_kernel(const StepParams* __restrict__ sp, int B, int D, int Dp,
+                                   OT* __restrict__ xh, float* __restrict__ xnorm) {
+  normalize_x_rows(sp, B, D, Dp, xh, xnorm, (int)blockIdx.x);
+}
+
 // Centre gather + normalisation (shardsim.hpp:234-247).  One warp per sampled column; W is
 // fp32 row-major [local classes][D] so each class is one contiguous row (128-bit loads).
 template <typename OT>

@@ -191,11 +191,25 @@ struct Ctx {
   StepParams* sp = nullptr;
   bool reset_status = true;  // false while asynchronous device steps are in flight
   // CUDA graph of the device step (one per batch size); step_begin is its first node
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  cudaGraphNode_t gbegin = nullptr;
-  int64_t gB = -1;
-  int64_t glaunches = 0;
+  // captured steps: slot 0 = device-resident I/O (pfc_gpu_step_device), slot 1 = the host
+  // drop-in with its copies inside the graph (pfc_gpu_step with pinned host buffers)
+  struct GraphSlot {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraphNode_t gbegin = nullptr;
+    cudaGraphNode_t cp_lab = nullptr, cp_x = nullptr, cp_dx = nullptr;  // slot 1 memcpy nodes
+    int64_t gB = -1;
+    int64_t glaunches = 0;
+  } gs[2];
+  // host drop-in with overlapped copies: X upload + conversion + normalisation run on s2 while
+  // the sampler and gather run; dX conversion + download on s2 while the dW GEMM runs
+  struct E2E {
+    bool on = false;
+    const double* xdb_h = nullptr;
+    const int64_t* lab_h = nullptr;
+    double* dxdb_h = nullptr;
+  } e2e;
+  cudaEvent_t ev_s = nullptr, ev_x = nullptr, ev_dx = nullptr, ev_out = nullptr;
   // tensor maps cached per batch
   int64_t tm_B = -1;
   CUtensorMap tm_x_k, tm_w_k, tm_e_st, tm_e_k, tm_w_mn, tm_e_mn, tm_xs_mn;
@@ -354,9 +368,26 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   cudaStream_t s = c->stream;
   const int bs = 256;
   if (int rc = ensure_maps(c, B)) return rc;
+  const bool e2e = c->e2e.on;
+  if (e2e)
+    CUDA_TRY(c, cudaMemcpyAsync(c->labels, c->e2e.lab_h, sizeof(int64_t) * B,
+                                cudaMemcpyHostToDevice, s));
   step_begin_kernel<<<1, 32, 0, s>>>(c->st, c->sp, a->seed, a->stream_id, (float)a->lr,
                                      c->reset_status ? 1 : 0, x, lab, dx_full);
   c->launches++;
+  if (e2e) {  // features: upload (D x B fp64), -> [B][D] fp32, normalise; joined before the GEMM
+    CUDA_TRY(c, cudaEventRecord(c->ev_s, s));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_s, 0));
+    CUDA_TRY(c, cudaMemcpyAsync(c->xdb, c->e2e.xdb_h, sizeof(double) * B * c->D,
+                                cudaMemcpyHostToDevice, c->s2));
+    dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+    x_from_dxb_kernel<<<grid, blk, 0, c->s2>>>(c->xdb, (int)c->D, (int)B, c->X);
+    normalize_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, c->s2>>>(
+        c->sp, (int)B, (int)c->D, (int)c->Dp, static_cast<OT*>(c->xh), c->xnorm);
+    c->launches += 2;
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaEventRecord(c->ev_x, c->s2));
+  }
   // ---- sampler (build_buffers, sampler.hpp:63-126)
   int P2 = 1;
   while (P2 < B) P2 <<= 1;
@@ -376,7 +407,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   OT* xh = static_cast<OT*>(c->xh);
   const int nbd = (int)ceil_div(nd, bs);
   // draws + (trailing blocks) x^ = x / |x|   (shardsim.hpp:196-232)
-  draws_kernel<OT><<<(unsigned)(nbd + ceil_div(B * 32, bs)), bs, 0, s>>>(
+  draws_kernel<OT><<<(unsigned)(nbd + (e2e ? 0 : ceil_div(B * 32, bs))), bs, 0, s>>>(
       c->meta, (int)c->nk, (int)c->cap, c->sp, (int)c->k0, c->pool_stride, c->head, c->nxt,
       c->jv, c->st, nbd, (int)B, (int)c->D, (int)c->Dp, xh, c->xnorm);
   // chain walk + (trailing blocks, one per shard) the exact sequential fallback
@@ -403,6 +434,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   OT* E = static_cast<OT*>(c->G);
   const float tau = (float)c->d.filter_threshold;
   const bool filt = c->d.has_filter != 0;
+  if (e2e) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_x, 0));
   // ---- logits GEMM + margin + E = exp(z - o) and its per-slice row sums (shardsim.hpp:249-318)
   const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, BN, 1, 0);
   {
@@ -485,6 +517,19 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
   }
+  if (e2e) {  // d_features: [sum over ranks], -> D x B fp64, download; overlaps the dW GEMM
+    CUDA_TRY(c, cudaEventRecord(c->ev_dx, s));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_dx, 0));
+    if (c->R > 1)  // the drop-in returns the FULL summed d_features on every rank
+      NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, c->s2));
+    dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+    dx_to_dxb_kernel<<<grid, blk, 0, c->s2>>>(c->dX, (int)c->D, (int)B, c->xdb);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaMemcpyAsync(c->e2e.dxdb_h, c->xdb, sizeof(double) * B * c->D,
+                                cudaMemcpyDeviceToHost, c->s2));
+    CUDA_TRY(c, cudaEventRecord(c->ev_out, c->s2));
+  }
   phase(c, "dx_gemm");
   CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));  // X^s and the positive corrections
   // ---- dwt = E^T (rowscale x^) + positive corrections; center_proj; fused momentum-SGD
@@ -518,6 +563,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     CUDA_TRY(c, err);
   }
   phase(c, "dw_update_gemm");
+  if (e2e) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_out, 0));
   return PFC_OK;
 }
 
@@ -537,11 +583,12 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
     }
     return pipeline();
   }
-  if (!c->gexec || c->gB != B) {  // capture the step once per batch size
-    if (c->gexec) {
-      cudaGraphExecDestroy(c->gexec);
-      cudaGraphDestroy(c->graph);
-      c->gexec = nullptr;
+  Ctx::GraphSlot& G = c->gs[c->e2e.on ? 1 : 0];
+  if (!G.gexec || G.gB != B) {  // capture the step once per batch size
+    if (G.gexec) {
+      cudaGraphExecDestroy(G.gexec);
+      cudaGraphDestroy(G.graph);
+      G.gexec = nullptr;
     }
     CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     const int rc = pipeline();
@@ -552,27 +599,37 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
       return rc;
     }
     CUDA_TRY(c, ce);
-    CUDA_TRY(c, cudaGraphInstantiate(&c->gexec, g, 0));
-    c->graph = g;
+    CUDA_TRY(c, cudaGraphInstantiate(&G.gexec, g, 0));
+    G.graph = g;
     size_t n = 0;
     CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &n));
     std::vector<cudaGraphNode_t> nodes(n);
     CUDA_TRY(c, cudaGraphGetNodes(g, nodes.data(), &n));
-    c->gbegin = nullptr;
+    G.gbegin = G.cp_lab = G.cp_x = G.cp_dx = nullptr;
     for (cudaGraphNode_t nd : nodes) {
       cudaGraphNodeType ty;
       cudaGraphNodeGetType(nd, &ty);
+      if (ty == cudaGraphNodeTypeMemcpy) {  // the host drop-in's copies (slot 1)
+        cudaMemcpy3DParms mp{};
+        if (cudaGraphMemcpyNodeGetParams(nd, &mp) != cudaSuccess) continue;
+        if (mp.dstPtr.ptr == c->labels) G.cp_lab = nd;
+        else if (mp.dstPtr.ptr == c->xdb) G.cp_x = nd;
+        else if (mp.srcPtr.ptr == c->xdb) G.cp_dx = nd;
+        continue;
+      }
       if (ty != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams kp{};
       if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
           kp.func == reinterpret_cast<void*>(step_begin_kernel))
-        c->gbegin = nd;
+        G.gbegin = nd;
     }
-    if (!c->gbegin) return fail(c, PFC_ERR_CUDA, "graph capture lost the step_begin node");
-    c->gB = B;
-    c->glaunches = c->launches;
+    if (!G.gbegin) return fail(c, PFC_ERR_CUDA, "graph capture lost the step_begin node");
+    if (c->e2e.on && (!G.cp_lab || !G.cp_x || !G.cp_dx))
+      return fail(c, PFC_ERR_CUDA, "graph capture lost a host copy node");
+    G.gB = B;
+    G.glaunches = c->launches;
   }
-  // per step, only step_begin's arguments change
+  // per step, only step_begin's arguments (and the host drop-in's host pointers) change
   StepStatus* st = c->st;
   StepParams* sp = c->sp;
   uint64_t seed = a->seed, stream = a->stream_id;
@@ -586,9 +643,19 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
   kp.sharedMemBytes = 0;
   kp.kernelParams = args;
   kp.extra = nullptr;
-  CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(c->gexec, c->gbegin, &kp));
-  CUDA_TRY(c, cudaGraphLaunch(c->gexec, c->stream));
-  c->launches = c->glaunches;
+  CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(G.gexec, G.gbegin, &kp));
+  if (c->e2e.on) {
+    CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_lab, c->labels, c->e2e.lab_h,
+                                                   sizeof(int64_t) * B, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_x, c->xdb, c->e2e.xdb_h,
+                                                   sizeof(double) * B * c->D,
+                                                   cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_dx, c->e2e.dxdb_h, c->xdb,
+                                                   sizeof(double) * B * c->D,
+                                                   cudaMemcpyDeviceToHost));
+  }
+  CUDA_TRY(c, cudaGraphLaunch(G.gexec, c->stream));
+  c->launches = G.glaunches;
   return PFC_OK;
 }
 
@@ -800,6 +867,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
   CT(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CT(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&c->ev_s, &c->ev_x, &c->ev_dx, &c->ev_out})
+    CT(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   const size_t ob = c->bf16 ? 2 : 4;  // operand bytes
   const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
   const int BN = c->bf16 ? kBN : kSimtBN;
@@ -864,8 +933,12 @@ int pfc_gpu_destroy(void* ctx) {
   if (!ctx) return PFC_OK;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
-  if (c->graph) cudaGraphDestroy(c->graph);
+  for (Ctx::GraphSlot& G : c->gs) {
+    if (G.gexec) cudaGraphExecDestroy(G.gexec);
+    if (G.graph) cudaGraphDestroy(G.graph);
+  }
+  for (cudaEvent_t e : {c->ev_s, c->ev_x, c->ev_dx, c->ev_out})
+    if (e) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
   if (c->st_host) cudaFreeHost(c->st_host);
@@ -974,6 +1047,16 @@ int pfc_gpu_device_state(void* ctx, float** w, float** m, int64_t* rows) {
 
 void* pfc_gpu_stream(void* ctx) { return static_cast<Ctx*>(ctx)->stream; }
 
+// page-locked (or registered) host memory: eligible for copies inside the captured step
+static bool pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
                  const pfc_gpu_step_args* a, double* dxdb, pfc_gpu_step_out* out) {
   Ctx* c = static_cast<Ctx*>(ctx);
@@ -987,6 +1070,19 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
     return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: batch %lld exceeds max_batch %lld", (long long)B,
                 (long long)c->maxB);
   cudaStream_t s = c->stream;
+  if (pinned(xdb) && pinned(labels) && pinned(dxdb)) {
+    // copies inside the step: X upload overlaps the sampler + gather, dX download the dW GEMM.
+    // On an error the contents of dxdb are unspecified (the reference throws instead).
+    c->e2e = {true, xdb, labels, dxdb};
+    const int rc = run_step(c, c->X, c->labels, B, a, c->dX);
+    c->e2e.on = false;
+    if (rc) return rc;
+    c->reset_status = true;
+    CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (int rc2 = finish_phase_timing(c)) return rc2;
+    return check_status(c, a->step_index, B, out);
+  }
   CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
   dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);

@@ -255,6 +255,51 @@ def test_graph_replay_equals_eager(port):
     assert np.array_equal(outs[0][3][0], outs[1][3][0]) and np.array_equal(outs[0][3][1], outs[1][3][1])
 
 
+def test_pinned_host_step_equals_pageable(port):
+    """pfc_gpu_step with page-locked buffers (copies captured inside the step graph, overlapped
+    with the sampler and the centre update) gives the same bits as the pageable path, graph
+    replay and eager alike, over steps with changing host buffers, seeds and lr."""
+    C_, K, D, B = 12000, 3, 256, 192
+    outs = []
+    for flags, pin in ((0, False), (0, True), (p.FLAG_NO_GRAPH, True)):
+        cfg = p.StepConfig(r=0.2, margin=p.MarginConfig.arcface_style())
+        sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, flags=flags)
+        sh.init_center_shards(5)
+        res = []
+        for step in range(3):
+            X, labels = port.bench_inputs(C_, D, B, 1, step)
+            if pin:  # fresh page-locked buffers every step: the graph's copy nodes are re-pointed
+                xh = torch.empty(D, B, dtype=torch.float64, pin_memory=True).numpy()
+                lh = torch.empty(B, dtype=torch.int64, pin_memory=True).numpy()
+                dxh = torch.empty(D, B, dtype=torch.float64, pin_memory=True).numpy()
+                xh[:] = X
+                lh[:] = labels
+                X, labels, out = xh, lh, dxh
+            else:
+                out = None
+            cfg.lr = 0.1 / (step + 1)
+            r = sh.step_host(X, labels, cfg, p.SeededRng(1, p.make_stream("iteration", step)), out=out)
+            res.append((r.loss, r.d_features.copy()))
+        res.append(sh.get_shard(2))
+        outs.append(res)
+        sh.close()
+    for other in outs[1:]:
+        for a, b in zip(outs[0][:3], other[:3]):
+            assert a[0] == b[0] and np.array_equal(a[1], b[1])
+        assert np.array_equal(outs[0][3][0], other[3][0]) and np.array_equal(outs[0][3][1], other[3][1])
+    # an error detected on the device still surfaces with the reference's text
+    cfg = p.StepConfig(r=0.1)
+    sh = p.CenterShards(p.ShardLayout(1000, 4), 8, cfg, max_batch=125)
+    sh.init_center_shards(1)
+    xh = torch.zeros(8, 125, dtype=torch.float64, pin_memory=True).numpy()
+    lh = torch.empty(125, dtype=torch.int64, pin_memory=True).numpy()
+    lh[:] = np.arange(125) * 8
+    dxh = torch.empty(8, 125, dtype=torch.float64, pin_memory=True).numpy()
+    with pytest.raises(p.CapacityError):
+        sh.step_host(xh, lh, cfg, p.SeededRng(1, 1), out=dxh)
+    sh.close()
+
+
 def test_async_device_steps_report_errors_on_sync():
     C_, K, D, B = 1000, 4, 64, 8
     cfg = p.StepConfig(r=0.1)

@@ -198,6 +198,7 @@ struct Ctx {
     cudaGraphExec_t gexec = nullptr;
     cudaGraphNode_t gbegin = nullptr;
     cudaGraphNode_t cp_lab = nullptr, cp_x = nullptr, cp_dx = nullptr;  // slot 1 memcpy nodes
+    const void* cp_ptr[3] = {nullptr, nullptr, nullptr};  // host pointers the nodes hold
     int64_t gB = -1;
     int64_t glaunches = 0;
   } gs[2];
@@ -628,6 +629,7 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
       return fail(c, PFC_ERR_CUDA, "graph capture lost a host copy node");
     G.gB = B;
     G.glaunches = c->launches;
+    G.cp_ptr[0] = G.cp_ptr[1] = G.cp_ptr[2] = nullptr;
   }
   // per step, only step_begin's arguments (and the host drop-in's host pointers) change
   StepStatus* st = c->st;
@@ -644,15 +646,21 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
   kp.kernelParams = args;
   kp.extra = nullptr;
   CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(G.gexec, G.gbegin, &kp));
-  if (c->e2e.on) {
-    CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_lab, c->labels, c->e2e.lab_h,
-                                                   sizeof(int64_t) * B, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_x, c->xdb, c->e2e.xdb_h,
-                                                   sizeof(double) * B * c->D,
-                                                   cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_dx, c->e2e.dxdb_h, c->xdb,
-                                                   sizeof(double) * B * c->D,
-                                                   cudaMemcpyDeviceToHost));
+  if (c->e2e.on) {  // re-point the copy nodes when the caller's host buffers changed
+    if (G.cp_ptr[0] != c->e2e.lab_h)
+      CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_lab, c->labels, c->e2e.lab_h,
+                                                     sizeof(int64_t) * B, cudaMemcpyHostToDevice));
+    if (G.cp_ptr[1] != c->e2e.xdb_h)
+      CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_x, c->xdb, c->e2e.xdb_h,
+                                                     sizeof(double) * B * c->D,
+                                                     cudaMemcpyHostToDevice));
+    if (G.cp_ptr[2] != c->e2e.dxdb_h)
+      CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_dx, c->e2e.dxdb_h, c->xdb,
+                                                     sizeof(double) * B * c->D,
+                                                     cudaMemcpyDeviceToHost));
+    G.cp_ptr[0] = c->e2e.lab_h;
+    G.cp_ptr[1] = c->e2e.xdb_h;
+    G.cp_ptr[2] = c->e2e.dxdb_h;
   }
   CUDA_TRY(c, cudaGraphLaunch(G.gexec, c->stream));
   c->launches = G.glaunches;

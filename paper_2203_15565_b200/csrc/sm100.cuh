@@ -186,6 +186,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// 4-byte LDGSTS (cached at all levels; the 16-byte form is cp_async16)
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
 // st.async: 4-byte store into a peer CTA's shared memory completing 4 tx bytes of its mbarrier
 __device__ __forceinline__ void st_async_f32(uint32_t caddr, float v, uint32_t cbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(caddr),

@@ -509,256 +509,6 @@ struct DwUpdateEpi {
   }
 };
 
-// ------------------------------------------------------------------------------- DwColEpi
-// dW GEMM in the transposed orientation: D^T = X^s^T E (TMEM lanes = dims, columns = classes).
-// A cluster of kCl = ceil(D/128) CTAs covers the dims of one 256-class block.  Warp (g, q) of
-// a CTA owns dims 32q .. 32q+31 of the CTA's 128-dim block for the 64 classes 64g .. 64g+63 of
-// the tile, so every W / momentum access of a class is a coalesced 128-byte piece of its row,
-// and the 16 warps x kCl CTAs touching a class row request its whole 2 KB together (DRAM page
-// locality: profiles/micro/rowupd.cu).  Loads stream through the per-warp cp.async ring (items
-// of 8 classes: W for the dot pass, W + momentum for the update pass; dw_ring schedule, across
-// tiles).  center_proj_j = w^_j . dwt_j: per-lane products, a register butterfly gives one
-// class per lane, the four dim-quarter warps of a warpgroup combine through shared memory, and
-// the kCl CTAs swap their 64 partials per warpgroup by st.async (summed in rank order).
-// Per-class scalars live in warpgroup tables read by broadcast (row offset, 1/|w|, center_proj).
-template <int kCl>
-struct DwColEpi {
-  static constexpr int kCluster = kCl;
-  static constexpr bool kNext = true;
-  static constexpr int kRingFloats = dw_ring::kCap * 256;  // per warp
-  static constexpr int kWarpBytes = kRingFloats * 4;
-  // per warpgroup (floats): qpart[2][4][64], rpart[2][kCl][64], inv[3][64], cp[2][64],
-  // rowoff (int64)[3][64], mbarrier[2]
-  static constexpr int kQPart = 2 * 4 * 64, kRPart = 2 * kCl * 64, kInv = 3 * 64, kCp = 2 * 64;
-  static constexpr int kFloats = kQPart + kRPart + kInv + kCp;
-  static constexpr int kSharedBytes = ((kFloats * 4 + 15) / 16) * 16 + 3 * 64 * 8 + 2 * 8;
-  static constexpr int kSmem = ((4 * kWarpBytes + kSharedBytes + 127) / 128) * 128;
-  int ncols, D;
-  const float* wnorm;       // [ncols]
-  const int32_t* lrow;      // [ncols] local row of W
-  const int32_t* pslot;     // [ncols] positive-correction slot or -1
-  const float* poscorr;     // [slots][D]: sum over rows with this label of delta_b x^_b
-  float* W;
-  float* Mom;
-  const StepParams* sp;     // lr of this step
-  float mu, wd;
-  const StepStatus* st;     // no update when the step failed (the reference throws before 412)
-
-  struct Pre {  // the warpgroup's 64 classes: lane l holds classes l and 32 + l
-    int r[2], ps[2];
-    float inv[2];
-  };
-  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int wg) const {
-    Pre p;
-    const int lane = row & 31;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = t.col0 + 64 * wg + 32 * h + lane;
-      p.r[h] = -1;
-      p.ps[h] = -1;
-      p.inv[h] = 0.f;
-      if (c < ncols) {
-        const float n = wnorm[c];
-        p.inv[h] = 1.0f / (n > 1e-12f ? n : 1e-12f);
-        p.r[h] = lrow[c];
-        p.ps[h] = pslot[c];
-      }
-    }
-    return p;
-  }
-  __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
-  __device__ __forceinline__ void finish(int, int) const {}
-  struct Tabs {
-    float *qpart, *rpart, *inv, *cp;
-    long long* rowoff;
-    uint64_t* mb;
-  };
-  __device__ __forceinline__ static Tabs tabs(uint8_t* wsm) {
-    Tabs T;
-    float* f = reinterpret_cast<float*>(wsm + 4 * kWarpBytes);
-    T.qpart = f;
-    T.rpart = T.qpart + kQPart;
-    T.inv = T.rpart + kRPart;
-    T.cp = T.inv + kInv;
-    uint8_t* b = reinterpret_cast<uint8_t*>(f) + ((kFloats * 4 + 15) / 16) * 16;
-    T.rowoff = reinterpret_cast<long long*>(b);
-    T.mb = reinterpret_cast<uint64_t*>(b + 3 * 64 * 8);
-    return T;
-  }
-  __device__ __forceinline__ void setup(uint8_t* epi_base) const {
-    if constexpr (kCl > 1) {
-      for (int g = 0; g < 4; ++g) {
-        uint64_t* mb = tabs(epi_base + g * kSmem).mb;
-        for (int i = 0; i < 2; ++i) pfc_sm100::mbar_init(&mb[i], 1);  // local arrive + tx bytes
-      }
-    }
-  }
-  // this warp's quarter (16 classes) of a tile's class table: row offsets (-1: no update)
-  __device__ __forceinline__ void put_tab(const Tabs& T, int slot, const Pre& P, int q, int lane,
-                                          bool live) const {
-    // lane l holds classes l and 32+l: warps q = 0, 1 write classes 32q + l
-    if (q < 2) {
-      const int j = 32 * q + lane;
-      const int r = P.r[q];
-      T.rowoff[slot * 64 + j] = (live && r >= 0) ? (long long)r * D : -1ll;
-      T.inv[slot * 64 + j] = P.inv[q];
-    }
-  }
-
-  template <int BN, int NWG, class Src>
-  __device__ __forceinline__ void run_next(const TileInfo& t, const Src& src, int row, int wg,
-                                           uint8_t* smem, const Pre& pre, const Pre& pre_next,
-                                           bool has_next) const {
-    static_assert(NWG == 4 && BN == 256, "DwColEpi: 4 warpgroups, 256-class tiles");
-    using namespace dw_ring;
-    const int q = row >> 5, lane = row & 31;
-    const int d = t.row0 + 32 * q + lane;  // this lane's dim
-    const bool dv = d < D;
-    const int dq = t.row0 + 32 * q + 4 * (lane & 7);  // first dim of this lane's 16-byte copies
-    const bool dg = dq < D;                            // D % 4 == 0: groups are all in or out
-    float* ring = reinterpret_cast<float*>(smem + q * kWarpBytes);
-    const Tabs T = tabs(smem);
-    const int par = t.iter & 1;
-    const int s3 = t.iter % 3, s3n = (t.iter + 1) % 3;
-    const bool failed = status_failed(st);
-    const float lr = sp->lr;
-    if constexpr (kCl > 1) {  // this tile's exchange: kCl x 64 partials arrive as tx bytes
-      if (q == 0 && lane == 0) pfc_sm100::mbar_arrive_expect_tx(&T.mb[par], (uint32_t)(kCl * 64 * 4));
-    }
-    // class tables: this tile's (first tile only; later ones were written a tile ahead) and the
-    // next tile's; slot (i % 3) was last read during tile i - 3 + 1 by every warp of the group
-    if (t.iter == 0) put_tab(T, s3, pre, q, lane, !failed);
-    put_tab(T, s3n, pre_next, q, lane, !failed && has_next);
-    if (t.iter == 0) pfc_sm100::named_bar_sync(1 + wg, 128);
-    const long long* ro = T.rowoff + s3 * 64;
-    const long long* ron = T.rowoff + s3n * 64;
-    const float* tinv = T.inv + s3 * 64;
-    const float* tcp = T.cp + par * 64;
-    // positive corrections are rare: one warp-uniform test per tile
-    const bool anyp = __any_sync(0xffffffffu, pre.ps[0] >= 0 || pre.ps[1] >= 0);
-    const uint32_t ring_s = pfc_sm100::smem_u32(ring);
-    // item i of the stream: classes 8*(i%8) .. +7 of this tile (i < 16) or the next (i >= 16);
-    // W only (i%16 < 8) or W + momentum (sub-slot p + 1)
-    auto issue = [&](auto ic) {
-      constexpr int i = decltype(ic)::value;
-      constexpr int ii = i % kItems;
-      constexpr int c8 = (ii < kNC ? ii : ii - kNC) * 8;
-      constexpr int p = pos(i);
-      const long long* rt = i < kItems ? ro : ron;
-      // 16 bytes per lane: lane l copies dims 4(l%8) .. +3 of class 4h + l/8 (h = 0, 1), so one
-      // instruction moves four 128-byte class pieces; the ring stays [8 classes][32 dims]
-      if (dg) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int jj = 4 * h + (lane >> 3);
-          const long long o = rt[c8 + jj];
-          if (o >= 0) {
-            const uint32_t so = (uint32_t)((jj * 32 + 4 * (lane & 7)) * 4);
-            pfc_sm100::cp_async16(ring_s + (uint32_t)(p * 1024) + so, W + o + dq);
-            if (ii >= kNC)
-              pfc_sm100::cp_async16(ring_s + (uint32_t)(((p + 1) % kCap) * 1024) + so, Mom + o + dq);
-          }
-        }
-      }
-      pfc_sm100::cp_async_commit();
-    };
-    auto add_pc = [&](float v, int j) {
-      if (anyp) {
-        const int ps = __shfl_sync(0xffffffffu, j < 32 ? pre.ps[0] : pre.ps[1], j & 31);
-        if (ps >= 0 && dv) v += poscorr[(size_t)ps * D + d];
-      }
-      return v;
-    };
-
-    if (t.iter == 0) static_range<0, kHead>(issue);  // otherwise issued by the previous tile
-    float v[32];  // TMEM columns of the current 32-class group (then products, then sums)
-    static_range<0, kItems>([&](auto kc) {
-      constexpr int k = decltype(kc)::value;
-      constexpr int c8 = (k < kNC ? k : k - kNC) * 8;  // first class of the item
-      constexpr int grp = c8 / 32;
-      if constexpr (c8 % 32 == 0) src.load(64 * wg + c8, v);  // classes 64g + c8 .. +31
-      if constexpr (k == kNC) {
-        // ---- dot pass done: warpgroup and cluster reduction of center_proj
-        pfc_sm100::named_bar_sync(1 + wg, 128);  // qpart[par] of all four dim quarters
-        if (q < 2) {  // warps 0, 1: classes 32q + lane
-          const int j = 32 * q + lane;
-          float sum = 0.f;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) sum += T.qpart[(par * 4 + qq) * 64 + j];
-          if constexpr (kCl > 1) {
-            const uint32_t me = pfc_sm100::cluster_ctarank();
-            const uint32_t la = pfc_sm100::smem_u32(T.rpart + (par * kCl + (int)me) * 64 + j);
-            const uint32_t lb = pfc_sm100::smem_u32(&T.mb[par]);
-#pragma unroll
-            for (int rk = 0; rk < kCl; ++rk)
-              pfc_sm100::st_async_f32(pfc_sm100::mapa_shared(la, (uint32_t)rk), sum,
-                                      pfc_sm100::mapa_shared(lb, (uint32_t)rk));
-          } else {
-            T.rpart[par * 64 + j] = sum;
-          }
-        }
-        if constexpr (kCl > 1) pfc_sm100::mbar_wait_cluster(&T.mb[par], (uint32_t)((t.iter >> 1) & 1));
-        else pfc_sm100::named_bar_sync(1 + wg, 128);
-        if (q < 2) {  // center_proj_j / |w_j|, summed over the cluster in rank order (shardsim.hpp:361-362)
-          const int j = 32 * q + lane;
-          float s = 0.f;
-#pragma unroll
-          for (int rk = 0; rk < kCl; ++rk) s += T.rpart[(par * kCl + rk) * 64 + j];
-          const float iv = tinv[j];
-          T.cp[par * 64 + j] = s * iv * iv;
-        }
-        pfc_sm100::named_bar_sync(1 + wg, 128);  // cp[par] complete
-      }
-      pfc_sm100::cp_async_wait<issued_before(k) - k - 1>();  // item k landed (this lane's pieces)
-      const float* sw = ring + pos(k) * 256;
-      if constexpr (k < kNC) {  // dot pass: products w_j,d * dwt_j,d
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int j = c8 + jj;
-          v[j & 31] = add_pc(v[j & 31], j) * sw[jj * 32 + lane];
-        }
-        if constexpr (c8 % 32 == 24) {
-          // butterfly: 32 classes x 32 dims -> lane l holds the warp's partial for class l
-          if (!dv) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-#pragma unroll
-          for (int w = 16; w >= 1; w >>= 1) {
-            const bool up = lane & w;
-#pragma unroll
-            for (int i = 0; i < w; ++i) {
-              const float lo = v[i], hi = v[i + w];
-              const float got = __shfl_xor_sync(0xffffffffu, up ? lo : hi, w);
-              v[i] = (up ? hi : lo) + got;
-            }
-          }
-          T.qpart[(par * 4 + q) * 64 + 32 * grp + lane] = v[0];
-        }
-      } else {  // update pass: dW and the momentum-SGD update of the 8 classes
-        const float* sm = ring + ((pos(k) + 1) % kCap) * 256;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int j = c8 + jj;
-          const long long o = ro[j];
-          const float a = add_pc(v[j & 31], j);  // all lanes: it may shuffle
-          if (dv && o >= 0) {
-            const float inv = tinv[j], cpj = tcp[j];
-            const float w = sw[jj * 32 + lane], m = sm[jj * 32 + lane];
-            const float dw = (a - cpj * w) * inv;  // (dwt - center_proj w^) / |w|: shardsim.hpp:382
-            const float g = dw + wd * w;           // shardsim.hpp:152-153
-            const float vv = mu * m + g;           // shardsim.hpp:154
-            Mom[o + d] = vv;
-            W[o + d] = w - lr * vv;                // shardsim.hpp:156
-          }
-        }
-      }
-      // refill the ring (reads of item k's sub-slots were consumed above: in-order issue)
-      static_range<issued_before(k), issued_before(k + 1)>(issue);
-    });
-  }
-};
-
 // -------------------------------------------------------------------- DwStoreEpi (SIMT path)
 struct DwStoreEpi : NoSetup {
   static constexpr int kSmem = 0;

@@ -117,9 +117,6 @@ int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 constexpr int kBN = 256;  // tcgen05 tile 128 x 256
 constexpr int kNWG = 2;
-#ifndef PFC_DW_COL
-#define PFC_DW_COL 1
-#endif
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
 #endif   // epilogue warpgroups per CTA on the tcgen05 engine
@@ -216,7 +213,7 @@ struct Ctx {
   cudaEvent_t ev_s = nullptr, ev_x = nullptr, ev_dx = nullptr, ev_out = nullptr;
   // tensor maps cached per batch
   int64_t tm_B = -1;
-  CUtensorMap tm_x_k, tm_w_k, tm_e_st, tm_e_k, tm_e_k256, tm_w_mn, tm_e_mn, tm_xs_mn;
+  CUtensorMap tm_x_k, tm_w_k, tm_e_st, tm_e_k, tm_w_mn, tm_e_mn, tm_xs_mn;
   // nccl
   ncclComm_t comm = nullptr;
   // bookkeeping
@@ -346,9 +343,6 @@ int ensure_maps(Ctx* c, int64_t B) {
   // B = rowscale * x^ MN-major
   ok &= make_map(&c->tm_e_k, c->G, B, c->ncols, c->ldg, 128);
   ok &= make_map(&c->tm_xs_mn, c->xs, c->Dp, B, c->Dp, 64);
-  // dW GEMM, transposed (M = d, N = classes, K = b): A = (rowscale x^)^T MN-major, B = E^T
-  // K-major in 256-class boxes
-  ok &= make_map(&c->tm_e_k256, c->G, B, c->ncols, c->ldg, 256);
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
   return PFC_OK;
@@ -544,23 +538,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   {
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
     cudaError_t err;
-    if constexpr (kUmma && PFC_DW_COL) {
-      // dims on the TMEM lanes: a cluster of ceil(D/128) CTAs per 256-class block
-      const GemmGeom gt = make_geom((int)c->D, (int)c->ncols, (int)B, BN, 1, 0);
-      auto go = [&](auto e) {
-        return launch_umma<kBN, PFC_DW_STAGES, 4, true, false>(c, c->tm_xs_mn, c->tm_e_k256, gt, e);
-      };
-#define PFC_DWC(K)                                                                           \
-  go(DwColEpi<K>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr, c->W, c->M, \
-                 c->sp, (float)c->d.momentum, (float)c->d.weight_decay, c->st})
-      switch (gt.m_tiles) {
-        case 1: err = PFC_DWC(1); break;
-        case 2: err = PFC_DWC(2); break;
-        case 3: err = PFC_DWC(3); break;
-        default: err = PFC_DWC(4); break;
-      }
-#undef PFC_DWC
-    } else if constexpr (kUmma) {
+    if constexpr (kUmma) {
       if (gw.n_tiles == 2)
         err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,

@@ -93,6 +93,8 @@ class Oracle:
         self._f("build_buffers", C.c_int, [i64, i64, vp, i64, dbl, u64, u64, vp, vp, C.c_char_p,
                                            C.c_int])
         self._f("init_centers", None, [i64, i64, i64, u64, vp])
+        self._f("diagnostics", C.c_int, [i64, i64, i64, vp, vp, vp, i64, vp, vp, vp, vp,
+                                         C.c_char_p, C.c_int])
         self._f("step", C.c_int, [C.POINTER(StepCfgC), i64, i64, i64, vp, vp, vp, vp, i64, u64,
                                   u64, C.POINTER(dbl), vp, vp, vp, vp, vp, C.c_char_p, C.c_int])
         if kind == "reference":
@@ -182,6 +184,28 @@ class Oracle:
             out["d_centers"] = dcent.reshape(K, D, cap)
             out["cos"] = cosm.reshape(K, B, cap)
         return out
+
+    # ---- metrics.hpp (the step's diagnostics, shardsim.hpp:401-410) -------------------
+    def diagnostics(self, C_: int, K: int, D: int, W: np.ndarray, X: np.ndarray, labels,
+                    class_identity=None, sample_identity=None) -> dict:
+        """apcs / amncs (+ conflicted / hard split) on shard-concatenated W and D x B X."""
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        labels = np.ascontiguousarray(labels, dtype=np.int64)
+        ci = None if class_identity is None else np.ascontiguousarray(class_identity, dtype=np.int64)
+        si = None if sample_identity is None else np.ascontiguousarray(sample_identity, dtype=np.int64)
+        out = np.zeros(4, dtype=np.float64)
+        flags = np.zeros(2, dtype=np.int32)
+        err = C.create_string_buffer(512)
+        st = self._diagnostics(C_, K, D, _ptr(np.ascontiguousarray(W, dtype=np.float64)), _ptr(X),
+                               _ptr(labels), len(labels), _ptr(ci), _ptr(si), _ptr(out),
+                               _ptr(flags), err, 512)
+        if st:
+            raise OracleError(st, err.value.decode())
+        res = {"apcs": float(out[0]), "amncs": float(out[1])}
+        if flags[1]:
+            res["amncs_hard"] = float(out[3])
+            res["amncs_conflicted"] = float(out[2]) if flags[0] else None
+        return res
 
     def bench_inputs(self, C_: int, D: int, B: int, seed: int, step: int):
         X = np.zeros((D, B), dtype=np.float64)

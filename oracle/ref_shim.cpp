@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "pfc/metrics.hpp"
 #include "pfc/shardsim.hpp"
 
 namespace {
@@ -174,6 +175,47 @@ int pfcr_step(const StepCfgC* c, int64_t C, int64_t K, int64_t D, double* W, dou
             }
         }
         store_shards(shards, W, M);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return status_of(e);
+    }
+}
+
+// apcs / amncs (metrics.hpp:56-146) on caller-provided shards, as the step computes them with
+// with_diagnostics (shardsim.hpp:401-410).
+int pfcr_diagnostics(int64_t C, int64_t K, int64_t D, const double* W, const double* X,
+                     const int64_t* labels, int64_t B, const int64_t* class_identity,
+                     const int64_t* sample_identity, double* out, int32_t* flags, char* err,
+                     int errlen) {
+    try {
+        const pfc::ShardLayout layout(C, K);
+        std::vector<pfc::CenterShard> shards;
+        for (int64_t k = 0; k < K; ++k) {
+            pfc::CenterShard s;
+            s.shard_id = k;
+            s.class_begin = layout.owned_begin(k);
+            s.class_end = layout.owned_end(k);
+            s.weights = pfc::Matrix(D, s.owned());
+            s.momentum = pfc::Matrix(D, s.owned());
+            shards.push_back(std::move(s));
+        }
+        std::vector<double> M(static_cast<size_t>(C * D), 0.0);
+        load_shards(shards, W, M.data());
+        const pfc::FeatureBatch batch = make_batch(X, labels, D, B);
+        out[0] = pfc::apcs(batch, shards);
+        pfc::ConflictInfo info;
+        const bool split = class_identity && sample_identity;
+        if (split) {
+            info.class_identity = std::span<const int64_t>(class_identity, static_cast<size_t>(C));
+            info.sample_identity = std::span<const int64_t>(sample_identity, static_cast<size_t>(B));
+        }
+        const pfc::AmncsResult a = pfc::amncs(batch, shards, split ? &info : nullptr);
+        out[1] = a.amncs;
+        out[2] = a.conflicted.value_or(0.0);
+        out[3] = a.hard.value_or(0.0);
+        flags[0] = a.conflicted.has_value() ? 1 : 0;
+        flags[1] = split ? 1 : 0;
         return 0;
     } catch (const std::exception& e) {
         set_err(err, errlen, e.what());

@@ -162,7 +162,37 @@ def step_golden(big: bool):
     return res
 
 
+# Diagnostics (metrics.hpp:56-146 via the step's with_diagnostics, shardsim.hpp:401-410).
+# Conflict ground truth: class_identity[j] = j // 3, sample_identity[b] = label_b // 3 except
+# every 5th row (b % 5 == 0), whose identity is (label_b // 3) + 1 (a foreign sibling group).
+DIAG_CASES = [("tiny", 40, 4, 8, 6), ("k1", 300, 1, 16, 24), ("k3", 1000, 3, 32, 50),
+              ("d64", 2000, 2, 64, 128), ("d512", 4000, 4, 512, 64)]
+
+
+def diag_identities(C_, labels):
+    ci = np.arange(C_, dtype=np.int64) // 3
+    si = labels // 3
+    si = np.where(np.arange(len(labels)) % 5 == 0, si + 1, si)
+    return ci, si
+
+
+def diag_golden():
+    out = []
+    for name, C_, K, D, B in DIAG_CASES:
+        W = R.init_centers(C_, K, D, 1)
+        X, labels = P.bench_inputs(C_, D, B, 1, 0)
+        ci, si = diag_identities(C_, labels)
+        plain = R.diagnostics(C_, K, D, W, X, labels)
+        split = R.diagnostics(C_, K, D, W, X, labels, ci, si)
+        out.append({"name": name, "C": C_, "K": K, "D": D, "B": B, "plain": plain, "split": split})
+    return out
+
+
 if __name__ == "__main__":
+    if "--diag-only" in sys.argv:
+        with open(os.path.join(OUT, "diag.json"), "w") as f:
+            json.dump(diag_golden(), f, indent=1)
+        sys.exit(0)
     big = "--big" in sys.argv
     with open(os.path.join(OUT, "rng.json"), "w") as f:
         json.dump(rng_golden(), f, indent=1)
@@ -172,4 +202,6 @@ if __name__ == "__main__":
     steps = step_golden(big)
     with open(os.path.join(OUT, "steps.json"), "w") as f:
         json.dump(steps, f, indent=1)
+    with open(os.path.join(OUT, "diag.json"), "w") as f:
+        json.dump(diag_golden(), f, indent=1)
     print("done")

@@ -182,3 +182,34 @@ def test_port_equals_compiled_reference_random():
         o2 = R.step(cfg, C_, K, D, W2, M2, X, labels, 3, 77)
         assert o1["loss"] == o2["loss"]
         assert np.array_equal(o1["dX"], o2["dX"]) and np.array_equal(W1, W2)
+
+
+def _diag_identities(C_, labels):
+    # tests/golden/make_golden.py: diag_identities
+    ci = np.arange(C_, dtype=np.int64) // 3
+    si = labels // 3
+    si = np.where(np.arange(len(labels)) % 5 == 0, si + 1, si)
+    return ci, si
+
+
+def test_diagnostics_match_reference_golden(port, golden_dir):
+    """apcs / amncs (+ conflicted / hard split): the C restatement of metrics.hpp:56-146 is
+    bit-identical to the compiled reference on every golden case."""
+    with open(os.path.join(golden_dir, "diag.json")) as f:
+        cases = json.load(f)
+    for cs in cases:
+        C_, K, D, B = cs["C"], cs["K"], cs["D"], cs["B"]
+        W = port.init_centers(C_, K, D, 1)
+        X, labels = port.bench_inputs(C_, D, B, 1, 0)
+        ci, si = _diag_identities(C_, labels)
+        assert port.diagnostics(C_, K, D, W, X, labels) == cs["plain"], cs["name"]
+        assert port.diagnostics(C_, K, D, W, X, labels, ci, si) == cs["split"], cs["name"]
+
+
+def test_diagnostics_errors(port):
+    W = port.init_centers(30, 2, 8, 1)
+    X = np.ones((8, 3))
+    with pytest.raises(OracleError, match="apcs: label 30 owned by no shard"):
+        port.diagnostics(30, 2, 8, W, X, np.array([0, 1, 30]))
+    with pytest.raises(OracleError, match="amncs: needs at least two classes"):
+        port.diagnostics(1, 1, 8, port.init_centers(1, 1, 8, 1), X, np.array([0, 0, 0]))

@@ -20,6 +20,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -104,6 +105,23 @@ class Session {
   // init_center_shards (shardsim.hpp:56-82) on the device
   void init_center_shards(uint64_t seed) { check(pfc_gpu_init_shards(ctx_, seed), ctx_); }
 
+  // apcs / amncs (metrics.hpp:56-146) of a batch against the current device shards
+  DiagnosticsSnapshot diagnostics(const FeatureBatch& batch,
+                                  const ConflictInfo* conflict = nullptr) {
+    batch.validate();
+    pfc_gpu_diag_out o{};
+    check(pfc_gpu_diagnostics(ctx_, batch.features.flat().data(), batch.labels.data(),
+                              batch.batch(), conflict ? conflict->class_identity.data() : nullptr,
+                              conflict ? conflict->sample_identity.data() : nullptr, &o),
+          ctx_);
+    DiagnosticsSnapshot d;
+    d.apcs = o.apcs;
+    d.amncs = o.amncs;
+    if (o.has_conflicted) d.amncs_conflicted = o.amncs_conflicted;
+    if (o.has_split) d.amncs_hard = o.amncs_hard;
+    return d;
+  }
+
   // == distributed_partial_step(shards, batch, cfg, iteration_rng) with the shards on the GPU.
   StepResult step(const FeatureBatch& batch, const StepConfig& cfg,
                   const SeededRng& iteration_rng) {
@@ -116,9 +134,18 @@ class Session {
       throw ContractError(
           "pfc::gpu::Session::step: StepConfig differs from the session's (only lr and "
           "step_index may change between steps)");
-    if (cfg.with_diagnostics)
-      throw ContractError("pfc::gpu::Session::step: with_diagnostics is not on the GPU path");
     if (batch.dim() != dim_) throw ShapeError("pfc::gpu::Session::step: feature dim mismatch");
+    std::optional<DiagnosticsSnapshot> diag;
+    if (cfg.with_diagnostics) {
+      // the reference reports them for the pre-update shards (shardsim.hpp:401-417), after its
+      // own label check (build_buffers): validate first, then measure, then step
+      for (int64_t l : batch.labels)
+        if (l < 0 || l >= layout_.num_classes)
+          throw ContractError("build_buffers: label " + std::to_string(l) + " outside [0, " +
+                              std::to_string(layout_.num_classes) + ")");
+      diag = diagnostics(batch, cfg.conflict);
+      diag->iteration = cfg.step_index;
+    }
     pfc_gpu_step_args a{iteration_rng.seed(), iteration_rng.stream_id(), cfg.lr, cfg.step_index};
     pfc_gpu_step_out o{};
     StepResult res;
@@ -126,6 +153,7 @@ class Session {
     check(pfc_gpu_step(ctx_, batch.features.flat().data(), batch.labels.data(), batch.batch(), &a,
                        res.d_features.flat().data(), &o),
           ctx_);
+    res.diagnostics = diag;
     res.loss = o.loss;
     res.trace.allgather_bytes = o.allgather_bytes;
     res.trace.reduce_scalar_bytes = o.reduce_scalar_bytes;

@@ -141,6 +141,26 @@ int pfc_gpu_get_buffers(void* ctx, int64_t shard, int64_t* class_indices, int64_
 /* The context's CUDA stream (cudaStream_t) for callers that enqueue around the step. */
 void* pfc_gpu_stream(void* ctx);
 
+/* ---- diagnostics (StepConfig::with_diagnostics, shardsim.hpp:401-410) -------------------- */
+typedef struct {
+  double apcs;              /* metrics.hpp:56-79 */
+  double amncs;             /* metrics.hpp:91-146 */
+  double amncs_conflicted;  /* valid when has_conflicted */
+  double amncs_hard;        /* valid when has_split */
+  int32_t has_conflicted;   /* AmncsResult::conflicted.has_value() */
+  int32_t has_split;        /* the conflict ground truth was given */
+  int32_t reserved[2];
+} pfc_gpu_diag_out;
+/* apcs / amncs of a (global, already gathered) batch against the CURRENT shards, i.e. what the
+ * reference step reports with with_diagnostics (computed there on the pre-update shards: call
+ * this before pfc_gpu_step).  X is D x B fp64 row-major, labels[B] (host).  class_identity[C]
+ * and sample_identity[B] (host, both or neither) give ConflictInfo (types.hpp:80-86).  Every
+ * rank calls it; the maxima are merged over ranks.  amncs is exact (fp64 re-evaluation of the
+ * bf16 GEMM's near-maximal classes).  Errors carry the reference's text. */
+int pfc_gpu_diagnostics(void* ctx, const double* features_d_by_b, const int64_t* labels,
+                        int64_t batch, const int64_t* class_identity,
+                        const int64_t* sample_identity, pfc_gpu_diag_out* out);
+
 /* ---- bench / test helpers --------------------------------------------------------------- */
 /* Synthetic inputs of the bench convention on the device:
  * labels[b] = SeededRng(seed, make_stream("bench-labels", step)).next_below(C) and

@@ -114,6 +114,39 @@ int main() {
           trace_ok ? "true" : "false", got.loss, want.loss, dl, dx, dw, pass ? "true" : "false");
     }
   }
+  // with_diagnostics (shardsim.hpp:401-410): apcs / amncs on the pre-update shards, with the
+  // conflict split; the GPU values are exact up to fp32 storage of W
+  {
+    const ShardLayout layout(4000, 4);
+    std::vector<CenterShard> ref = init_center_shards(layout, 512, 1);
+    StepConfig cfg;
+    cfg.margin = MarginConfig::arcface_style();
+    cfg.with_diagnostics = true;
+    cfg.step_index = 3;
+    gpu::Session session(layout, 512, cfg, 64);
+    session.upload(ref);
+    const FeatureBatch batch = bench_batch(4000, 512, 64, 0);
+    std::vector<int64_t> cid(4000), sid(64);
+    for (int64_t j = 0; j < 4000; ++j) cid[j] = j / 3;
+    for (int64_t b = 0; b < 64; ++b) sid[b] = batch.labels[b] / 3 + (b % 5 == 0 ? 1 : 0);
+    const ConflictInfo info{std::span<const int64_t>(cid), std::span<const int64_t>(sid)};
+    cfg.conflict = &info;
+    const SeededRng it(1, make_stream("iteration", 0));
+    const StepResult want = distributed_partial_step(ref, batch, cfg, it);
+    const StepResult got = session.step(batch, cfg, it);
+    const auto& a = *got.diagnostics;
+    const auto& b = *want.diagnostics;
+    const double e = std::max({std::fabs(a.apcs - b.apcs), std::fabs(a.amncs - b.amncs),
+                               std::fabs(*a.amncs_hard - *b.amncs_hard),
+                               std::fabs(*a.amncs_conflicted - *b.amncs_conflicted)});
+    const bool pass = got.diagnostics && want.diagnostics && a.iteration == b.iteration &&
+                      a.amncs_hard.has_value() == b.amncs_hard.has_value() && e <= 1e-6 &&
+                      std::fabs(got.loss - want.loss) / std::fabs(want.loss) <= 1e-4;
+    ok = ok && pass;
+    std::printf("{\"case\": \"with_diagnostics\", \"apcs\": %.12f, \"apcs_ref\": %.12f, "
+                "\"amncs\": %.12f, \"amncs_ref\": %.12f, \"max_abs\": %.3e, \"pass\": %s}\n",
+                a.apcs, b.apcs, a.amncs, b.amncs, e, pass ? "true" : "false");
+  }
   // the unchanged-signature free function on host shards + the reference's error text
   {
     const ShardLayout layout(1000, 4);

@@ -142,7 +142,7 @@ class MarginConfig:
 
 @dataclass
 class StepConfig:
-    """shardsim.hpp:117-127 (with_diagnostics / conflict are outside this path)."""
+    """shardsim.hpp:117-127.  ``conflict`` (ConflictInfo) is used when with_diagnostics."""
     r: float = 0.1
     margin: MarginConfig = field(default_factory=MarginConfig.cosface_style)
     filter_threshold: float | None = None
@@ -151,6 +151,30 @@ class StepConfig:
     weight_decay: float = 5e-4
     with_diagnostics: bool = False
     step_index: int = -1
+    conflict: "ConflictInfo | None" = None
+
+
+@dataclass
+class ConflictInfo:
+    """types.hpp:80-86: true identity of every class [C] and of every batch sample [B]."""
+    class_identity: np.ndarray
+    sample_identity: np.ndarray
+
+
+@dataclass
+class DiagnosticsSnapshot:
+    """types.hpp:72-78 (metrics.hpp:56-146 as the step reports them)."""
+    iteration: int = 0
+    apcs: float = 0.0
+    amncs: float = 0.0
+    amncs_conflicted: float | None = None
+    amncs_hard: float | None = None
+
+
+class DiagOut(C.Structure):
+    _fields_ = [("apcs", C.c_double), ("amncs", C.c_double), ("amncs_conflicted", C.c_double),
+                ("amncs_hard", C.c_double), ("has_conflicted", C.c_int32),
+                ("has_split", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 @dataclass
@@ -177,6 +201,7 @@ class StepResult:
     d_features: np.ndarray | None
     trace: CollectiveTrace
     buffers: list
+    diagnostics: DiagnosticsSnapshot | None = None
 
 
 class ShardLayout:
@@ -281,6 +306,7 @@ def load_library(path: str | None = None) -> C.CDLL:
                                           C.c_int]),
         "pfc_gpu_set_phase_timing": (C.c_int, [vp, C.c_int]),
         "pfc_gpu_launches_per_step": (i64, [vp]),
+        "pfc_gpu_diagnostics": (C.c_int, [vp, vp, vp, i64, vp, vp, C.POINTER(DiagOut)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -422,6 +448,26 @@ class CenterShards:
                              out.reduce_ops)
         return StepResult(out.loss, dx, tr, [])
 
+    def diagnostics(self, features_dxb: np.ndarray, labels, conflict: ConflictInfo | None = None
+                    ) -> DiagnosticsSnapshot:
+        """apcs / amncs of the batch against the current shards (metrics.hpp:56-146)."""
+        x = np.ascontiguousarray(features_dxb, dtype=np.float64)
+        lab = np.ascontiguousarray(labels, dtype=np.int64)
+        if x.ndim != 2 or x.shape[1] != lab.shape[0] or x.shape[0] != self.dim:
+            raise ShapeError("FeatureBatch: label count != feature columns")
+        ci = si = None
+        if conflict is not None:
+            ci = np.ascontiguousarray(conflict.class_identity, dtype=np.int64)
+            si = np.ascontiguousarray(conflict.sample_identity, dtype=np.int64)
+            if ci.shape != (self.layout.num_classes,) or si.shape != lab.shape:
+                raise ShapeError("ConflictInfo: identity sizes must be C and B")
+        out = DiagOut()
+        _check(_lib.pfc_gpu_diagnostics(self._h, _ptr(x), _ptr(lab), lab.shape[0], _ptr(ci),
+                                        _ptr(si), C.byref(out)), self._h)
+        return DiagnosticsSnapshot(0, out.apcs, out.amncs,
+                                   out.amncs_conflicted if out.has_conflicted else None,
+                                   out.amncs_hard if out.has_split else None)
+
     def step_device(self, x_local_ptr: int, labels_local_ptr: int, b_local: int, dx_local_ptr: int,
                     cfg: StepConfig, iteration_rng: SeededRng, sync: bool = True):
         args = StepArgs(iteration_rng.seed, iteration_rng.stream_id, cfg.lr, cfg.step_index)
@@ -452,8 +498,18 @@ def distributed_partial_step(shards: CenterShards, features_dxb: np.ndarray, lab
             cfg.momentum != shards.cfg.momentum or cfg.weight_decay != shards.cfg.weight_decay:
         raise ContractError("distributed_partial_step: StepConfig differs from the one the "
                             "device shards were created with (only lr / step_index may vary)")
+    diag = None
     if cfg.with_diagnostics:
-        raise ContractError("distributed_partial_step: with_diagnostics is outside this path")
+        # the reference reports them for the pre-update shards (shardsim.hpp:401-417); its label
+        # check (build_buffers) comes first, so validate before measuring
+        lab = np.ascontiguousarray(labels, dtype=np.int64)
+        bad = lab[(lab < 0) | (lab >= shards.layout.num_classes)]
+        if bad.size:
+            raise ContractError(f"build_buffers: label {int(np.sort(bad)[0])} outside "
+                                f"[0, {shards.layout.num_classes})")
+        diag = shards.diagnostics(features_dxb, lab, cfg.conflict)
+        diag.iteration = cfg.step_index
     res = shards.step_host(features_dxb, labels, cfg, iteration_rng)
     res.buffers = shards.buffers()
+    res.diagnostics = diag
     return res

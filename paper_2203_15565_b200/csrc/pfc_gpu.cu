@@ -29,6 +29,7 @@
 #include "epilogues.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "diag.cuh"
 #include "sampler.cu"
 
 namespace pfc {
@@ -41,8 +42,8 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct {
   char internal[128];
 } ncclUniqueId;
-enum { ncclInt8 = 0, ncclInt32 = 2, ncclInt64 = 4, ncclFloat32 = 7, ncclFloat64 = 8 };
-enum { ncclSum = 0 };
+enum { ncclInt8 = 0, ncclInt32 = 2, ncclInt64 = 4, ncclUint64 = 5, ncclFloat32 = 7, ncclFloat64 = 8 };
+enum { ncclSum = 0, ncclMax = 2 };
 struct Nccl {
   void* h = nullptr;
   int (*GetUniqueId)(ncclUniqueId*) = nullptr;
@@ -158,6 +159,15 @@ struct Ctx {
   int32_t* pool_scratch = nullptr;
   // features / centres
   float* X = nullptr;  // global batch rows [B][D] fp32 (world > 1 / host path)
+  // diagnostics (pfc_gpu_diagnostics), allocated on first use
+  void* dwall = nullptr;  // w^ of every local class, operand dtype [rows_pad][Dp]
+  double *dwinv = nullptr, *dxinv = nullptr, *dapcs = nullptr;
+  uint32_t* drmax = nullptr;
+  unsigned long long* demax = nullptr;
+  int* dhasc = nullptr;
+  int64_t *dcid = nullptr, *dsid = nullptr;
+  int64_t diag_rows_pad = 0;
+  CUtensorMap tm_wall;
   float* xnorm = nullptr;
   void* xh = nullptr;  // [maxB][Dp] bf16 or fp32
   void* wh = nullptr;  // [ncols_pad][Dp]
@@ -798,6 +808,62 @@ int validate_desc(const pfc_gpu_desc* d) {
 
 using namespace pfc;
 
+__global__ void diag_fill_kernel(uint32_t* rmax, unsigned long long* emax, int* hasc, int n3,
+                                 int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n3) {
+    rmax[i] = pfc::enc_f32(-INFINITY);
+    emax[i] = pfc::enc_f64(-INFINITY);
+  }
+  if (i < n) hasc[i] = 0;
+}
+
+template <typename OT, bool kUmma>
+int run_diagnostics(Ctx* c, int64_t B, bool split) {
+  cudaStream_t s = c->stream;
+  const int bs = 256;
+  OT* xh = static_cast<OT*>(c->xh);
+  OT* wall = static_cast<OT*>(c->dwall);
+  diag_norm_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(c->X, (int)B, (int)c->D,
+                                                                       (int)c->Dp, xh, c->dxinv);
+  diag_norm_w_kernel<OT><<<(unsigned)ceil_div(c->diag_rows_pad * 32, bs), bs, 0, s>>>(
+      c->W, c->rows, c->diag_rows_pad, (int)c->D, (int)c->Dp, wall, c->dwinv);
+  diag_fill_kernel<<<(unsigned)ceil_div(B * 3, bs), bs, 0, s>>>(c->drmax, c->demax, c->dhasc,
+                                                                (int)(B * 3), (int)B);
+  CUDA_TRY(c, cudaGetLastError());
+  DiagMaxEpi e{};
+  e.B = (int)B;
+  e.D = (int)c->D;
+  e.rows = c->rows;
+  e.cls_lo = c->cls_lo;
+  e.labels = c->labels;
+  e.cid = split ? c->dcid : nullptr;
+  e.sid = split ? c->dsid : nullptr;
+  e.rmax = c->drmax;
+  e.emax = c->demax;
+  e.hasc = c->dhasc;
+  e.X = c->X;
+  e.xinv = c->dxinv;
+  e.W = c->W;
+  e.winv = c->dwinv;
+  cudaError_t err;
+  if constexpr (kUmma) {
+    if (int rc = ensure_maps(c, B)) return rc;
+    const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kBN, 1, 0);
+    err = launch_umma<kBN, 4, 2, false, false>(c, c->tm_x_k, c->tm_wall, g, e);
+  } else {
+    const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kSimtBN, 1, 0);
+    err = launch_simt<false, false>(c, (const float*)xh, (int)c->Dp, (const float*)wall,
+                                    (int)c->Dp, g, e);
+  }
+  CUDA_TRY(c, err);
+  diag_apcs_kernel<<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(c->X, c->dxinv, c->W, c->dwinv,
+                                                           c->labels, (int)B, (int)c->D,
+                                                           c->cls_lo, c->rows, c->dapcs);
+  CUDA_TRY(c, cudaGetLastError());
+  return PFC_OK;
+}
+
 extern "C" {
 
 const char* pfc_gpu_version(void) { return "pfc_gpu 0.1 (sm_100a tcgen05)"; }
@@ -1141,6 +1207,96 @@ int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_l
   c->reset_status = true;
   if (int rc = finish_phase_timing(c)) return rc;
   return check_status(c, a->step_index, B, out);
+}
+
+int pfc_gpu_diagnostics(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
+                        const int64_t* class_identity, const int64_t* sample_identity,
+                        pfc_gpu_diag_out* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (B < 1 || B > c->maxB)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: batch %lld outside [1, max_batch=%lld]", (long long)B,
+                (long long)c->maxB);
+  if ((class_identity == nullptr) != (sample_identity == nullptr))
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_diagnostics: give both identities or neither");
+  // apcs (metrics.hpp:56-79) validates the labels first, then l2_normalize_columns (matrix.hpp:141)
+  for (int64_t b = 0; b < B; ++b)
+    if (labels[b] < 0 || labels[b] >= c->C)
+      return fail(c, PFC_ERR_CONTRACT, "apcs: label %lld owned by no shard", (long long)labels[b]);
+  for (int64_t i = 0; i < B * c->D; ++i)
+    if (!std::isfinite(xdb[i]))
+      return fail(c, PFC_ERR_NUMERICAL, "l2_normalize_columns: non-finite entry in %lldx%lld result",
+                  (long long)c->D, (long long)B);
+  if (c->C < 2) return fail(c, PFC_ERR_CONTRACT, "amncs: needs at least two classes");
+  const bool split = class_identity != nullptr;
+  cudaStream_t s = c->stream;
+  if (!c->dwall) {  // w^ of every local class, kept across calls
+    c->diag_rows_pad = round_up(std::max<int64_t>(c->rows, 1), 256);
+    const size_t ob = c->bf16 ? 2 : 4;
+    CUDA_TRY(c, dalloc(c, reinterpret_cast<uint8_t**>(&c->dwall), (size_t)c->diag_rows_pad * c->Dp * ob));
+    CUDA_TRY(c, dalloc(c, &c->dwinv, (size_t)c->diag_rows_pad));
+    CUDA_TRY(c, dalloc(c, &c->dxinv, (size_t)c->maxB));
+    CUDA_TRY(c, dalloc(c, &c->dapcs, (size_t)c->maxB));
+    CUDA_TRY(c, dalloc(c, &c->drmax, (size_t)c->maxB * 3));
+    CUDA_TRY(c, dalloc(c, &c->demax, (size_t)c->maxB * 3));
+    CUDA_TRY(c, dalloc(c, &c->dhasc, (size_t)c->maxB));
+    CUDA_TRY(c, dalloc(c, &c->dcid, (size_t)std::max<int64_t>(c->rows, 1)));
+    CUDA_TRY(c, dalloc(c, &c->dsid, (size_t)c->maxB));
+    if (c->bf16 && !make_map(&c->tm_wall, c->dwall, c->Dp, c->rows, c->Dp, kBN))
+      return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
+  if (split) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->dcid, class_identity + c->cls_lo, sizeof(int64_t) * c->rows,
+                                cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(c->dsid, sample_identity, sizeof(int64_t) * B,
+                                cudaMemcpyHostToDevice, s));
+  }
+  dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+  x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
+  const int rc = c->bf16 ? run_diagnostics<__nv_bfloat16, true>(c, B, split)
+                         : run_diagnostics<float, false>(c, B, split);
+  if (rc) return rc;
+  if (c->R > 1) {  // merge over ranks: maxima, sibling flags, the owner's apcs term
+    NCCL_TRY(c, g_nccl.AllReduce(c->demax, c->demax, B * 3, ncclUint64, ncclMax, c->comm, s));
+    NCCL_TRY(c, g_nccl.AllReduce(c->dhasc, c->dhasc, B, ncclInt32, ncclMax, c->comm, s));
+    NCCL_TRY(c, g_nccl.AllReduce(c->dapcs, c->dapcs, B, ncclFloat64, ncclSum, c->comm, s));
+  }
+  std::vector<unsigned long long> em((size_t)B * 3);
+  std::vector<int> hc((size_t)B);
+  std::vector<double> ap((size_t)B);
+  CUDA_TRY(c, cudaMemcpyAsync(em.data(), c->demax, sizeof(unsigned long long) * B * 3,
+                              cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(hc.data(), c->dhasc, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(ap.data(), c->dapcs, sizeof(double) * B, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  // means in the reference's order (b ascending, metrics.hpp:76-78, 118-146)
+  double apcs = 0.0, total = 0.0, hard = 0.0, conf = 0.0;
+  int64_t conf_rows = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    apcs += ap[b];
+    const double m0 = dec_f64(em[b * 3]), m1 = dec_f64(em[b * 3 + 1]), m2 = dec_f64(em[b * 3 + 2]);
+    total += split ? std::max(m1, m2) : m0;
+    if (split) {
+      hard += m2;
+      if (hc[b]) {
+        conf += m1;
+        ++conf_rows;
+      }
+    }
+  }
+  *out = pfc_gpu_diag_out{};
+  out->apcs = apcs / (double)B;
+  out->amncs = total / (double)B;
+  out->has_split = split ? 1 : 0;
+  if (split) {
+    out->amncs_hard = hard / (double)B;
+    if (conf_rows > 0) {
+      out->amncs_conflicted = conf / (double)conf_rows;
+      out->has_conflicted = 1;
+    }
+  }
+  return PFC_OK;
 }
 
 int pfc_gpu_sync(void* ctx, pfc_gpu_step_out* out) {

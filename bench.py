@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--r", type=float, default=0.1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-diag", action="store_true", help="skip timing the diagnostics call")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     return ap.parse_args()
 
@@ -328,6 +329,24 @@ def main():
                              "formula": "6*B*cap_local*d / bf16_sustained + 20*cap_local*d / hbm "
                                         "(SURVEY.md 8d)"}
     line["phases_ms"] = phases
+
+    # ---- diagnostics (with_diagnostics): apcs + exact amncs over all C
+    #      classes (a 2 B d C screening GEMM); wall time of the host call, X / labels from host
+    if not args.no_diag:
+        X0 = xs[0].t().double().cpu().numpy()
+        L0 = ls[0].cpu().numpy()
+        sh.diagnostics(X0, L0)  # builds the all-class operand once
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nd = 3
+        for _ in range(nd):
+            dg = sh.diagnostics(X0, L0)
+        dms = (time.perf_counter() - t0) / nd * 1e3
+        gf = 2.0 * B * C_ / ws * D
+        line["diagnostics"] = {"ms_per_call": dms, "apcs": dg.apcs, "amncs": dg.amncs,
+                               "screen_gemm_flop": gf, "effective_tflops": gf / (dms / 1e3) / 1e12,
+                               "note": "host call incl. X upload and the fp32 -> bf16 pass over "
+                                       "all local W rows; amncs exact (fp64 re-evaluation)"}
 
     # ---- e2e through the reference-facing host API (pfc_gpu_step: host X / labels in,
     #      host dX + loss out, copies inside the timed region), full global batch on each rank

@@ -85,34 +85,44 @@ __device__ __forceinline__ double diag_dot_exact(const float* __restrict__ X, do
   return s;
 }
 
-// apcs rows: the owner rank's exact cosine to the sample's own centre, 0 elsewhere
+// apcs rows: the owner rank's exact cosine to the sample's own centre, 0 elsewhere (warp/row)
 __global__ void diag_apcs_kernel(const float* __restrict__ X, const double* __restrict__ xinv,
                                  const float* __restrict__ W, const double* __restrict__ winv,
                                  const int64_t* __restrict__ labels, int B, int D, int64_t cls_lo,
                                  int64_t rows, double* __restrict__ apcs_row) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (b >= B) return;
   const int64_t r = labels[b] - cls_lo;
-  apcs_row[b] = (r >= 0 && r < rows)
-                    ? diag_dot_exact(X + (size_t)b * D, xinv[b], W + (size_t)r * D, winv[r], D)
-                    : 0.0;
+  double s = 0.0;
+  if (r >= 0 && r < rows) {
+    const float* x = X + (size_t)b * D;
+    const float* w = W + (size_t)r * D;
+    const double xi = xinv[b], wi = winv[r];
+    for (int d = lane; d < D; d += 32) s += ((double)x[d] * xi) * ((double)w[d] * wi);
+    s = warp_sum(s);
+  }
+  if (lane == 0) apcs_row[b] = s;
 }
+
+struct DiagCand {  // a class within kBand of its bucket's running maximum when it was seen
+  int32_t b, k;
+  int64_t j;
+  float v, pad;
+};
 
 struct DiagMaxEpi : NoSetup {
   static constexpr int kSmem = 0;
   static constexpr float kBand = 1.0f / 64.0f;  // > 2 x (2^-8 + fp32 accumulation)
-  int B, D;
+  int B;
   int64_t rows, cls_lo;
   const int64_t* labels;   // [B] global
   const int64_t* cid;      // [rows] class identity of the local classes, or nullptr (no split)
   const int64_t* sid;      // [B] sample identity, or nullptr
   uint32_t* rmax;          // [B][3] running bf16 maximum per bucket (enc_f32)
-  unsigned long long* emax;  // [B][3] exact maximum per bucket (enc_f64)
   int* hasc;               // [B] a sibling class exists
-  const float* X;          // [B][D]
-  const double* xinv;      // [B]
-  const float* W;          // [rows][D]
-  const double* winv;      // [rows]
+  DiagCand* cand;          // candidate list for the exact pass
+  unsigned long long* ncand;
+  unsigned long long cap;
 
   struct Pre {};
   __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
@@ -136,7 +146,31 @@ struct DiagMaxEpi : NoSetup {
       src.load(c0, v);  // all lanes: tcgen05.ld is warp-collective
       const int64_t colb = t.col0 + c0;
       if (!rv || colb >= rows) continue;
-      // per-column bucket: 0 without split; 1 = sibling, 2 = other with split; -1 = excluded
+      if (!cid) {  // no split: one bucket; the per-column work runs only near the maximum
+        float cm = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int64_t j = colb + q;
+          cm = (j < rows && j != lab) ? fmaxf(cm, v[q]) : cm;
+        }
+        if (cm > rm[0]) {
+          rm[0] = cm;
+          atomicMax(rmax + b * 3, enc_f32(cm));
+        }
+        if (cm < rm[0] - kBand) continue;
+#pragma unroll 1
+        for (int q = 0; q < 32; ++q) {
+          const int64_t j = colb + q;
+          float vq = v[0];
+#pragma unroll
+          for (int u = 1; u < 32; ++u) vq = (u == q) ? v[u] : vq;
+          if (j >= rows || j == lab || vq < rm[0] - kBand) continue;
+          const unsigned long long i = atomicAdd(ncand, 1ull);
+          if (i < cap) cand[i] = DiagCand{b, 0, j, vq, 0.f};
+        }
+        continue;
+      }
+      // per-column bucket: 1 = sibling, 2 = other (with the conflict split); -1 = excluded
       int bk[32];
       float cm[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -154,17 +188,41 @@ struct DiagMaxEpi : NoSetup {
           rm[k] = cm[k];
           atomicMax(rmax + b * 3 + k, enc_f32(cm[k]));
         }
-      // candidates: within kBand of the running maximum of their bucket -> exact fp64 cosine
+      // candidates: within kBand of the running maximum of their bucket; evaluated exactly by
+      // diag_exact_kernel (which drops those below the FINAL maximum minus kBand)
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
         const int k = bk[q];
         if (k < 0 || v[q] < rm[k] - kBand) continue;
-        const int64_t j = colb + q;
-        const double e = diag_dot_exact(X + (size_t)b * D, xinv[b], W + (size_t)j * D, winv[j], D);
-        atomicMax(emax + b * 3 + k, enc_f64(e));
+        const unsigned long long i = atomicAdd(ncand, 1ull);
+        if (i < cap) cand[i] = DiagCand{b, k, colb + q, v[q], 0.f};
       }
     }
   }
 };
+
+// One warp per candidate: exact fp64 cosine (lanes stride d, fixed-order warp reduction) of the
+// candidates within kBand of their row's final bf16 maximum; atomic max into emax.
+__global__ void diag_exact_kernel(const DiagCand* __restrict__ cand,
+                                  const unsigned long long* __restrict__ ncand,
+                                  unsigned long long cap, const uint32_t* __restrict__ rmax,
+                                  const float* __restrict__ X, const double* __restrict__ xinv,
+                                  const float* __restrict__ W, const double* __restrict__ winv,
+                                  int D, unsigned long long* __restrict__ emax) {
+  const unsigned long long n = min(*ncand, cap);
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+    const DiagCand c = cand[i];
+    if (c.v < dec_f32(rmax[c.b * 3 + c.k]) - DiagMaxEpi::kBand) continue;  // warp-uniform
+    const float* x = X + (size_t)c.b * D;
+    const float* w = W + (size_t)c.j * D;
+    const double xi = xinv[c.b], wi = winv[c.j];
+    double s = 0.0;
+    for (int d = lane; d < D; d += 32) s += ((double)x[d] * xi) * ((double)w[d] * wi);
+    s = warp_sum(s);
+    if (lane == 0) atomicMax(emax + c.b * 3 + c.k, enc_f64(s));
+  }
+}
 
 }  // namespace pfc

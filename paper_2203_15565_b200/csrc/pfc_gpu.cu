@@ -167,6 +167,9 @@ struct Ctx {
   int* dhasc = nullptr;
   int64_t *dcid = nullptr, *dsid = nullptr;
   int64_t diag_rows_pad = 0;
+  DiagCand* dcand = nullptr;
+  unsigned long long* dncand = nullptr;
+  int64_t dcand_cap = 0;
   CUtensorMap tm_wall;
   float* xnorm = nullptr;
   void* xh = nullptr;  // [maxB][Dp] bf16 or fp32
@@ -833,31 +836,42 @@ int run_diagnostics(Ctx* c, int64_t B, bool split) {
   CUDA_TRY(c, cudaGetLastError());
   DiagMaxEpi e{};
   e.B = (int)B;
-  e.D = (int)c->D;
   e.rows = c->rows;
   e.cls_lo = c->cls_lo;
   e.labels = c->labels;
   e.cid = split ? c->dcid : nullptr;
   e.sid = split ? c->dsid : nullptr;
   e.rmax = c->drmax;
-  e.emax = c->demax;
   e.hasc = c->dhasc;
-  e.X = c->X;
-  e.xinv = c->dxinv;
-  e.W = c->W;
-  e.winv = c->dwinv;
-  cudaError_t err;
-  if constexpr (kUmma) {
-    if (int rc = ensure_maps(c, B)) return rc;
-    const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kBN, 1, 0);
-    err = launch_umma<kBN, 4, 2, false, false>(c, c->tm_x_k, c->tm_wall, g, e);
-  } else {
-    const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kSimtBN, 1, 0);
-    err = launch_simt<false, false>(c, (const float*)xh, (int)c->Dp, (const float*)wall,
-                                    (int)c->Dp, g, e);
+  e.cand = c->dcand;
+  e.ncand = c->dncand;
+  e.cap = (unsigned long long)c->dcand_cap;
+  // screening GEMM; if the candidate list overflowed (running maxima still low early on), screen
+  // again from the final maxima, which keeps only near-maximal classes
+  for (int pass = 0; pass < 2; ++pass) {
+    CUDA_TRY(c, cudaMemsetAsync(c->dncand, 0, sizeof(unsigned long long), s));
+    cudaError_t err;
+    if constexpr (kUmma) {
+      if (int rc = ensure_maps(c, B)) return rc;
+      const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kBN, 1, 0);
+      err = launch_umma<kBN, 4, 2, false, false>(c, c->tm_x_k, c->tm_wall, g, e);
+    } else {
+      const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kSimtBN, 1, 0);
+      err = launch_simt<false, false>(c, (const float*)xh, (int)c->Dp, (const float*)wall,
+                                      (int)c->Dp, g, e);
+    }
+    CUDA_TRY(c, err);
+    unsigned long long n = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&n, c->dncand, sizeof(n), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (n <= (unsigned long long)c->dcand_cap) break;
+    if (pass == 1) return fail(c, PFC_ERR_CUDA, "pfc_gpu_diagnostics: candidate list overflow");
   }
-  CUDA_TRY(c, err);
-  diag_apcs_kernel<<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(c->X, c->dxinv, c->W, c->dwinv,
+  diag_exact_kernel<<<(unsigned)(c->num_sms * 8), 256, 0, s>>>(
+      c->dcand, c->dncand, (unsigned long long)c->dcand_cap, c->drmax, c->X, c->dxinv, c->W,
+      c->dwinv, (int)c->D, c->demax);
+  CUDA_TRY(c, cudaGetLastError());
+  diag_apcs_kernel<<<(unsigned)ceil_div(B * 32, bs), bs, 0, s>>>(c->X, c->dxinv, c->W, c->dwinv,
                                                            c->labels, (int)B, (int)c->D,
                                                            c->cls_lo, c->rows, c->dapcs);
   CUDA_TRY(c, cudaGetLastError());
@@ -1241,6 +1255,9 @@ int pfc_gpu_diagnostics(void* ctx, const double* xdb, const int64_t* labels, int
     CUDA_TRY(c, dalloc(c, &c->dhasc, (size_t)c->maxB));
     CUDA_TRY(c, dalloc(c, &c->dcid, (size_t)std::max<int64_t>(c->rows, 1)));
     CUDA_TRY(c, dalloc(c, &c->dsid, (size_t)c->maxB));
+    c->dcand_cap = (int64_t)1 << 22;  // 4M candidates (64 MB)
+    CUDA_TRY(c, dalloc(c, &c->dcand, (size_t)c->dcand_cap));
+    CUDA_TRY(c, dalloc(c, &c->dncand, (size_t)1));
     if (c->bf16 && !make_map(&c->tm_wall, c->dwall, c->Dp, c->rows, c->Dp, kBN))
       return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }

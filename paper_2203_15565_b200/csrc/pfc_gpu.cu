@@ -1151,16 +1151,11 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
   Ctx* c = static_cast<Ctx*>(ctx);
   if (!(a->lr >= 0.0)) return fail(c, PFC_ERR_CONTRACT, "distributed_partial_step: lr must be >= 0");
   if (B < 0) return fail(c, PFC_ERR_SHAPE, "FeatureBatch: label count != feature columns");
-  if (int rc = host_validate(c, labels, B)) return rc;
-  if (B == 0)
-    return fail(c, PFC_ERR_NUMERICAL, "distributed_partial_step: non-finite loss at step %lld",
-                (long long)a->step_index);
-  if (B > c->maxB)
-    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: batch %lld exceeds max_batch %lld", (long long)B,
-                (long long)c->maxB);
   cudaStream_t s = c->stream;
-  if (pinned(xdb) && pinned(labels) && pinned(dxdb)) {
+  if (B > 0 && B <= c->maxB && pinned(xdb) && pinned(labels) && pinned(dxdb)) {
     // copies inside the step: X upload overlaps the sampler + gather, dX download the dW GEMM.
+    // The host-side label / capacity check runs while the GPU works: the device sampler makes
+    // the same checks and skips every update on failure, so launching first is safe.
     // On an error the contents of dxdb are unspecified (the reference throws instead).
     c->e2e = {true, xdb, labels, dxdb};
     const int rc = run_step(c, c->X, c->labels, B, a, c->dX);
@@ -1168,10 +1163,19 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
     if (rc) return rc;
     c->reset_status = true;
     CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
+    const int vrc = host_validate(c, labels, B);
     CUDA_TRY(c, cudaStreamSynchronize(s));
     if (int rc2 = finish_phase_timing(c)) return rc2;
+    if (vrc) return vrc;
     return check_status(c, a->step_index, B, out);
   }
+  if (int rc = host_validate(c, labels, B)) return rc;
+  if (B == 0)
+    return fail(c, PFC_ERR_NUMERICAL, "distributed_partial_step: non-finite loss at step %lld",
+                (long long)a->step_index);
+  if (B > c->maxB)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: batch %lld exceeds max_batch %lld", (long long)B,
+                (long long)c->maxB);
   CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
   dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);

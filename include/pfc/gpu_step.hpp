@@ -37,6 +37,7 @@ namespace pfc::gpu {
     case PFC_ERR_CAPACITY: throw CapacityError(m);
     case PFC_ERR_CONFIG: throw ConfigError(m);
     case PFC_ERR_NUMERICAL: throw NumericalError(m);
+    case PFC_ERR_IO: throw DataError(m);
     default: throw Error(m);
   }
 }

@@ -39,7 +39,8 @@ typedef enum {
   PFC_ERR_CONFIG = 4,     /* pfc::ConfigError */
   PFC_ERR_NUMERICAL = 5,  /* pfc::NumericalError */
   PFC_ERR_CUDA = 6,       /* CUDA runtime / driver failure (no reference counterpart) */
-  PFC_ERR_NCCL = 7        /* NCCL failure (no reference counterpart) */
+  PFC_ERR_NCCL = 7,       /* NCCL failure (no reference counterpart) */
+  PFC_ERR_IO = 8          /* pfc::DataError (checkpoint streams, io.hpp) */
 } pfc_status;
 
 typedef enum { /* MarginKind, margin.hpp:11 */
@@ -160,6 +161,18 @@ typedef struct {
 int pfc_gpu_diagnostics(void* ctx, const double* features_d_by_b, const int64_t* labels,
                         int64_t batch, const int64_t* class_identity,
                         const int64_t* sample_identity, pfc_gpu_diag_out* out);
+
+/* ---- checkpoints (trainer.hpp:235-338 shard section; io.hpp:18-91 encoding) --------------- */
+/* Write this rank's shard section in the reference's checkpoint encoding: int64 count, then per
+ * local shard int64 shard_id, class_begin, class_end and weights, momentum as put_matrix
+ * (int64 rows = D, int64 cols = owned, D x owned fp64 row-major).  append != 0 appends (after
+ * a caller-written header, as save_checkpoint's sections follow one another). */
+int pfc_gpu_write_shards(void* ctx, const char* path, int append);
+/* Read a shard section starting at byte `offset` of `path` (written by the reference's
+ * save_checkpoint or by pfc_gpu_write_shards) into the device state; shards of other ranks are
+ * skipped; *end_offset (may be NULL) receives the offset after the section.  Matrices larger
+ * than the reference reader's 2^32-element cap (io.hpp:78) are accepted. */
+int pfc_gpu_read_shards(void* ctx, const char* path, int64_t offset, int64_t* end_offset);
 
 /* ---- bench / test helpers --------------------------------------------------------------- */
 /* Synthetic inputs of the bench convention on the device:

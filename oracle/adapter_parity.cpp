@@ -16,6 +16,8 @@
 
 #include "pfc/gpu_step.hpp"
 #include "pfc/shardsim.hpp"
+#include "pfc/io.hpp"
+#include "pfc/trainer.hpp"
 
 using namespace pfc;
 
@@ -146,6 +148,58 @@ int main() {
     std::printf("{\"case\": \"with_diagnostics\", \"apcs\": %.12f, \"apcs_ref\": %.12f, "
                 "\"amncs\": %.12f, \"amncs_ref\": %.12f, \"max_abs\": %.3e, \"pass\": %s}\n",
                 a.apcs, b.apcs, a.amncs, b.amncs, e, pass ? "true" : "false");
+  }
+  // checkpoint (trainer.hpp:235-338): the reference's save_checkpoint writes the shards; the
+  // device reads its shard section in place; a device-written section parses with the
+  // reference's BinaryReader
+  {
+    const ShardLayout layout(5000, 4);
+    detail::CheckpointState cs;
+    cs.next_step = 7;
+    cs.shards = init_center_shards(layout, 64, 9);
+    // fp32-representable values (the device keeps fp32 master weights), so the round trip is
+    // an equality
+    for (auto& sh : cs.shards) {
+      for (double& v : sh.weights.flat()) v = static_cast<double>(static_cast<float>(v));
+      for (size_t i = 0; i < sh.momentum.flat().size(); ++i)
+        sh.momentum.flat()[i] = static_cast<double>(1e-3f * static_cast<float>(i % 97));
+    }
+    const std::string path = "/tmp/pfc_adapter_ckpt.bin";
+    detail::save_checkpoint(path, cs, 0x1234);
+    // section offset: magic, version, digest, next_step, loss_sum, metrics_lines, 4 matrices
+    int64_t off = 8 + 4 + 8 + 8 + 8 + 8;
+    for (const Matrix* m : {&cs.backbone.w1, &cs.backbone.b1, &cs.backbone.w2, &cs.backbone.b2})
+      off += 16 + 8 * m->rows() * m->cols();
+    StepConfig cfg;
+    gpu::Session session(layout, 64, cfg, 16);
+    int64_t end = 0;
+    gpu::check(pfc_gpu_read_shards(session.handle(), path.c_str(), off, &end), session.handle());
+    std::vector<CenterShard> got = cs.shards;
+    session.download(got);
+    auto eq = [](const Matrix& a, const Matrix& b) {
+      return a.flat().size() == b.flat().size() &&
+             std::equal(a.flat().begin(), a.flat().end(), b.flat().begin());
+    };
+    bool same = true;
+    for (size_t k = 0; k < got.size(); ++k)
+      same = same && eq(got[k].weights, cs.shards[k].weights) &&
+             eq(got[k].momentum, cs.shards[k].momentum);
+    // and back: the device's section read by the reference reader
+    const std::string p2 = "/tmp/pfc_adapter_ckpt2.bin";
+    gpu::check(pfc_gpu_write_shards(session.handle(), p2.c_str(), 0), session.handle());
+    BinaryReader r(p2);
+    bool back = r.get<int64_t>() == 4;
+    for (int64_t k = 0; k < 4 && back; ++k) {
+      back = r.get<int64_t>() == k && r.get<int64_t>() == layout.owned_begin(k) &&
+             r.get<int64_t>() == layout.owned_end(k);
+      const Matrix w = r.get_matrix(), m = r.get_matrix();
+      back = back && eq(w, cs.shards[k].weights) && eq(m, cs.shards[k].momentum);
+    }
+    const bool pass = same && back && end > off;
+    ok = ok && pass;
+    std::printf("{\"case\": \"checkpoint_reference_format\", \"device_reads_reference\": %s, "
+                "\"reference_reads_device\": %s, \"pass\": %s}\n",
+                same ? "true" : "false", back ? "true" : "false", pass ? "true" : "false");
   }
   // the unchanged-signature free function on host shards + the reference's error text
   {

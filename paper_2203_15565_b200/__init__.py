@@ -60,6 +60,10 @@ class NumericalError(Error):
     pass
 
 
+class DataError(Error):
+    """error.hpp DataError (checkpoint streams, io.hpp)"""
+
+
 class CudaError(Error):
     pass
 
@@ -69,7 +73,7 @@ class NcclError(Error):
 
 
 _ERRORS = {1: ShapeError, 2: ContractError, 3: CapacityError, 4: ConfigError, 5: NumericalError,
-           6: CudaError, 7: NcclError}
+           6: CudaError, 7: NcclError, 8: DataError}
 
 
 # ----------------------------------------------------------------------------- rng.hpp mirror
@@ -307,6 +311,8 @@ def load_library(path: str | None = None) -> C.CDLL:
         "pfc_gpu_set_phase_timing": (C.c_int, [vp, C.c_int]),
         "pfc_gpu_launches_per_step": (i64, [vp]),
         "pfc_gpu_diagnostics": (C.c_int, [vp, vp, vp, i64, vp, vp, C.POINTER(DiagOut)]),
+        "pfc_gpu_write_shards": (C.c_int, [vp, C.c_char_p, C.c_int]),
+        "pfc_gpu_read_shards": (C.c_int, [vp, C.c_char_p, i64, C.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -467,6 +473,16 @@ class CenterShards:
         return DiagnosticsSnapshot(0, out.apcs, out.amncs,
                                    out.amncs_conflicted if out.has_conflicted else None,
                                    out.amncs_hard if out.has_split else None)
+
+    def write_shards(self, path: str, append: bool = False) -> None:
+        """This rank's shard section in the reference checkpoint encoding (trainer.hpp:235-338)."""
+        _check(_lib.pfc_gpu_write_shards(self._h, os.fsencode(path), 1 if append else 0), self._h)
+
+    def read_shards(self, path: str, offset: int = 0) -> int:
+        """Load a shard section at `offset`; returns the offset after it."""
+        end = C.c_int64(0)
+        _check(_lib.pfc_gpu_read_shards(self._h, os.fsencode(path), offset, C.byref(end)), self._h)
+        return end.value
 
     def step_device(self, x_local_ptr: int, labels_local_ptr: int, b_local: int, dx_local_ptr: int,
                     cfg: StepConfig, iteration_rng: SeededRng, sync: bool = True):

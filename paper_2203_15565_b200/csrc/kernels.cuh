@@ -527,6 +527,37 @@ __global__ void shard_out_kernel(const float* __restrict__ W, int D, int n, int6
   }
 }
 
+// Dim-row block [d0, d0 + dn) x n classes of the reference's D x owned layout <-> rows
+// [row0, row0 + n) of the fp32 row-major state (checkpoint streams, io.hpp put_matrix order).
+__global__ void dims_out_kernel(const float* __restrict__ W, int D, int n, int64_t row0, int d0,
+                                int dn, double* __restrict__ blk) {
+  __shared__ float tile[32][33];
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int j = j0 + i, dd = i0 + threadIdx.x;
+    tile[i][threadIdx.x] = (j < n && dd < dn) ? W[(size_t)(row0 + j) * D + d0 + dd] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int dd = i0 + i, j = j0 + threadIdx.x;
+    if (dd < dn && j < n) blk[(size_t)dd * n + j] = (double)tile[threadIdx.x][i];
+  }
+}
+__global__ void dims_in_kernel(const double* __restrict__ blk, int D, int n, int64_t row0, int d0,
+                               int dn, float* __restrict__ W) {
+  __shared__ float tile[32][33];
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int dd = i0 + i, j = j0 + threadIdx.x;
+    tile[i][threadIdx.x] = (dd < dn && j < n) ? (float)blk[(size_t)dd * n + j] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int j = j0 + i, dd = i0 + threadIdx.x;
+    if (j < n && dd < dn) W[(size_t)(row0 + j) * D + d0 + dd] = tile[threadIdx.x][i];
+  }
+}
+
 __global__ void buffers_out_kernel(const int32_t* __restrict__ buf, int n, int64_t* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = buf[i];

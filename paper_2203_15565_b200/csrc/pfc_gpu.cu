@@ -1102,6 +1102,115 @@ static int shard_io(Ctx* c, int64_t k, double* wbuf, double* mbuf, bool in) {
   return PFC_OK;
 }
 
+// ---- checkpoint streams (trainer.hpp:235-338 shard section, io.hpp:18-91 encoding) ---------
+// One matrix (int64 rows = D, int64 cols = n, then D x n fp64 row-major) moved in dim-row chunks:
+// chunk [d0, d0 + dn) is a contiguous span of the file.
+static int ckpt_matrix(Ctx* c, FILE* f, float* dev, int64_t row0, int64_t n, bool write,
+                       double* dstage, double* hstage, int64_t stage_elems) {
+  const int64_t D = c->D;
+  if (write) {
+    const int64_t hdr[2] = {D, n};
+    if (fwrite(hdr, sizeof(int64_t), 2, f) != 2) return fail(c, PFC_ERR_IO, "write failed");
+  } else {
+    int64_t hdr[2];
+    if (fread(hdr, sizeof(int64_t), 2, f) != 2) return fail(c, PFC_ERR_IO, "truncated checkpoint");
+    // the reference caps rows * cols at 2^32 (io.hpp:78); the device reader does not
+    if (hdr[0] != D || hdr[1] != n)
+      return fail(c, PFC_ERR_IO, "checkpoint matrix %lldx%lld does not match the shard (%lldx%lld)",
+                  (long long)hdr[0], (long long)hdr[1], (long long)D, (long long)n);
+  }
+  if (n == 0) return PFC_OK;
+  const int64_t dn = std::max<int64_t>(1, std::min<int64_t>(D, stage_elems / n));
+  for (int64_t d0 = 0; d0 < D; d0 += dn) {
+    const int64_t m = std::min(dn, D - d0);
+    dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(m, 32)), blk(32, 8);
+    if (write) {
+      dims_out_kernel<<<grid, blk, 0, c->stream>>>(dev, (int)D, (int)n, row0, (int)d0, (int)m, dstage);
+      CUDA_TRY(c, cudaMemcpyAsync(hstage, dstage, sizeof(double) * m * n, cudaMemcpyDeviceToHost,
+                                  c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      if (fwrite(hstage, sizeof(double), (size_t)(m * n), f) != (size_t)(m * n))
+        return fail(c, PFC_ERR_IO, "write failed");
+    } else {
+      if (fread(hstage, sizeof(double), (size_t)(m * n), f) != (size_t)(m * n))
+        return fail(c, PFC_ERR_IO, "truncated checkpoint");
+      CUDA_TRY(c, cudaMemcpyAsync(dstage, hstage, sizeof(double) * m * n, cudaMemcpyHostToDevice,
+                                  c->stream));
+      dims_in_kernel<<<grid, blk, 0, c->stream>>>(dstage, (int)D, (int)n, row0, (int)d0, (int)m, dev);
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+  }
+  return PFC_OK;
+}
+
+static int ckpt_shards(Ctx* c, const char* path, int64_t offset, int mode, int64_t* end_offset) {
+  // mode 0: write (truncate), 1: write (append), 2: read at offset
+  const bool write = mode != 2;
+  FILE* f = fopen(path, mode == 0 ? "wb" : (mode == 1 ? "ab" : "rb"));
+  if (!f) return fail(c, PFC_ERR_IO, write ? "cannot open for writing: %s" : "cannot open: %s", path);
+  const int64_t stage_elems = (int64_t)(32ll << 20) / 8;  // 32 MB staging
+  double *dstage = nullptr, *hstage = nullptr;
+  int rc = PFC_OK;
+  auto done = [&](int r) {
+    if (dstage) cudaFree(dstage);
+    if (hstage) cudaFreeHost(hstage);
+    fclose(f);
+    return r;
+  };
+  if (cudaMalloc(&dstage, sizeof(double) * stage_elems) != cudaSuccess ||
+      cudaMallocHost(&hstage, sizeof(double) * stage_elems) != cudaSuccess)
+    return done(fail(c, PFC_ERR_CUDA, "checkpoint staging allocation failed"));
+  if (write) {
+    const int64_t count = c->nk;
+    if (fwrite(&count, sizeof(int64_t), 1, f) != 1) return done(fail(c, PFC_ERR_IO, "write failed"));
+    for (int64_t kk = 0; kk < c->nk; ++kk) {
+      const int64_t k = c->k0 + kk;
+      const int64_t lo = std::min(k * c->blk, c->C), hi = std::min((k + 1) * c->blk, c->C);
+      const int64_t hdr[3] = {k, lo, hi};
+      if (fwrite(hdr, sizeof(int64_t), 3, f) != 3) return done(fail(c, PFC_ERR_IO, "write failed"));
+      for (float* dev : {c->W, c->M})
+        if ((rc = ckpt_matrix(c, f, dev, lo - c->cls_lo, hi - lo, true, dstage, hstage, stage_elems)))
+          return done(rc);
+    }
+  } else {
+    if (fseeko(f, (off_t)offset, SEEK_SET) != 0) return done(fail(c, PFC_ERR_IO, "truncated checkpoint"));
+    int64_t count = 0;
+    if (fread(&count, sizeof(int64_t), 1, f) != 1) return done(fail(c, PFC_ERR_IO, "truncated checkpoint"));
+    for (int64_t i = 0; i < count; ++i) {
+      int64_t hdr[3];
+      if (fread(hdr, sizeof(int64_t), 3, f) != 3) return done(fail(c, PFC_ERR_IO, "truncated checkpoint"));
+      const int64_t k = hdr[0], lo = hdr[1], hi = hdr[2];
+      if (k < 0 || k >= c->K || lo != std::min(k * c->blk, c->C) || hi != std::min((k + 1) * c->blk, c->C))
+        return done(fail(c, PFC_ERR_CONTRACT,
+                         "checkpoint shard %lld [%lld, %lld) does not match the contiguous equal "
+                         "partition", (long long)k, (long long)lo, (long long)hi));
+      const bool local = k >= c->k0 && k < c->k0 + c->nk;
+      for (float* dev : {c->W, c->M}) {
+        if (local) {
+          if ((rc = ckpt_matrix(c, f, dev, lo - c->cls_lo, hi - lo, false, dstage, hstage, stage_elems)))
+            return done(rc);
+        } else {  // another rank's shard: skip its matrix
+          int64_t mh[2];
+          if (fread(mh, sizeof(int64_t), 2, f) != 2 ||
+              fseeko(f, (off_t)(mh[0] * mh[1] * (int64_t)sizeof(double)), SEEK_CUR) != 0)
+            return done(fail(c, PFC_ERR_IO, "truncated checkpoint"));
+        }
+      }
+    }
+  }
+  if (end_offset) *end_offset = (int64_t)ftello(f);
+  if (write && fflush(f) != 0) return done(fail(c, PFC_ERR_IO, "write failed"));
+  return done(PFC_OK);
+}
+
+int pfc_gpu_write_shards(void* ctx, const char* path, int append) {
+  return ckpt_shards(static_cast<Ctx*>(ctx), path, 0, append ? 1 : 0, nullptr);
+}
+
+int pfc_gpu_read_shards(void* ctx, const char* path, int64_t offset, int64_t* end_offset) {
+  return ckpt_shards(static_cast<Ctx*>(ctx), path, offset, 2, end_offset);
+}
+
 int pfc_gpu_set_shard(void* ctx, int64_t k, const double* w, const double* m) {
   return shard_io(static_cast<Ctx*>(ctx), k, const_cast<double*>(w), const_cast<double*>(m), true);
 }

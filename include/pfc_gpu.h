@@ -162,6 +162,11 @@ int pfc_gpu_diagnostics(void* ctx, const double* features_d_by_b, const int64_t*
                         int64_t batch, const int64_t* class_identity,
                         const int64_t* sample_identity, pfc_gpu_diag_out* out);
 
+/* mics (metrics.hpp:150-164): per class, the maximum cosine to any other class centre, for the
+ * current shards; out[C] (class order).  Exact (fp64 re-evaluation of the bf16 screening GEMM's
+ * near-maximal pairs).  O(C^2 D): a final-state diagnostic.  Single-rank contexts only. */
+int pfc_gpu_mics(void* ctx, double* out);
+
 /* ---- checkpoints (trainer.hpp:235-338 shard section; io.hpp:18-91 encoding) --------------- */
 /* Write this rank's shard section in the reference's checkpoint encoding: int64 count, then per
  * local shard int64 shard_id, class_begin, class_end and weights, momentum as put_matrix

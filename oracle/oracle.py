@@ -95,6 +95,7 @@ class Oracle:
         self._f("init_centers", None, [i64, i64, i64, u64, vp])
         self._f("diagnostics", C.c_int, [i64, i64, i64, vp, vp, vp, i64, vp, vp, vp, vp,
                                          C.c_char_p, C.c_int])
+        self._f("mics", C.c_int, [i64, i64, i64, vp, vp, C.c_char_p, C.c_int])
         self._f("step", C.c_int, [C.POINTER(StepCfgC), i64, i64, i64, vp, vp, vp, vp, i64, u64,
                                   u64, C.POINTER(dbl), vp, vp, vp, vp, vp, C.c_char_p, C.c_int])
         if kind == "reference":
@@ -206,6 +207,15 @@ class Oracle:
             res["amncs_hard"] = float(out[3])
             res["amncs_conflicted"] = float(out[2]) if flags[0] else None
         return res
+
+    def mics(self, C_: int, K: int, D: int, W: np.ndarray) -> np.ndarray:
+        """metrics.hpp:150-164: per class, the max cosine to any other class centre."""
+        out = np.zeros(C_, dtype=np.float64)
+        err = C.create_string_buffer(512)
+        st = self._mics(C_, K, D, _ptr(np.ascontiguousarray(W, dtype=np.float64)), _ptr(out), err, 512)
+        if st:
+            raise OracleError(st, err.value.decode())
+        return out
 
     def bench_inputs(self, C_: int, D: int, B: int, seed: int, step: int):
         X = np.zeros((D, B), dtype=np.float64)

@@ -223,6 +223,31 @@ int pfcr_diagnostics(int64_t C, int64_t K, int64_t D, const double* W, const dou
     }
 }
 
+// mics (metrics.hpp:150-164) on caller-provided shards
+int pfcr_mics(int64_t C, int64_t K, int64_t D, const double* W, double* out, char* err, int errlen) {
+    try {
+        const pfc::ShardLayout layout(C, K);
+        std::vector<pfc::CenterShard> shards;
+        for (int64_t k = 0; k < K; ++k) {
+            pfc::CenterShard s;
+            s.shard_id = k;
+            s.class_begin = layout.owned_begin(k);
+            s.class_end = layout.owned_end(k);
+            s.weights = pfc::Matrix(D, s.owned());
+            s.momentum = pfc::Matrix(D, s.owned());
+            shards.push_back(std::move(s));
+        }
+        std::vector<double> M(static_cast<size_t>(C * D), 0.0);
+        load_shards(shards, W, M.data());
+        const std::vector<double> r = pfc::mics(shards);
+        std::memcpy(out, r.data(), r.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return status_of(e);
+    }
+}
+
 // Persistent session: shards live inside the reference's own types, so timing a
 // step measures only pfc::distributed_partial_step (bench.py --impl reference).
 void* pfcr_session_create(int64_t C, int64_t K, int64_t D, uint64_t seed) {

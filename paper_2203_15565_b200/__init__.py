@@ -312,6 +312,7 @@ def load_library(path: str | None = None) -> C.CDLL:
         "pfc_gpu_launches_per_step": (i64, [vp]),
         "pfc_gpu_diagnostics": (C.c_int, [vp, vp, vp, i64, vp, vp, C.POINTER(DiagOut)]),
         "pfc_gpu_write_shards": (C.c_int, [vp, C.c_char_p, C.c_int]),
+        "pfc_gpu_mics": (C.c_int, [vp, vp]),
         "pfc_gpu_read_shards": (C.c_int, [vp, C.c_char_p, i64, C.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
@@ -473,6 +474,12 @@ class CenterShards:
         return DiagnosticsSnapshot(0, out.apcs, out.amncs,
                                    out.amncs_conflicted if out.has_conflicted else None,
                                    out.amncs_hard if out.has_split else None)
+
+    def mics(self) -> np.ndarray:
+        """metrics.hpp:150-164 for the current shards: per class, the max cosine to any other."""
+        out = np.zeros(self.layout.num_classes, dtype=np.float64)
+        _check(_lib.pfc_gpu_mics(self._h, _ptr(out)), self._h)
+        return out
 
     def write_shards(self, path: str, append: bool = False) -> None:
         """This rank's shard section in the reference checkpoint encoding (trainer.hpp:235-338)."""

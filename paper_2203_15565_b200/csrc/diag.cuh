@@ -115,7 +115,8 @@ struct DiagMaxEpi : NoSetup {
   static constexpr float kBand = 1.0f / 64.0f;  // > 2 x (2^-8 + fp32 accumulation)
   int B;
   int64_t rows, cls_lo;
-  const int64_t* labels;   // [B] global
+  const int64_t* labels;   // [B] global; nullptr: mics mode, row r excludes column row_base + r
+  int64_t row_base;        // mics mode: local class of the first row of this launch
   const int64_t* cid;      // [rows] class identity of the local classes, or nullptr (no split)
   const int64_t* sid;      // [B] sample identity, or nullptr
   uint32_t* rmax;          // [B][3] running bf16 maximum per bucket (enc_f32)
@@ -135,7 +136,7 @@ struct DiagMaxEpi : NoSetup {
     constexpr int CW = BN / NWG;
     const int b = t.row0 + row;
     const bool rv = b < B;
-    const int64_t lab = rv ? labels[b] - cls_lo : -1;
+    const int64_t lab = !rv ? -1 : (labels ? labels[b] - cls_lo : row_base + b);
     const int64_t sb = (rv && sid) ? sid[b] : 0;
     float rm[3];
 #pragma unroll

@@ -821,6 +821,76 @@ __global__ void diag_fill_kernel(uint32_t* rmax, unsigned long long* emax, int* 
   if (i < n) hasc[i] = 0;
 }
 
+int diag_alloc(Ctx* c) {
+  if (c->dwall) return PFC_OK;  // w^ of every local class + per-row scratch, kept across calls
+  c->diag_rows_pad = round_up(std::max<int64_t>(c->rows, 1), 256);
+  const size_t ob = c->bf16 ? 2 : 4;
+  CUDA_TRY(c, dalloc(c, reinterpret_cast<uint8_t**>(&c->dwall), (size_t)c->diag_rows_pad * c->Dp * ob));
+  CUDA_TRY(c, dalloc(c, &c->dwinv, (size_t)c->diag_rows_pad));
+  CUDA_TRY(c, dalloc(c, &c->dxinv, (size_t)c->maxB));
+  CUDA_TRY(c, dalloc(c, &c->dapcs, (size_t)c->maxB));
+  CUDA_TRY(c, dalloc(c, &c->drmax, (size_t)c->maxB * 3));
+  CUDA_TRY(c, dalloc(c, &c->demax, (size_t)c->maxB * 3));
+  CUDA_TRY(c, dalloc(c, &c->dhasc, (size_t)c->maxB));
+  CUDA_TRY(c, dalloc(c, &c->dcid, (size_t)std::max<int64_t>(c->rows, 1)));
+  CUDA_TRY(c, dalloc(c, &c->dsid, (size_t)c->maxB));
+  c->dcand_cap = (int64_t)1 << 22;  // 4M candidates (64 MB)
+  CUDA_TRY(c, dalloc(c, &c->dcand, (size_t)c->dcand_cap));
+  CUDA_TRY(c, dalloc(c, &c->dncand, (size_t)1));
+  if (c->bf16 && !make_map(&c->tm_wall, c->dwall, c->Dp, c->rows, c->Dp, kBN))
+    return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return PFC_OK;
+}
+
+// mics over rows [r0, r0 + nr) of the local classes against all of them (one screening launch
+// + exact pass); per-row maxima in emax[3 * r] (bucket 0)
+template <typename OT, bool kUmma>
+int run_mics_block(Ctx* c, int64_t r0, int64_t nr, uint32_t* rmax, unsigned long long* emax,
+                   int* hasc) {
+  cudaStream_t s = c->stream;
+  OT* wall = static_cast<OT*>(c->dwall);
+  DiagMaxEpi e{};
+  e.B = (int)nr;
+  e.rows = c->rows;
+  e.cls_lo = c->cls_lo;
+  e.labels = nullptr;
+  e.row_base = r0;
+  e.cid = nullptr;
+  e.sid = nullptr;
+  e.rmax = rmax;
+  e.hasc = hasc;
+  e.cand = c->dcand;
+  e.ncand = c->dncand;
+  e.cap = (unsigned long long)c->dcand_cap;
+  for (int pass = 0; pass < 2; ++pass) {
+    CUDA_TRY(c, cudaMemsetAsync(c->dncand, 0, sizeof(unsigned long long), s));
+    cudaError_t err;
+    if constexpr (kUmma) {
+      CUtensorMap ta;
+      if (!make_map(&ta, wall + (size_t)r0 * c->Dp, c->Dp, nr, c->Dp, 128))
+        return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kBN, 1, 0);
+      err = launch_umma<kBN, 4, 2, false, false>(c, ta, c->tm_wall, g, e);
+    } else {
+      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kSimtBN, 1, 0);
+      err = launch_simt<false, false>(c, (const float*)(wall + (size_t)r0 * c->Dp), (int)c->Dp,
+                                      (const float*)wall, (int)c->Dp, g, e);
+    }
+    CUDA_TRY(c, err);
+    unsigned long long n = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&n, c->dncand, sizeof(n), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (n <= (unsigned long long)c->dcand_cap) break;
+    if (pass == 1) return fail(c, PFC_ERR_CUDA, "pfc_gpu_mics: candidate list overflow");
+  }
+  // rows of this block are the "samples": X = the W rows, xinv = their 1/|w|
+  diag_exact_kernel<<<(unsigned)(c->num_sms * 8), 256, 0, s>>>(
+      c->dcand, c->dncand, (unsigned long long)c->dcand_cap, rmax, c->W + (size_t)r0 * c->D,
+      c->dwinv + r0, c->W, c->dwinv, (int)c->D, emax);
+  CUDA_TRY(c, cudaGetLastError());
+  return PFC_OK;
+}
+
 template <typename OT, bool kUmma>
 int run_diagnostics(Ctx* c, int64_t B, bool split) {
   cudaStream_t s = c->stream;
@@ -1203,6 +1273,52 @@ static int ckpt_shards(Ctx* c, const char* path, int64_t offset, int mode, int64
   return done(PFC_OK);
 }
 
+int pfc_gpu_mics(void* ctx, double* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (c->C < 2) return fail(c, PFC_ERR_CONTRACT, "mics: needs at least two classes");
+  if (c->R > 1) return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_mics: single-rank contexts only");
+  if (int rc = diag_alloc(c)) return rc;
+  cudaStream_t s = c->stream;
+  const int bs = 256;
+  // w^ of every class (bf16 operand rows + fp64 1/|w|)
+  if (c->bf16)
+    diag_norm_w_kernel<__nv_bfloat16><<<(unsigned)ceil_div(c->diag_rows_pad * 32, bs), bs, 0, s>>>(
+        c->W, c->rows, c->diag_rows_pad, (int)c->D, (int)c->Dp, static_cast<__nv_bfloat16*>(c->dwall),
+        c->dwinv);
+  else
+    diag_norm_w_kernel<float><<<(unsigned)ceil_div(c->diag_rows_pad * 32, bs), bs, 0, s>>>(
+        c->W, c->rows, c->diag_rows_pad, (int)c->D, (int)c->Dp, static_cast<float*>(c->dwall), c->dwinv);
+  CUDA_TRY(c, cudaGetLastError());
+  const int64_t blk = std::min<int64_t>(c->rows, 1 << 17);  // rows per screening launch
+  uint32_t* rmax = nullptr;
+  unsigned long long* emax = nullptr;
+  int* hasc = nullptr;
+  CUDA_TRY(c, cudaMalloc(&rmax, sizeof(uint32_t) * blk * 3));
+  CUDA_TRY(c, cudaMalloc(&emax, sizeof(unsigned long long) * blk * 3));
+  CUDA_TRY(c, cudaMalloc(&hasc, sizeof(int) * blk));
+  std::vector<unsigned long long> em((size_t)blk * 3);
+  int rc = PFC_OK;
+  for (int64_t r0 = 0; r0 < c->rows && rc == PFC_OK; r0 += blk) {
+    const int64_t nr = std::min(blk, c->rows - r0);
+    diag_fill_kernel<<<(unsigned)ceil_div(nr * 3, bs), bs, 0, s>>>(rmax, emax, hasc, (int)(nr * 3), (int)nr);
+    rc = c->bf16 ? run_mics_block<__nv_bfloat16, true>(c, r0, nr, rmax, emax, hasc)
+                 : run_mics_block<float, false>(c, r0, nr, rmax, emax, hasc);
+    if (rc) break;
+    // on the context stream: the legacy default stream does not wait for a non-blocking stream
+    if (cudaMemcpyAsync(em.data(), emax, sizeof(unsigned long long) * nr * 3, cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      rc = fail(c, PFC_ERR_CUDA, "pfc_gpu_mics: copy failed");
+      break;
+    }
+    for (int64_t r = 0; r < nr; ++r) out[c->cls_lo + r0 + r] = dec_f64(em[(size_t)r * 3]);
+  }
+  cudaFree(rmax);
+  cudaFree(emax);
+  cudaFree(hasc);
+  return rc;
+}
+
 int pfc_gpu_write_shards(void* ctx, const char* path, int append) {
   return ckpt_shards(static_cast<Ctx*>(ctx), path, 0, append ? 1 : 0, nullptr);
 }
@@ -1356,24 +1472,7 @@ int pfc_gpu_diagnostics(void* ctx, const double* xdb, const int64_t* labels, int
   if (c->C < 2) return fail(c, PFC_ERR_CONTRACT, "amncs: needs at least two classes");
   const bool split = class_identity != nullptr;
   cudaStream_t s = c->stream;
-  if (!c->dwall) {  // w^ of every local class, kept across calls
-    c->diag_rows_pad = round_up(std::max<int64_t>(c->rows, 1), 256);
-    const size_t ob = c->bf16 ? 2 : 4;
-    CUDA_TRY(c, dalloc(c, reinterpret_cast<uint8_t**>(&c->dwall), (size_t)c->diag_rows_pad * c->Dp * ob));
-    CUDA_TRY(c, dalloc(c, &c->dwinv, (size_t)c->diag_rows_pad));
-    CUDA_TRY(c, dalloc(c, &c->dxinv, (size_t)c->maxB));
-    CUDA_TRY(c, dalloc(c, &c->dapcs, (size_t)c->maxB));
-    CUDA_TRY(c, dalloc(c, &c->drmax, (size_t)c->maxB * 3));
-    CUDA_TRY(c, dalloc(c, &c->demax, (size_t)c->maxB * 3));
-    CUDA_TRY(c, dalloc(c, &c->dhasc, (size_t)c->maxB));
-    CUDA_TRY(c, dalloc(c, &c->dcid, (size_t)std::max<int64_t>(c->rows, 1)));
-    CUDA_TRY(c, dalloc(c, &c->dsid, (size_t)c->maxB));
-    c->dcand_cap = (int64_t)1 << 22;  // 4M candidates (64 MB)
-    CUDA_TRY(c, dalloc(c, &c->dcand, (size_t)c->dcand_cap));
-    CUDA_TRY(c, dalloc(c, &c->dncand, (size_t)1));
-    if (c->bf16 && !make_map(&c->tm_wall, c->dwall, c->Dp, c->rows, c->Dp, kBN))
-      return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  }
+  if (int rc = diag_alloc(c)) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
   if (split) {

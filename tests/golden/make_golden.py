@@ -188,10 +188,24 @@ def diag_golden():
     return out
 
 
+MICS_CASES = [("tiny", 40, 4, 8), ("k3", 700, 3, 32), ("d512", 1500, 2, 512)]
+
+
+def mics_golden():
+    out = []
+    for name, C_, K, D in MICS_CASES:
+        W = R.init_centers(C_, K, D, 5)
+        m = R.mics(C_, K, D, W)
+        out.append({"name": name, "C": C_, "K": K, "D": D, "seed": 5, "mics": m.tolist()})
+    return out
+
+
 if __name__ == "__main__":
     if "--diag-only" in sys.argv:
         with open(os.path.join(OUT, "diag.json"), "w") as f:
             json.dump(diag_golden(), f, indent=1)
+        with open(os.path.join(OUT, "mics.json"), "w") as f:
+            json.dump(mics_golden(), f)
         sys.exit(0)
     big = "--big" in sys.argv
     with open(os.path.join(OUT, "rng.json"), "w") as f:
@@ -204,4 +218,6 @@ if __name__ == "__main__":
         json.dump(steps, f, indent=1)
     with open(os.path.join(OUT, "diag.json"), "w") as f:
         json.dump(diag_golden(), f, indent=1)
+    with open(os.path.join(OUT, "mics.json"), "w") as f:
+        json.dump(mics_golden(), f)
     print("done")

@@ -114,3 +114,30 @@ def test_step_with_diagnostics_reports_pre_update_state(port):
     with pytest.raises(p.NumericalError, match="l2_normalize_columns: non-finite entry in 512x64 result"):
         sh.diagnostics(Xn, labels)
     sh.close()
+
+
+@pytest.mark.parametrize("precision", PREC, ids=["bf16", "fp32"])
+def test_mics_matches_reference_and_oracle(precision, port):
+    """mics (metrics.hpp:150-164): within 1e-6 of the reference golden values at init, and
+    within 1e-9 of the oracle on the device's own state (exact, not bf16)."""
+    with open(os.path.join(GOLDEN, "mics.json")) as f:
+        cases = json.load(f)
+    for cs in cases:
+        C_, K, D = cs["C"], cs["K"], cs["D"]
+        sh = p.CenterShards(p.ShardLayout(C_, K), D, p.StepConfig(), max_batch=8, precision=precision)
+        sh.init_center_shards(cs["seed"])
+        got = sh.mics()
+        assert np.max(np.abs(got - np.array(cs["mics"]))) <= 1e-6, cs["name"]
+        want = port.mics(C_, K, D, device_state(sh, C_, K, D))
+        assert np.max(np.abs(got - want)) <= 1e-9, cs["name"]
+        sh.close()
+    # a larger case with trained (moved) centres
+    C_, K, D, B = 20000, 2, 128, 64
+    cfg = p.StepConfig(r=0.2, margin=p.MarginConfig.arcface_style())
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, precision=precision)
+    sh.init_center_shards(3)
+    X, labels = port.bench_inputs(C_, D, B, 1, 0)
+    p.distributed_partial_step(sh, X, labels, cfg, p.SeededRng(1, 1))
+    want = port.mics(C_, K, D, device_state(sh, C_, K, D))
+    assert np.max(np.abs(sh.mics() - want)) <= 1e-9
+    sh.close()

@@ -213,3 +213,14 @@ def test_diagnostics_errors(port):
         port.diagnostics(30, 2, 8, W, X, np.array([0, 1, 30]))
     with pytest.raises(OracleError, match="amncs: needs at least two classes"):
         port.diagnostics(1, 1, 8, port.init_centers(1, 1, 8, 1), X, np.array([0, 0, 0]))
+
+
+def test_mics_matches_reference_golden(port, golden_dir):
+    """metrics.hpp:150-164: the C restatement is bit-identical to the compiled reference."""
+    with open(os.path.join(golden_dir, "mics.json")) as f:
+        cases = json.load(f)
+    for cs in cases:
+        W = port.init_centers(cs["C"], cs["K"], cs["D"], cs["seed"])
+        assert port.mics(cs["C"], cs["K"], cs["D"], W).tolist() == cs["mics"], cs["name"]
+    with pytest.raises(OracleError, match="mics: needs at least two classes"):
+        port.mics(1, 1, 4, port.init_centers(1, 1, 4, 1))

@@ -869,10 +869,12 @@ int run_mics_block(Ctx* c, int64_t r0, int64_t nr, uint32_t* rmax, unsigned long
       CUtensorMap ta;
       if (!make_map(&ta, wall + (size_t)r0 * c->Dp, c->Dp, nr, c->Dp, 128))
         return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kBN, 1, 0);
+      // n fastest: all CTAs sweep the columns of the same 128 rows together, so the running
+      // maxima converge within the first wave and later tiles yield few candidates
+      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kBN, 1, 1);
       err = launch_umma<kBN, 4, 2, false, false>(c, ta, c->tm_wall, g, e);
     } else {
-      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kSimtBN, 1, 0);
+      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kSimtBN, 1, 1);
       err = launch_simt<false, false>(c, (const float*)(wall + (size_t)r0 * c->Dp), (int)c->Dp,
                                       (const float*)wall, (int)c->Dp, g, e);
     }

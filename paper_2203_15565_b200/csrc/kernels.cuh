@@ -150,10 +150,19 @@ __global__ void gather_w_kernel(const float* __restrict__ W, int D, int Dp,
     for (int i = 0; i < 8; ++i)
       if (i < nv) {
         const int d = (i * 32 + lane) * 4;
-        store_out(o + d, v[i].x * inv);
-        store_out(o + d + 1, v[i].y * inv);
-        store_out(o + d + 2, v[i].z * inv);
-        store_out(o + d + 3, v[i].w * inv);
+        if constexpr (std::is_same<OT, __nv_bfloat16>::value) {  // one 8-byte store per lane
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x * inv, v[i].y * inv);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(v[i].z * inv, v[i].w * inv);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&lo);
+          u.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(o + d) = u;
+        } else {
+          store_out(o + d, v[i].x * inv);
+          store_out(o + d + 1, v[i].y * inv);
+          store_out(o + d + 2, v[i].z * inv);
+          store_out(o + d + 3, v[i].w * inv);
+        }
       }
     for (int d = D + lane; d < Dp; d += 32) store_out(o + d, 0.f);
     if (lane == 0) {

@@ -228,38 +228,46 @@ __global__ void __launch_bounds__(256) finalize_stats_kernel(
     const float* __restrict__ epos, const int32_t* __restrict__ pos_col,
     const int* __restrict__ hasval, int has_filter, MarginDev mg, ST* __restrict__ rowscale,
     ST* __restrict__ delta, double* __restrict__ loss_row, StepStatus* st) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  [&] {
-    if (b >= B || sampler_failed(st)) return;
-    rowscale[b] = 0;
-    delta[b] = 0;
-    loss_row[b] = 0;
-    if (has_filter && hasval[b] == 0) {  // every buffer column masked (shardsim.hpp:294-297)
-      atomicMin(&st->masked_row, b);
-      return;
-    }
-    double S = 0.0;
+  // one warp per row: lanes sum the segments (fixed lane order + fixed shuffle tree), lane 0
+  // finishes the row
+  const int lane = threadIdx.x & 31;
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool live = b < B && !sampler_failed(st);
+  double S = 0.0;
+  if (live) {
     if (seg) {
       double s = 0.0;
-      for (int i = 0; i < nseg; ++i) s += (double)seg[(size_t)i * B + b];
+      for (int i = lane; i < nseg; i += 32) s += (double)seg[(size_t)i * B + b];
+      s = warp_sum(s);
       S = (double)(ST)s;
     } else {
       for (int r = 0; r < R; ++r) S += (double)ls[(size_t)r * B + b];
     }
-    if (!(S > 1e-30) || !isfinite(S)) {
-      atomicMin(&st->underflow_row, b);
-      return;
-    }
-    const double invB = 1.0 / (double)B;
-    const double rs = mg.sd * invB / S;
-    rowscale[b] = (ST)rs;
-    loss_row[b] = log(S) + mg.offd - zpos[b];
-    if (pos_col[b] >= 0) {
-      const double p = exp(zpos[b] - mg.offd) / S;
-      const double g = (p - 1.0) * invB * margin_deriv_pos(mg, cpos[b]);
-      delta[b] = (ST)(g - (double)(ST)rs * (double)epos[b]);
-    }
-  }();
+  }
+  if (live && lane == 0) {
+    [&] {
+      rowscale[b] = 0;
+      delta[b] = 0;
+      loss_row[b] = 0;
+      if (has_filter && hasval[b] == 0) {  // every buffer column masked (shardsim.hpp:294-297)
+        atomicMin(&st->masked_row, b);
+        return;
+      }
+      if (!(S > 1e-30) || !isfinite(S)) {
+        atomicMin(&st->underflow_row, b);
+        return;
+      }
+      const double invB = 1.0 / (double)B;
+      const double rs = mg.sd * invB / S;
+      rowscale[b] = (ST)rs;
+      loss_row[b] = log(S) + mg.offd - zpos[b];
+      if (pos_col[b] >= 0) {
+        const double p = exp(zpos[b] - mg.offd) / S;
+        const double g = (p - 1.0) * invB * margin_deriv_pos(mg, cpos[b]);
+        delta[b] = (ST)(g - (double)(ST)rs * (double)epos[b]);
+      }
+    }();
+  }
   __threadfence();
   __shared__ bool last;
   __syncthreads();

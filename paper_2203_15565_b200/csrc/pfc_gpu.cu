@@ -489,7 +489,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   }
   ST* rsc = static_cast<ST*>(c->rowscale);
   ST* dlt = static_cast<ST*>(c->delta);
-  finalize_stats_kernel<ST><<<(unsigned)ceil_div(B, 256), 256, 0, s>>>(
+  finalize_stats_kernel<ST><<<(unsigned)ceil_div(B * 32, 256), 256, 0, s>>>(
       ls, c->R, c->R > 1 ? nullptr : seg, nseg, (int)B, c->zpos, c->cpos, c->epos, c->pos_col,
       c->hasval, filt ? 1 : 0, c->mg, rsc, dlt, c->loss_row, c->st);
   c->launches++;

@@ -200,7 +200,7 @@ def mics_golden():
     return out
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--northstar" not in sys.argv:
     if "--diag-only" in sys.argv:
         with open(os.path.join(OUT, "diag.json"), "w") as f:
             json.dump(diag_golden(), f, indent=1)
@@ -221,3 +221,51 @@ if __name__ == "__main__":
     with open(os.path.join(OUT, "mics.json"), "w") as f:
         json.dump(mics_golden(), f)
     print("done")
+
+
+def northstar_golden():
+    """One reference step at the north-star size: 2M classes, K=8, B=1024, d=512, r=0.1,
+    ArcFace(64, 0.5).  Too big to store W: keep the loss, the full dX,
+    the buffers' checksums, |W' - W|_F over the sampled rows, and W' of a few sampled rows.
+    Run with --northstar (needs ~20 GB RAM, a few minutes on 8 cores)."""
+    C, K, B, D, r = 2_000_000, 8, 1024, 512, 0.1
+    cfg = OracleCfg(r=r, margin="arcface", scale=64.0, m=0.5, lr=0.1, momentum=0.9, weight_decay=5e-4)
+    W = R.init_centers(C, K, D, 1)
+    M = np.zeros_like(W)
+    X, labels = P.bench_inputs(C, D, B, 1, 0)
+    stream = R.make_stream("iteration", 0)
+    bufs, npos = R.build_buffers(C, K, labels, r, 1, stream)
+    rows = np.unique(bufs.ravel())
+
+    def gather(Wf):  # rows of the shard-concatenated D x owned layout, without a full copy
+        out = np.empty((len(rows), D))
+        blk = (C + K - 1) // K
+        off = 0
+        for k in range(K):
+            lo, hi = min(k * blk, C), min((k + 1) * blk, C)
+            n = hi - lo
+            sel = rows[(rows >= lo) & (rows < hi)]
+            out_idx = np.searchsorted(rows, sel)
+            out[out_idx] = Wf[off:off + D * n].reshape(D, n)[:, sel - lo].T
+            off += D * n
+        return out
+
+    Wb = gather(W)
+    o = R.step(cfg, C, K, D, W, M, X, labels, 1, stream)
+    assert np.array_equal(o["buffers"], bufs)
+    Wa = gather(W)
+    sel = np.arange(0, len(rows), max(1, len(rows) // 64))
+    entry = {"C": C, "K": K, "B": B, "D": D, "r": r, "margin": "arcface", "m": 0.5,
+             "loss": o["loss"], "dX_fro": float(np.linalg.norm(o["dX"])),
+             "dW_fro": float(np.linalg.norm(Wa - Wb)),
+             "buffers_fnv": [fnv64(o["buffers"][k]) for k in range(K)],
+             "npos": o["npos"].tolist()}
+    np.savez_compressed(os.path.join(OUT, "step_webface2m_k8_d512.npz"), dX=o["dX"],
+                        rows_sub=rows[sel], W_sub=Wa[sel])
+    with open(os.path.join(OUT, "northstar.json"), "w") as f:
+        json.dump(entry, f, indent=1)
+    print("northstar", entry["loss"], entry["dX_fro"], entry["dW_fro"])
+
+
+if __name__ == "__main__" and "--northstar" in sys.argv:
+    northstar_golden()

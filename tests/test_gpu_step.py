@@ -321,3 +321,42 @@ def test_async_device_steps_report_errors_on_sync():
     out = sh.step_device(x.data_ptr(), good.data_ptr(), B, dx.data_ptr(), cfg, p.SeededRng(1, 4))
     assert np.isfinite(out.loss)
     sh.close()
+
+
+@pytest.mark.parametrize("precision", [p.PRECISION_BF16, p.PRECISION_FP32], ids=["bf16", "fp32"])
+def test_northstar_size_matches_reference(precision, port):
+    """The bench configuration itself (2M classes, K=8 on one GPU, B=1024, d=512, r=0.1,
+    ArcFace): one step against the compiled reference's step (tests/golden/northstar.json,
+    make_golden.py --northstar): sampled buffers bit-exact, loss / dX / updated W within the
+    tolerance contract."""
+    g = golden("northstar.json")
+    arr = np.load(os.path.join(GOLDEN, "step_webface2m_k8_d512.npz"))
+    C_, K, D, B = g["C"], g["K"], g["D"], g["B"]
+    cfg = p.StepConfig(r=g["r"], margin=p.MarginConfig.arcface_style(64.0, g["m"]), lr=0.1)
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, precision=precision)
+    sh.init_center_shards(1)
+    X, labels = port.bench_inputs(C_, D, B, 1, 0)
+    res = p.distributed_partial_step(sh, X, labels, cfg, p.SeededRng(1, p.make_stream("iteration", 0)))
+    assert [fnv64(b.class_indices) for b in res.buffers] == g["buffers_fnv"]
+    assert [b.num_positives for b in res.buffers] == g["npos"]
+    tol = TOL[precision]
+    rec = {"case": "webface2m_k8_d512 (north star)", "precision": "bf16" if precision == p.PRECISION_BF16 else "fp32",
+           "loss": res.loss, "loss_ref": g["loss"], "loss_rel": abs(res.loss - g["loss"]) / abs(g["loss"]),
+           "dX_fro": rel_fro(res.d_features, arr["dX"]), "dX_maxmax": rel_max(res.d_features, arr["dX"])}
+    # updated centres on a sample of the sampled rows (W' = W - lr v; the reference is fp64)
+    rows, want = arr["rows_sub"], arr["W_sub"]
+    layout = p.ShardLayout(C_, K)
+    got = np.empty_like(want)
+    for k in range(K):
+        lo, hi = layout.owned_begin(k), layout.owned_end(k)
+        m = (rows >= lo) & (rows < hi)
+        if m.any():
+            w, _ = sh.get_shard(k)
+            got[m] = w[:, rows[m] - lo].T
+    rec["W_maxmax"] = rel_max(got, want)
+    os.makedirs(os.path.dirname(RESULTS), exist_ok=True)
+    with open(RESULTS, "a") as f:
+        f.write(json.dumps(rec) + "\n")
+    assert rec["loss_rel"] <= tol[0] and rec["dX_fro"] <= tol[1] and rec["dX_maxmax"] <= tol[2]
+    assert rec["W_maxmax"] <= tol[3]
+    sh.close()

@@ -93,6 +93,9 @@ STEP_CASES = [  # name, C, K, B, D, r, margin, m, tau, steps
     ("cos_10k_full_d512", 10000, 1, 128, 512, 1.0, "cosface", 0.4, None, 1),
     ("arc_40k_k4_b256", 40000, 4, 256, 512, 0.1, "arcface", 0.5, None, 2),
     ("arc_b300_ragged", 7000, 3, 300, 200, 0.2, "arcface", 0.5, None, 1),
+    # 256 < D < 512: the second CTA of the dW pair owns a partial dim half
+    ("arc_d384_pair", 5000, 2, 96, 384, 0.2, "arcface", 0.5, None, 2),
+    ("cos_d260_pair_ragged", 3000, 3, 72, 260, 0.3, "cosface", 0.4, None, 2),
 ]
 
 TOL = {  # precision -> (loss rel, dX fro, dX max/max, W' max/max)

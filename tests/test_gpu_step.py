@@ -96,6 +96,8 @@ STEP_CASES = [  # name, C, K, B, D, r, margin, m, tau, steps
     # 256 < D < 512: the second CTA of the dW pair owns a partial dim half
     ("arc_d384_pair", 5000, 2, 96, 384, 0.2, "arcface", 0.5, None, 2),
     ("cos_d260_pair_ragged", 3000, 3, 72, 260, 0.3, "cosface", 0.4, None, 2),
+    # largest batch class: B = 8191 (odd, > 1024: shared-memory bitonic sort, ragged E rows)
+    ("arc_b8191", 60000, 4, 8191, 128, 0.25, "arcface", 0.5, None, 1),
 ]
 
 TOL = {  # precision -> (loss rel, dX fro, dX max/max, W' max/max)

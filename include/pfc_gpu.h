@@ -94,6 +94,10 @@ typedef struct {
   int64_t capacity;          /* per-shard buffer size (buffer_capacity) */
   int32_t rejection_shards;  /* shards that needed the exact sequential sampler this step */
   int32_t reserved;
+  /* bytes this rank handed to NCCL collectives in the step (buffer sizes of the all-gathers,
+   * all-reduces and reduce-scatters; 0 with one rank): what the GPU path actually moves, next to
+   * the reference's closed-form trace above (costmodel.hpp:37-69) */
+  uint64_t nccl_bytes;
 } pfc_gpu_step_out;
 
 /* ---- lifecycle ------------------------------------------------------------------------ */

@@ -261,7 +261,8 @@ class StepOut(C.Structure):
     _fields_ = [("loss", C.c_double), ("allgather_bytes", C.c_uint64),
                 ("reduce_scalar_bytes", C.c_uint64), ("reduce_grad_bytes", C.c_uint64),
                 ("reduce_ops", C.c_uint64), ("capacity", C.c_int64),
-                ("rejection_shards", C.c_int32), ("reserved", C.c_int32)]
+                ("rejection_shards", C.c_int32), ("reserved", C.c_int32),
+                ("nccl_bytes", C.c_uint64)]
 
 
 PRECISION_BF16, PRECISION_FP32 = 0, 1

@@ -159,6 +159,7 @@ struct Ctx {
   int32_t* pool_scratch = nullptr;
   // features / centres
   float* X = nullptr;  // global batch rows [B][D] fp32 (world > 1 / host path)
+  uint64_t step_nccl_bytes = 0;  // bytes handed to NCCL by the last step (pfc_gpu_step_out)
   // diagnostics (pfc_gpu_diagnostics), allocated on first use
   void* dwall = nullptr;  // w^ of every local class, operand dtype [rows_pad][Dp]
   double *dwinv = nullptr, *dxinv = nullptr, *dapcs = nullptr;
@@ -585,6 +586,13 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
 int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gpu_step_args* a,
              float* dx_full) {
   c->lastB = B;
+  // NCCL payload of the pipeline: stats exchange (+ the host drop-in's dX all-reduce)
+  c->step_nccl_bytes = 0;
+  if (c->R > 1) {
+    const uint64_t sb = c->bf16 ? 4 : 8, b = (uint64_t)B;
+    c->step_nccl_bytes = (uint64_t)c->R * b * sb + b * 8 + (c->d.has_filter ? b * 4 : 0) +
+                         (c->e2e.on ? b * (uint64_t)c->D * 4 : 0);
+  }
   const bool graph = !(c->d.flags & PFC_FLAG_NO_GRAPH) && !c->pt.enabled;
   auto pipeline = [&]() {
     c->launches = 0;
@@ -731,6 +739,7 @@ int check_status(Ctx* c, int64_t step_index, int64_t B, pfc_gpu_step_out* out) {
   if (out) {
     out->loss = st.loss;
     out->rejection_shards = st.rejection_shards;
+  out->nccl_bytes = c->step_nccl_bytes;
     trace_closed_form(c, B, out);
   }
   return PFC_OK;
@@ -1409,8 +1418,10 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
   x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
   if (int rc = run_step(c, c->X, c->labels, B, a, c->dX)) return rc;
   c->reset_status = true;
-  if (c->R > 1)  // the drop-in returns the FULL summed d_features on every rank
+  if (c->R > 1) {  // the drop-in returns the FULL summed d_features on every rank
     NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, s));
+    c->step_nccl_bytes += (uint64_t)B * c->D * 4;
+  }
   dx_to_dxb_kernel<<<grid, blk, 0, s>>>(c->dX, (int)c->D, (int)B, c->xdb);
   CUDA_TRY(c, cudaGetLastError());
   CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
@@ -1442,6 +1453,8 @@ int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_l
     dxf = c->dX;
   }
   if (int rc = run_step(c, x, lab, B, a, dxf)) return rc;
+  if (c->R > 1)  // feature + label all-gathers, dX reduce-scatter
+    c->step_nccl_bytes += (uint64_t)B * c->D * 4 * 2 + (uint64_t)B * 8;
   c->reset_status = false;  // errors stay on the device until a synchronous check
   if (c->R > 1)  // collective 3 (shardsim.hpp:387-399) as a reduce-scatter to the owners
     NCCL_TRY(c, g_nccl.ReduceScatter(c->dX, dx_local, b_local * c->D, ncclFloat32, ncclSum,

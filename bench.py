@@ -25,7 +25,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "PFC fwd+bwd+update samples/s at 2M classes r=0.1"
+METRIC = "PFC fwd+bwd+update samples/s at 2M classes r=0.1; GEMM tensor-pipe util"  # BASELINE.json; util: gemm_tensor_util
 UNIT = "samples/s"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
@@ -185,8 +185,15 @@ def run_reference(args, ws, rank):
     return 0
 
 
+def workload_name(args):
+    # BASELINE.json configs: CPU-ref 10k, Glint360K, WebFace42M-scale 2M, full-FC 360k, 10M stress
+    tag = {10_000: "cpu_ref_10k", 360_000: "glint360k" if args.r < 1.0 else "fullfc_360k",
+           2_000_000: "webface2m", 10_000_000: "stress_10m"}.get(args.classes, "pfc")
+    return f"{tag}_c{args.classes}_d{args.dim}_b{args.batch}_r{args.r}_k{args.shards}"
+
+
 def workload_config(args):
-    return {"workload": f"webface2m_c{args.classes}_d{args.dim}_b{args.batch}_r{args.r}_k{args.shards}",
+    return {"workload": workload_name(args),
             "classes": args.classes, "dim": args.dim, "global_batch": args.batch, "r": args.r,
             "reference_shards": args.shards, "margin": "arcface s=64 m=0.5",
             "parallelism": f"class-sharded x{args.gpus}",
@@ -329,6 +336,19 @@ def main():
                              "formula": "6*B*cap_local*d / bf16_sustained + 20*cap_local*d / hbm "
                                         "(SURVEY.md 8d)"}
     line["phases_ms"] = phases
+    # BASELINE.json's metric also names GEMM tensor-pipe utilisation: achieved / sustained bf16
+    # peak per GEMM (event-timed phases: the logits phase includes its fused epilogue, the dX
+    # phase its split-K finalize, the dW phase the fused centre update)
+    util = {}
+    tot_t = 0.0
+    for k in ("logits_gemm", "dx_gemm", "dw_update_gemm"):
+        if k in acc:
+            util[k] = F1 / (acc[k] / 1e3) / 1e12 / tf_peak
+            tot_t += acc[k] / 1e3
+    if tot_t > 0:
+        util["all_gemms"] = 3 * F1 / tot_t / 1e12 / tf_peak
+    util["peak_tflops"] = tf_peak
+    line["gemm_tensor_util"] = util
 
     # ---- diagnostics (with_diagnostics): apcs + exact amncs over all C
     #      classes (a 2 B d C screening GEMM); wall time of the host call, X / labels from host

@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
   constexpr uint32_t A_BYTES = 128 * 64 * 2;
   constexpr uint32_t B_BYTES = BN * 64 * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = 2 * BN;
+  // two accumulator buffers at columns 0 and BN; the allocation is a power of two >= 2 BN
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
-  static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "tmem cols pow2");
 
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B, by pointer arithmetic (keeps the shared state space)

@@ -117,6 +117,14 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 constexpr int kBN = 256;  // tcgen05 tile 128 x 256
+#ifndef PFC_FWD_BN
+#define PFC_FWD_BN 256
+#endif
+#ifndef PFC_FWD_NWG
+#define PFC_FWD_NWG 2
+#endif
+constexpr int kFwdBN = PFC_FWD_BN;    // logits GEMM tile width (classes)
+constexpr int kFwdNWG = PFC_FWD_NWG;  // logits GEMM epilogue warpgroups (kFwdBN / 64 / kFwdNWG chunks)
 constexpr int kNWG = 2;
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
@@ -348,7 +356,7 @@ int ensure_maps(Ctx* c, int64_t B) {
   // logits GEMM (M = b, N = classes): A = X^ [B][Dp], B = W^ [ncols][Dp], both K-major;
   // its epilogue stores E^T [ncols][ldg] (per-warp box 32 b x 32 classes, 64B swizzle)
   ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128);
-  ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kBN);
+  ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kFwdBN);
   ok &= make_map(&c->tm_e_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   // dX GEMM (M = b, N = d, K = classes): A = E^T read MN-major (b contiguous); B = W^ MN-major
   ok &= make_map(&c->tm_e_mn, c->G, B, c->ncols, c->ldg, 64);
@@ -445,18 +453,19 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   if (c->d.has_filter) CUDA_TRY(c, cudaMemsetAsync(c->hasval, 0, sizeof(int) * B, s));
 
   constexpr int BN = kUmma ? kBN : kSimtBN;
-  constexpr int NWG = kUmma ? kNWG : 1;
+  constexpr int FBN = kUmma ? kFwdBN : kSimtBN;  // logits GEMM tile width
+  constexpr int NWG = kUmma ? kFwdNWG : 1;         // logits GEMM epilogue warpgroups
   ST* ps = static_cast<ST*>(c->part_s);
   OT* E = static_cast<OT*>(c->G);
   const float tau = (float)c->d.filter_threshold;
   const bool filt = c->d.has_filter != 0;
   if (e2e) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_x, 0));
   // ---- logits GEMM + margin + E = exp(z - o) and its per-slice row sums (shardsim.hpp:249-318)
-  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, BN, 1, 0);
+  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, FBN, 1, 0);
   {
     cudaError_t err;
     auto go = [&](auto e) {
-      if constexpr (kUmma) return launch_umma<kBN, 4, kNWG, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
+      if constexpr (kUmma) return launch_umma<kFwdBN, 4, kFwdNWG, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
       else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
                                             (const float*)c->wh, (int)c->Dp, gf, e);
     };
@@ -1061,7 +1070,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->wh), (size_t)c->ncols_pad * c->Dp * ob));
   CT(dalloc(c, &c->wnorm, (size_t)c->ncols_pad));
   CT(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(T * kNWG * B) * sb));
+  const int64_t Tf = c->bf16 ? ceil_div(std::max<int64_t>(c->ncols, 1), kFwdBN) * kFwdNWG : T;
+  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(Tf * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->seg_s), (size_t)(kMergeSegs * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->ls), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->rowscale), (size_t)B * sb));

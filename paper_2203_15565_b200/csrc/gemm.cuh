@@ -31,6 +31,7 @@ struct GemmGeom {
   int m_tiles, n_tiles, splits, kb_per_split, kb_total;
   int n_fastest;  // tile order: 0 -> m fastest, 1 -> n fastest
   int BN, BK;
+  int BM;         // 128, or 256 for a CTA-pair GEMM (the kernel adds 128 x cluster rank)
   __host__ __device__ int total() const { return m_tiles * n_tiles * splits; }
   __host__ __device__ TileInfo tile(int t) const {
     TileInfo ti;
@@ -44,7 +45,7 @@ struct GemmGeom {
       ti.m_tile = r % m_tiles;
       ti.n_tile = r / m_tiles;
     }
-    ti.row0 = ti.m_tile * 128;
+    ti.row0 = ti.m_tile * BM;
     ti.col0 = ti.n_tile * BN;
     ti.kb0 = ti.split * kb_per_split;
     ti.kb1 = ti.kb0 + kb_per_split < kb_total ? ti.kb0 + kb_per_split : kb_total;
@@ -53,14 +54,15 @@ struct GemmGeom {
   }
 };
 
-inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest) {
+inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest, int BM = 128) {
   GemmGeom g{};
+  g.BM = BM;
   g.M = M;
   g.N = N;
   g.K = K;
   g.BN = BN;
   g.BK = 64;
-  g.m_tiles = (M + 127) / 128;
+  g.m_tiles = (M + BM - 1) / BM;
   g.n_tiles = (N + BN - 1) / BN;
   g.kb_total = (K + 63) / 64;
   if (splits < 1) splits = 1;
@@ -73,9 +75,9 @@ inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest
 
 constexpr int kEpiSmemBytes = 20 * 1024;  // SIMT engine epilogue scratch
 
-template <int BN, int STAGES, int NWG, class Epi>
+template <int BN, int STAGES, int NWG, class Epi, int CG = 1>
 constexpr int umma_smem_bytes() {
-  return 1024 /*align slack*/ + STAGES * (128 * 64 * 2 + BN * 64 * 2) + 1024 /*barriers*/ +
+  return 1024 /*align slack*/ + STAGES * (128 * 64 * 2 + (BN / CG) * 64 * 2) + 1024 /*barriers*/ +
          NWG * Epi::kSmem;
 }
 
@@ -92,19 +94,27 @@ struct TmemSrc {
 #ifndef PFC_CTRL_WARPS
 #define PFC_CTRL_WARPS 2
 #endif
-template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi>
+// CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair (2-CTA cluster) per 256 x BN tile with
+// tcgen05.mma.cta_group::2 issued by the leader: each CTA loads its own 128 rows of A and BN/2
+// rows of B (both signal the leader's full barrier), so per CTA the operand bytes per FLOP drop
+// by a third (A 128 + B 128 rows per 128 x BN block instead of 128 + BN); each CTA's TMEM holds
+// its 128 accumulator rows, so the epilogue functors are the same as for CG = 1.
+template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi, int CG = 1>
 __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, const GemmGeom g,
                      const __grid_constant__ Epi epi) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using namespace pfc_sm100;
+  static_assert(CG == 1 || CG == 2, "CG");
+  static_assert(CG == 1 || Epi::kCluster == 1, "a CTA-pair GEMM has no epilogue cluster");
+  constexpr int BNL = BN / CG;  // rows of B this CTA loads
   constexpr uint32_t A_BYTES = 128 * 64 * 2;
-  constexpr uint32_t B_BYTES = BN * 64 * 2;
+  constexpr uint32_t B_BYTES = BNL * 64 * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   // two accumulator buffers at columns 0 and BN; the allocation is a power of two >= 2 BN
   constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
-  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256 && BNL % 64 == 0, "BN");
 
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B, by pointer arithmetic (keeps the shared state space)
@@ -119,6 +129,8 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
   uint8_t* epi_smem = smem + STAGES * STAGE_BYTES + 1024;  // 1024-aligned per-WG scratch
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -130,52 +142,68 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128 * NWG);
+      mbar_init(&tempty[i], 128 * NWG * CG);  // CG = 2: both CTAs' epilogues release the leader
     }
     epi.setup(epi_smem);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    else tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if constexpr (Epi::kCluster > 1) cluster_sync_all();  // partner barriers initialised
+  if constexpr (Epi::kCluster > 1 || CG == 2) cluster_sync_all();  // peer barriers initialised
   const uint32_t tmem_base = *tmem_slot;
   const int total = g.total();
+  // persistent schedule over tiles (CG = 2: over pair tiles, one per cluster)
+  const int first = (int)blockIdx.x / CG, stride = (int)gridDim.x / CG;
+  auto tile_at = [&](int t) {
+    TileInfo ti = g.tile(t);
+    ti.row0 += (int)rank * 128;
+    return ti;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t kbc = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileInfo ti = g.tile(t);
+      // CG = 2: the leader expects both CTAs' bytes; the peer's loads complete on it remotely
+      const uint32_t full_c = CG == 2 ? mapa_shared(smem_u32(full), 0) : 0u;
+      for (int t = first; t < total; t += stride) {
+        const TileInfo ti = tile_at(t);
+        const int bcol = ti.col0 + (int)rank * BNL;
         for (int kb = ti.kb0; kb < ti.kb1; ++kb, ++kbc) {
           const uint32_t s = kbc % STAGES, ph = (kbc / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[s], STAGE_BYTES * CG);
           const int k0 = kb * 64;
           uint8_t* a = sA + s * A_BYTES;
           uint8_t* b = sB + s * B_BYTES;
+          auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1) {
+            if constexpr (CG == 2) tma_load_2d_pair(m, full_c + s * 8u, dst, c0, c1);
+            else tma_load_2d(m, &full[s], dst, c0, c1);
+          };
           if (!A_MN) {
-            tma_load_2d(&tmA, &full[s], a, k0, ti.row0);
+            load(&tmA, a, k0, ti.row0);
           } else {
 #pragma unroll
-            for (int i = 0; i < 2; ++i) tma_load_2d(&tmA, &full[s], a + i * 8192, ti.row0 + 64 * i, k0);
+            for (int i = 0; i < 2; ++i) load(&tmA, a + i * 8192, ti.row0 + 64 * i, k0);
           }
           if (!B_MN) {
-            tma_load_2d(&tmB, &full[s], b, k0, ti.col0);
+            load(&tmB, b, k0, bcol);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(&tmB, &full[s], b + i * 8192, ti.col0 + 64 * i, k0);
+            for (int i = 0; i < BNL / 64; ++i) load(&tmB, b + i * 8192, bcol + 64 * i, k0);
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(128, BN, A_MN, B_MN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN, A_MN, B_MN);
       uint32_t kbc = 0, it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      for (int t = first; t < total; t += stride, ++it) {
         const TileInfo ti = g.tile(t);
         const uint32_t as = it & 1, aph = (it >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
@@ -193,11 +221,15 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
                                      : make_sdesc_sw128(a_base + k * 32, 0, 1024);
             const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
                                      : make_sdesc_sw128(b_base + k * 32, 0, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb > ti.kb0 || k > 0) ? 1u : 0u);
+            const uint32_t acc = (kb > ti.kb0 || k > 0) ? 1u : 0u;
+            if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, acc);
+            else umma_bf16(d_tmem, ad, bd, idesc, acc);
           }
-          umma_commit(&empty[s]);
+          if constexpr (CG == 2) umma_commit_pair(&empty[s]);
+          else umma_commit(&empty[s]);
         }
-        umma_commit(&tfull[as]);
+        if constexpr (CG == 2) umma_commit_pair(&tfull[as]);
+        else umma_commit(&tfull[as]);
       }
     }
   } else if (warp >= PFC_CTRL_WARPS) {
@@ -207,21 +239,21 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
     const int row = ((warp & 3) << 5) | lane;
     uint8_t* wsm = epi_smem + wg * Epi::kSmem;
     uint32_t it = 0;
+    const uint32_t tempty_c = CG == 2 ? mapa_shared(smem_u32(tempty), 0) : 0u;
     // per-tile operands of the epilogue are loaded two tiles ahead (registers), so their
     // global-memory latency hides behind the current tile; epi.prefetch(next tile) runs on values
     // that have already arrived (e.g. bulk L2 prefetch of the rows the next tile updates)
     typename Epi::Pre pre{}, pre_n{};
-    const int stride = (int)gridDim.x;
-    if ((int)blockIdx.x < total) pre = epi.preload(g.tile(blockIdx.x), row, wg);
-    if ((int)blockIdx.x + stride < total) pre_n = epi.preload(g.tile(blockIdx.x + stride), row, wg);
-    if ((int)blockIdx.x < total) epi.prefetch(g.tile(blockIdx.x), row, wg, pre);
-    for (int t = blockIdx.x; t < total; t += stride, ++it) {
-      TileInfo ti = g.tile(t);
+    if (first < total) pre = epi.preload(tile_at(first), row, wg);
+    if (first + stride < total) pre_n = epi.preload(tile_at(first + stride), row, wg);
+    if (first < total) epi.prefetch(tile_at(first), row, wg, pre);
+    for (int t = first; t < total; t += stride, ++it) {
+      TileInfo ti = tile_at(t);
       ti.iter = (int)it;
       const uint32_t as = it & 1, aph = (it >> 1) & 1;
-      if (t + stride < total) epi.prefetch(g.tile(t + stride), row, wg, pre_n);
+      if (t + stride < total) epi.prefetch(tile_at(t + stride), row, wg, pre_n);
       typename Epi::Pre pre_n2{};
-      if (t + 2 * stride < total) pre_n2 = epi.preload(g.tile(t + 2 * stride), row, wg);
+      if (t + 2 * stride < total) pre_n2 = epi.preload(tile_at(t + 2 * stride), row, wg);
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const TmemSrc src{tmem_base + as * BN + ((uint32_t)((warp & 3) * 32) << 16)};
@@ -230,15 +262,19 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
       else
         epi.template run<BN, NWG>(ti, src, row, wg, wsm, pre);
       tc_fence_before();
-      mbar_arrive(&tempty[as]);
+      if constexpr (CG == 2) mbar_arrive_cluster(tempty_c + as * 8u);
+      else mbar_arrive(&tempty[as]);
       pre = pre_n;
       pre_n = pre_n2;
     }
     epi.finish(row, wg);
   }
   __syncthreads();
-  if constexpr (Epi::kCluster > 1) cluster_sync_all();  // no CTA leaves while its partner writes
-  if (warp == 1) tmem_dealloc(tmem_base, TMEM_COLS);
+  if constexpr (Epi::kCluster > 1 || CG == 2) cluster_sync_all();  // no CTA leaves while its partner writes
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else tmem_dealloc(tmem_base, TMEM_COLS);
+  }
 #endif
 }
 

@@ -125,6 +125,18 @@ constexpr int kBN = 256;  // tcgen05 tile 128 x 256
 #endif
 constexpr int kFwdBN = PFC_FWD_BN;    // logits GEMM tile width (classes)
 constexpr int kFwdNWG = PFC_FWD_NWG;  // logits GEMM epilogue warpgroups (kFwdBN / 64 / kFwdNWG chunks)
+#ifndef PFC_FWD_CG
+#define PFC_FWD_CG 1
+#endif
+#ifndef PFC_DX_CG
+#define PFC_DX_CG 1
+#endif
+constexpr int kFwdCG = PFC_FWD_CG;  // logits GEMM: 1 = one CTA per 128-row tile, 2 = CTA pair
+constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
+#ifndef PFC_DIAG_CG
+#define PFC_DIAG_CG 1
+#endif
+constexpr int kDiagCG = PFC_DIAG_CG;  // diagnostics / mics screening GEMMs likewise
 constexpr int kNWG = 2;
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
@@ -292,11 +304,11 @@ void phase(Ctx* c, const char* name) {
 }
 
 // ------------------------------------------------------------------ GEMM launchers
-template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi>
+template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi, int CG = 1>
 cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, const GemmGeom& g,
                         const Epi& epi) {
-  auto kern = umma_gemm_kernel<BN, STAGES, NWG, A_MN, B_MN, Epi>;
-  constexpr int smem = umma_smem_bytes<BN, STAGES, NWG, Epi>();
+  auto kern = umma_gemm_kernel<BN, STAGES, NWG, A_MN, B_MN, Epi, CG>;
+  constexpr int smem = umma_smem_bytes<BN, STAGES, NWG, Epi, CG>();
   static_assert(smem <= 232448, "shared memory budget");
   static bool configured = false;
   if (!configured) {
@@ -305,13 +317,15 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
     configured = true;
   }
   const int total = g.total();
-  int grid = total < c->num_sms ? total : c->num_sms;
-  if (grid <= 0) return cudaSuccess;
-  if constexpr (Epi::kCluster > 1) {
-    // clusters of kCluster CTAs own the dim blocks of the same class block: the grid (the tile
-    // stride of the persistent schedule) is a multiple of the cluster size
-    grid = (c->num_sms / Epi::kCluster) * Epi::kCluster;
-    if (grid > total) grid = total;
+  if (total <= 0) return cudaSuccess;
+  constexpr int kCl = CG > Epi::kCluster ? CG : Epi::kCluster;
+  if constexpr (kCl > 1) {
+    // clusters of kCl CTAs: the grid (the tile stride of the persistent schedule) is a multiple
+    // of the cluster size.  Epilogue clusters (kCluster) own the dim blocks of one class block,
+    // one tile per CTA; CTA pairs (CG = 2) own one pair tile per cluster.
+    int grid = (c->num_sms / kCl) * kCl;
+    const int need = CG == 2 ? total * 2 : total;
+    if (grid > need) grid = need;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(32 * PFC_CTRL_WARPS + 128 * NWG);
@@ -319,7 +333,7 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = Epi::kCluster;
+    at[0].val.clusterDim.x = kCl;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -327,6 +341,7 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
     c->launches++;
     return cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epi);
   } else {
+    const int grid = total < c->num_sms ? total : c->num_sms;
     kern<<<grid, 32 * PFC_CTRL_WARPS + 128 * NWG, smem, c->stream>>>(ta, tb, g, epi);
     c->launches++;
     return cudaGetLastError();
@@ -356,7 +371,7 @@ int ensure_maps(Ctx* c, int64_t B) {
   // logits GEMM (M = b, N = classes): A = X^ [B][Dp], B = W^ [ncols][Dp], both K-major;
   // its epilogue stores E^T [ncols][ldg] (per-warp box 32 b x 32 classes, 64B swizzle)
   ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128);
-  ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kFwdBN);
+  ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kFwdBN / kFwdCG);
   ok &= make_map(&c->tm_e_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   // dX GEMM (M = b, N = d, K = classes): A = E^T read MN-major (b contiguous); B = W^ MN-major
   ok &= make_map(&c->tm_e_mn, c->G, B, c->ncols, c->ldg, 64);
@@ -372,7 +387,7 @@ int ensure_maps(Ctx* c, int64_t B) {
 
 int dx_splits(Ctx* c, int64_t B) {
   if (c->bf16) {
-    const int64_t tiles = ceil_div(B, 128) * ceil_div(c->D, kBN);
+    const int64_t tiles = ceil_div(B, 128 * kDxCG) * kDxCG * ceil_div(c->D, kBN);  // CTAs per split
     int64_t s = c->num_sms / (tiles > 0 ? tiles : 1);
     if (s < 1) s = 1;
     return (int)std::min<int64_t>(s, c->max_splits);
@@ -461,11 +476,12 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const bool filt = c->d.has_filter != 0;
   if (e2e) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_x, 0));
   // ---- logits GEMM + margin + E = exp(z - o) and its per-slice row sums (shardsim.hpp:249-318)
-  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, FBN, 1, 0);
+  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, FBN, 1, 0, kUmma ? 128 * kFwdCG : 128);
   {
     cudaError_t err;
     auto go = [&](auto e) {
-      if constexpr (kUmma) return launch_umma<kFwdBN, 4, kFwdNWG, false, false>(c, c->tm_x_k, c->tm_w_k, gf, e);
+      if constexpr (kUmma)
+        return launch_umma<kFwdBN, 4, kFwdNWG, false, false, decltype(e), kFwdCG>(c, c->tm_x_k, c->tm_w_k, gf, e);
       else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
                                             (const float*)c->wh, (int)c->Dp, gf, e);
     };
@@ -522,10 +538,10 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- dX = rowscale * E W^ + delta w^_pos (split-K), tangent projection (shardsim.hpp:363-376)
   {
     const int S = dx_splits(c, B);
-    const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0);
+    const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0, kUmma ? 128 * kDxCG : 128);
     DxPartEpi e{{}, (int)B, (int)c->D, c->dx_part};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, true, true>(c, c->tm_e_mn, c->tm_w_mn, gx, e);
+    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, true, true, DxPartEpi, kDxCG>(c, c->tm_e_mn, c->tm_w_mn, gx, e);
     else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
                                        (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
@@ -855,7 +871,7 @@ int diag_alloc(Ctx* c) {
   c->dcand_cap = (int64_t)1 << 22;  // 4M candidates (64 MB)
   CUDA_TRY(c, dalloc(c, &c->dcand, (size_t)c->dcand_cap));
   CUDA_TRY(c, dalloc(c, &c->dncand, (size_t)1));
-  if (c->bf16 && !make_map(&c->tm_wall, c->dwall, c->Dp, c->rows, c->Dp, kBN))
+  if (c->bf16 && !make_map(&c->tm_wall, c->dwall, c->Dp, c->rows, c->Dp, kBN / kDiagCG))
     return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return PFC_OK;
 }
@@ -889,8 +905,8 @@ int run_mics_block(Ctx* c, int64_t r0, int64_t nr, uint32_t* rmax, unsigned long
         return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
       // n fastest: all CTAs sweep the columns of the same 128 rows together, so the running
       // maxima converge within the first wave and later tiles yield few candidates
-      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kBN, 1, 1);
-      err = launch_umma<kBN, 4, 2, false, false>(c, ta, c->tm_wall, g, e);
+      const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kBN, 1, 1, 128 * kDiagCG);
+      err = launch_umma<kBN, 4, 2, false, false, DiagMaxEpi, kDiagCG>(c, ta, c->tm_wall, g, e);
     } else {
       const GemmGeom g = make_geom((int)nr, (int)c->rows, (int)c->Dp, kSimtBN, 1, 1);
       err = launch_simt<false, false>(c, (const float*)(wall + (size_t)r0 * c->Dp), (int)c->Dp,
@@ -943,8 +959,8 @@ int run_diagnostics(Ctx* c, int64_t B, bool split) {
     cudaError_t err;
     if constexpr (kUmma) {
       if (int rc = ensure_maps(c, B)) return rc;
-      const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kBN, 1, 0);
-      err = launch_umma<kBN, 4, 2, false, false>(c, c->tm_x_k, c->tm_wall, g, e);
+      const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kBN, 1, 0, 128 * kDiagCG);
+      err = launch_umma<kBN, 4, 2, false, false, DiagMaxEpi, kDiagCG>(c, c->tm_x_k, c->tm_wall, g, e);
     } else {
       const GemmGeom g = make_geom((int)B, (int)c->rows, (int)c->Dp, kSimtBN, 1, 0);
       err = launch_simt<false, false>(c, (const float*)xh, (int)c->Dp, (const float*)wall,

@@ -183,6 +183,51 @@ int pfc_gpu_write_shards(void* ctx, const char* path, int append);
  * than the reference reader's 2^32-element cap (io.hpp:78) are accepted. */
 int pfc_gpu_read_shards(void* ctx, const char* path, int64_t offset, int64_t* end_offset);
 
+/* ---- device-resident FeatureBatch ------------------------------------------------------- */
+/* pfc_gpu_step with the FeatureBatch in DEVICE memory: features D x B fp64 row-major and
+ * labels[B] int64; d_features_dev (D x B fp64, device; NULL = leave it in the context) receives
+ * the full summed gradient.  Same kernels and results as pfc_gpu_step on the same values; the
+ * label / capacity errors come from the device sampler's checks.  Synchronous. */
+int pfc_gpu_step_features(void* ctx, const double* features_d_by_b_dev, const int64_t* labels_dev,
+                          int64_t batch, const pfc_gpu_step_args* args, double* d_features_d_by_b_dev,
+                          pfc_gpu_step_out* out);
+
+/* ---- trainer integration (trainer.hpp:362-581) --------------------------
+ * The caller of the step with its backbone on the device: the dataset points (SyntheticDataset,
+ * datasynth.hpp:47-75) are uploaded once, the backbone (trainer.hpp:51-126: hidden =
+ * tanh(w1 x + b1), output = w2 hidden + b2, fp64, products summed like matmul, matrix.hpp:86-105)
+ * runs on the device, and the step's features and d_features never leave it: per step the host
+ * sends the batch's point ids and reads the status.  Single-rank contexts; the context must
+ * outlive the trainer.  The loop (split, shuffle, schedule, checkpoints, final metrics) is
+ * pfc::gpu::train in include/pfc/gpu_trainer.hpp. */
+/* points: input_dim x num_points fp64 row-major (host); observed_labels[num_points].  The
+ * backbone is Backbone::init(input_dim, hidden_dim, embed_dim, seed) (trainer.hpp:65-77), bit
+ * for bit; embed_dim must equal the context's dim. */
+int pfc_gpu_trainer_create(void* ctx, const double* points, int64_t input_dim, int64_t num_points,
+                           const int64_t* observed_labels, int64_t hidden_dim, int64_t embed_dim,
+                           uint64_t seed, void** trainer_out);
+int pfc_gpu_trainer_destroy(void* trainer);
+/* backbone parameters in the reference layouts (host fp64): w1 hidden x input, b1 hidden,
+ * w2 embed x hidden, b2 embed (checkpoints, trainer.hpp:264-267) */
+int pfc_gpu_trainer_get_backbone(void* trainer, double* w1, double* b1, double* w2, double* b2);
+int pfc_gpu_trainer_set_backbone(void* trainer, const double* w1, const double* b1,
+                                 const double* w2, const double* b2);
+/* Backbone::forward of the batch point_ids[batch] (host ids); the features stay on the device */
+int pfc_gpu_trainer_forward(void* trainer, const int64_t* point_ids, int64_t batch);
+/* apcs / amncs of the forward batch against the current shards (with_diagnostics; call between
+ * forward and step, as the reference reports them for the pre-update shards) */
+int pfc_gpu_trainer_diagnostics(void* trainer, const int64_t* class_identity,
+                                const int64_t* sample_identity, pfc_gpu_diag_out* out);
+/* distributed_partial_step on the forward batch; d_features stay on the device */
+int pfc_gpu_trainer_step(void* trainer, const pfc_gpu_step_args* args, pfc_gpu_step_out* out);
+/* Backbone::apply_gradient(inputs, act, d_features, lr) (trainer.hpp:99-125) with the cached
+ * activations and the step's d_features; asynchronous: a non-finite product is reported by the
+ * next forward-dependent call with the reference's "matmul: non-finite entry" text */
+int pfc_gpu_trainer_apply_gradient(void* trainer, double lr);
+/* forward-only embeddings of point_ids[n] into emb (embed x n fp64, host), chunked by max_batch
+ * (evaluation: nearest-centre accuracy, verification); discards the cached activations */
+int pfc_gpu_trainer_embed(void* trainer, const int64_t* point_ids, int64_t n, double* emb);
+
 /* ---- bench / test helpers --------------------------------------------------------------- */
 /* Synthetic inputs of the bench convention on the device:
  * labels[b] = SeededRng(seed, make_stream("bench-labels", step)).next_below(C) and

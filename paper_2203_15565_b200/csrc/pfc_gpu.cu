@@ -1408,6 +1408,26 @@ static bool pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+// The step on a FeatureBatch already on the device: D x B fp64 features in c->xdb, labels in
+// c->labels.  Leaves the summed D x B fp64 d_features in c->xdb; synchronous.
+static int step_from_xdb(Ctx* c, int64_t B, const pfc_gpu_step_args* a, pfc_gpu_step_out* out) {
+  cudaStream_t s = c->stream;
+  dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+  x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
+  if (int rc = run_step(c, c->X, c->labels, B, a, c->dX)) return rc;
+  c->reset_status = true;
+  if (c->R > 1) {  // the drop-in returns the FULL summed d_features on every rank
+    NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, s));
+    c->step_nccl_bytes += (uint64_t)B * c->D * 4;
+  }
+  dx_to_dxb_kernel<<<grid, blk, 0, s>>>(c->dX, (int)c->D, (int)B, c->xdb);
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  if (int rc = finish_phase_timing(c)) return rc;
+  return check_status(c, a->step_index, B, out);
+}
+
 int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
                  const pfc_gpu_step_args* a, double* dxdb, pfc_gpu_step_out* out) {
   Ctx* c = static_cast<Ctx*>(ctx);
@@ -1440,20 +1460,7 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
                 (long long)c->maxB);
   CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
-  dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
-  x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
-  if (int rc = run_step(c, c->X, c->labels, B, a, c->dX)) return rc;
-  c->reset_status = true;
-  if (c->R > 1) {  // the drop-in returns the FULL summed d_features on every rank
-    NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, s));
-    c->step_nccl_bytes += (uint64_t)B * c->D * 4;
-  }
-  dx_to_dxb_kernel<<<grid, blk, 0, s>>>(c->dX, (int)c->D, (int)B, c->xdb);
-  CUDA_TRY(c, cudaGetLastError());
-  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(c, cudaStreamSynchronize(s));
-  if (int rc = finish_phase_timing(c)) return rc;
-  if (int rc = check_status(c, a->step_index, B, out)) return rc;
+  if (int rc = step_from_xdb(c, B, a, out)) return rc;
   CUDA_TRY(c, cudaMemcpy(dxdb, c->xdb, sizeof(double) * B * c->D, cudaMemcpyDeviceToHost));
   return PFC_OK;
 }
@@ -1493,10 +1500,9 @@ int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_l
   return check_status(c, a->step_index, B, out);
 }
 
-int pfc_gpu_diagnostics(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
-                        const int64_t* class_identity, const int64_t* sample_identity,
-                        pfc_gpu_diag_out* out) {
-  Ctx* c = static_cast<Ctx*>(ctx);
+// the reference's checks ahead of apcs / amncs (metrics.hpp:56-79, 91-146)
+static int diag_validate(Ctx* c, const int64_t* labels, int64_t B, const int64_t* class_identity,
+                         const int64_t* sample_identity) {
   if (B < 1 || B > c->maxB)
     return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: batch %lld outside [1, max_batch=%lld]", (long long)B,
                 (long long)c->maxB);
@@ -1506,22 +1512,13 @@ int pfc_gpu_diagnostics(void* ctx, const double* xdb, const int64_t* labels, int
   for (int64_t b = 0; b < B; ++b)
     if (labels[b] < 0 || labels[b] >= c->C)
       return fail(c, PFC_ERR_CONTRACT, "apcs: label %lld owned by no shard", (long long)labels[b]);
-  for (int64_t i = 0; i < B * c->D; ++i)
-    if (!std::isfinite(xdb[i]))
-      return fail(c, PFC_ERR_NUMERICAL, "l2_normalize_columns: non-finite entry in %lldx%lld result",
-                  (long long)c->D, (long long)B);
-  if (c->C < 2) return fail(c, PFC_ERR_CONTRACT, "amncs: needs at least two classes");
-  const bool split = class_identity != nullptr;
+  return PFC_OK;
+}
+
+// apcs / amncs of the batch whose D x B fp64 features are in c->xdb and labels in c->labels
+// (device), identities (split) in c->dcid / c->dsid; the labels were validated by the caller.
+static int diagnostics_device(Ctx* c, int64_t B, bool split, pfc_gpu_diag_out* out) {
   cudaStream_t s = c->stream;
-  if (int rc = diag_alloc(c)) return rc;
-  CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
-  if (split) {
-    CUDA_TRY(c, cudaMemcpyAsync(c->dcid, class_identity + c->cls_lo, sizeof(int64_t) * c->rows,
-                                cudaMemcpyHostToDevice, s));
-    CUDA_TRY(c, cudaMemcpyAsync(c->dsid, sample_identity, sizeof(int64_t) * B,
-                                cudaMemcpyHostToDevice, s));
-  }
   dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
   x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
   const int rc = c->bf16 ? run_diagnostics<__nv_bfloat16, true>(c, B, split)
@@ -1567,6 +1564,30 @@ int pfc_gpu_diagnostics(void* ctx, const double* xdb, const int64_t* labels, int
     }
   }
   return PFC_OK;
+}
+
+int pfc_gpu_diagnostics(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
+                        const int64_t* class_identity, const int64_t* sample_identity,
+                        pfc_gpu_diag_out* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (int rc = diag_validate(c, labels, B, class_identity, sample_identity)) return rc;
+  for (int64_t i = 0; i < B * c->D; ++i)
+    if (!std::isfinite(xdb[i]))
+      return fail(c, PFC_ERR_NUMERICAL, "l2_normalize_columns: non-finite entry in %lldx%lld result",
+                  (long long)c->D, (long long)B);
+  if (c->C < 2) return fail(c, PFC_ERR_CONTRACT, "amncs: needs at least two classes");
+  const bool split = class_identity != nullptr;
+  cudaStream_t s = c->stream;
+  if (int rc = diag_alloc(c)) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb, sizeof(double) * B * c->D, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
+  if (split) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->dcid, class_identity + c->cls_lo, sizeof(int64_t) * c->rows,
+                                cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(c->dsid, sample_identity, sizeof(int64_t) * B,
+                                cudaMemcpyHostToDevice, s));
+  }
+  return diagnostics_device(c, B, split, out);
 }
 
 int pfc_gpu_sync(void* ctx, pfc_gpu_step_out* out) {
@@ -1651,5 +1672,348 @@ int pfc_gpu_phase_times(void* ctx, float* ms, const char** names, int n) {
 }
 
 int64_t pfc_gpu_launches_per_step(void* ctx) { return static_cast<Ctx*>(ctx)->launches; }
+
+}  // extern "C"
+
+// ====================================================================== trainer integration
+// the reference's training loop (trainer.hpp:362-581) drives the step with a
+// backbone in front of it.  Here the dataset points, the backbone (trainer.hpp:51-126, fp64), the
+// step's features X and its d_features dX all live on the device; per step the host sends the
+// batch's point ids and reads back the step status (loss).  The loop itself (split, shuffle,
+// schedule, checkpoints, final metrics) is include/pfc/gpu_trainer.hpp.
+#include "backbone.cuh"
+
+namespace {
+
+struct Trainer {
+  Ctx* c = nullptr;
+  int64_t in_dim = 0, npts = 0, H = 0, E = 0, maxB = 0;
+  std::vector<void*> allocs;
+  std::vector<int64_t> plabels_h;          // observed labels (host copy: validation, diagnostics)
+  double* points = nullptr;                // in_dim x npts (device, the dataset)
+  int64_t* plabels = nullptr;              // npts
+  double *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;  // H x in, H, E x H, E
+  double *inputs = nullptr, *hidden = nullptr, *feat = nullptr;        // in x B, H x B, E x B
+  double *dw2 = nullptr, *dhid = nullptr, *dw1 = nullptr;              // E x H, H x B, H x in
+  int64_t* ids = nullptr;                  // maxB (device)
+  int64_t* ids_h = nullptr;                // maxB (pinned)
+  int* flag = nullptr;                     // non-finite product bits (device)
+  int* flag_h = nullptr;                   // pinned
+  std::vector<int64_t> batch_labels;       // labels of the last forward batch
+  int64_t B = 0;                           // batch of the cached activations (0: none)
+  bool stepped = false;                    // the cached batch has a d_features in c->xdb
+
+  template <typename T>
+  cudaError_t alloc(T** p, size_t n) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return e;
+  }
+};
+
+// the reference's shape strings of the products whose require_finite failed (matrix.hpp:103)
+int trainer_flag_error(Trainer* t, int bits, int64_t B) {
+  const int64_t shapes[5][2] = {{t->H, B}, {t->E, B}, {t->E, t->H}, {t->H, B}, {t->H, t->in_dim}};
+  for (int w = 0; w < 5; ++w)
+    if (bits & (1 << w))
+      return fail(t->c, PFC_ERR_NUMERICAL, "matmul: non-finite entry in %lldx%lld result",
+                  (long long)shapes[w][0], (long long)shapes[w][1]);
+  return PFC_OK;
+}
+
+// reads and clears the device flag (synchronises the context stream)
+int trainer_check(Trainer* t, int64_t B) {
+  Ctx* c = t->c;
+  CUDA_TRY(c, cudaMemcpyAsync(t->flag_h, t->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  const int bits = *t->flag_h;
+  if (bits) {
+    CUDA_TRY(c, cudaMemsetAsync(t->flag, 0, sizeof(int), c->stream));
+    return trainer_flag_error(t, bits, B);
+  }
+  return PFC_OK;
+}
+
+template <int EPI>
+cudaError_t bb_matmul(Trainer* t, const double* A, int64_t a_i, int64_t a_k, const double* Bm,
+                      int64_t b_k, int64_t b_j, double* C, int64_t rows, int64_t cols,
+                      int64_t inner, const double* aux, int which) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  dim3 grid((unsigned)ceil_div(cols, 128), (unsigned)rows);
+  bb_matmul_kernel<EPI><<<grid, 128, 0, t->c->stream>>>(A, a_i, a_k, Bm, b_k, b_j, C, (int)rows,
+                                                        (int)cols, (int)inner, aux, t->flag, which);
+  t->c->launches++;
+  return cudaGetLastError();
+}
+
+// Backbone::forward (trainer.hpp:79-96) of `n` dataset points into t->feat (E x n, the step's
+// FeatureBatch layout); caches inputs and hidden for apply_gradient.
+int trainer_forward(Trainer* t, const int64_t* ids, int64_t n) {
+  Ctx* c = t->c;
+  cudaStream_t s = c->stream;
+  for (int64_t b = 0; b < n; ++b)
+    if (ids[b] < 0 || ids[b] >= t->npts)
+      return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_trainer: point id %lld outside [0, %lld)",
+                  (long long)ids[b], (long long)t->npts);
+  std::memcpy(t->ids_h, ids, sizeof(int64_t) * n);
+  CUDA_TRY(c, cudaMemcpyAsync(t->ids, t->ids_h, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+  bb_gather_kernel<<<dim3((unsigned)ceil_div(n, 128), (unsigned)t->in_dim), 128, 0, s>>>(
+      t->points, t->npts, (int)t->in_dim, t->ids, (int)n, t->plabels, t->inputs, c->labels);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  // hidden = tanh(w1 inputs + b1); output = w2 hidden + b2
+  CUDA_TRY(c, bb_matmul<kBbTanhBias>(t, t->w1, t->in_dim, 1, t->inputs, n, 1, t->hidden, t->H, n,
+                                     t->in_dim, t->b1, 0));
+  CUDA_TRY(c, bb_matmul<kBbBias>(t, t->w2, t->H, 1, t->hidden, n, 1, t->feat, t->E, n, t->H,
+                                 t->b2, 1));
+  t->batch_labels.resize((size_t)n);
+  for (int64_t b = 0; b < n; ++b) t->batch_labels[(size_t)b] = t->plabels_h[(size_t)ids[b]];
+  t->B = n;
+  t->stepped = false;
+  return PFC_OK;
+}
+
+// Backbone::init (trainer.hpp:65-77) on the host: the same counter-based streams and Box-Muller
+// (rng.hpp:77-81) with the host libm, so the initial weights equal the reference's bit for bit.
+void backbone_init_host(int64_t rows, int64_t cols, uint64_t seed, const char* tag,
+                        std::vector<double>& w) {
+  uint64_t h = 0xcbf29ce484222325ULL;  // fnv1a(tag) (rng.hpp:26-32)
+  for (const char* p = tag; *p; ++p) {
+    h ^= (unsigned char)*p;
+    h *= 0x100000001b3ULL;
+  }
+  h = mix64(h ^ mix64(0 + kPhi));  // make_stream(tag, 0, 0) (rng.hpp:91-96)
+  h = mix64(h ^ mix64(0 + 0x2545f4914f6cdd1dULL));
+  const uint64_t key = rng_key(seed, h);
+  const double sc = 1.0 / std::sqrt((double)cols);
+  w.assign((size_t)(rows * cols), 0.0);
+  uint64_t ctr = 0;
+  for (double& v : w) {
+    const double u1 = ((double)(rng_draw(key, ++ctr) >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = (double)(rng_draw(key, ++ctr) >> 11) * 0x1.0p-53;
+    v = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2) * sc;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pfc_gpu_step_features(void* ctx, const double* xdb_dev, const int64_t* labels_dev, int64_t B,
+                          const pfc_gpu_step_args* a, double* dxdb_dev, pfc_gpu_step_out* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!(a->lr >= 0.0)) return fail(c, PFC_ERR_CONTRACT, "distributed_partial_step: lr must be >= 0");
+  if (B < 0) return fail(c, PFC_ERR_SHAPE, "FeatureBatch: label count != feature columns");
+  if (B == 0)
+    return fail(c, PFC_ERR_NUMERICAL, "distributed_partial_step: non-finite loss at step %lld",
+                (long long)a->step_index);
+  if (B > c->maxB)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: batch %lld exceeds max_batch %lld", (long long)B,
+                (long long)c->maxB);
+  cudaStream_t s = c->stream;
+  // labels are checked on the device by the sampler (same errors as build_buffers)
+  if (xdb_dev != c->xdb)
+    CUDA_TRY(c, cudaMemcpyAsync(c->xdb, xdb_dev, sizeof(double) * B * c->D, cudaMemcpyDeviceToDevice, s));
+  if (labels_dev != c->labels)
+    CUDA_TRY(c, cudaMemcpyAsync(c->labels, labels_dev, sizeof(int64_t) * B, cudaMemcpyDeviceToDevice, s));
+  if (int rc = step_from_xdb(c, B, a, out)) return rc;
+  if (dxdb_dev && dxdb_dev != c->xdb)
+    CUDA_TRY(c, cudaMemcpyAsync(dxdb_dev, c->xdb, sizeof(double) * B * c->D, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_create(void* ctx, const double* points, int64_t input_dim, int64_t num_points,
+                           const int64_t* observed_labels, int64_t hidden_dim, int64_t embed_dim,
+                           uint64_t seed, void** trainer_out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  *trainer_out = nullptr;
+  if (c->R > 1)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_trainer: single-rank contexts only");
+  if (input_dim < 1 || num_points < 1 || hidden_dim < 1 || embed_dim < 2)
+    return fail(c, PFC_ERR_CONFIG, "train: bad backbone dims");
+  if (embed_dim != c->D)
+    return fail(c, PFC_ERR_SHAPE, "pfc_gpu_trainer: embed_dim %lld != the context's dim %lld",
+                (long long)embed_dim, (long long)c->D);
+  auto* t = new Trainer();
+  t->c = c;
+  t->in_dim = input_dim;
+  t->npts = num_points;
+  t->H = hidden_dim;
+  t->E = embed_dim;
+  t->maxB = c->maxB;
+  t->plabels_h.assign(observed_labels, observed_labels + num_points);
+  const size_t mb = (size_t)t->maxB;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  A(t->alloc(&t->points, (size_t)(input_dim * num_points)));
+  A(t->alloc(&t->plabels, (size_t)num_points));
+  A(t->alloc(&t->w1, (size_t)(hidden_dim * input_dim)));
+  A(t->alloc(&t->b1, (size_t)hidden_dim));
+  A(t->alloc(&t->w2, (size_t)(embed_dim * hidden_dim)));
+  A(t->alloc(&t->b2, (size_t)embed_dim));
+  A(t->alloc(&t->inputs, (size_t)input_dim * mb));
+  A(t->alloc(&t->hidden, (size_t)hidden_dim * mb));
+  A(t->alloc(&t->feat, (size_t)embed_dim * mb));
+  A(t->alloc(&t->dw2, (size_t)(embed_dim * hidden_dim)));
+  A(t->alloc(&t->dhid, (size_t)hidden_dim * mb));
+  A(t->alloc(&t->dw1, (size_t)(hidden_dim * input_dim)));
+  A(t->alloc(&t->ids, mb));
+  A(t->alloc(&t->flag, 1));
+  A(cudaMallocHost(&t->ids_h, sizeof(int64_t) * mb));
+  A(cudaMallocHost(&t->flag_h, sizeof(int)));
+  if (e == cudaSuccess) {
+    cudaStream_t s = c->stream;
+    std::vector<double> w1, w2, zh((size_t)hidden_dim, 0.0), ze((size_t)embed_dim, 0.0);
+    backbone_init_host(hidden_dim, input_dim, seed, "backbone-w1", w1);
+    backbone_init_host(embed_dim, hidden_dim, seed, "backbone-w2", w2);
+    A(cudaMemcpyAsync(t->points, points, sizeof(double) * input_dim * num_points, cudaMemcpyHostToDevice, s));
+    A(cudaMemcpyAsync(t->plabels, observed_labels, sizeof(int64_t) * num_points, cudaMemcpyHostToDevice, s));
+    A(cudaMemcpyAsync(t->w1, w1.data(), sizeof(double) * w1.size(), cudaMemcpyHostToDevice, s));
+    A(cudaMemcpyAsync(t->w2, w2.data(), sizeof(double) * w2.size(), cudaMemcpyHostToDevice, s));
+    A(cudaMemcpyAsync(t->b1, zh.data(), sizeof(double) * zh.size(), cudaMemcpyHostToDevice, s));
+    A(cudaMemcpyAsync(t->b2, ze.data(), sizeof(double) * ze.size(), cudaMemcpyHostToDevice, s));
+    A(cudaMemsetAsync(t->flag, 0, sizeof(int), s));
+    A(cudaStreamSynchronize(s));
+  }
+  if (e != cudaSuccess) {
+    for (void* p : t->allocs) cudaFree(p);
+    if (t->ids_h) cudaFreeHost(t->ids_h);
+    if (t->flag_h) cudaFreeHost(t->flag_h);
+    delete t;
+    return fail(c, PFC_ERR_CUDA, "pfc_gpu_trainer_create: %s", cudaGetErrorString(e));
+  }
+  *trainer_out = t;
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_destroy(void* tr) {
+  if (!tr) return PFC_OK;
+  auto* t = static_cast<Trainer*>(tr);
+  cudaStreamSynchronize(t->c->stream);
+  for (void* p : t->allocs) cudaFree(p);
+  if (t->ids_h) cudaFreeHost(t->ids_h);
+  if (t->flag_h) cudaFreeHost(t->flag_h);
+  delete t;
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_get_backbone(void* tr, double* w1, double* b1, double* w2, double* b2) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c, cudaMemcpyAsync(w1, t->w1, sizeof(double) * t->H * t->in_dim, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(b1, t->b1, sizeof(double) * t->H, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(w2, t->w2, sizeof(double) * t->E * t->H, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(b2, t->b2, sizeof(double) * t->E, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_set_backbone(void* tr, const double* w1, const double* b1, const double* w2,
+                                 const double* b2) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c, cudaMemcpyAsync(t->w1, w1, sizeof(double) * t->H * t->in_dim, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(t->b1, b1, sizeof(double) * t->H, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(t->w2, w2, sizeof(double) * t->E * t->H, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(t->b2, b2, sizeof(double) * t->E, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  t->B = 0;
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_forward(void* tr, const int64_t* point_ids, int64_t batch) {
+  auto* t = static_cast<Trainer*>(tr);
+  if (batch < 1 || batch > t->maxB)
+    return fail(t->c, PFC_ERR_CONTRACT, "pfc_gpu_trainer: batch %lld outside [1, max_batch=%lld]",
+                (long long)batch, (long long)t->maxB);
+  return trainer_forward(t, point_ids, batch);
+}
+
+int pfc_gpu_trainer_diagnostics(void* tr, const int64_t* class_identity,
+                                const int64_t* sample_identity, pfc_gpu_diag_out* out) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  if (t->B < 1 || t->stepped)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_trainer_diagnostics: call after forward, before step");
+  const int64_t B = t->B;
+  if (int rc = diag_validate(c, t->batch_labels.data(), B, class_identity, sample_identity)) return rc;
+  if (int rc = trainer_check(t, B)) return rc;  // the features are finite (matmul checks)
+  if (c->C < 2) return fail(c, PFC_ERR_CONTRACT, "amncs: needs at least two classes");
+  const bool split = class_identity != nullptr;
+  cudaStream_t s = c->stream;
+  if (int rc = diag_alloc(c)) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(c->xdb, t->feat, sizeof(double) * B * c->D, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->labels, t->batch_labels.data(), sizeof(int64_t) * B,
+                              cudaMemcpyHostToDevice, s));
+  if (split) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->dcid, class_identity + c->cls_lo, sizeof(int64_t) * c->rows,
+                                cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(c->dsid, sample_identity, sizeof(int64_t) * B,
+                                cudaMemcpyHostToDevice, s));
+  }
+  return diagnostics_device(c, B, split, out);
+}
+
+int pfc_gpu_trainer_step(void* tr, const pfc_gpu_step_args* a, pfc_gpu_step_out* out) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  if (t->B < 1 || t->stepped)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_trainer_step: call after forward");
+  if (!(a->lr >= 0.0)) return fail(c, PFC_ERR_CONTRACT, "distributed_partial_step: lr must be >= 0");
+  const int64_t B = t->B;
+  if (int rc = host_validate(c, t->batch_labels.data(), B)) return rc;
+  cudaStream_t s = c->stream;
+  // the batch labels were gathered into c->labels by the forward
+  CUDA_TRY(c, cudaMemcpyAsync(c->xdb, t->feat, sizeof(double) * B * c->D, cudaMemcpyDeviceToDevice, s));
+  if (int rc = trainer_check(t, B)) return rc;  // Backbone::forward's matmul checks come first
+  if (int rc = step_from_xdb(c, B, a, out)) return rc;
+  t->stepped = true;  // d_features (D x B fp64) are in c->xdb
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_apply_gradient(void* tr, double lr) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  if (!t->stepped)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_trainer_apply_gradient: call after a successful step");
+  const int64_t B = t->B, H = t->H, E = t->E, I = t->in_dim;
+  const double* dout = c->xdb;  // E x B
+  // d_w2 = d_out hidden^T; d_hidden = (w2^T d_out) * (1 - h^2); d_w1 = d_hidden inputs^T
+  CUDA_TRY(c, bb_matmul<kBbPlain>(t, dout, B, 1, t->hidden, 1, B, t->dw2, E, H, B, nullptr, 2));
+  CUDA_TRY(c, bb_matmul<kBbTanhGrad>(t, t->w2, 1, H, dout, B, 1, t->dhid, H, B, E, t->hidden, 3));
+  CUDA_TRY(c, bb_matmul<kBbPlain>(t, t->dhid, B, 1, t->inputs, 1, B, t->dw1, H, I, B, nullptr, 4));
+  // SGD, w2 rows then w1 rows (trainer.hpp:113-124)
+  bb_sgd_rows_kernel<<<(unsigned)E, 128, 0, c->stream>>>(t->w2, t->b2, t->dw2, dout, (int)H, (int)B, lr);
+  bb_sgd_rows_kernel<<<(unsigned)H, 128, 0, c->stream>>>(t->w1, t->b1, t->dw1, t->dhid, (int)I, (int)B, lr);
+  c->launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  t->stepped = false;
+  t->B = 0;
+  // the products' finiteness is checked before the next forward's features are used
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_embed(void* tr, const int64_t* point_ids, int64_t n, double* emb) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  for (int64_t at = 0; at < n; at += t->maxB) {
+    const int64_t m = std::min<int64_t>(t->maxB, n - at);
+    if (int rc = trainer_forward(t, point_ids + at, m)) return rc;
+    if (int rc = trainer_check(t, m)) return rc;
+    std::vector<double> blk((size_t)(t->E * m));
+    CUDA_TRY(c, cudaMemcpyAsync(blk.data(), t->feat, sizeof(double) * t->E * m,
+                                cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int64_t e = 0; e < t->E; ++e)
+      std::memcpy(emb + e * n + at, blk.data() + e * m, sizeof(double) * m);
+  }
+  t->B = 0;  // the cached activations are not a training batch
+  return PFC_OK;
+}
 
 }  // extern "C"

@@ -301,6 +301,8 @@ def load_library(path: str | None = None) -> C.CDLL:
         "pfc_gpu_init_shards": (C.c_int, [vp, C.c_uint64]),
         "pfc_gpu_device_state": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)]),
         "pfc_gpu_step": (C.c_int, [vp, vp, vp, i64, C.POINTER(StepArgs), vp, C.POINTER(StepOut)]),
+        "pfc_gpu_step_features": (C.c_int, [vp, vp, vp, i64, C.POINTER(StepArgs), vp,
+                                            C.POINTER(StepOut)]),
         "pfc_gpu_step_device": (C.c_int, [vp, vp, vp, i64, C.POINTER(StepArgs), vp,
                                           C.POINTER(StepOut)]),
         "pfc_gpu_sync": (C.c_int, [vp, C.POINTER(StepOut)]),
@@ -455,6 +457,33 @@ class CenterShards:
         tr = CollectiveTrace(out.allgather_bytes, out.reduce_scalar_bytes, out.reduce_grad_bytes,
                              out.reduce_ops)
         return StepResult(out.loss, dx, tr, [])
+
+    def step_features(self, features_dxb, labels, cfg: StepConfig, iteration_rng: SeededRng,
+                      out=None) -> StepResult:
+        """pfc_gpu_step_features: the drop-in step on a FeatureBatch already in device memory.
+        features_dxb is a contiguous D x B float64 CUDA tensor, labels an int64 CUDA tensor;
+        d_features go to ``out`` (D x B float64 CUDA tensor, allocated when None).  Same kernels and
+        results as step_host on the same values."""
+        import torch
+        if not (features_dxb.is_cuda and labels.is_cuda):
+            raise ContractError("step_features: features and labels must be CUDA tensors")
+        x = features_dxb.contiguous()
+        lab = labels.contiguous()
+        if x.dtype != torch.float64 or lab.dtype != torch.int64:
+            raise ShapeError("step_features: features float64, labels int64")
+        if x.dim() != 2 or x.shape[1] != lab.shape[0]:
+            raise ShapeError("FeatureBatch: label count != feature columns")
+        if x.shape[0] != self.dim:
+            raise ShapeError(f"pfc_gpu: feature dim {x.shape[0]} != {self.dim}")
+        dx = torch.empty_like(x) if out is None else out
+        so = StepOut()
+        args = StepArgs(iteration_rng.seed, iteration_rng.stream_id, cfg.lr, cfg.step_index)
+        torch.cuda.current_stream().synchronize()  # the library works on its own stream
+        _check(_lib.pfc_gpu_step_features(self._h, x.data_ptr(), lab.data_ptr(), lab.shape[0],
+                                          C.byref(args), dx.data_ptr(), C.byref(so)), self._h)
+        tr = CollectiveTrace(so.allgather_bytes, so.reduce_scalar_bytes, so.reduce_grad_bytes,
+                             so.reduce_ops)
+        return StepResult(so.loss, dx, tr, [])
 
     def diagnostics(self, features_dxb: np.ndarray, labels, conflict: ConflictInfo | None = None
                     ) -> DiagnosticsSnapshot:

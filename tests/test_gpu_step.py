@@ -305,6 +305,45 @@ def test_pinned_host_step_equals_pageable(port):
     sh.close()
 
 
+def test_device_featurebatch_step_equals_host_step(port):
+    """pfc_gpu_step_features (FeatureBatch in device memory, the trainer integration's entry)
+    gives the same bits as the host drop-in over several steps; device-detected label and
+    capacity errors carry the reference's text."""
+    C_, K, D, B = 9000, 3, 128, 160
+    outs = []
+    for dev in (False, True):
+        cfg = p.StepConfig(r=0.2, margin=p.MarginConfig.cosface_style())
+        sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B)
+        sh.init_center_shards(3)
+        res = []
+        for step in range(3):
+            X, labels = port.bench_inputs(C_, D, B, 1, step)
+            cfg.lr = 0.05 * (step + 1)
+            rng = p.SeededRng(1, p.make_stream("iteration", step))
+            if dev:
+                r = sh.step_features(torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda(),
+                                     cfg, rng)
+                res.append((r.loss, r.d_features.cpu().numpy()))
+            else:
+                r = sh.step_host(X, labels, cfg, rng)
+                res.append((r.loss, r.d_features.copy()))
+        res.append(sh.get_shard(1))
+        outs.append(res)
+        sh.close()
+    for a, b in zip(outs[0][:3], outs[1][:3]):
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    assert np.array_equal(outs[0][3][0], outs[1][3][0]) and np.array_equal(outs[0][3][1], outs[1][3][1])
+    cfg = p.StepConfig(r=0.1)
+    sh = p.CenterShards(p.ShardLayout(1000, 4), 8, cfg, max_batch=125)
+    sh.init_center_shards(1)
+    x = torch.zeros(8, 125, dtype=torch.float64, device="cuda")
+    with pytest.raises(p.CapacityError, match="shard 0 received 32 distinct positives"):
+        sh.step_features(x, torch.arange(125, dtype=torch.int64, device="cuda") * 8, cfg, p.SeededRng(1, 1))
+    with pytest.raises(p.ContractError, match="label 1000 outside"):
+        sh.step_features(x, torch.full((125,), 1000, dtype=torch.int64, device="cuda"), cfg, p.SeededRng(1, 1))
+    sh.close()
+
+
 def test_async_device_steps_report_errors_on_sync():
     C_, K, D, B = 1000, 4, 64, 8
     cfg = p.StepConfig(r=0.1)

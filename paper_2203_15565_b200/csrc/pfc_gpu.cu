@@ -131,6 +131,10 @@ constexpr int kFwdNWG = PFC_FWD_NWG;  // logits GEMM epilogue warpgroups (kFwdBN
 #ifndef PFC_DX_CG
 #define PFC_DX_CG 1
 #endif
+#ifndef PFC_FWD_STAGES
+#define PFC_FWD_STAGES 4
+#endif
+constexpr int kFwdStages = PFC_FWD_STAGES;  // logits GEMM operand ring depth
 constexpr int kFwdCG = PFC_FWD_CG;  // logits GEMM: 1 = one CTA per 128-row tile, 2 = CTA pair
 constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
 #ifndef PFC_DIAG_CG
@@ -481,7 +485,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     auto go = [&](auto e) {
       if constexpr (kUmma)
-        return launch_umma<kFwdBN, 4, kFwdNWG, false, false, decltype(e), kFwdCG>(c, c->tm_x_k, c->tm_w_k, gf, e);
+        return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), kFwdCG>(c, c->tm_x_k, c->tm_w_k, gf, e);
       else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
                                             (const float*)c->wh, (int)c->Dp, gf, e);
     };

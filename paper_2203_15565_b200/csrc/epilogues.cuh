@@ -103,15 +103,6 @@ struct alignas(64) FwdEpi : NoSetup {
     for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32, ++kk) {
       float v[32];
       src.load(c0, v);
-#if defined(PFC_FWD_PROBE) && PFC_FWD_PROBE == 1  // timing probe: TMEM read only
-      {
-        float s0 = 0.f;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) s0 += v[q];
-        sum += s0;
-        continue;
-      }
-#endif
       const int colb = t.col0 + c0;
       if (colb >= ncols) {  // uniform: past the buffer (an empty group keeps the TMA ring even)
         if (kTma && lane == 0) pfc_sm100::bulk_commit();
@@ -133,9 +124,6 @@ struct alignas(64) FwdEpi : NoSetup {
           sum += s1 + s2;
           any = true;
           done = true;
-#if defined(PFC_FWD_PROBE) && PFC_FWD_PROBE == 2  // timing probe: TMEM read + exp + sums
-          continue;
-#endif
         }
       }
       if (!done) {
@@ -194,9 +182,7 @@ struct alignas(64) FwdEpi : NoSetup {
         pfc_sm100::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-#if !(defined(PFC_FWD_PROBE) && PFC_FWD_PROBE == 3)  // timing probe 3: everything but the store
           pfc_sm100::tma_store_2d(&tm, sb, t.row0 + wig * 32, colb);
-#endif
           pfc_sm100::bulk_commit();
         }
       } else if (rv) {

@@ -141,7 +141,6 @@ constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
 #define PFC_DIAG_CG 1
 #endif
 constexpr int kDiagCG = PFC_DIAG_CG;  // diagnostics / mics screening GEMMs likewise
-constexpr int kNWG = 2;
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
 #endif   // epilogue warpgroups per CTA on the tcgen05 engine
@@ -434,7 +433,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- sampler (build_buffers, sampler.hpp:63-126)
   int P2 = 1;
   while (P2 < B) P2 <<= 1;
-  const size_t sort_smem = 2 * sizeof(int64_t) * (size_t)P2;  // keys + sorted unique labels
+  const size_t sort_smem = 2 * sizeof(int32_t) * (size_t)P2;  // keys + sorted unique labels
   static bool sort_cfg = false;
   if (!sort_cfg) {
     CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -18,13 +18,29 @@ namespace pfc {
 
 constexpr int kMaxSortBatch = 8192;
 
-__device__ __forceinline__ int lower_bound_i64(const int64_t* a, int n, int64_t v) {
+// first index with a[i] >= v in the sorted keys a[0..n)
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int64_t v) {
   int lo = 0, hi = n;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1; else hi = mid;
+    if ((int64_t)a[mid] < v) lo = mid + 1; else hi = mid;
   }
   return lo;
+}
+
+// minimum over the block (every thread gets it); red: 32 shared slots
+__device__ __forceinline__ int64_t block_min_i64(int64_t v, int64_t* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int64_t r = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = red[w] < r ? red[w] : r;
+  __syncthreads();
+  return r;
 }
 
 // Exclusive block scan of one int per thread (blockDim.x == 1024).
@@ -62,12 +78,31 @@ __global__ void __launch_bounds__(1024) positives_kernel(
     int nk, int64_t* __restrict__ uniq, ShardMeta* __restrict__ meta,
     int32_t* __restrict__ buf_cls, int32_t* __restrict__ pos_col, StepStatus* st,
     int force_sequential) {
-  extern __shared__ int64_t keys[];
+  extern __shared__ int32_t keys[];  // dynamic smem = 2 x P keys (P = B rounded up to a power of 2)
   __shared__ int warp_tmp[32];
   __shared__ int nuniq_s;
+  __shared__ int64_t red[32];
   const int64_t* __restrict__ labels = sp->labels;
   if (B > kMaxSortBatch) {
     if (threadIdx.x == 0) st->batch_too_large = 1;
+    return;
+  }
+  // validation (sampler.hpp:72-78) reports the first invalid label of the SORTED unique list:
+  // the smallest negative one, else the smallest one >= C.  With every label in [0, C),
+  // C < 2^31, the sort and the searches below run on 32-bit keys.
+  int64_t mn = INT64_MAX, mc = INT64_MAX;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    const int64_t y = labels[i];
+    mn = y < mn ? y : mn;
+    if (y >= C && y < mc) mc = y;
+  }
+  mn = block_min_i64(mn, red);
+  mc = block_min_i64(mc, red);
+  if (mn < 0 || mc != INT64_MAX) {
+    if (threadIdx.x == 0) {
+      st->label_oob = 1;
+      st->oob_label = mn < 0 ? mn : mc;
+    }
     return;
   }
   int P = 1;
@@ -75,10 +110,10 @@ __global__ void __launch_bounds__(1024) positives_kernel(
   if (P <= (int)blockDim.x) {
     // one key per thread: register bitonic sort, warp shuffles for partner distance < 32
     const int i = threadIdx.x;
-    int64_t key = i < B ? labels[i] : INT64_MAX;
+    int32_t key = i < B ? (int32_t)labels[i] : INT32_MAX;
     for (int k = 2; k <= P; k <<= 1) {
       for (int j = k >> 1; j > 0; j >>= 1) {
-        int64_t other;
+        int32_t other;
         if (j >= 32) {
           if (i < P) keys[i] = key;
           __syncthreads();
@@ -88,21 +123,20 @@ __global__ void __launch_bounds__(1024) positives_kernel(
           other = __shfl_xor_sync(0xffffffffu, key, j);
         }
         const bool asc = (i & k) == 0, lower = i < (i ^ j);
-        const int64_t lo = key < other ? key : other, hi = key < other ? other : key;
-        key = (asc == lower) ? lo : hi;
+        key = (asc == lower) ? min(key, other) : max(key, other);
       }
     }
     if (i < P) keys[i] = key;
     __syncthreads();
   } else {
-    for (int i = threadIdx.x; i < P; i += blockDim.x) keys[i] = i < B ? labels[i] : INT64_MAX;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) keys[i] = i < B ? (int32_t)labels[i] : INT32_MAX;
     __syncthreads();
     for (int k = 2; k <= P; k <<= 1) {
       for (int j = k >> 1; j > 0; j >>= 1) {
         for (int i = threadIdx.x; i < P; i += blockDim.x) {
           const int ixj = i ^ j;
           if (ixj > i) {
-            const int64_t a = keys[i], b = keys[ixj];
+            const int32_t a = keys[i], b = keys[ixj];
             const bool asc = (i & k) == 0;
             if (asc ? (a > b) : (a < b)) {
               keys[i] = b;
@@ -115,7 +149,7 @@ __global__ void __launch_bounds__(1024) positives_kernel(
     }
   }
   // unique (sorted) into shared memory: each thread owns a contiguous run of keys
-  int64_t* us = keys + P;  // dynamic smem = 2 x P keys (P = B rounded up to a power of two)
+  int32_t* us = keys + P;
   __shared__ int bad_shard_s;
   const int per = (B + blockDim.x - 1) / blockDim.x;
   const int beg = threadIdx.x * per, end = min(B, beg + per);
@@ -131,39 +165,26 @@ __global__ void __launch_bounds__(1024) positives_kernel(
   }
   __syncthreads();
   const int nu = nuniq_s;
-  if (threadIdx.x == 0) {
-    // validation in sorted order (sampler.hpp:72-78): negatives first, then >= C
-    int bad = -1;
-    if (nu > 0 && us[0] < 0) bad = 0;
-    else {
-      const int i = lower_bound_i64(us, nu, C);
-      if (i < nu) bad = i;
-    }
-    if (bad >= 0) {
-      st->label_oob = 1;
-      st->oob_label = us[bad];
-    }
-  }
   // capacity checks for ALL shards; the first failing shard in ascending order wins
   // (sampler.hpp:84-98)
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
-    const int np = lower_bound_i64(us, nu, hi) - lower_bound_i64(us, nu, lo);
+    const int np = lower_bound_i32(us, nu, hi) - lower_bound_i32(us, nu, lo);
     if (np > cap || hi - lo < cap) atomicMin(&bad_shard_s, k);
   }
   __syncthreads();
-  if (threadIdx.x == 0 && !st->label_oob && bad_shard_s < K) {
+  if (threadIdx.x == 0 && bad_shard_s < K) {
     const int k = bad_shard_s;
     const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
     st->capacity_shard = k;
-    st->capacity_npos = lower_bound_i64(us, nu, hi) - lower_bound_i64(us, nu, lo);
+    st->capacity_npos = lower_bound_i32(us, nu, hi) - lower_bound_i32(us, nu, lo);
   }
   __syncthreads();
-  if (st->label_oob || st->capacity_shard >= 0) return;
+  if (bad_shard_s < K) return;
   for (int kk = threadIdx.x; kk < nk; kk += blockDim.x) {
     const int k = k0 + kk;
     const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
-    const int us0 = lower_bound_i64(us, nu, lo), ue = lower_bound_i64(us, nu, hi);
+    const int us0 = lower_bound_i32(us, nu, lo), ue = lower_bound_i32(us, nu, hi);
     ShardMeta m;
     m.lo = lo;
     m.hi = hi;
@@ -177,21 +198,21 @@ __global__ void __launch_bounds__(1024) positives_kernel(
   }
   // positives first, ascending (sampler.hpp:100-104)
   for (int i = threadIdx.x; i < nu; i += blockDim.x) {
-    const int64_t y = us[i];
-    const int k = (int)(y / blk);
+    const int32_t y = us[i];
+    const int k = (int)((uint32_t)y / (uint32_t)blk);
     if (k >= k0 && k < k0 + nk) {
       const int64_t lo = min((int64_t)k * blk, C);
-      const int u0 = lower_bound_i64(us, nu, lo);
-      buf_cls[(int64_t)(k - k0) * cap + (i - u0)] = (int32_t)y;
+      const int u0 = lower_bound_i32(us, nu, lo);
+      buf_cls[(int64_t)(k - k0) * cap + (i - u0)] = y;
     }
   }
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    const int64_t y = labels[b];
-    const int k = (int)(y / blk);
+    const int32_t y = (int32_t)labels[b];
+    const int k = (int)((uint32_t)y / (uint32_t)blk);
     int col = -1;
     if (k >= k0 && k < k0 + nk) {
       const int64_t lo = min((int64_t)k * blk, C);
-      col = (k - k0) * cap + (lower_bound_i64(us, nu, y) - lower_bound_i64(us, nu, lo));
+      col = (k - k0) * cap + (lower_bound_i32(us, nu, y) - lower_bound_i32(us, nu, lo));
     }
     pos_col[b] = col;
   }

@@ -143,7 +143,7 @@ constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
 constexpr int kDiagCG = PFC_DIAG_CG;  // diagnostics / mics screening GEMMs likewise
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
-#endif   // epilogue warpgroups per CTA on the tcgen05 engine
+#endif  // dW GEMM operand ring depth (2: leaves shared memory to the W / momentum ring)
 constexpr int kSimtBN = 64;
 
 struct PhaseTimer {

@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128 * NWG * CG);  // CG = 2: both CTAs' epilogues release the leader
+      // CG = 1: every epilogue thread arrives locally.  CG = 2: both CTAs' epilogues release the
+      // leader, one remote arrive per warp (a cluster-scope release per thread costs a fence each)
+      mbar_init(&tempty[i], CG == 2 ? 2 * 4 * NWG : 128 * NWG);
     }
     epi.setup(epi_smem);
     fence_barrier_init();
@@ -262,8 +264,12 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
       else
         epi.template run<BN, NWG>(ti, src, row, wg, wsm, pre);
       tc_fence_before();
-      if constexpr (CG == 2) mbar_arrive_cluster(tempty_c + as * 8u);
-      else mbar_arrive(&tempty[as]);
+      if constexpr (CG == 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_c + as * 8u);
+      } else {
+        mbar_arrive(&tempty[as]);
+      }
       pre = pre_n;
       pre_n = pre_n2;
     }

@@ -234,7 +234,7 @@ struct Ctx {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
     cudaGraphNode_t gbegin = nullptr;
-    cudaGraphNode_t cp_lab = nullptr, cp_x = nullptr, cp_dx = nullptr;  // slot 1 memcpy nodes
+    cudaGraphNode_t cp_x = nullptr, cp_dx = nullptr;  // slot 1 memcpy nodes
     const void* cp_ptr[3] = {nullptr, nullptr, nullptr};  // host pointers the nodes hold
     int64_t gB = -1;
     int64_t glaunches = 0;
@@ -411,9 +411,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const int bs = 256;
   if (int rc = ensure_maps(c, B)) return rc;
   const bool e2e = c->e2e.on;
-  if (e2e)
-    CUDA_TRY(c, cudaMemcpyAsync(c->labels, c->e2e.lab_h, sizeof(int64_t) * B,
-                                cudaMemcpyHostToDevice, s));
+  // (host drop-in: `lab` is the caller's page-locked labels, read by the sampler over PCIe)
   step_begin_kernel<<<1, 32, 0, s>>>(c->st, c->sp, a->seed, a->stream_id, (float)a->lr,
                                      c->reset_status ? 1 : 0, x, lab, dx_full);
   c->launches++;
@@ -433,11 +431,12 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- sampler (build_buffers, sampler.hpp:63-126)
   int P2 = 1;
   while (P2 < B) P2 <<= 1;
-  const size_t sort_smem = 2 * sizeof(int32_t) * (size_t)P2;  // keys + sorted unique labels
+  // keys + sorted unique labels (int32) + the staged batch labels (int64)
+  const size_t sort_smem = (2 * sizeof(int32_t) + sizeof(int64_t)) * (size_t)P2;
   static bool sort_cfg = false;
   if (!sort_cfg) {
     CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(2 * sizeof(int64_t) * kMaxSortBatch)));
+                                     (int)((2 * sizeof(int32_t) + sizeof(int64_t)) * kMaxSortBatch)));
     sort_cfg = true;
   }
   positives_kernel<<<1, 1024, sort_smem, s>>>(
@@ -572,6 +571,10 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(c->e2e.dxdb_h, c->xdb, sizeof(double) * B * c->D,
                                 cudaMemcpyDeviceToHost, c->s2));
+    // the step status is final after dx_finalize (the dW GEMM only reads it): its download rides
+    // the same copy stream instead of trailing the step
+    CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost,
+                                c->s2));
     CUDA_TRY(c, cudaEventRecord(c->ev_out, c->s2));
   }
   phase(c, "dx_gemm");
@@ -656,15 +659,14 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
     CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &n));
     std::vector<cudaGraphNode_t> nodes(n);
     CUDA_TRY(c, cudaGraphGetNodes(g, nodes.data(), &n));
-    G.gbegin = G.cp_lab = G.cp_x = G.cp_dx = nullptr;
+    G.gbegin = G.cp_x = G.cp_dx = nullptr;
     for (cudaGraphNode_t nd : nodes) {
       cudaGraphNodeType ty;
       cudaGraphNodeGetType(nd, &ty);
       if (ty == cudaGraphNodeTypeMemcpy) {  // the host drop-in's copies (slot 1)
         cudaMemcpy3DParms mp{};
         if (cudaGraphMemcpyNodeGetParams(nd, &mp) != cudaSuccess) continue;
-        if (mp.dstPtr.ptr == c->labels) G.cp_lab = nd;
-        else if (mp.dstPtr.ptr == c->xdb) G.cp_x = nd;
+        if (mp.dstPtr.ptr == c->xdb) G.cp_x = nd;
         else if (mp.srcPtr.ptr == c->xdb) G.cp_dx = nd;
         continue;
       }
@@ -675,7 +677,7 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
         G.gbegin = nd;
     }
     if (!G.gbegin) return fail(c, PFC_ERR_CUDA, "graph capture lost the step_begin node");
-    if (c->e2e.on && (!G.cp_lab || !G.cp_x || !G.cp_dx))
+    if (c->e2e.on && (!G.cp_x || !G.cp_dx))
       return fail(c, PFC_ERR_CUDA, "graph capture lost a host copy node");
     G.gB = B;
     G.glaunches = c->launches;
@@ -697,9 +699,6 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
   kp.extra = nullptr;
   CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(G.gexec, G.gbegin, &kp));
   if (c->e2e.on) {  // re-point the copy nodes when the caller's host buffers changed
-    if (G.cp_ptr[0] != c->e2e.lab_h)
-      CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_lab, c->labels, c->e2e.lab_h,
-                                                     sizeof(int64_t) * B, cudaMemcpyHostToDevice));
     if (G.cp_ptr[1] != c->e2e.xdb_h)
       CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_x, c->xdb, c->e2e.xdb_h,
                                                      sizeof(double) * B * c->D,
@@ -708,7 +707,6 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
       CUDA_TRY(c, cudaGraphExecMemcpyNodeSetParams1D(G.gexec, G.cp_dx, c->e2e.dxdb_h, c->xdb,
                                                      sizeof(double) * B * c->D,
                                                      cudaMemcpyDeviceToHost));
-    G.cp_ptr[0] = c->e2e.lab_h;
     G.cp_ptr[1] = c->e2e.xdb_h;
     G.cp_ptr[2] = c->e2e.dxdb_h;
   }
@@ -1401,6 +1399,16 @@ int pfc_gpu_device_state(void* ctx, float** w, float** m, int64_t* rows) {
 
 void* pfc_gpu_stream(void* ctx) { return static_cast<Ctx*>(ctx)->stream; }
 
+// the device-side address of page-locked host memory (the same address under UVA)
+static const int64_t* dev_view(const int64_t* h) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess || !at.devicePointer) {
+    cudaGetLastError();
+    return h;
+  }
+  return static_cast<const int64_t*>(at.devicePointer);
+}
+
 // page-locked (or registered) host memory: eligible for copies inside the captured step
 static bool pinned(const void* p) {
   cudaPointerAttributes at{};
@@ -1443,11 +1451,10 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
     // the same checks and skips every update on failure, so launching first is safe.
     // On an error the contents of dxdb are unspecified (the reference throws instead).
     c->e2e = {true, xdb, labels, dxdb};
-    const int rc = run_step(c, c->X, c->labels, B, a, c->dX);
+    const int rc = run_step(c, c->X, dev_view(labels), B, a, c->dX);
     c->e2e.on = false;
     if (rc) return rc;
-    c->reset_status = true;
-    CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
+    c->reset_status = true;  // the status download is part of the step (run_pipeline)
     const int vrc = host_validate(c, labels, B);
     CUDA_TRY(c, cudaStreamSynchronize(s));
     if (int rc2 = finish_phase_timing(c)) return rc2;

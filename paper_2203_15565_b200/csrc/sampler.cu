@@ -78,21 +78,27 @@ __global__ void __launch_bounds__(1024) positives_kernel(
     int nk, int64_t* __restrict__ uniq, ShardMeta* __restrict__ meta,
     int32_t* __restrict__ buf_cls, int32_t* __restrict__ pos_col, StepStatus* st,
     int force_sequential) {
-  extern __shared__ int32_t keys[];  // dynamic smem = 2 x P keys (P = B rounded up to a power of 2)
+  // dynamic smem: keys[P] and the sorted unique labels us[P] (int32), then the batch labels[P]
+  // (int64), staged once: in the host drop-in they are read from the caller's page-locked buffer
+  // over PCIe (P = B rounded up to a power of 2)
+  extern __shared__ int32_t keys[];
   __shared__ int warp_tmp[32];
   __shared__ int nuniq_s;
   __shared__ int64_t red[32];
-  const int64_t* __restrict__ labels = sp->labels;
   if (B > kMaxSortBatch) {
     if (threadIdx.x == 0) st->batch_too_large = 1;
     return;
   }
+  int P = 1;
+  while (P < B) P <<= 1;
+  int64_t* labels = reinterpret_cast<int64_t*>(keys + 2 * P);
   // validation (sampler.hpp:72-78) reports the first invalid label of the SORTED unique list:
   // the smallest negative one, else the smallest one >= C.  With every label in [0, C),
   // C < 2^31, the sort and the searches below run on 32-bit keys.
   int64_t mn = INT64_MAX, mc = INT64_MAX;
   for (int i = threadIdx.x; i < B; i += blockDim.x) {
-    const int64_t y = labels[i];
+    const int64_t y = sp->labels[i];
+    labels[i] = y;
     mn = y < mn ? y : mn;
     if (y >= C && y < mc) mc = y;
   }
@@ -105,8 +111,6 @@ __global__ void __launch_bounds__(1024) positives_kernel(
     }
     return;
   }
-  int P = 1;
-  while (P < B) P <<= 1;
   if (P <= (int)blockDim.x) {
     // one key per thread: register bitonic sort, warp shuffles for partner distance < 32
     const int i = threadIdx.x;

@@ -103,6 +103,107 @@ __global__ void upd_d(float* __restrict__ W, float* __restrict__ M, const float*
   }
 }
 
+// (e) W and momentum interleaved per row: WM[r][2][D] (one 4 KB span per row), grouped loads
+template <int U, bool kF4>  // kF4: float4-interleaved WM[r][D/4][2] instead
+__global__ void upd_e(float* __restrict__ WM, const float* __restrict__ src,
+                      const int* __restrict__ rows, int n, float lr) {
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int sub = lane >> 3, q = (lane & 7) * 4;
+  constexpr int RB = 4 * U;
+  for (int blk = warp; blk < n / RB * (D / 32); blk += nw) {
+    const int r0 = (blk / (D / 32)) * RB, d = (blk % (D / 32)) * 32 + q;
+    float4 w[U], m[U], a[U];
+    size_t ow[U], om[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int rr = r0 + u * 4 + sub;
+      const size_t base = (size_t)__ldg(rows + rr) * 2 * D;
+      ow[u] = kF4 ? base + (size_t)d * 2 : base + d;
+      om[u] = kF4 ? ow[u] + 4 : base + D + d;
+      w[u] = *reinterpret_cast<const float4*>(WM + ow[u]);
+      m[u] = *reinterpret_cast<const float4*>(WM + om[u]);
+      a[u] = __ldg(reinterpret_cast<const float4*>(src + (size_t)rr * D + d));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      m[u].x = 0.9f * m[u].x + a[u].x; m[u].y = 0.9f * m[u].y + a[u].y;
+      m[u].z = 0.9f * m[u].z + a[u].z; m[u].w = 0.9f * m[u].w + a[u].w;
+      w[u].x -= lr * m[u].x; w[u].y -= lr * m[u].y; w[u].z -= lr * m[u].z; w[u].w -= lr * m[u].w;
+      *reinterpret_cast<float4*>(WM + ow[u]) = w[u];
+      *reinterpret_cast<float4*>(WM + om[u]) = m[u];
+    }
+  }
+}
+
+// (f) the dW epilogue's ownership: a warp owns 8 rows x 256 dims (one CTA's half of each row; the
+// other half is the adjacent warp's).  kRowMajor = false: chunk-major (all 8 rows' 128 B chunk c,
+// then c+1: the current epilogue order, NR rows per batch of loads); true: row-major (a row's
+// whole 1 KB span per step: lanes cover 256 dims with 2 float4 each, NR rows per batch).
+template <bool kRowMajor, int NR>
+__global__ void upd_f(float* __restrict__ W, float* __restrict__ M, const float* __restrict__ src,
+                      const int* __restrict__ rows, int n, float lr) {
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int blk = warp; blk < n / 8 * 2; blk += nw) {
+    const int r0 = (blk >> 1) * 8, h = (blk & 1) * 256;
+    if (!kRowMajor) {
+      const int sub = lane >> 3, q = (lane & 7) * 4;  // 4 rows x 32 dims per op
+      for (int c = 0; c < 8; ++c) {
+        const int d = h + c * 32 + q;
+        float4 w[2], m[2], a[2];
+        size_t o[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int rr = r0 + u * 4 + sub;
+          o[u] = (size_t)__ldg(rows + rr) * D + d;
+          w[u] = *reinterpret_cast<const float4*>(W + o[u]);
+          m[u] = *reinterpret_cast<const float4*>(M + o[u]);
+          a[u] = __ldg(reinterpret_cast<const float4*>(src + (size_t)rr * D + d));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          m[u].x = 0.9f * m[u].x + a[u].x; m[u].y = 0.9f * m[u].y + a[u].y;
+          m[u].z = 0.9f * m[u].z + a[u].z; m[u].w = 0.9f * m[u].w + a[u].w;
+          w[u].x -= lr * m[u].x; w[u].y -= lr * m[u].y; w[u].z -= lr * m[u].z; w[u].w -= lr * m[u].w;
+          *reinterpret_cast<float4*>(W + o[u]) = w[u];
+          *reinterpret_cast<float4*>(M + o[u]) = m[u];
+        }
+      }
+    } else {
+      for (int r1 = 0; r1 < 8; r1 += NR) {
+        float4 w[NR][2], m[NR][2], a[NR][2];
+        size_t o[NR][2];
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+          const int rr = r0 + r1 + u;
+          const size_t base = (size_t)__ldg(rows + rr) * D + h;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int d = k * 128 + lane * 4;
+            o[u][k] = base + d;
+            w[u][k] = *reinterpret_cast<const float4*>(W + o[u][k]);
+            m[u][k] = *reinterpret_cast<const float4*>(M + o[u][k]);
+            a[u][k] = __ldg(reinterpret_cast<const float4*>(src + (size_t)rr * D + h + d));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < NR; ++u)
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            float4& mm = m[u][k];
+            float4& ww = w[u][k];
+            const float4& aa = a[u][k];
+            mm.x = 0.9f * mm.x + aa.x; mm.y = 0.9f * mm.y + aa.y; mm.z = 0.9f * mm.z + aa.z; mm.w = 0.9f * mm.w + aa.w;
+            ww.x -= lr * mm.x; ww.y -= lr * mm.y; ww.z -= lr * mm.z; ww.w -= lr * mm.w;
+            *reinterpret_cast<float4*>(W + o[u][k]) = ww;
+            *reinterpret_cast<float4*>(M + o[u][k]) = mm;
+          }
+      }
+    }
+  }
+}
+
 int main() {
   const int C = 2000000, n = 200000;
   float *W, *M, *src;
@@ -111,6 +212,9 @@ int main() {
   cudaMalloc(&M, (size_t)C * D * 4);
   cudaMalloc(&src, (size_t)n * D * 4);
   cudaMalloc(&rows, n * 4);
+  float* WM;  // interleaved W + momentum for (e): same 8.2 GB as W and M together
+  cudaMalloc(&WM, (size_t)C * 2 * D * 4);
+  cudaMemset(WM, 0, (size_t)C * 2 * D * 4);
   cudaMemset(W, 0, (size_t)C * D * 4);
   cudaMemset(M, 0, (size_t)C * D * 4);
   cudaMemset(src, 0, (size_t)n * D * 4);
@@ -156,6 +260,25 @@ int main() {
     run("spread G=8 16warps/SM", upd_d<8>, 148, 512);
     run("spread G=32 16warps/SM", upd_d<32>, 148, 512);
     run("spread G=128 16warps/SM", upd_d<128>, 148, 512);
+    run("dW ownership chunk-major 16warps/SM", upd_f<false, 1>, 148, 512);
+    run("dW ownership row-major NR=1 16warps/SM", upd_f<true, 1>, 148, 512);
+    run("dW ownership row-major NR=2 16warps/SM", upd_f<true, 2>, 148, 512);
+    run("dW ownership row-major NR=4 16warps/SM", upd_f<true, 4>, 148, 512);
+    auto run_e = [&](const char* name, auto kern, int blocks, int threads) {
+      for (int i = 0; i < 3; ++i) kern<<<blocks, threads>>>(WM, src, rows, n, 0.1f);
+      cudaEventRecord(e0);
+      for (int i = 0; i < 10; ++i) kern<<<blocks, threads>>>(WM, src, rows, n, 0.1f);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= 10;
+      printf("%s: %.1f us  %.0f GB/s\n", name, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+    };
+    run_e("interleaved [r][2][D] U=4 16warps/SM", upd_e<4, false>, 148, 512);
+    run_e("interleaved [r][2][D] U=8 16warps/SM", upd_e<8, false>, 148, 512);
+    run_e("interleaved [r][D/4][2] U=4 16warps/SM", upd_e<4, true>, 148, 512);
+    run_e("interleaved [r][D/4][2] U=8 16warps/SM", upd_e<8, true>, 148, 512);
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }

@@ -99,15 +99,64 @@ struct alignas(64) FwdEpi : NoSetup {
     ST sum = ST(0);
     bool any = false;
     int kk = 0;
+    // fragment path (tcgen05 engine, no filter): per-thread partial sums of rows t/4, t/4 + 8,
+    // 16 + t/4, 24 + t/4 of the warp's 32 rows (t = lane)
+    float qs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
     for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32, ++kk) {
-      float v[32];
-      src.load(c0, v);
       const int colb = t.col0 + c0;
       if (colb >= ncols) {  // uniform: past the buffer (an empty group keeps the TMA ring even)
         if (kTma && lane == 0) pfc_sm100::bulk_commit();
         continue;
       }
+      if constexpr (kTma && std::is_same<ST, float>::value && !kFilter) {
+        // 32 valid negatives in every row of the warp: read the accumulator in the MMA-fragment
+        // layout (tcgen05.ld 16x256b), whose bf16x2 pairs are stmatrix.trans operands, so the
+        // E^T staging needs no shuffles (stmatrix stores class rows of 8 b values)
+        if (__all_sync(0xffffffffu, colb + 32 <= ncols && (unsigned)(pc - colb) >= 32u)) {
+          uint32_t ra[16], rb[16];
+          pfc_sm100::tmem_ld_16x256b_x4(src.taddr + (uint32_t)c0, ra);
+          pfc_sm100::tmem_ld_16x256b_x4(src.taddr + (16u << 16) + (uint32_t)c0, rb);
+          pfc_sm100::tmem_wait_ld();
+          uint32_t pa[8], pb[8];  // [2j + h]: rows (h ? t/4 + 8 : t/4) (+16 for pb), classes 8j..
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = i >> 1, h = i & 1;
+            const float a0 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(ra[4 * j + 2 * h]), A, -O));
+            const float a1 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(ra[4 * j + 2 * h + 1]), A, -O));
+            const float b0 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(rb[4 * j + 2 * h]), A, -O));
+            const float b1 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(rb[4 * j + 2 * h + 1]), A, -O));
+            qs[h] += a0 + a1;
+            qs[2 + h] += b0 + b1;
+            __nv_bfloat162 x = __floats2bfloat162_rn(a0, a1), y = __floats2bfloat162_rn(b0, b1);
+            pa[i] = *reinterpret_cast<uint32_t*>(&x);
+            pb[i] = *reinterpret_cast<uint32_t*>(&y);
+          }
+          uint8_t* sb = stage + (kk & 1) * 2048;
+          if (lane == 0) pfc_sm100::bulk_wait_read<1>();  // this buffer's store, 2 groups ago
+          __syncwarp();
+          // stmatrix j: matrices i = (rows 0-7, 8-15, 16-23, 24-31) x classes 8j..8j+7; thread
+          // 8i + r addresses class row 8j + r, b chunk i (16 B, swizzled by the class row)
+          const int mi = lane >> 3, mr = lane & 7;
+          const uint32_t sbase = pfc_sm100::smem_u32(sb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int q = 8 * j + mr;
+            pfc_sm100::stmatrix_x4_trans(sbase + q * 64 + ((mi ^ ((q >> 1) & 3)) << 4), pa[2 * j],
+                                         pa[2 * j + 1], pb[2 * j], pb[2 * j + 1]);
+          }
+          pfc_sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            pfc_sm100::tma_store_2d(&tm, sb, t.row0 + wig * 32, colb);
+            pfc_sm100::bulk_commit();
+          }
+          any = true;
+          continue;
+        }
+      }
+      float v[32];
+      src.load(c0, v);
       float e[32];
       const int jp = pc - colb;
       bool done = false;
@@ -191,6 +240,21 @@ struct alignas(64) FwdEpi : NoSetup {
         for (int q = 0; q < 32; ++q)
           if (colb + q < ncols) store_out1(E + (size_t)(colb + q) * lde + b, e[q]);
       }
+    }
+    if constexpr (kTma && std::is_same<ST, float>::value && !kFilter) {
+      // fragment-path sums: reduce over the quad, then row r (lane r) takes slot r / 8 of quad r % 8
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        qs[k] += __shfl_xor_sync(0xffffffffu, qs[k], 1);
+        qs[k] += __shfl_xor_sync(0xffffffffu, qs[k], 2);
+      }
+      float mine = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float v = __shfl_sync(0xffffffffu, qs[k], (lane & 7) * 4);
+        mine = (lane >> 3) == k ? v : mine;
+      }
+      sum += mine;
     }
     if (rv) {
       part_s[(size_t)(t.n_tile * NWG + wg) * B + b] = sum;

@@ -204,6 +204,48 @@ __global__ void upd_f(float* __restrict__ W, float* __restrict__ M, const float*
   }
 }
 
+// (g) the epilogue's actual ring depth: a warp owns 8 rows x 256 dims, chunk-major, with NC
+// consecutive 128 B chunks of its 8 rows in flight (the cp.async ring holds ~6), W and momentum
+// only (dwt comes from TMEM in the kernel); traffic counted as 4 streams
+template <int NC>
+__global__ void upd_g(float* __restrict__ W, float* __restrict__ M, const int* __restrict__ rows,
+                      int n, float lr) {
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int sub = lane >> 3, q = (lane & 7) * 4;
+  for (int blk = warp; blk < n / 8 * 2; blk += nw) {
+    const int r0 = (blk >> 1) * 8, h = (blk & 1) * 256;
+    size_t rb[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) rb[u] = (size_t)__ldg(rows + r0 + u * 4 + sub) * D + h + q;
+    for (int c0 = 0; c0 < 8; c0 += NC) {
+      float4 w[NC][2], m[NC][2];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (c0 + c < 8) {
+            w[c][u] = *reinterpret_cast<const float4*>(W + rb[u] + (c0 + c) * 32);
+            m[c][u] = *reinterpret_cast<const float4*>(M + rb[u] + (c0 + c) * 32);
+          }
+        }
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (c0 + c < 8) {
+            float4& mm = m[c][u];
+            float4& ww = w[c][u];
+            mm.x = 0.9f * mm.x + 1e-3f; mm.y = 0.9f * mm.y + 1e-3f; mm.z = 0.9f * mm.z + 1e-3f; mm.w = 0.9f * mm.w + 1e-3f;
+            ww.x -= lr * mm.x; ww.y -= lr * mm.y; ww.z -= lr * mm.z; ww.w -= lr * mm.w;
+            *reinterpret_cast<float4*>(W + rb[u] + (c0 + c) * 32) = ww;
+            *reinterpret_cast<float4*>(M + rb[u] + (c0 + c) * 32) = mm;
+          }
+        }
+    }
+  }
+}
+
 int main() {
   const int C = 2000000, n = 200000;
   float *W, *M, *src;
@@ -264,6 +306,22 @@ int main() {
     run("dW ownership row-major NR=1 16warps/SM", upd_f<true, 1>, 148, 512);
     run("dW ownership row-major NR=2 16warps/SM", upd_f<true, 2>, 148, 512);
     run("dW ownership row-major NR=4 16warps/SM", upd_f<true, 4>, 148, 512);
+    auto run_g = [&](const char* name, auto kern) {
+      const double b4 = (double)n * D * 4 * 4;
+      for (int i = 0; i < 3; ++i) kern<<<148, 512>>>(W, M, rows, n, 0.1f);
+      cudaEventRecord(e0);
+      for (int i = 0; i < 10; ++i) kern<<<148, 512>>>(W, M, rows, n, 0.1f);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= 10;
+      printf("%s: %.1f us  %.0f GB/s\n", name, ms * 1e3, b4 / (ms * 1e-3) / 1e9);
+    };
+    run_g("ring emulation W+M chunk-major NC=1 16warps/SM", upd_g<1>);
+    run_g("ring emulation W+M chunk-major NC=2 16warps/SM", upd_g<2>);
+    run_g("ring emulation W+M chunk-major NC=4 16warps/SM", upd_g<4>);
+    run_g("ring emulation W+M chunk-major NC=8 (whole row) 16warps/SM", upd_g<8>);
     auto run_e = [&](const char* name, auto kern, int blocks, int threads) {
       for (int i = 0; i < 3; ++i) kern<<<blocks, threads>>>(WM, src, rows, n, 0.1f);
       cudaEventRecord(e0);

@@ -141,6 +141,12 @@ constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
 #define PFC_DIAG_CG 1
 #endif
 constexpr int kDiagCG = PFC_DIAG_CG;  // diagnostics / mics screening GEMMs likewise
+#ifndef PFC_DW_ROW
+#define PFC_DW_ROW 0  // 1: dW epilogue with a row-major W / momentum stream (DwRowEpi)
+#endif
+#ifndef PFC_DWR_STAGES
+#define PFC_DWR_STAGES 2  // operand stages of the DwRowEpi GEMM (32 KB each)
+#endif
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
 #endif  // dW GEMM operand ring depth (2: leaves shared memory to the W / momentum ring)
@@ -584,6 +590,15 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
     cudaError_t err;
     if constexpr (kUmma) {
+#if PFC_DW_ROW
+      if (c->D > 384 && c->D <= 512) {  // row-major W / momentum stream, 4-CTA clusters
+        const GemmGeom gw4 = make_geom((int)c->ncols, (int)c->D, (int)B, 128, 1, 1);
+        err = launch_umma<128, PFC_DWR_STAGES, 4, false, true>(
+            c, c->tm_e_k, c->tm_xs_mn, gw4,
+            DwRowEpi{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr, c->W,
+                     c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay, c->st});
+      } else
+#endif
       if (gw.n_tiles == 2)
         err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,

@@ -586,7 +586,7 @@ struct DwUpdateEpi {
 // against 0.46 ms for DwUpdateEpi. Per tile it is bound by instruction latency (row-by-row
 // dependent waits, warp reductions, ring address arithmetic), not by the memory order; see DESIGN.md.
 #ifndef PFC_DWR_SLOTS
-#define PFC_DWR_SLOTS 9
+#define PFC_DWR_SLOTS 8
 #endif
 struct DwRowEpi {
   static constexpr int kCluster = 4;
@@ -595,7 +595,11 @@ struct DwRowEpi {
   static constexpr int kItems = 3 * kRows;         // W row i (dot pass), then W row i + momentum row i
   static constexpr int kSlots = PFC_DWR_SLOTS;     // ring slots of 512 B
   static constexpr int kAhead = kSlots - 1;        // items in flight after the consumed one
-  static_assert(kAhead <= kItems, "DwRowEpi ring");
+  // rows per ring wait: dot pass kGD rows (kGD items), update pass kGU rows (2 kGU items)
+  static constexpr int kGD = kAhead >= 4 ? 4 : (kAhead >= 2 ? 2 : 1);
+  static constexpr int kGU = kAhead >= 4 ? 2 : 1;
+  static_assert(kAhead >= 2 && kAhead <= kItems, "DwRowEpi ring");
+  static_assert(kItems % kSlots == 0, "slot of item k is k % kSlots in every tile");
   static constexpr int kStageBytes = kRows * 128 * 4;       // dwt rows, float4 columns XOR-swizzled
   static constexpr int kRingBytes = kSlots * 512;
   static constexpr int kScalarBytes = 2 * 3 * kRows * 4;    // [2 tile parity][inv | row | pslot]
@@ -681,7 +685,6 @@ struct DwRowEpi {
     const bool dv = d < D;
     // item k of the stream (k >= kItems: the next tile's item k - kItems; an empty group when
     // there is none): W row k (k < 8), else W (even) / momentum (odd) row (k - 8) / 2
-    const int gbase = t.iter * kItems;
     auto issue = [&](int k) {
       const bool nx = k >= kItems;
       const int kk = nx ? k - kItems : k;
@@ -689,12 +692,12 @@ struct DwRowEpi {
       const bool mom = kk >= kRows && ((kk - kRows) & 1);
       const int r = nx ? s_row_n[r8] : s_row[r8];
       if (r >= 0 && dv)
-        pfc_sm100::cp_async16(ring_s + (uint32_t)(((gbase + k) % kSlots) * 512 + lane * 16),
+        pfc_sm100::cp_async16(ring_s + (uint32_t)((k % kSlots) * 512 + lane * 16),
                               (mom ? Mom : W) + (size_t)r * D + d);
       pfc_sm100::cp_async_commit();
     };
     auto slot4 = [&](int k) {
-      return *reinterpret_cast<const float4*>(ring + ((gbase + k) % kSlots) * 128 + lane * 4);
+      return *reinterpret_cast<const float4*>(ring + (k % kSlots) * 128 + lane * 4);
     };
     // dwt of this warp's rows, staged row-major: lane i's TMEM row is row 32q + 8wg + i
 #pragma unroll 1
@@ -722,18 +725,29 @@ struct DwRowEpi {
     };
     if (t.iter == 0)
       for (int k = 0; k < kAhead; ++k) issue(k);  // otherwise issued by the previous tile
-    // ---- dot pass: the CTA's quarter of w . dwt per row
+    // ---- dot pass: the CTA's quarter of w . dwt per row, GD rows per ring wait (independent
+    // FMA / shuffle chains)
     float dots[kRows];
 #pragma unroll
-    for (int i = 0; i < kRows; ++i) {
-      pfc_sm100::cp_async_wait<kAhead - 1>();
-      const float4 w = slot4(i);
-      issue(i + kAhead);
-      const float4 a = dwt4(i);
-      float p = dv ? a.x * w.x + a.y * w.y + a.z * w.z + a.w * w.w : 0.f;
+    for (int i0 = 0; i0 < kRows; i0 += kGD) {
+      pfc_sm100::cp_async_wait<kAhead - kGD>();  // items i0 .. i0 + kGD - 1 landed
+      float4 w[kGD];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-      dots[i] = p;
+      for (int j = 0; j < kGD; ++j) w[j] = slot4(i0 + j);
+#pragma unroll
+      for (int j = 0; j < kGD; ++j) issue(i0 + j + kAhead);  // refills the slots just read
+      float p[kGD];
+#pragma unroll
+      for (int j = 0; j < kGD; ++j) {
+        const float4 a = dwt4(i0 + j);
+        p[j] = dv ? a.x * w[j].x + a.y * w[j].y + a.z * w[j].z + a.w * w[j].w : 0.f;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < kGD; ++j) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
+#pragma unroll
+      for (int j = 0; j < kGD; ++j) dots[i0 + j] = p[j];
     }
     // ---- swap quarter-dots with the 3 peers; totals in rank order (identical on every CTA)
     float* hp = hq + par * 512;
@@ -757,34 +771,39 @@ struct DwRowEpi {
       for (int r = 0; r < 4; ++r) tot += (uint32_t)r == rank ? dots[i] : hp[r * 128 + rbase + i];
       rcp[i] = tot * s_inv[i];  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
     }
-    // ---- update pass: dW and the momentum-SGD update of the sampled rows
+    // ---- update pass: dW and the momentum-SGD update, GU rows (2 GU items) per ring wait
 #pragma unroll
-    for (int i = 0; i < kRows; ++i) {
-      const int k = kRows + 2 * i;
-      pfc_sm100::cp_async_wait<kAhead - 1>();
-      const float4 w4 = slot4(k);
-      pfc_sm100::cp_async_wait<kAhead - 2>();
-      const float4 m4 = slot4(k + 1);
-      issue(k + kAhead);
-      issue(k + 1 + kAhead);
-      const int r = s_row[i];
-      if (r < 0 || !dv) continue;
-      const float4 a4 = dwt4(i);
-      const float inv = s_inv[i], cpj = rcp[i];
-      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-      float wv[4] = {w4.x, w4.y, w4.z, w4.w};
-      float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+    for (int i0 = 0; i0 < kRows; i0 += kGU) {
+      const int k0 = kRows + 2 * i0;
+      pfc_sm100::cp_async_wait<kAhead - 2 * kGU>();
+      float4 wm[2 * kGU];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const float dw = (av[x] - cpj * (wv[x] * inv)) * inv;  // shardsim.hpp:382
-        const float g = dw + wd * wv[x];                       // shardsim.hpp:152-153
-        const float vv = mu * mv[x] + g;                       // shardsim.hpp:154
-        mv[x] = vv;
-        wv[x] = wv[x] - lr * vv;                               // shardsim.hpp:156
+      for (int j = 0; j < 2 * kGU; ++j) wm[j] = slot4(k0 + j);
+#pragma unroll
+      for (int j = 0; j < 2 * kGU; ++j) issue(k0 + j + kAhead);
+#pragma unroll
+      for (int jr = 0; jr < kGU; ++jr) {
+        const int i = i0 + jr;
+        const int r = s_row[i];
+        if (r < 0 || !dv) continue;
+        const float4 a4 = dwt4(i);
+        const float inv = s_inv[i], cpj = rcp[i];
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+        const float4 w4 = wm[2 * jr], m4 = wm[2 * jr + 1];
+        float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+        float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const float dw = (av[x] - cpj * (wv[x] * inv)) * inv;  // shardsim.hpp:382
+          const float g = dw + wd * wv[x];                       // shardsim.hpp:152-153
+          const float vv = mu * mv[x] + g;                       // shardsim.hpp:154
+          mv[x] = vv;
+          wv[x] = wv[x] - lr * vv;                               // shardsim.hpp:156
+        }
+        const size_t o = (size_t)r * D + d;
+        *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+        *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
       }
-      const size_t o = (size_t)r * D + d;
-      *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-      *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
     }
   }
 };

@@ -12,6 +12,12 @@ METRICS = [
     "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
     "sm__inst_executed_pipe_tc.sum", "lts__t_bytes.sum", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
+    # this ncu build's names for the north star's evidence: achieved DRAM bandwidth and
+    # tensor-pipe activity (the bench line's gemm_tensor_util is the FLOP-based figure)
+    "dram__bytes.sum.per_second", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 

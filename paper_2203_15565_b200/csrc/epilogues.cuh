@@ -61,9 +61,13 @@ struct NoSetup {
 };
 
 // ------------------------------------------------------------------------------------ FwdEpi
+#ifndef PFC_FWD_STBUF
+#define PFC_FWD_STBUF 2
+#endif
 template <typename ST, typename OT, bool kFilter, bool kTma>
 struct alignas(64) FwdEpi : NoSetup {
-  static constexpr int kWarpBytes = 4096;  // 2 x [32 rows][64 B] E staging per warp
+  static constexpr int kStageBufs = PFC_FWD_STBUF;  // E^T staging buffers per warp (TMA store in flight)
+  static constexpr int kWarpBytes = kStageBufs * 2048;  // [32 classes][64 B] each
   static constexpr int kSmem = kTma ? 4 * kWarpBytes : 0;
   CUtensorMap tm;   // E^T store map: inner = b (box 32, SWIZZLE_64B), outer = classes (box 32)
   int B, ncols, lde;  // lde = row stride of E^T (>= B)
@@ -132,8 +136,8 @@ struct alignas(64) FwdEpi : NoSetup {
             pa[i] = *reinterpret_cast<uint32_t*>(&x);
             pb[i] = *reinterpret_cast<uint32_t*>(&y);
           }
-          uint8_t* sb = stage + (kk & 1) * 2048;
-          if (lane == 0) pfc_sm100::bulk_wait_read<1>();  // this buffer's store, 2 groups ago
+          uint8_t* sb = stage + (kk % kStageBufs) * 2048;
+          if (lane == 0) pfc_sm100::bulk_wait_read<kStageBufs - 1>();  // this buffer's last store
           __syncwarp();
           // stmatrix j: matrices i = (rows 0-7, 8-15, 16-23, 24-31) x classes 8j..8j+7; thread
           // 8i + r addresses class row 8j + r, b chunk i (16 B, swizzled by the class row)
@@ -209,8 +213,8 @@ struct alignas(64) FwdEpi : NoSetup {
       }
       if constexpr (kTma) {
         // transposed staging: E^T chunk [32 classes][32 rows b] (64 B per class, 64B swizzle)
-        uint8_t* sb = stage + (kk & 1) * 2048;
-        if (lane == 0) pfc_sm100::bulk_wait_read<1>();  // this buffer's store, 2 groups ago
+        uint8_t* sb = stage + (kk % kStageBufs) * 2048;
+        if (lane == 0) pfc_sm100::bulk_wait_read<kStageBufs - 1>();  // this buffer's last store
         __syncwarp();
         // element (class q, row b) lives at byte q*64 + b*2, its 16-byte chunk swizzled by q.
         // Lanes b, b^1 swap halves of their packed (q, q+1) pairs so that each stores one

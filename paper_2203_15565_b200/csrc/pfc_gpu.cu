@@ -1134,6 +1134,10 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
     std::memcpy(id.internal, desc->nccl_id, 128);
     const int r = g_nccl.CommInitRank(&c->comm, c->R, id, c->rank);
     if (r != 0) return bail(fail(c, PFC_ERR_NCCL, "ncclCommInitRank failed (%d)", r));
+    // one collective outside any graph capture: NCCL may set up its connections lazily at the
+    // first collective, which the step's captured graph must not be the one to trigger
+    const int w = g_nccl.AllReduce(c->st, c->st, 1, ncclInt32, ncclMax, c->comm, c->stream);
+    if (w != 0) return bail(fail(c, PFC_ERR_NCCL, "NCCL warm-up all-reduce failed (%d)", w));
   }
   CT(cudaStreamSynchronize(c->stream));
 #undef CT

@@ -46,8 +46,8 @@ struct StepStatus {
   uint32_t fin_blocks;        // finalize_stats blocks done (last one reduces the loss)
 };
 
-// Per-step scalars, written on the device by step_begin_kernel (the only graph node whose
-// arguments change between steps) and read by the kernels that need them.
+// Per-step scalars, written on the device by step_begin (thread 0 of positives_kernel, the only
+// graph node whose arguments change between steps) and read by the kernels that need them.
 struct StepParams {
   uint64_t seed;    // iteration_rng.seed()
   uint64_t stream;  // iteration_rng.stream_id()

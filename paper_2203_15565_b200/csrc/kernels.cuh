@@ -11,13 +11,13 @@ __device__ __forceinline__ bool step_failed(const StepStatus* st) {
   return sampler_failed(st) || st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx;
 }
 
-// First node of every step: per-step scalars + a fresh status block.  Errors are sticky
-// across asynchronous steps (pfc_gpu_sync reports and clears them), like the reference,
-// which stops at the first throwing step.
-__global__ void step_begin_kernel(StepStatus* st, StepParams* sp, uint64_t seed, uint64_t stream,
-                                  float lr, int reset, const float* x, const int64_t* labels,
-                                  float* dx) {
-  if (threadIdx.x != 0) return;
+// Opens a step (thread 0 of the sampler's first kernel): per-step scalars + a fresh status block.
+// Errors are sticky across asynchronous steps (pfc_gpu_sync reports and clears them), like the
+// reference, which stops at the first throwing step: the status is kept and lr = 0 skips every
+// update.
+__device__ __forceinline__ void step_begin(StepStatus* st, StepParams* sp, uint64_t seed,
+                                           uint64_t stream, float lr, int reset, const float* x,
+                                           const int64_t* labels, float* dx) {
   sp->x = x;
   sp->labels = labels;
   sp->dx = dx;

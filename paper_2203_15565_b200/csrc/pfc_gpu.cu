@@ -233,7 +233,9 @@ struct Ctx {
   StepStatus* st_host = nullptr;
   StepParams* sp = nullptr;
   bool reset_status = true;  // false while asynchronous device steps are in flight
-  // CUDA graph of the device step (one per batch size); step_begin is its first node
+  size_t sort_smem = 0;  // dynamic shared memory of positives_kernel at the captured batch size
+  // CUDA graph of the device step (one per batch size); positives_kernel (which opens the step)
+  // is the node whose arguments change per step
   // captured steps: slot 0 = device-resident I/O (pfc_gpu_step_device), slot 1 = the host
   // drop-in with its copies inside the graph (pfc_gpu_step with pinned host buffers)
   struct GraphSlot {
@@ -241,6 +243,7 @@ struct Ctx {
     cudaGraphExec_t gexec = nullptr;
     cudaGraphNode_t gbegin = nullptr;
     cudaGraphNode_t cp_x = nullptr, cp_dx = nullptr;  // slot 1 memcpy nodes
+    size_t psmem = 0;  // the step-opening node's dynamic shared memory (captured)
     const void* cp_ptr[3] = {nullptr, nullptr, nullptr};  // host pointers the nodes hold
     int64_t gB = -1;
     int64_t glaunches = 0;
@@ -417,9 +420,23 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const int bs = 256;
   if (int rc = ensure_maps(c, B)) return rc;
   const bool e2e = c->e2e.on;
+  // ---- sampler (build_buffers, sampler.hpp:63-126); its first kernel also opens the step.
   // (host drop-in: `lab` is the caller's page-locked labels, read by the sampler over PCIe)
-  step_begin_kernel<<<1, 32, 0, s>>>(c->st, c->sp, a->seed, a->stream_id, (float)a->lr,
-                                     c->reset_status ? 1 : 0, x, lab, dx_full);
+  int P2 = 1;
+  while (P2 < B) P2 <<= 1;
+  // keys + sorted unique labels (int32) + the staged batch labels (int64)
+  const size_t sort_smem = (2 * sizeof(int32_t) + sizeof(int64_t)) * (size_t)P2;
+  static bool sort_cfg = false;
+  if (!sort_cfg) {
+    CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((2 * sizeof(int32_t) + sizeof(int64_t)) * kMaxSortBatch)));
+    sort_cfg = true;
+  }
+  c->sort_smem = sort_smem;
+  positives_kernel<<<1, 1024, sort_smem, s>>>(
+      c->st, c->sp, a->seed, a->stream_id, (float)a->lr, c->reset_status ? 1 : 0, x, lab, dx_full,
+      (int)B, c->C, (int)c->K, c->blk, (int)c->cap, (int)c->k0, (int)c->nk, c->uniq, c->meta,
+      c->buf_cls, c->pos_col, (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0);
   c->launches++;
   if (e2e) {  // features: upload (D x B fp64), -> [B][D] fp32, normalise; joined before the GEMM
     CUDA_TRY(c, cudaEventRecord(c->ev_s, s));
@@ -434,21 +451,6 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaEventRecord(c->ev_x, c->s2));
   }
-  // ---- sampler (build_buffers, sampler.hpp:63-126)
-  int P2 = 1;
-  while (P2 < B) P2 <<= 1;
-  // keys + sorted unique labels (int32) + the staged batch labels (int64)
-  const size_t sort_smem = (2 * sizeof(int32_t) + sizeof(int64_t)) * (size_t)P2;
-  static bool sort_cfg = false;
-  if (!sort_cfg) {
-    CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((2 * sizeof(int32_t) + sizeof(int64_t)) * kMaxSortBatch)));
-    sort_cfg = true;
-  }
-  positives_kernel<<<1, 1024, sort_smem, s>>>(
-      c->sp, (int)B, c->C, (int)c->K, c->blk, (int)c->cap, (int)c->k0, (int)c->nk, c->uniq,
-      c->meta, c->buf_cls, c->pos_col, c->st, (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0);
-  c->launches++;
   CUDA_TRY(c, cudaMemsetAsync(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride, s));
   const int64_t nd = c->nk * c->cap;
   OT* xh = static_cast<OT*>(c->xh);
@@ -688,28 +690,38 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
       if (ty != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams kp{};
       if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
-          kp.func == reinterpret_cast<void*>(step_begin_kernel))
+          kp.func == reinterpret_cast<void*>(positives_kernel))
         G.gbegin = nd;
     }
-    if (!G.gbegin) return fail(c, PFC_ERR_CUDA, "graph capture lost the step_begin node");
+    if (!G.gbegin) return fail(c, PFC_ERR_CUDA, "graph capture lost the step-opening node");
     if (c->e2e.on && (!G.cp_x || !G.cp_dx))
       return fail(c, PFC_ERR_CUDA, "graph capture lost a host copy node");
     G.gB = B;
     G.glaunches = c->launches;
+    G.psmem = c->sort_smem;
     G.cp_ptr[0] = G.cp_ptr[1] = G.cp_ptr[2] = nullptr;
   }
-  // per step, only step_begin's arguments (and the host drop-in's host pointers) change
+  // per step, only the step-opening kernel's arguments (and the host drop-in's host pointers)
+  // change; the other arguments and the launch shape are the captured ones
   StepStatus* st = c->st;
   StepParams* sp = c->sp;
   uint64_t seed = a->seed, stream = a->stream_id;
   float lr = (float)a->lr;
   int reset = c->reset_status ? 1 : 0;
-  void* args[] = {&st, &sp, &seed, &stream, &lr, &reset, &x, &lab, &dx_full};
+  int iB = (int)B, iK = (int)c->K, icap = (int)c->cap, ik0 = (int)c->k0, ink = (int)c->nk;
+  int64_t C = c->C, blk = c->blk;
+  int64_t* uniq = c->uniq;
+  ShardMeta* meta = c->meta;
+  int32_t* buf_cls = c->buf_cls;
+  int32_t* pos_col = c->pos_col;
+  int force = (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0;
+  void* args[] = {&st, &sp, &seed, &stream, &lr, &reset, &x, &lab, &dx_full, &iB, &C, &iK,
+                  &blk, &icap, &ik0, &ink, &uniq, &meta, &buf_cls, &pos_col, &force};
   cudaKernelNodeParams kp{};
-  kp.func = reinterpret_cast<void*>(step_begin_kernel);
+  kp.func = reinterpret_cast<void*>(positives_kernel);
   kp.gridDim = dim3(1);
-  kp.blockDim = dim3(32);
-  kp.sharedMemBytes = 0;
+  kp.blockDim = dim3(1024);
+  kp.sharedMemBytes = (unsigned)G.psmem;
   kp.kernelParams = args;
   kp.extra = nullptr;
   CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(G.gexec, G.gbegin, &kp));

@@ -73,11 +73,15 @@ __device__ int block_exclusive_scan(int v, int* smem_warp, int* total) {
 // One CTA of 1024 threads: sort + unique the global batch labels, validate them, route
 // positives to shards (sampler.hpp:68-80), check capacity in the reference's shard order
 // (sampler.hpp:84-98), and locate every row's positive column (shardsim.hpp:207-213).
+// Its thread 0 first opens the step (step_begin: the step's parameters and a status reset), so
+// this kernel is the one node of the step's graph whose arguments change from step to step.
 __global__ void __launch_bounds__(1024) positives_kernel(
-    const StepParams* __restrict__ sp, int B, int64_t C, int K, int64_t blk, int cap, int k0,
-    int nk, int64_t* __restrict__ uniq, ShardMeta* __restrict__ meta,
-    int32_t* __restrict__ buf_cls, int32_t* __restrict__ pos_col, StepStatus* st,
-    int force_sequential) {
+    StepStatus* st, StepParams* sp, uint64_t seed, uint64_t stream, float lr, int reset,
+    const float* x, const int64_t* labels_in, float* dx, int B, int64_t C, int K, int64_t blk,
+    int cap, int k0, int nk, int64_t* __restrict__ uniq, ShardMeta* __restrict__ meta,
+    int32_t* __restrict__ buf_cls, int32_t* __restrict__ pos_col, int force_sequential) {
+  if (threadIdx.x == 0) step_begin(st, sp, seed, stream, lr, reset, x, labels_in, dx);
+  __syncthreads();  // the block sees the step's parameters and the reset status
   // dynamic smem: keys[P] and the sorted unique labels us[P] (int32), then the batch labels[P]
   // (int64), staged once: in the host drop-in they are read from the caller's page-locked buffer
   // over PCIe (P = B rounded up to a power of 2)
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(1024) positives_kernel(
   // C < 2^31, the sort and the searches below run on 32-bit keys.
   int64_t mn = INT64_MAX, mc = INT64_MAX;
   for (int i = threadIdx.x; i < B; i += blockDim.x) {
-    const int64_t y = sp->labels[i];
+    const int64_t y = labels_in[i];
     labels[i] = y;
     mn = y < mn ? y : mn;
     if (y >= C && y < mc) mc = y;

@@ -85,12 +85,12 @@ __global__ void dx_to_dxb_kernel(const float* __restrict__ dX, int D, int B,
 // Feature normalisation (shardsim.hpp:196-204): |x| (fp64 accumulate), x^ = x * 1/max(|x|,1e-12),
 // written zero-padded to Dp columns in the GEMM operand type.  One warp per row.
 template <typename OT>
-__device__ __forceinline__ void normalize_x_rows(const StepParams* __restrict__ sp, int B, int D,
+__device__ __forceinline__ void normalize_x_rows(const float* __restrict__ xs, int B, int D,
                                                  int Dp, OT* __restrict__ xh,
                                                  float* __restrict__ xnorm, int blk) {
   const int warp = (blk * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= B) return;
-  const float* x = sp->x + (size_t)warp * D;
+  const float* x = xs + (size_t)warp * D;
   double ss = 0.0;
   for (int d = lane; d < D; d += 32) ss += (double)x[d] * (double)x[d];
   ss = warp_sum(ss);
@@ -102,9 +102,9 @@ __device__ __forceinline__ void normalize_x_rows(const StepParams* __restrict__ 
 }
 
 template <typename OT>
-__global__ void normalize_x_kernel(const StepParams* __restrict__ sp, int B, int D, int Dp,
+__global__ void normalize_x_kernel(const float* __restrict__ x, int B, int D, int Dp,
                                    OT* __restrict__ xh, float* __restrict__ xnorm) {
-  normalize_x_rows(sp, B, D, Dp, xh, xnorm, (int)blockIdx.x);
+  normalize_x_rows(x, B, D, Dp, xh, xnorm, (int)blockIdx.x);
 }
 
 // Centre gather + normalisation (shardsim.hpp:234-247).  One warp per sampled column; W is

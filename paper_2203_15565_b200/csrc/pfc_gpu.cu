@@ -420,6 +420,20 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const int bs = 256;
   if (int rc = ensure_maps(c, B)) return rc;
   const bool e2e = c->e2e.on;
+  if (e2e) {  // features: upload (D x B fp64), -> [B][D] fp32, normalise; joined before the GEMM.
+    // Needs nothing from the step's first kernel, so it forks before it.
+    CUDA_TRY(c, cudaEventRecord(c->ev_s, s));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_s, 0));
+    CUDA_TRY(c, cudaMemcpyAsync(c->xdb, c->e2e.xdb_h, sizeof(double) * B * c->D,
+                                cudaMemcpyHostToDevice, c->s2));
+    dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+    x_from_dxb_kernel<<<grid, blk, 0, c->s2>>>(c->xdb, (int)c->D, (int)B, c->X);
+    normalize_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, c->s2>>>(
+        c->X, (int)B, (int)c->D, (int)c->Dp, static_cast<OT*>(c->xh), c->xnorm);
+    c->launches += 2;
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaEventRecord(c->ev_x, c->s2));
+  }
   // ---- sampler (build_buffers, sampler.hpp:63-126); its first kernel also opens the step.
   // (host drop-in: `lab` is the caller's page-locked labels, read by the sampler over PCIe)
   int P2 = 1;
@@ -438,19 +452,6 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
       (int)B, c->C, (int)c->K, c->blk, (int)c->cap, (int)c->k0, (int)c->nk, c->uniq, c->meta,
       c->buf_cls, c->pos_col, (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0);
   c->launches++;
-  if (e2e) {  // features: upload (D x B fp64), -> [B][D] fp32, normalise; joined before the GEMM
-    CUDA_TRY(c, cudaEventRecord(c->ev_s, s));
-    CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_s, 0));
-    CUDA_TRY(c, cudaMemcpyAsync(c->xdb, c->e2e.xdb_h, sizeof(double) * B * c->D,
-                                cudaMemcpyHostToDevice, c->s2));
-    dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
-    x_from_dxb_kernel<<<grid, blk, 0, c->s2>>>(c->xdb, (int)c->D, (int)B, c->X);
-    normalize_x_kernel<OT><<<(unsigned)ceil_div(B * 32, bs), bs, 0, c->s2>>>(
-        c->sp, (int)B, (int)c->D, (int)c->Dp, static_cast<OT*>(c->xh), c->xnorm);
-    c->launches += 2;
-    CUDA_TRY(c, cudaGetLastError());
-    CUDA_TRY(c, cudaEventRecord(c->ev_x, c->s2));
-  }
   CUDA_TRY(c, cudaMemsetAsync(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride, s));
   const int64_t nd = c->nk * c->cap;
   OT* xh = static_cast<OT*>(c->xh);

@@ -236,7 +236,7 @@ __global__ void draws_kernel(ShardMeta* __restrict__ meta, int nk, int cap,
                              int32_t* __restrict__ jv, const StepStatus* st, int nblk_draws,
                              int B, int D, int Dp, OT* __restrict__ xh, float* __restrict__ xnorm) {
   if ((int)blockIdx.x >= nblk_draws) {
-    normalize_x_rows(sp, B, D, Dp, xh, xnorm, (int)blockIdx.x - nblk_draws);
+    normalize_x_rows(sp->x, B, D, Dp, xh, xnorm, (int)blockIdx.x - nblk_draws);
     return;
   }
   if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;

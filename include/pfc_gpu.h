@@ -50,7 +50,8 @@ typedef enum { /* MarginKind, margin.hpp:11 */
 } pfc_margin_kind;
 
 typedef enum {
-  PFC_PRECISION_BF16 = 0, /* tcgen05 kind::f16 GEMMs, fp32 accumulate, fp32 master W / momentum */
+  PFC_PRECISION_BF16 = 0, /* tcgen05 kind::f16 GEMMs, fp32 accumulate, fp32 master W / momentum;
+                             needs dim % 4 == 0 and dim <= 512 (pfc_gpu_create: PFC_ERR_CONFIG) */
   PFC_PRECISION_FP32 = 1  /* fp32 validation mode: SIMT fp32 GEMMs, fp64 softmax / gradient stage */
 } pfc_precision;
 

@@ -1,5 +1,5 @@
 """GPU: a seeded sweep of step configurations against the oracle (same contract as
-test_gpu_step.py).  The 16 cases are drawn once from a fixed generator, so every run tests the
+test_gpu_step.py), two steps each (the second update carries momentum).  The 16 cases are drawn once from a fixed generator, so every run tests the
 same ones; they cover the paths the hand-picked cases may miss:
   * class counts that leave a ragged last tile and a short last shard;
   * batches that are not multiples of 32 (the logits epilogue's fragment path: a warp's 32 rows
@@ -80,11 +80,17 @@ def test_fuzz_step_matches_oracle(case, port):
         sh.close()
         return
     W0 = port.init_centers(C_, K, D, 1)
+    # two steps (the second update carries momentum, mu * m != 0); the second only when its
+    # labels also fit the shards' capacity
     W, M = W0.copy(), np.zeros_like(W0)
-    ref = port.step(oracle_cfg(mg, m, r, tau), C_, K, D, W, M, X, labels, 1, stream)
-    Wr, Mr = shards_to_rows(W, C_, K, D), shards_to_rows(M, C_, K, D)
-    rows = np.unique(ref["buffers"].ravel())
-    untouched = np.setdiff1d(np.arange(C_), rows)
+    refs = []
+    for step in range(2):
+        Xs, ls = (X, labels) if step == 0 else port.bench_inputs(C_, D, B, 1, step)
+        if step > 0 and np.bincount(np.unique(ls) // blk, minlength=K).max() > cap:
+            break
+        st = port.make_stream("iteration", step)
+        ref = port.step(oracle_cfg(mg, m, r, tau), C_, K, D, W, M, Xs, ls, 1, st)
+        refs.append((Xs, ls, st, ref, shards_to_rows(W, C_, K, D), shards_to_rows(M, C_, K, D)))
     precisions = [p.PRECISION_FP32]
     if D > 512:  # the bf16 path refuses it (dW covers two 256-dim halves); fp32 runs it
         with pytest.raises(p.ConfigError, match="dim <= 512"):
@@ -95,23 +101,29 @@ def test_fuzz_step_matches_oracle(case, port):
     for precision in precisions:
         tl, tdf, tdm, tw = TOL[precision]
         sh = make_shards(W0, np.zeros_like(W0), C_, K, D, step_cfg(mg, m, r, tau), B, precision)
-        Wd0, Md0 = device_rows(sh, C_, K, D)
-        res = p.distributed_partial_step(sh, X, labels, step_cfg(mg, m, r, tau), p.SeededRng(1, stream))
-        for k, buf in enumerate(res.buffers):
-            assert np.array_equal(buf.class_indices, ref["buffers"][k]), (name, k)
-            assert buf.num_positives == ref["npos"][k]
-        Wd, Md = device_rows(sh, C_, K, D)
-        rec = {"case": name, "precision": "fp32" if precision else "bf16",
-               "loss_rel": abs(res.loss - ref["loss"]) / abs(ref["loss"]),
-               "dX_fro": rel_fro(res.d_features, ref["dX"]), "dX_maxmax": rel_max(res.d_features, ref["dX"]),
-               "W_maxmax": rel_max(Wd[rows], Wr[rows])}
-        os.makedirs(os.path.dirname(RESULTS), exist_ok=True)
-        with open(RESULTS, "a") as f:
-            f.write(json.dumps(rec) + "\n")
-        assert rec["loss_rel"] <= tl, rec
-        assert rec["dX_fro"] <= tdf, rec
-        assert rec["dX_maxmax"] <= tdm, rec
-        assert rec["W_maxmax"] <= tw, rec
-        assert np.array_equal(Wd[untouched], Wd0[untouched])
-        assert np.array_equal(Md[untouched], Md0[untouched])
+        for step, (Xs, ls, st, ref, Wr, Mr) in enumerate(refs):
+            rows = np.unique(ref["buffers"].ravel())
+            untouched = np.setdiff1d(np.arange(C_), rows)
+            Wd0, Md0 = device_rows(sh, C_, K, D)
+            res = p.distributed_partial_step(sh, Xs, ls, step_cfg(mg, m, r, tau), p.SeededRng(1, st))
+            for k, buf in enumerate(res.buffers):
+                assert np.array_equal(buf.class_indices, ref["buffers"][k]), (name, step, k)
+                assert buf.num_positives == ref["npos"][k]
+            Wd, Md = device_rows(sh, C_, K, D)
+            rec = {"case": name, "precision": "fp32" if precision else "bf16", "step": step,
+                   "loss_rel": abs(res.loss - ref["loss"]) / abs(ref["loss"]),
+                   "dX_fro": rel_fro(res.d_features, ref["dX"]),
+                   "dX_maxmax": rel_max(res.d_features, ref["dX"]),
+                   "W_maxmax": rel_max(Wd[rows], Wr[rows]), "mom_maxmax": rel_max(Md[rows], Mr[rows])}
+            os.makedirs(os.path.dirname(RESULTS), exist_ok=True)
+            with open(RESULTS, "a") as f:
+                f.write(json.dumps(rec) + "\n")
+            assert rec["loss_rel"] <= tl, rec
+            assert rec["dX_fro"] <= tdf, rec
+            assert rec["dX_maxmax"] <= tdm, rec
+            assert rec["W_maxmax"] <= tw, rec
+            if precision == p.PRECISION_FP32:
+                assert rec["mom_maxmax"] <= 3e-5, rec
+            assert np.array_equal(Wd[untouched], Wd0[untouched])
+            assert np.array_equal(Md[untouched], Md0[untouched])
         sh.close()

@@ -113,74 +113,75 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_reference_time(C_full, K, D, B, r, steps, warmup, target_s=2.0):
-    """The reference's own distributed_partial_step (oracle/_ref, compiled from the unmodified
-    headers) on the host cores, on a bounded sample of the workload: C scaled down so one
-    step takes ~target_s; per-step cost is linear in cap = C*r/K (B x cap x D loops,
-    shardsim.hpp:249-256, 349-376), so samples/s is scaled by cap_sample / cap_full."""
+def cpu_reference_time(C_full, K, D, B, r, steps, warmup):
+    """The reference's own pfc::distributed_partial_step (oracle/_ref/libpfc_ref.so: the
+    unmodified headers compiled in place, reference flags) on the host cores, AT THE STATED
+    WORKLOAD (no scaling): C_full classes in K shards, the global batch B of the bench input
+    convention, ArcFace s=64 m=0.5, PFC_SIM_THREADS = all host cores (the reference runs one
+    thread per shard, so min(K, cores) are busy).  The shards are the reference's
+    init_center_shards values built by host threads (pfcr_session_create_par; timed separately,
+    outside the steps).  `warmup` untimed steps, then `steps` timed ones; the best is reported."""
     from oracle.oracle import Oracle, OracleCfg, ref_available
-    kind = "reference" if ref_available() else "port"
-    o = Oracle(kind)
+    import ctypes as C
+    import numpy as np
     cores = os.cpu_count() or 1
     os.environ["PFC_SIM_THREADS"] = str(cores)
     cfg = OracleCfg(r=r, margin="arcface", scale=64.0, m=0.5, lr=0.1)
     P = Oracle("port")
-    C_s = max(K * 200, C_full // 40)
-    cap_full, cap_s = P.capacity(C_full, K, r), P.capacity(C_s, K, r)
     X, labels = P.bench_inputs(C_full, D, B, 1, 0)
-    labels = labels % C_s
-    import numpy as np
-    if kind == "reference":
-        h = o._session_create(C_s, K, D, 1)
-        loss = __import__("ctypes").c_double()
-        err = __import__("ctypes").create_string_buffer(512)
-        Xc = np.ascontiguousarray(X)
-
-        def one(step):
-            st = o._session_step(h, __import__("ctypes").byref(cfg.c()), Xc.ctypes.data,
-                                 labels.ctypes.data, B, 1, o.make_stream("iteration", step),
-                                 __import__("ctypes").byref(loss), None, err, 512)
-            assert st == 0, err.value
-    else:
-        W = P.init_centers(C_s, K, D, 1)
-        M = np.zeros_like(W)
-
-        def one(step):
-            P.step(cfg, C_s, K, D, W, M, X, labels, 1, P.make_stream("iteration", step))
+    if not ref_available():
+        raise RuntimeError("oracle/_ref/libpfc_ref.so missing (build it with make -C oracle where "
+                           "/root/reference exists)")
+    o = Oracle("reference")
+    t0 = time.perf_counter()
+    h = o._session_create_par(C_full, K, D, 1, cores)
+    init_s = time.perf_counter() - t0
+    loss = C.c_double()
+    err = C.create_string_buffer(512)
+    Xc = np.ascontiguousarray(X)
     times = []
-    for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        one(i)
-        if i >= warmup:
-            times.append(time.perf_counter() - t0)
-    if kind == "reference":
+    try:
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            st = o._session_step(h, C.byref(cfg.c()), Xc.ctypes.data, labels.ctypes.data, B, 1,
+                                 o.make_stream("iteration", i), C.byref(loss), None, err, 512)
+            dt = time.perf_counter() - t0
+            assert st == 0, err.value
+            if i >= warmup:
+                times.append(dt)
+    finally:
         o._session_destroy(h)
-    t = statistics.median(times)
-    scale = cap_full / cap_s
-    threads = min(K, cores) if kind == "reference" else 1
-    return {"value": B / (t * scale), "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": (f"reference distributed_partial_step at C={C_s} (cap {cap_s}/shard vs "
-                       f"{cap_full}), K={K}, B={B}, d={D}, r={r}, ArcFace; median of {steps} steps "
-                       f"= {t:.3f} s, scaled x{scale:.1f} (work is linear in cap); "
-                       f"the reference runs one thread per shard: {threads} threads on "
-                       f"{cores} host cores"),
-            "step_s_sample": t, "host_cores": cores}
+    t = min(times)
+    threads = min(K, cores)
+    return {"value": B / t, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": (f"reference distributed_partial_step at the full workload C={C_full}, K={K}, "
+                       f"B={B}, d={D}, r={r}, ArcFace s=64 m=0.5 (no scaling); best of {steps} "
+                       f"step(s) after {warmup} warm-up: {t:.2f} s/step (all: "
+                       f"{', '.join(f'{x:.2f}' for x in times)}); PFC_SIM_THREADS={cores} host "
+                       f"cores, {threads} busy (one thread per shard); host init of the "
+                       f"{C_full}x{D} fp64 shards {init_s:.1f} s, untimed"),
+            "step_s": t, "step_s_all": times, "host_init_s": init_s, "host_cores": cores,
+            "last_loss": loss.value}
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return 0
-    steps = max(1, min(args.steps, 3))
+    # each step of the stated workload takes about a minute on the host: a bounded number of
+    # them (one warm-up, then the best of two) keeps the run within a few minutes
+    steps = 2
     warm = 1
     cb = cpu_reference_time(args.classes, args.shards, args.dim, args.batch, args.r, steps, warm)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": steps, "warmup": warm, "ms_per_step": args.batch / cb["value"] * 1e3,
+            "steps": steps, "warmup": warm, "ms_per_step": cb["step_s"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": workload_config(args),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "host_init_s": cb["host_init_s"], "step_s_all": cb["step_s_all"],
+            "last_loss": cb["last_loss"]}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -296,7 +297,10 @@ def main():
             acc[k] = acc.get(k, 0.0) + v / reps
     sh.set_phase_timing(False)
     cap, F1 = sh.capacity, 2.0 * B * ncols * D  # one B x ncols x D GEMM
-    tf_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    # the burst cuBLAS figure (1646.5 TFLOP/s measured); the sustained one is an
+    # extra, labelled field
+    tf_peak = peaks["bf16_tflops"]
+    tf_sus = peaks.get("bf16_tflops_sustained")
     hbm = peaks["hbm_gbs"]
     phases = {}
     algo = {  # phase -> (bound, algorithmic amount per launch, unit)
@@ -327,16 +331,19 @@ def main():
     line["roofline"] = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                         "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
                         "kernel": dom, "peak_source": f"{peak_src} MEASURED_PEAKS.json "
-                        f"({'bf16_tflops_sustained' if d['bound'] == 'tensor' else 'hbm_gbs'})"}
+                        f"({'bf16_tflops' if d['bound'] == 'tensor' else 'hbm_gbs'})"}
     F = 6.0 * B * ncols * D
     Q = 20.0 * ncols * D
     t_roof = F / (tf_peak * 1e12) + Q / (hbm * 1e9)
     line["step_roofline"] = {"flops": F, "bytes": Q, "roofline_us": t_roof * 1e6,
                              "measured_us": ms * 1e3, "frac": t_roof / (ms / 1e3),
-                             "formula": "6*B*cap_local*d / bf16_sustained + 20*cap_local*d / hbm "
-                                        "(SURVEY.md 8d)"}
+                             "formula": "6*B*cap_local*d / bf16_tflops (burst) + 20*cap_local*d / "
+                                        "hbm_gbs (SURVEY.md 8d)"}
+    if tf_sus:
+        t_sus = F / (tf_sus * 1e12) + Q / (hbm * 1e9)
+        line["step_roofline"]["frac_vs_sustained_peak"] = t_sus / (ms / 1e3)
     line["phases_ms"] = phases
-    # BASELINE.json's metric also names GEMM tensor-pipe utilisation: achieved / sustained bf16
+    # BASELINE.json's metric also names GEMM tensor-pipe utilisation: achieved / burst bf16
     # peak per GEMM (event-timed phases: the logits phase includes its fused epilogue, the dX
     # phase its split-K finalize, the dW phase the fused centre update)
     util = {}
@@ -348,6 +355,11 @@ def main():
     if tot_t > 0:
         util["all_gemms"] = 3 * F1 / tot_t / 1e12 / tf_peak
     util["peak_tflops"] = tf_peak
+    util["peak_source"] = "MEASURED_PEAKS.json bf16_tflops (burst cuBLAS 8192^3)"
+    if tf_sus:
+        util["vs_sustained_peak"] = {k: v * tf_peak / tf_sus for k, v in util.items()
+                                     if isinstance(v, float) and k != "peak_tflops"}
+        util["peak_tflops_sustained"] = tf_sus
     line["gemm_tensor_util"] = util
 
     # ---- diagnostics (with_diagnostics): apcs + exact amncs over all C
@@ -400,9 +412,9 @@ def main():
                        "d2h_bytes_per_step": D * B * 8 + 64,
                        "api": "pfc_gpu_step (C ABI, host fp64 D x B features, pinned)"}
     if rank == 0 and ws == 1 and not args.no_cpu:
-        try:
+        try:  # one step of the stated workload (about a minute of host time), no warm-up
             line["cpu_baseline"] = {k: v for k, v in cpu_reference_time(
-                C_, K, D, B, args.r, 2, 1).items() if k in ("value", "unit", "cores", "kind", "sample")}
+                C_, K, D, B, args.r, 1, 0).items() if k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # the baseline is reported, never the target
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "none",
                                     "sample": f"unavailable: {e}"}

@@ -72,12 +72,18 @@ typedef struct {
   int32_t device;          /* CUDA device ordinal of this rank */
   int32_t rank;            /* this process's rank, 0 <= rank < world_size */
   int32_t world_size;      /* GPUs (ranks); must divide num_shards */
-  const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from pfc_gpu_nccl_unique_id (world_size > 1) */
+  const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from pfc_gpu_nccl_unique_id (world_size > 1),
+                              or a loopback id from pfc_gpu_loopback_id */
   int32_t flags;           /* PFC_FLAG_* */
 } pfc_gpu_desc;
 
 #define PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER 1 /* test hook: always use the exact sequential FY */
 #define PFC_FLAG_NO_GRAPH 2                  /* do not capture the step in a CUDA graph */
+#define PFC_FLAG_EXACT_SOFTMAX 4             /* per-row max softmax offsets on every step (the
+                                                default above margin_scale 64; below it a fixed
+                                                offset, rerun per row if a row underflows) */
+#define PFC_FLAG_DEBUG_LOGITS 8              /* test hook: keep the last step's logits
+                                                (pfc_gpu_debug_logits) */
 
 typedef struct {
   uint64_t seed;       /* iteration_rng.seed()      (rng.hpp:44) */
@@ -99,6 +105,11 @@ typedef struct {
    * all-reduces and reduce-scatters; 0 with one rank): what the GPU path actually moves, next to
    * the reference's closed-form trace above (costmodel.hpp:37-69) */
   uint64_t nccl_bytes;
+  /* the same collectives under the ring model of the reference's cost model (costmodel.hpp:37-69,
+   * "totals across workers, per step"): (R-1) S per all-gather / reduce-scatter and 2 (R-1) S per
+   * all-reduce of S bytes in total, summed over the collectives the step issued (every rank
+   * reports the same total; 0 with one rank) */
+  uint64_t wire_bytes;
 } pfc_gpu_step_out;
 
 /* ---- lifecycle ------------------------------------------------------------------------ */
@@ -107,6 +118,12 @@ int pfc_gpu_destroy(void* ctx);
 /* Message of the last failure on ctx (or of the last failed create on this thread if NULL). */
 const char* pfc_gpu_last_error(const void* ctx);
 int pfc_gpu_nccl_unique_id(uint8_t out[128]);
+/* Test hook: an id that makes world_size contexts created in ONE process (one host thread each,
+ * any device, e.g. all on one GPU) ranks of a loopback communicator instead of NCCL.  The
+ * collectives are host-synchronised (CUDA events, no kernel waits on another rank), summed in
+ * ascending rank order, and never captured in a graph.  Every rank must call pfc_gpu_create
+ * with the same id concurrently. */
+int pfc_gpu_loopback_id(uint8_t out[128]);
 const char* pfc_gpu_version(void);
 
 /* ---- shape queries (ShardLayout / buffer_capacity) ------------------------------------ */
@@ -238,6 +255,10 @@ int pfc_gpu_bench_inputs(void* ctx, uint64_t seed, uint64_t step, int64_t batch,
 /* Kernel timing of the last step (ms, CUDA events around each phase); n <= 16 entries. */
 int pfc_gpu_phase_times(void* ctx, float* ms, const char** names, int n);
 int pfc_gpu_set_phase_timing(void* ctx, int enabled);
+/* Test hook (PFC_FLAG_DEBUG_LOGITS): the last step's logits z of this rank, B x local columns
+ * fp32 row-major (columns: local shards in order, cap each): s cos (margin on the positive),
+ * -inf where the filter masked the column (shardsim.hpp:258-281). */
+int pfc_gpu_debug_logits(void* ctx, float* out_b_by_cols);
 /* Number of kernels (ours) launched by one step at the current batch shape. */
 int64_t pfc_gpu_launches_per_step(void* ctx);
 

@@ -19,6 +19,10 @@
 #include "pfc/io.hpp"
 #include "pfc/trainer.hpp"
 
+#ifndef PFC_SRC_HASH  // sha256 prefix of the sources this program was built from (Makefile)
+#define PFC_SRC_HASH "unknown"
+#endif
+
 using namespace pfc;
 
 namespace {
@@ -66,7 +70,11 @@ struct Case {
 
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "--source-hash") {
+    std::printf("%s\n", PFC_SRC_HASH);
+    return 0;
+  }
   const Case cases[] = {
       {"tiny_cos_fp32", 400, 4, 32, 32, 0.5, MarginConfig::cosface_style(), std::nullopt,
        PFC_PRECISION_FP32, 1e-6, 1e-5, 1e-6},

@@ -98,8 +98,13 @@ class Oracle:
         self._f("mics", C.c_int, [i64, i64, i64, vp, vp, C.c_char_p, C.c_int])
         self._f("step", C.c_int, [C.POINTER(StepCfgC), i64, i64, i64, vp, vp, vp, vp, i64, u64,
                                   u64, C.POINTER(dbl), vp, vp, vp, vp, vp, C.c_char_p, C.c_int])
+        if kind == "port":
+            self._f("step_ex", C.c_int, [C.POINTER(StepCfgC), i64, i64, i64, vp, vp, vp, vp, i64,
+                                         u64, u64, C.POINTER(dbl), vp, vp, vp, vp, vp, vp,
+                                         C.c_char_p, C.c_int])
         if kind == "reference":
             self._f("session_create", vp, [i64, i64, i64, u64])
+            self._f("session_create_par", vp, [i64, i64, i64, u64, C.c_int])
             self._f("session_destroy", None, [vp])
             self._f("session_get", None, [vp, vp, vp])
             self._f("session_step", C.c_int, [vp, C.POINTER(StepCfgC), vp, vp, i64, u64, u64,
@@ -160,8 +165,10 @@ class Oracle:
         return W
 
     def step(self, cfg: OracleCfg, C_: int, K: int, D: int, W: np.ndarray, M: np.ndarray,
-             X: np.ndarray, labels, seed: int, stream: int, want_extra: bool = False):
-        """One distributed_partial_step; W and M (shard-concatenated) are updated in place."""
+             X: np.ndarray, labels, seed: int, stream: int, want_extra: bool = False,
+             mask: np.ndarray | None = None):
+        """One distributed_partial_step; W and M (shard-concatenated) are updated in place.
+        ``mask`` (port only, K x B x cap bool, True = masked) replaces the filter rule."""
         X = np.ascontiguousarray(X, dtype=np.float64)
         labels = np.ascontiguousarray(labels, dtype=np.int64)
         B = len(labels)
@@ -175,9 +182,16 @@ class Oracle:
         loss = C.c_double(0.0)
         err = C.create_string_buffer(512)
         cc = cfg.c()
-        st = self._step(C.byref(cc), C_, K, D, _ptr(W), _ptr(M), _ptr(X), _ptr(labels), B, seed,
-                        stream, C.byref(loss), _ptr(dX), _ptr(bufs), _ptr(npos), _ptr(dcent),
-                        _ptr(cosm), err, 512)
+        if mask is not None:
+            mk = np.ascontiguousarray(mask, dtype=np.uint8)
+            assert mk.shape == (K, B, cap)
+            st = self._step_ex(C.byref(cc), C_, K, D, _ptr(W), _ptr(M), _ptr(X), _ptr(labels), B,
+                               seed, stream, C.byref(loss), _ptr(dX), _ptr(bufs), _ptr(npos),
+                               _ptr(dcent), _ptr(cosm), _ptr(mk), err, 512)
+        else:
+            st = self._step(C.byref(cc), C_, K, D, _ptr(W), _ptr(M), _ptr(X), _ptr(labels), B,
+                            seed, stream, C.byref(loss), _ptr(dX), _ptr(bufs), _ptr(npos),
+                            _ptr(dcent), _ptr(cosm), err, 512)
         if st:
             raise OracleError(st, err.value.decode())
         out = {"loss": loss.value, "dX": dX, "buffers": bufs, "npos": npos}

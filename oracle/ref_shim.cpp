@@ -14,6 +14,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "pfc/metrics.hpp"
@@ -253,6 +254,45 @@ int pfcr_mics(int64_t C, int64_t K, int64_t D, const double* W, double* out, cha
 void* pfcr_session_create(int64_t C, int64_t K, int64_t D, uint64_t seed) {
     auto* s = new Session{C, K, D, pfc::init_center_shards(pfc::ShardLayout(C, K), D, seed)};
     return s;
+}
+
+// The same shards as init_center_shards (shardsim.hpp:56-82) -- every class column drawn from its
+// own SeededRng(seed, make_stream("center-init", class)) with the reference's next_normal and
+// unit-normalised -- filled by `threads` host threads over contiguous class ranges (the per-class
+// streams make the result independent of the split).  Used by the bench's reference arm, whose
+// 2M-class init would otherwise take ~80 s single-threaded before the timed steps.
+void* pfcr_session_create_par(int64_t C, int64_t K, int64_t D, uint64_t seed, int threads) {
+    const pfc::ShardLayout layout(C, K);
+    std::vector<pfc::CenterShard> shards(static_cast<size_t>(K));
+    for (int64_t k = 0; k < K; ++k) {
+        pfc::CenterShard& s = shards[static_cast<size_t>(k)];
+        s.shard_id = k;
+        s.class_begin = layout.owned_begin(k);
+        s.class_end = layout.owned_end(k);
+        s.weights = pfc::Matrix(D, s.owned());
+        s.momentum = pfc::Matrix(D, s.owned());
+    }
+    if (threads < 1) threads = 1;
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            const int64_t c0 = C * t / threads, c1 = C * (t + 1) / threads;
+            for (int64_t c = c0; c < c1; ++c) {
+                pfc::CenterShard& s = shards[static_cast<size_t>(layout.owner(c))];
+                const int64_t j = c - s.class_begin;
+                pfc::SeededRng rng(seed, pfc::make_stream("center-init", static_cast<uint64_t>(c)));
+                double norm = 0.0;
+                for (int64_t d = 0; d < D; ++d) {
+                    const double v = rng.next_normal();
+                    s.weights(d, j) = v;
+                    norm += v * v;
+                }
+                const double inv = 1.0 / std::max(std::sqrt(norm), 1e-12);
+                for (int64_t d = 0; d < D; ++d) s.weights(d, j) *= inv;
+            }
+        });
+    for (auto& th : pool) th.join();
+    return new Session{C, K, D, std::move(shards)};
 }
 
 void pfcr_session_destroy(void* h) { delete static_cast<Session*>(h); }

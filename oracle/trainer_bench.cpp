@@ -5,6 +5,7 @@
 // pfc/gpu_trainer.hpp: backbone, step and diagnostics on the GPU) run the same SyntheticDataset
 // and TrainConfig for `steps` steps (stop_after_step, so the reference's O(N C d) final
 // evaluation is not timed).  Prints one JSON line with ms per training step for each.
+#include <string>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -12,9 +13,17 @@
 #include "pfc/gpu_trainer.hpp"
 #include "pfc/trainer.hpp"
 
+#ifndef PFC_SRC_HASH  // sha256 prefix of the sources this program was built from (Makefile)
+#define PFC_SRC_HASH "unknown"
+#endif
+
 using namespace pfc;
 
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "--source-hash") {
+    std::printf("%s\n", PFC_SRC_HASH);
+    return 0;
+  }
   const int64_t identities = argc > 1 ? std::atoll(argv[1]) : 20000;
   const int64_t steps = argc > 2 ? std::atoll(argv[2]) : 100;
   SynthConfig sc;

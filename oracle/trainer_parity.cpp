@@ -21,6 +21,10 @@
 #include "pfc/gpu_trainer.hpp"
 #include "pfc/trainer.hpp"
 
+#ifndef PFC_SRC_HASH  // sha256 prefix of the sources this program was built from (Makefile)
+#define PFC_SRC_HASH "unknown"
+#endif
+
 using namespace pfc;
 
 namespace {
@@ -143,7 +147,11 @@ double now_ms() {
 
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "--source-hash") {
+    std::printf("%s\n", PFC_SRC_HASH);
+    return 0;
+  }
   bool ok = true;
   // ---- end results against the reference (fp32 validation mode and bf16 tensor cores)
   struct Run {

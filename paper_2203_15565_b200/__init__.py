@@ -206,6 +206,9 @@ class StepResult:
     trace: CollectiveTrace
     buffers: list
     diagnostics: DiagnosticsSnapshot | None = None
+    # not in the reference's StepResult: what the GPU path moved (pfc_gpu_step_out)
+    nccl_bytes: int = 0
+    wire_bytes: int = 0
 
 
 class ShardLayout:
@@ -262,11 +265,11 @@ class StepOut(C.Structure):
                 ("reduce_scalar_bytes", C.c_uint64), ("reduce_grad_bytes", C.c_uint64),
                 ("reduce_ops", C.c_uint64), ("capacity", C.c_int64),
                 ("rejection_shards", C.c_int32), ("reserved", C.c_int32),
-                ("nccl_bytes", C.c_uint64)]
+                ("nccl_bytes", C.c_uint64), ("wire_bytes", C.c_uint64)]
 
 
 PRECISION_BF16, PRECISION_FP32 = 0, 1
-FLAG_FORCE_SEQUENTIAL_SAMPLER, FLAG_NO_GRAPH = 1, 2
+FLAG_FORCE_SEQUENTIAL_SAMPLER, FLAG_NO_GRAPH, FLAG_EXACT_SOFTMAX, FLAG_DEBUG_LOGITS = 1, 2, 4, 8
 
 _lib = None
 
@@ -292,6 +295,8 @@ def load_library(path: str | None = None) -> C.CDLL:
         "pfc_gpu_destroy": (C.c_int, [vp]),
         "pfc_gpu_last_error": (C.c_char_p, [vp]),
         "pfc_gpu_nccl_unique_id": (C.c_int, [u8p]),
+        "pfc_gpu_loopback_id": (C.c_int, [u8p]),
+        "pfc_gpu_debug_logits": (C.c_int, [vp, vp]),
         "pfc_gpu_version": (C.c_char_p, []),
         "pfc_gpu_capacity": (i64, [vp]),
         "pfc_gpu_local_shards": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)]),
@@ -335,6 +340,15 @@ def nccl_unique_id() -> bytes:
     lib = load_library()
     buf = (C.c_uint8 * 128)()
     _check(lib.pfc_gpu_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def loopback_id() -> bytes:
+    """Id of a loopback communicator: world_size CenterShards created in this process (one thread
+    each, e.g. all on cuda:0) act as the ranks of one job (pfc_gpu_loopback_id)."""
+    lib = load_library()
+    buf = (C.c_uint8 * 128)()
+    _check(lib.pfc_gpu_loopback_id(buf))
     return bytes(buf)
 
 
@@ -416,6 +430,13 @@ class CenterShards:
     def stream(self) -> int:
         return _lib.pfc_gpu_stream(self._h)
 
+    def debug_logits(self, batch: int) -> np.ndarray:
+        """Last step's logits z of this rank (FLAG_DEBUG_LOGITS): [B][local shards][cap] float32,
+        -inf where the filter masked the column."""
+        z = np.empty((batch, len(self.local_shards), self.capacity), dtype=np.float32)
+        _check(_lib.pfc_gpu_debug_logits(self._h, _ptr(z)), self._h)
+        return z
+
     def set_phase_timing(self, on: bool):
         _lib.pfc_gpu_set_phase_timing(self._h, 1 if on else 0)
 
@@ -456,7 +477,8 @@ class CenterShards:
                                  _ptr(dx), C.byref(out)), self._h)
         tr = CollectiveTrace(out.allgather_bytes, out.reduce_scalar_bytes, out.reduce_grad_bytes,
                              out.reduce_ops)
-        return StepResult(out.loss, dx, tr, [])
+        return StepResult(out.loss, dx, tr, [], nccl_bytes=out.nccl_bytes,
+                          wire_bytes=out.wire_bytes)
 
     def step_features(self, features_dxb, labels, cfg: StepConfig, iteration_rng: SeededRng,
                       out=None) -> StepResult:

@@ -12,8 +12,12 @@
 // so G = diag(rowscale) E + (sparse positive correction) and no B x cap gradient matrix or
 // logits recompute is needed: the logits GEMM writes E once (bf16), the dX GEMM consumes E
 // (row scale applied in its finalize), and the dW GEMM consumes E against rowscale * x^.
-// A row whose every logit is below o - 80 would underflow; it is flagged as a NumericalError
-// (at s = 64 that needs every cosine of the row, positive included, below -0.98).
+// The offset is either fixed (s <= 64: o = max(0, s - 40), no extra pass) or per row (s > 64, or
+// after a fixed-offset underflow, or forced): o_b = max over the row's unmasked logits across all
+// ranks, taken by a preceding max-only pass of the same GEMM (MaxEpi) -- the reference's own
+// max-subtracted form (shardsim.hpp:270-318), valid for any s > 0.  A fixed-offset row whose sum
+// S_b falls below 1e-20 (every logit far below o) is flagged; the host drop-in then reruns the
+// step with per-row offsets (no update was applied: the dW epilogue skips a failed step).
 //
 //   FwdEpi       rows = batch rows b, cols = buffered classes j: cos tile -> margin + filter
 //                mask -> E (bf16, per-warp TMA stores) + per-(row, column slice) sums of E.
@@ -80,6 +84,8 @@ struct alignas(64) FwdEpi : NoSetup {
   float* epos;      // [B] E of the positive as stored (after OT rounding)
   int* hasval;      // [B] 1 when the row has an unmasked column (filter only)
   OT* E;            // E^T [ncols][lde]: class-major, so the dW GEMM streams whole class blocks
+  const float* offr;  // [B] per-row softmax offset o_b (exact mode), nullptr: the fixed mg.off
+  float* dbgz;      // [B][ncols] debug export of z (masked: -inf), nullptr: off
 
   struct Pre {};
   __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
@@ -97,8 +103,17 @@ struct alignas(64) FwdEpi : NoSetup {
     const int b = t.row0 + row;
     const bool rv = b < B;
     const int pc = rv ? pos_col[b] : -1;
-    const float A = mg.s * kLog2e, O = mg.off * kLog2e;
+    const float A = mg.s * kLog2e;
+    const float O = (offr && rv ? offr[b] : mg.off) * kLog2e;  // this thread's row
+    const double offd = offr && rv ? (double)offr[b] : mg.offd;
     const int wig = row >> 5, lane = row & 31;
+    // fragment-path rows of this thread: t/4 + 8h (ra) and 16 + t/4 + 8h (rb) of the warp's 32
+    float Of[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int bf = t.row0 + wig * 32 + (k >> 1) * 16 + (lane >> 2) + (k & 1) * 8;
+      Of[k] = (offr && bf < B ? offr[bf] : mg.off) * kLog2e;
+    }
     uint8_t* stage = smem + wig * kWarpBytes;
     ST sum = ST(0);
     bool any = false;
@@ -117,7 +132,7 @@ struct alignas(64) FwdEpi : NoSetup {
         // 32 valid negatives in every row of the warp: read the accumulator in the MMA-fragment
         // layout (tcgen05.ld 16x256b), whose bf16x2 pairs are stmatrix.trans operands, so the
         // E^T staging needs no shuffles (stmatrix stores class rows of 8 b values)
-        if (__all_sync(0xffffffffu, colb + 32 <= ncols && (unsigned)(pc - colb) >= 32u)) {
+        if (__all_sync(0xffffffffu, dbgz == nullptr && colb + 32 <= ncols && (unsigned)(pc - colb) >= 32u)) {
           uint32_t ra[16], rb[16];
           pfc_sm100::tmem_ld_16x256b_x4(src.taddr + (uint32_t)c0, ra);
           pfc_sm100::tmem_ld_16x256b_x4(src.taddr + (16u << 16) + (uint32_t)c0, rb);
@@ -126,10 +141,10 @@ struct alignas(64) FwdEpi : NoSetup {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int j = i >> 1, h = i & 1;
-            const float a0 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(ra[4 * j + 2 * h]), A, -O));
-            const float a1 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(ra[4 * j + 2 * h + 1]), A, -O));
-            const float b0 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(rb[4 * j + 2 * h]), A, -O));
-            const float b1 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(rb[4 * j + 2 * h + 1]), A, -O));
+            const float a0 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(ra[4 * j + 2 * h]), A, -Of[h]));
+            const float a1 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(ra[4 * j + 2 * h + 1]), A, -Of[h]));
+            const float b0 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(rb[4 * j + 2 * h]), A, -Of[2 + h]));
+            const float b1 = pfc_sm100::ex2_approx(fmaf(__uint_as_float(rb[4 * j + 2 * h + 1]), A, -Of[2 + h]));
             qs[h] += a0 + a1;
             qs[2 + h] += b0 + b1;
             __nv_bfloat162 x = __floats2bfloat162_rn(a0, a1), y = __floats2bfloat162_rn(b0, b1);
@@ -165,7 +180,7 @@ struct alignas(64) FwdEpi : NoSetup {
       const int jp = pc - colb;
       bool done = false;
       if constexpr (std::is_same<ST, float>::value && !kFilter) {
-        if (colb + 32 <= ncols && (unsigned)jp >= 32u) {  // 32 valid negatives
+        if (dbgz == nullptr && colb + 32 <= ncols && (unsigned)jp >= 32u) {  // 32 valid negatives
           float s1 = 0.f, s2 = 0.f;
 #pragma unroll
           for (int q = 0; q < 32; q += 2) {
@@ -189,8 +204,10 @@ struct alignas(64) FwdEpi : NoSetup {
           if constexpr (std::is_same<ST, float>::value)
             eq = pfc_sm100::ex2_approx(fmaf(v[q], A, -O));
           else
-            eq = exp((double)mg.s * (double)v[q] - mg.offd);
+            eq = exp((double)mg.s * (double)v[q] - offd);
           eq = masked ? ST(0) : eq;
+          if (dbgz && rv && colb + q < ncols)  // debug export of the logit the softmax used
+            dbgz[(size_t)b * ncols + colb + q] = masked ? -INFINITY : mg.s * v[q];
           any = any || !masked;
           e[q] = (float)eq;
           if (q != jp) acc += eq;
@@ -200,7 +217,8 @@ struct alignas(64) FwdEpi : NoSetup {
 #pragma unroll
           for (int q = 0; q < 32; ++q) vp = (q == jp) ? v[q] : vp;
           const double zp = margin_pos(mg, (double)vp);
-          const double ep = exp(zp - mg.offd);
+          const double ep = exp(zp - offd);
+          if (dbgz && rv) dbgz[(size_t)b * ncols + colb + jp] = (float)zp;
           const float eps = round_to(E, (float)ep);
           zpos[b] = zp;
           cpos[b] = (double)vp;
@@ -264,6 +282,55 @@ struct alignas(64) FwdEpi : NoSetup {
       part_s[(size_t)(t.n_tile * NWG + wg) * B + b] = sum;
       if (kFilter && any) hasval[b] = 1;
     }
+  }
+};
+
+// ------------------------------------------------------------------------------------ MaxEpi
+// Max-only pass of the per-row offset mode (same GEMM geometry as FwdEpi): per (row, column
+// slice) the largest unmasked negative cosine (fp32, -inf if none; the filter rule of
+// shardsim.hpp:258-268), and for a local positive its margined logit z_pos (fp64,
+// margin.hpp:41-54) -- the local max of shardsim.hpp:270-281 up to the scale s.
+template <bool kFilter>
+struct MaxEpi : NoSetup {
+  static constexpr int kSmem = 0;
+  int B, ncols;
+  const int32_t* pos_col;
+  MarginDev mg;
+  float tau;
+  float* part_m;  // [n_tiles * NWG][B]
+  double* zpos;   // [B]
+  struct Pre {};
+  __device__ __forceinline__ Pre preload(const TileInfo&, int, int) const { return {}; }
+  __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
+  __device__ __forceinline__ void finish(int, int) const {}
+  template <int BN, int NWG, class Src>
+  __device__ __forceinline__ void run(const TileInfo& t, const Src& src, int row, int wg,
+                                      uint8_t*, const Pre&) const {
+    constexpr int CW = BN / NWG;
+    const int b = t.row0 + row;
+    const bool rv = b < B;
+    const int pc = rv ? pos_col[b] : -1;
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int c0 = wg * CW; c0 < (wg + 1) * CW; c0 += 32) {
+      const int colb = t.col0 + c0;
+      if (colb >= ncols) continue;  // uniform
+      float v[32];
+      src.load(c0, v);
+      const int jp = pc - colb;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const bool use = colb + q < ncols && q != jp && !(kFilter && v[q] > tau);
+        mx = use ? fmaxf(mx, v[q]) : mx;
+      }
+      if ((unsigned)jp < 32u) {
+        float vp = 0.f;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) vp = (q == jp) ? v[q] : vp;
+        zpos[b] = margin_pos(mg, (double)vp);
+      }
+    }
+    if (rv) part_m[(size_t)(t.n_tile * NWG + wg) * B + b] = mx;
   }
 };
 

@@ -214,6 +214,23 @@ __global__ void sum_segments_kernel(const ST* __restrict__ seg, int nseg, int B,
   ls[b] = (ST)s;
 }
 
+// Per-row softmax offset of the exact mode: o_b = max over the row's unmasked logits on this
+// rank (s * the largest negative cosine of the MaxEpi slices, the local positive's z_pos), the
+// rank-local max of shardsim.hpp:270-281; ranks then take the maximum (collective 1, 284-299).
+// A row with nothing unmasked here gets -1e30 (its E values are all masked to 0).
+__global__ void row_offset_kernel(const float* __restrict__ part_m, int T, int B,
+                                  const int32_t* __restrict__ pos_col,
+                                  const double* __restrict__ zpos, MarginDev mg,
+                                  float* __restrict__ offr) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  float m = -INFINITY;
+  for (int t = 0; t < T; ++t) m = fmaxf(m, part_m[(size_t)t * B + b]);
+  double o = (double)mg.s * (double)m;
+  if (pos_col[b] >= 0) o = fmax(o, zpos[b]);
+  offr[b] = isfinite(o) ? (float)o : -1e30f;
+}
+
 // Cross-rank sum in ascending rank order (collectives 1 + 2, shardsim.hpp:284-338), the loss
 // terms, the row scale of G and the positive's correction:
 //   S = sum_r ls[r];  loss_b = log S + o - z_pos;  rowscale = s / (B S)
@@ -226,8 +243,9 @@ __global__ void __launch_bounds__(256) finalize_stats_kernel(
     const ST* __restrict__ ls, int R, const ST* __restrict__ seg, int nseg, int B,
     const double* __restrict__ zpos, const double* __restrict__ cpos,
     const float* __restrict__ epos, const int32_t* __restrict__ pos_col,
-    const int* __restrict__ hasval, int has_filter, MarginDev mg, ST* __restrict__ rowscale,
-    ST* __restrict__ delta, double* __restrict__ loss_row, StepStatus* st) {
+    const int* __restrict__ hasval, int has_filter, MarginDev mg, const float* __restrict__ offr,
+    ST* __restrict__ rowscale, ST* __restrict__ delta, double* __restrict__ loss_row,
+    StepStatus* st) {
   // one warp per row: lanes sum the segments (fixed lane order + fixed shuffle tree), lane 0
   // finishes the row
   const int lane = threadIdx.x & 31;
@@ -253,16 +271,20 @@ __global__ void __launch_bounds__(256) finalize_stats_kernel(
         atomicMin(&st->masked_row, b);
         return;
       }
-      if (!(S > 1e-30) || !isfinite(S)) {
+      // S_b >= 1 with a per-row offset; with the fixed one, a tiny S_b means every logit of the
+      // row sits far below the offset (terms under 2^-126 were flushed): flagged, so the host
+      // drop-in reruns the step with per-row offsets
+      if (!(S > 1e-20) || !isfinite(S)) {
         atomicMin(&st->underflow_row, b);
         return;
       }
+      const double off = offr ? (double)offr[b] : mg.offd;
       const double invB = 1.0 / (double)B;
       const double rs = mg.sd * invB / S;
       rowscale[b] = (ST)rs;
-      loss_row[b] = log(S) + mg.offd - zpos[b];
+      loss_row[b] = log(S) + off - zpos[b];
       if (pos_col[b] >= 0) {
-        const double p = exp(zpos[b] - mg.offd) / S;
+        const double p = exp(zpos[b] - off) / S;
         const double g = (p - 1.0) * invB * margin_deriv_pos(mg, cpos[b]);
         delta[b] = (ST)(g - (double)(ST)rs * (double)epos[b]);
       }
@@ -308,8 +330,11 @@ __global__ void xs_kernel(const StepParams* __restrict__ sp, const float* __rest
     store_out(o + d, d < D ? (float)(rs * (ST)(x[d] * inv)) : 0.f);
 }
 
-// Positive corrections of dwt: poscorr[slot(j)] = sum over rows b with pos_col[b] == j (in
-// ascending b) of delta_b x^_b; pslot[j] = slot for this step's positive columns.
+// Positive corrections of dwt: poscorr[slot(j)] = sum over EVERY row b with pos_col[b] == j (in
+// ascending b, like the reference's dwt accumulation, shardsim.hpp:349-376) of delta_b x^_b;
+// pslot[j] = slot for this step's positive columns.  The batch is scanned in 256-row chunks;
+// each chunk's matching rows are compacted in order and added to the running sums (kept in the
+// output row between chunks, so a label may repeat any number of times).
 __global__ void __launch_bounds__(256) poscorr_kernel(
     const ShardMeta* __restrict__ meta, int cap, int pmax, const int32_t* __restrict__ pos_col,
     int B, const StepParams* __restrict__ sp, const float* __restrict__ xnorm, int D,
@@ -320,41 +345,40 @@ __global__ void __launch_bounds__(256) poscorr_kernel(
   if (i >= meta[kk].npos) return;
   const int col = kk * cap + i, slot = kk * pmax + i;
   __shared__ int rows[256];
-  __shared__ int nrows;
   __shared__ int warp_cnt[8];
-  if (threadIdx.x == 0) nrows = 0;
-  __syncthreads();
-  for (int b0 = 0; b0 < B; b0 += 256) {  // ordered compaction of matching rows
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* out = poscorr + (size_t)slot * D;
+  bool first = true;  // no rows accumulated yet (every positive column has at least one row)
+  for (int b0 = 0; b0 < B; b0 += 256) {
     const int b = b0 + threadIdx.x;
     const bool hit = b < B && pos_col[b] == col;
     const unsigned m = __ballot_sync(0xffffffffu, hit);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) warp_cnt[w] = __popc(m);
     __syncthreads();
-    int before = nrows;
-    for (int q = 0; q < w; ++q) before += warp_cnt[q];
-    if (hit && before + __popc(m & ((1u << lane) - 1)) < 256) rows[before + __popc(m & ((1u << lane) - 1))] = b;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = nrows;
-      for (int q = 0; q < 8; ++q) tot += warp_cnt[q];
-      nrows = min(tot, 256);
+    int before = 0, nr = 0;
+    for (int q = 0; q < 8; ++q) {
+      before += q < w ? warp_cnt[q] : 0;
+      nr += warp_cnt[q];
     }
+    if (hit) rows[before + __popc(m & ((1u << lane) - 1))] = b;
     __syncthreads();
+    if (nr > 0) {  // uniform across the block
+      for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        float acc = first ? 0.f : out[d];
+        for (int q = 0; q < nr; ++q) {
+          const int bb = rows[q];
+          const float n = xnorm[bb];
+          const float xh = sp->x[(size_t)bb * D + d] * (1.0f / (n > 1e-12f ? n : 1e-12f));
+          const float dl = delta_f ? delta_f[bb] : (float)delta_d[bb];
+          acc += dl * xh;
+        }
+        out[d] = acc;
+      }
+      first = false;
+    }
+    __syncthreads();  // rows[] / warp_cnt[] are rewritten by the next chunk
   }
   if (threadIdx.x == 0) pslot[col] = slot;
-  const int nr = nrows;
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float acc = 0.f;
-    for (int q = 0; q < nr; ++q) {
-      const int b = rows[q];
-      const float n = xnorm[b];
-      const float xh = sp->x[(size_t)b * D + d] * (1.0f / (n > 1e-12f ? n : 1e-12f));
-      const float dl = delta_f ? delta_f[b] : (float)delta_d[b];
-      acc += dl * xh;
-    }
-    poscorr[(size_t)slot * D + d] = acc;
-  }
 }
 
 // dX = (r - feat_proj * x^) / max(|x|, 1e-12)  (shardsim.hpp:371-375) with

@@ -26,6 +26,7 @@
 
 #include "../../include/pfc_gpu.h"
 #include "common.cuh"
+#include "comm.cuh"
 #include "epilogues.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
@@ -37,46 +38,6 @@ namespace {
 
 thread_local std::string g_create_error;
 
-// ------------------------------------------------------------------ NCCL (dlopen'ed lazily)
-typedef struct ncclComm* ncclComm_t;
-typedef struct {
-  char internal[128];
-} ncclUniqueId;
-enum { ncclInt8 = 0, ncclInt32 = 2, ncclInt64 = 4, ncclUint64 = 5, ncclFloat32 = 7, ncclFloat64 = 8 };
-enum { ncclSum = 0, ncclMax = 2 };
-struct Nccl {
-  void* h = nullptr;
-  int (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  int (*CommDestroy)(ncclComm_t) = nullptr;
-  int (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-  int (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-  const char* (*GetErrorString)(int) = nullptr;
-  bool load(std::string& err) {
-    if (h) return true;
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    for (const char* n : names)
-      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
-    if (!h) {
-      err = "NCCL not found (dlopen libnccl.so.2 failed)";
-      return false;
-    }
-    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
-    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
-    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
-    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
-    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
-    ReduceScatter = (decltype(ReduceScatter))dlsym(h, "ncclReduceScatter");
-    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-    if (!GetUniqueId || !CommInitRank || !AllGather || !AllReduce || !ReduceScatter) {
-      err = "NCCL symbols missing";
-      return false;
-    }
-    return true;
-  }
-};
-Nccl g_nccl;
 
 // ------------------------------------------------------------------ TMA descriptor encode
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -189,6 +150,7 @@ struct Ctx {
   // features / centres
   float* X = nullptr;  // global batch rows [B][D] fp32 (world > 1 / host path)
   uint64_t step_nccl_bytes = 0;  // bytes handed to NCCL by the last step (pfc_gpu_step_out)
+  uint64_t step_wire_bytes = 0;  // the same collectives under the ring model (all ranks)
   // diagnostics (pfc_gpu_diagnostics), allocated on first use
   void* dwall = nullptr;  // w^ of every local class, operand dtype [rows_pad][Dp]
   double *dwinv = nullptr, *dxinv = nullptr, *dapcs = nullptr;
@@ -217,6 +179,11 @@ struct Ctx {
   float* epos = nullptr;
   int* hasval = nullptr;
   double* loss_row = nullptr;
+  float* offr = nullptr;      // [maxB] per-row softmax offsets (exact mode)
+  float* dbgz = nullptr;      // [maxB][ncols] debug logits (PFC_FLAG_DEBUG_LOGITS)
+  bool exact = false;         // per-row offsets on every step (s > kFixedOffsetMaxScale or forced)
+  bool exact_retry = false;   // this step reruns a fixed-offset step that underflowed
+  bool underflowed = false;   // the last checked step failed with a fixed-offset underflow
   // backward
   void* G = nullptr;       // E^T [ncols_pad][ldg]: exp(z - o) (bf16 / fp32), class-major
   void* xs = nullptr;      // [maxB][Dp] rowscale * x^
@@ -247,7 +214,8 @@ struct Ctx {
     const void* cp_ptr[3] = {nullptr, nullptr, nullptr};  // host pointers the nodes hold
     int64_t gB = -1;
     int64_t glaunches = 0;
-  } gs[2];
+    uint64_t gbytes = 0, gwire = 0;  // collective bytes per replay
+  } gs[4];  // + 2: the per-row offset (exact) variants
   // host drop-in with overlapped copies: X upload + conversion + normalisation run on s2 while
   // the sampler and gather run; dX conversion + download on s2 while the dW GEMM runs
   struct E2E {
@@ -260,14 +228,21 @@ struct Ctx {
   // tensor maps cached per batch
   int64_t tm_B = -1;
   CUtensorMap tm_x_k, tm_w_k, tm_e_st, tm_e_k, tm_w_mn, tm_e_mn, tm_xs_mn;
-  // nccl
+  // collectives: NCCL communicator, or the loopback group (comm.cuh)
   ncclComm_t comm = nullptr;
+  std::shared_ptr<LoopGroup> loop;
+  uint8_t loop_id[128] = {};
   // bookkeeping
   int64_t lastB = 0;
   int64_t launches = 0;
   PhaseTimer pt;
   std::vector<void*> allocs;
 };
+
+// Largest margin scale that keeps the fixed softmax offset o = max(0, s - 40): above it every
+// step takes per-row offsets from a max-only pass (epilogues.cuh header).
+constexpr double kFixedOffsetMaxScale = 64.0;
+inline bool exact_now(const Ctx* c) { return c->exact || c->exact_retry; }
 
 int fail(Ctx* c, int code, const char* fmt, ...) {
   char buf[1024];
@@ -294,6 +269,47 @@ int fail(Ctx* c, int code, const char* fmt, ...) {
     if (r_ != 0)                                                                            \
       return fail((c), PFC_ERR_NCCL, "NCCL error %d (%s) at %s:%d", r_,                     \
                   g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "?", __FILE__, __LINE__); \
+  } while (0)
+
+// One collective through the context's communicator.  kind 0: all-gather (count per rank),
+// 1: all-reduce (count), 2: reduce-scatter (count per rank).  The bytes this rank hands to it
+// (the larger of its send and receive buffers) are added to the step's accounting.
+int comm_call(Ctx* c, int kind, const void* send, void* recv, size_t count, CommDt dt, CommOp op,
+              cudaStream_t s) {
+  const uint64_t es = dt_size(dt);
+  const uint64_t S = (kind == 1 ? 1 : (uint64_t)c->R) * (uint64_t)count * es;  // whole buffer
+  c->step_nccl_bytes += S;
+  c->step_wire_bytes += (kind == 1 ? 2 : 1) * (uint64_t)(c->R - 1) * S;
+  if (c->loop) {
+    const cudaError_t e = loop_collective(*c->loop, c->rank, kind, send, recv, count, dt, op, s);
+    if (e != cudaSuccess)
+      return fail(c, PFC_ERR_CUDA, "loopback collective failed: %s", cudaGetErrorString(e));
+    return PFC_OK;
+  }
+  int r;
+  if (kind == 0) r = g_nccl.AllGather(send, recv, count, nccl_dt(dt), c->comm, s);
+  else if (kind == 1) r = g_nccl.AllReduce(send, recv, count, nccl_dt(dt), nccl_op(op), c->comm, s);
+  else r = g_nccl.ReduceScatter(send, recv, count, nccl_dt(dt), nccl_op(op), c->comm, s);
+  if (r != 0)
+    return fail(c, PFC_ERR_NCCL, "NCCL error %d (%s)", r,
+                g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+  return PFC_OK;
+}
+inline int comm_all_gather(Ctx* c, const void* send, void* recv, size_t count, CommDt dt,
+                           cudaStream_t s) {
+  return comm_call(c, 0, send, recv, count, dt, kSum, s);
+}
+inline int comm_all_reduce(Ctx* c, const void* send, void* recv, size_t count, CommDt dt,
+                           CommOp op, cudaStream_t s) {
+  return comm_call(c, 1, send, recv, count, dt, op, s);
+}
+inline int comm_reduce_scatter(Ctx* c, const void* send, void* recv, size_t count, CommDt dt,
+                               CommOp op, cudaStream_t s) {
+  return comm_call(c, 2, send, recv, count, dt, op, s);
+}
+#define COMM_TRY(expr)               \
+  do {                               \
+    if (int rc_ = (expr)) return rc_; \
   } while (0)
 
 template <typename T>
@@ -486,8 +502,32 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const float tau = (float)c->d.filter_threshold;
   const bool filt = c->d.has_filter != 0;
   if (e2e) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_x, 0));
-  // ---- logits GEMM + margin + E = exp(z - o) and its per-slice row sums (shardsim.hpp:249-318)
   const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, FBN, 1, 0, kUmma ? 128 * kFwdCG : 128);
+  const bool exact = exact_now(c);
+  if (exact) {
+    // ---- per-row offsets: max-only pass of the logits GEMM -> o_b (rank max: collective 1,
+    // shardsim.hpp:270-299).  Its slice maxima reuse the row-sum slices (consumed before the
+    // logits pass rewrites them).
+    float* pm = reinterpret_cast<float*>(c->part_s);
+    cudaError_t err;
+    auto go = [&](auto e) {
+      if constexpr (kUmma)
+        return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), kFwdCG>(c, c->tm_x_k, c->tm_w_k, gf, e);
+      else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
+                                            (const float*)c->wh, (int)c->Dp, gf, e);
+    };
+    if (filt) err = go(MaxEpi<true>{{}, (int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, c->zpos});
+    else err = go(MaxEpi<false>{{}, (int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, c->zpos});
+    CUDA_TRY(c, err);
+    row_offset_kernel<<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(pm, gf.n_tiles * NWG, (int)B,
+                                                              c->pos_col, c->zpos, c->mg, c->offr);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    if (c->R > 1) COMM_TRY(comm_all_reduce(c, c->offr, c->offr, B, kF32, kMax, s));
+    phase(c, "row_offsets");
+  }
+  const float* offr = exact ? c->offr : nullptr;
+  // ---- logits GEMM + margin + E = exp(z - o) and its per-slice row sums (shardsim.hpp:249-318)
   {
     cudaError_t err;
     auto go = [&](auto e) {
@@ -498,10 +538,12 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     };
     if (filt)
       err = go(FwdEpi<ST, OT, true, kUmma>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
-                                           c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E});
+                                           c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E,
+                                           offr, c->dbgz});
     else
       err = go(FwdEpi<ST, OT, false, kUmma>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
-                                            c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E});
+                                            c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E,
+                                            offr, c->dbgz});
     CUDA_TRY(c, err);
   }
   phase(c, "logits_gemm");
@@ -519,16 +561,16 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     c->launches++;
   }
   if (c->R > 1) {
-    const int dt = sizeof(ST) == 8 ? ncclFloat64 : ncclFloat32;
-    NCCL_TRY(c, g_nccl.AllGather(ls + c->rank * B, ls, B, dt, c->comm, s));
-    NCCL_TRY(c, g_nccl.AllReduce(c->zpos, c->zpos, B, ncclFloat64, ncclSum, c->comm, s));
-    if (filt) NCCL_TRY(c, g_nccl.AllReduce(c->hasval, c->hasval, B, ncclInt32, ncclSum, c->comm, s));
+    const CommDt dt = sizeof(ST) == 8 ? kF64 : kF32;
+    COMM_TRY(comm_all_gather(c, ls + c->rank * B, ls, B, dt, s));
+    COMM_TRY(comm_all_reduce(c, c->zpos, c->zpos, B, kF64, kSum, s));
+    if (filt) COMM_TRY(comm_all_reduce(c, c->hasval, c->hasval, B, kI32, kSum, s));
   }
   ST* rsc = static_cast<ST*>(c->rowscale);
   ST* dlt = static_cast<ST*>(c->delta);
   finalize_stats_kernel<ST><<<(unsigned)ceil_div(B * 32, 256), 256, 0, s>>>(
       ls, c->R, c->R > 1 ? nullptr : seg, nseg, (int)B, c->zpos, c->cpos, c->epos, c->pos_col,
-      c->hasval, filt ? 1 : 0, c->mg, rsc, dlt, c->loss_row, c->st);
+      c->hasval, filt ? 1 : 0, c->mg, offr, rsc, dlt, c->loss_row, c->st);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   phase(c, "softmax_stats");
@@ -573,7 +615,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     CUDA_TRY(c, cudaEventRecord(c->ev_dx, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_dx, 0));
     if (c->R > 1)  // the drop-in returns the FULL summed d_features on every rank
-      NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, c->s2));
+      COMM_TRY(comm_all_reduce(c, c->dX, c->dX, B * c->D, kF32, kSum, c->s2));
     dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
     dx_to_dxb_kernel<<<grid, blk, 0, c->s2>>>(c->dX, (int)c->D, (int)B, c->xdb);
     c->launches++;
@@ -635,14 +677,8 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
 int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gpu_step_args* a,
              float* dx_full) {
   c->lastB = B;
-  // NCCL payload of the pipeline: stats exchange (+ the host drop-in's dX all-reduce)
-  c->step_nccl_bytes = 0;
-  if (c->R > 1) {
-    const uint64_t sb = c->bf16 ? 4 : 8, b = (uint64_t)B;
-    c->step_nccl_bytes = (uint64_t)c->R * b * sb + b * 8 + (c->d.has_filter ? b * 4 : 0) +
-                         (c->e2e.on ? b * (uint64_t)c->D * 4 : 0);
-  }
-  const bool graph = !(c->d.flags & PFC_FLAG_NO_GRAPH) && !c->pt.enabled;
+  // the loopback communicator synchronises host threads: it cannot be captured
+  const bool graph = !(c->d.flags & PFC_FLAG_NO_GRAPH) && !c->pt.enabled && !c->loop;
   auto pipeline = [&]() {
     c->launches = 0;
     if (c->bf16) return run_pipeline<float, __nv_bfloat16, true>(c, x, lab, B, a, dx_full);
@@ -655,8 +691,9 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
     }
     return pipeline();
   }
-  Ctx::GraphSlot& G = c->gs[c->e2e.on ? 1 : 0];
+  Ctx::GraphSlot& G = c->gs[(c->e2e.on ? 1 : 0) + (exact_now(c) ? 2 : 0)];
   if (!G.gexec || G.gB != B) {  // capture the step once per batch size
+    const uint64_t bytes0 = c->step_nccl_bytes, wire0 = c->step_wire_bytes;
     if (G.gexec) {
       cudaGraphExecDestroy(G.gexec);
       cudaGraphDestroy(G.graph);
@@ -699,6 +736,10 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
       return fail(c, PFC_ERR_CUDA, "graph capture lost a host copy node");
     G.gB = B;
     G.glaunches = c->launches;
+    G.gbytes = c->step_nccl_bytes - bytes0;
+    G.gwire = c->step_wire_bytes - wire0;
+    c->step_nccl_bytes = bytes0;
+    c->step_wire_bytes = wire0;
     G.psmem = c->sort_smem;
     G.cp_ptr[0] = G.cp_ptr[1] = G.cp_ptr[2] = nullptr;
   }
@@ -740,6 +781,8 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
   }
   CUDA_TRY(c, cudaGraphLaunch(G.gexec, c->stream));
   c->launches = G.glaunches;
+  c->step_nccl_bytes += G.gbytes;  // the collectives the graph replays
+  c->step_wire_bytes += G.gwire;
   return PFC_OK;
 }
 
@@ -756,6 +799,7 @@ void trace_closed_form(Ctx* c, int64_t B, pfc_gpu_step_out* o) {
 // Check the device status block; map to the reference's error types and messages.
 int check_status(Ctx* c, int64_t step_index, int64_t B, pfc_gpu_step_out* out) {
   const StepStatus& st = *c->st_host;
+  c->underflowed = false;
   if (st.batch_too_large)
     return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: global batch %lld exceeds the supported %d",
                 (long long)B, kMaxSortBatch);
@@ -778,11 +822,15 @@ int check_status(Ctx* c, int64_t step_index, int64_t B, pfc_gpu_step_out* out) {
   if (st.masked_row != 0x7fffffff)
     return fail(c, PFC_ERR_CONTRACT,
                 "distributed_partial_step: all buffer columns masked for row %d", st.masked_row);
-  if (st.underflow_row != 0x7fffffff)
+  if (st.underflow_row != 0x7fffffff) {
+    c->underflowed = !exact_now(c);
     return fail(c, PFC_ERR_NUMERICAL,
-                "pfc_gpu: row %d: every logit is below the fixed softmax offset range "
-                "(exp(z - max(0, s - 40)) underflows); use PFC_PRECISION_FP32 semantics",
+                "pfc_gpu: row %d: every logit lies far below the fixed softmax offset "
+                "max(0, s - 40) (no update was applied); the synchronous step calls rerun such a "
+                "step with per-row offsets, asynchronous device steps report it (create the "
+                "context with PFC_FLAG_EXACT_SOFTMAX to always use per-row offsets)",
                 st.underflow_row);
+  }
   if (st.nonfinite_loss)
     return fail(c, PFC_ERR_NUMERICAL, "distributed_partial_step: non-finite loss at step %lld",
                 (long long)step_index);
@@ -794,9 +842,25 @@ int check_status(Ctx* c, int64_t step_index, int64_t B, pfc_gpu_step_out* out) {
     out->loss = st.loss;
     out->rejection_shards = st.rejection_shards;
   out->nccl_bytes = c->step_nccl_bytes;
+    out->wire_bytes = c->step_wire_bytes;
     trace_closed_form(c, B, out);
   }
   return PFC_OK;
+}
+
+// Runs a synchronous step; when it failed only because the fixed softmax offset underflowed
+// (nothing was updated), reruns it with per-row offsets.  Every rank sees the same global row
+// sums, so all ranks take the same branch (their collectives stay matched).
+template <class F>
+int with_exact_retry(Ctx* c, F&& once) {
+  int rc = once();
+  if (rc == PFC_ERR_NUMERICAL && c->underflowed) {
+    c->exact_retry = true;
+    c->reset_status = true;
+    rc = once();
+    c->exact_retry = false;
+  }
+  return rc;
 }
 
 int finish_phase_timing(Ctx* c) {
@@ -1022,6 +1086,21 @@ const char* pfc_gpu_last_error(const void* ctx) {
   return static_cast<const Ctx*>(ctx)->err.c_str();
 }
 
+int pfc_gpu_loopback_id(uint8_t out[128]) {
+  loop_new_id(out);
+  return PFC_OK;
+}
+
+int pfc_gpu_debug_logits(void* ctx, float* out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c->dbgz)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_debug_logits: create with PFC_FLAG_DEBUG_LOGITS");
+  CUDA_TRY(c, cudaMemcpyAsync(out, c->dbgz, sizeof(float) * c->lastB * c->ncols,
+                              cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PFC_OK;
+}
+
 int pfc_gpu_nccl_unique_id(uint8_t out[128]) {
   std::string e;
   if (!g_nccl.load(e)) return fail(nullptr, PFC_ERR_NCCL, "%s", e.c_str());
@@ -1064,6 +1143,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->mg.md = desc->margin_m;
   c->mg.offd = std::max(0.0, desc->margin_scale - 40.0);  // E = exp(z - o) <= e^40
   c->mg.off = (float)c->mg.offd;
+  c->exact = desc->margin_scale > kFixedOffsetMaxScale || (desc->flags & PFC_FLAG_EXACT_SOFTMAX);
   int64_t B = c->maxB;
   auto bail = [&](int rc) {
     g_create_error = c->err;
@@ -1126,6 +1206,9 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->epos, (size_t)B));
   CT(dalloc(c, &c->hasval, (size_t)B));
   CT(dalloc(c, &c->loss_row, (size_t)B));
+  CT(dalloc(c, &c->offr, (size_t)B));
+  if (desc->flags & PFC_FLAG_DEBUG_LOGITS)
+    CT(dalloc(c, &c->dbgz, (size_t)B * std::max<int64_t>(c->ncols, 1)));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->xs), (size_t)B * c->Dp * ob));
   c->pmax = std::max<int64_t>(1, std::min<int64_t>(c->cap, B));
@@ -1140,17 +1223,25 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(cudaMallocHost(&c->st_host, sizeof(StepStatus)));
   for (int i = 0; i <= PhaseTimer::kMax; ++i) CT(cudaEventCreate(&c->pt.ev[i]));
   if (c->R > 1) {
-    std::string e;
-    if (!g_nccl.load(e)) return bail(fail(c, PFC_ERR_NCCL, "%s", e.c_str()));
     if (!desc->nccl_id) return bail(fail(c, PFC_ERR_NCCL, "world_size > 1 needs nccl_id"));
-    ncclUniqueId id;
-    std::memcpy(id.internal, desc->nccl_id, 128);
-    const int r = g_nccl.CommInitRank(&c->comm, c->R, id, c->rank);
-    if (r != 0) return bail(fail(c, PFC_ERR_NCCL, "ncclCommInitRank failed (%d)", r));
+    std::string e;
+    if (is_loop_id(desc->nccl_id)) {  // R ranks as R contexts of this process (comm.cuh)
+      std::memcpy(c->loop_id, desc->nccl_id, 128);
+      const size_t scratch = (size_t)B * (size_t)std::max<int64_t>(c->D * 4, 3 * 8);
+      c->loop = loop_join(c->loop_id, c->R, c->rank, desc->device, scratch, e);
+      if (!c->loop) return bail(fail(c, PFC_ERR_NCCL, "%s", e.c_str()));
+    } else {
+      if (!g_nccl.load(e)) return bail(fail(c, PFC_ERR_NCCL, "%s", e.c_str()));
+      ncclUniqueId id;
+      std::memcpy(id.internal, desc->nccl_id, 128);
+      const int r = g_nccl.CommInitRank(&c->comm, c->R, id, c->rank);
+      if (r != 0) return bail(fail(c, PFC_ERR_NCCL, "ncclCommInitRank failed (%d)", r));
+    }
     // one collective outside any graph capture: NCCL may set up its connections lazily at the
     // first collective, which the step's captured graph must not be the one to trigger
-    const int w = g_nccl.AllReduce(c->st, c->st, 1, ncclInt32, ncclMax, c->comm, c->stream);
-    if (w != 0) return bail(fail(c, PFC_ERR_NCCL, "NCCL warm-up all-reduce failed (%d)", w));
+    if (comm_all_reduce(c, c->st, c->st, 1, kI32, kMax, c->stream) != PFC_OK)
+      return bail(fail(c, PFC_ERR_NCCL, "warm-up all-reduce failed: %s", c->err.c_str()));
+    c->step_nccl_bytes = c->step_wire_bytes = 0;
   }
   CT(cudaStreamSynchronize(c->stream));
 #undef CT
@@ -1169,6 +1260,7 @@ int pfc_gpu_destroy(void* ctx) {
   for (cudaEvent_t e : {c->ev_s, c->ev_x, c->ev_dx, c->ev_out})
     if (e) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->loop) loop_leave(c->loop, c->loop_id, c->rank);
   for (void* p : c->allocs) cudaFree(p);
   if (c->st_host) cudaFreeHost(c->st_host);
   for (int i = 0; i <= PhaseTimer::kMax; ++i)
@@ -1453,15 +1545,13 @@ static bool pinned(const void* p) {
 
 // The step on a FeatureBatch already on the device: D x B fp64 features in c->xdb, labels in
 // c->labels.  Leaves the summed D x B fp64 d_features in c->xdb; synchronous.
-static int step_from_xdb(Ctx* c, int64_t B, const pfc_gpu_step_args* a, pfc_gpu_step_out* out) {
+static int step_from_X(Ctx* c, int64_t B, const pfc_gpu_step_args* a, pfc_gpu_step_out* out) {
   cudaStream_t s = c->stream;
   dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
-  x_from_dxb_kernel<<<grid, blk, 0, s>>>(c->xdb, (int)c->D, (int)B, c->X);
   if (int rc = run_step(c, c->X, c->labels, B, a, c->dX)) return rc;
   c->reset_status = true;
   if (c->R > 1) {  // the drop-in returns the FULL summed d_features on every rank
-    NCCL_TRY(c, g_nccl.AllReduce(c->dX, c->dX, B * c->D, ncclFloat32, ncclSum, c->comm, s));
-    c->step_nccl_bytes += (uint64_t)B * c->D * 4;
+    COMM_TRY(comm_all_reduce(c, c->dX, c->dX, B * c->D, kF32, kSum, s));
   }
   dx_to_dxb_kernel<<<grid, blk, 0, s>>>(c->dX, (int)c->D, (int)B, c->xdb);
   CUDA_TRY(c, cudaGetLastError());
@@ -1469,6 +1559,14 @@ static int step_from_xdb(Ctx* c, int64_t B, const pfc_gpu_step_args* a, pfc_gpu_
   CUDA_TRY(c, cudaStreamSynchronize(s));
   if (int rc = finish_phase_timing(c)) return rc;
   return check_status(c, a->step_index, B, out);
+}
+static int step_from_xdb(Ctx* c, int64_t B, const pfc_gpu_step_args* a, pfc_gpu_step_out* out) {
+  dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
+  x_from_dxb_kernel<<<grid, blk, 0, c->stream>>>(c->xdb, (int)c->D, (int)B, c->X);
+  CUDA_TRY(c, cudaGetLastError());
+  c->step_nccl_bytes = c->step_wire_bytes = 0;
+  // the features stay in c->X (c->xdb receives d_features), so a rerun starts from there
+  return with_exact_retry(c, [&] { return step_from_X(c, B, a, out); });
 }
 
 int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
@@ -1482,16 +1580,19 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
     // The host-side label / capacity check runs while the GPU works: the device sampler makes
     // the same checks and skips every update on failure, so launching first is safe.
     // On an error the contents of dxdb are unspecified (the reference throws instead).
-    c->e2e = {true, xdb, labels, dxdb};
-    const int rc = run_step(c, c->X, dev_view(labels), B, a, c->dX);
-    c->e2e.on = false;
-    if (rc) return rc;
-    c->reset_status = true;  // the status download is part of the step (run_pipeline)
-    const int vrc = host_validate(c, labels, B);
-    CUDA_TRY(c, cudaStreamSynchronize(s));
-    if (int rc2 = finish_phase_timing(c)) return rc2;
-    if (vrc) return vrc;
-    return check_status(c, a->step_index, B, out);
+    c->step_nccl_bytes = c->step_wire_bytes = 0;
+    return with_exact_retry(c, [&]() -> int {
+      c->e2e = {true, xdb, labels, dxdb};
+      const int rc = run_step(c, c->X, dev_view(labels), B, a, c->dX);
+      c->e2e.on = false;
+      if (rc) return rc;
+      c->reset_status = true;  // the status download is part of the step (run_pipeline)
+      const int vrc = host_validate(c, labels, B);
+      CUDA_TRY(c, cudaStreamSynchronize(s));
+      if (int rc2 = finish_phase_timing(c)) return rc2;
+      if (vrc) return vrc;
+      return check_status(c, a->step_index, B, out);
+    });
   }
   if (int rc = host_validate(c, labels, B)) return rc;
   if (B == 0)
@@ -1507,6 +1608,10 @@ int pfc_gpu_step(void* ctx, const double* xdb, const int64_t* labels, int64_t B,
   return PFC_OK;
 }
 
+static int step_device_once(Ctx* c, const float* x_local, const int64_t* labels_local,
+                            int64_t b_local, const pfc_gpu_step_args* a, float* dx_local,
+                            pfc_gpu_step_out* out);
+
 int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_local,
                         int64_t b_local, const pfc_gpu_step_args* a, float* dx_local,
                         pfc_gpu_step_out* out) {
@@ -1516,24 +1621,31 @@ int pfc_gpu_step_device(void* ctx, const float* x_local, const int64_t* labels_l
   if (B < 1 || B > c->maxB)
     return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: global batch %lld outside [1, max_batch=%lld]",
                 (long long)B, (long long)c->maxB);
+  c->step_nccl_bytes = c->step_wire_bytes = 0;
+  if (!out) return step_device_once(c, x_local, labels_local, b_local, a, dx_local, out);
+  return with_exact_retry(
+      c, [&] { return step_device_once(c, x_local, labels_local, b_local, a, dx_local, out); });
+}
+
+static int step_device_once(Ctx* c, const float* x_local, const int64_t* labels_local,
+                            int64_t b_local, const pfc_gpu_step_args* a, float* dx_local,
+                            pfc_gpu_step_out* out) {
+  const int64_t B = b_local * c->R;
   cudaStream_t s = c->stream;
   const float* x = x_local;
   const int64_t* lab = labels_local;
   float* dxf = dx_local;
   if (c->R > 1) {  // feature all-gather (rank-major, all_gather_features shardsim.hpp:86-115)
-    NCCL_TRY(c, g_nccl.AllGather(x_local, c->X, b_local * c->D, ncclFloat32, c->comm, s));
-    NCCL_TRY(c, g_nccl.AllGather(labels_local, c->labels, b_local, ncclInt64, c->comm, s));
+    COMM_TRY(comm_all_gather(c, x_local, c->X, b_local * c->D, kF32, s));
+    COMM_TRY(comm_all_gather(c, labels_local, c->labels, b_local, kI64, s));
     x = c->X;
     lab = c->labels;
     dxf = c->dX;
   }
   if (int rc = run_step(c, x, lab, B, a, dxf)) return rc;
-  if (c->R > 1)  // feature + label all-gathers, dX reduce-scatter
-    c->step_nccl_bytes += (uint64_t)B * c->D * 4 * 2 + (uint64_t)B * 8;
   c->reset_status = false;  // errors stay on the device until a synchronous check
   if (c->R > 1)  // collective 3 (shardsim.hpp:387-399) as a reduce-scatter to the owners
-    NCCL_TRY(c, g_nccl.ReduceScatter(c->dX, dx_local, b_local * c->D, ncclFloat32, ncclSum,
-                                     c->comm, s));
+    COMM_TRY(comm_reduce_scatter(c, c->dX, dx_local, b_local * c->D, kF32, kSum, s));
   if (!out) return PFC_OK;
   CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -1567,9 +1679,9 @@ static int diagnostics_device(Ctx* c, int64_t B, bool split, pfc_gpu_diag_out* o
                          : run_diagnostics<float, false>(c, B, split);
   if (rc) return rc;
   if (c->R > 1) {  // merge over ranks: maxima, sibling flags, the owner's apcs term
-    NCCL_TRY(c, g_nccl.AllReduce(c->demax, c->demax, B * 3, ncclUint64, ncclMax, c->comm, s));
-    NCCL_TRY(c, g_nccl.AllReduce(c->dhasc, c->dhasc, B, ncclInt32, ncclMax, c->comm, s));
-    NCCL_TRY(c, g_nccl.AllReduce(c->dapcs, c->dapcs, B, ncclFloat64, ncclSum, c->comm, s));
+    COMM_TRY(comm_all_reduce(c, c->demax, c->demax, B * 3, kU64, kMax, s));
+    COMM_TRY(comm_all_reduce(c, c->dhasc, c->dhasc, B, kI32, kMax, s));
+    COMM_TRY(comm_all_reduce(c, c->dapcs, c->dapcs, B, kF64, kSum, s));
   }
   std::vector<unsigned long long> em((size_t)B * 3);
   std::vector<int> hc((size_t)B);

@@ -1,5 +1,8 @@
 """Shared test helpers: build device shards from oracle state and compare per the tolerance
 contract of SURVEY.md §8(c) / DESIGN.md."""
+import hashlib
+import os
+
 import numpy as np
 
 import paper_2203_15565_b200 as p
@@ -45,3 +48,32 @@ def rel_fro(a, b):
 
 def rel_max(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the sources each prebuilt parity program embeds a hash of (oracle/Makefile *_SRCS, same order)
+PARITY_SOURCES = {
+    "adapter_parity": ["oracle/adapter_parity.cpp", "include/pfc/gpu_step.hpp", "include/pfc_gpu.h"],
+    "trainer_parity": ["oracle/trainer_parity.cpp", "include/pfc/gpu_trainer.hpp",
+                       "include/pfc/gpu_step.hpp", "include/pfc_gpu.h"],
+    "trainer_bench": ["oracle/trainer_bench.cpp", "include/pfc/gpu_trainer.hpp",
+                      "include/pfc/gpu_step.hpp", "include/pfc_gpu.h"],
+}
+
+
+def source_hash(name: str) -> str:
+    h = hashlib.sha256()
+    for f in PARITY_SOURCES[name]:
+        with open(os.path.join(ROOT, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def assert_fresh_binary(exe: str) -> None:
+    """A prebuilt parity program must come from the current sources (it cannot be rebuilt on a
+    box without the reference headers)."""
+    import subprocess
+    name = os.path.basename(exe)
+    got = subprocess.run([exe, "--source-hash"], capture_output=True, text=True, timeout=60).stdout.strip()
+    assert got == source_hash(name), (f"{exe} is stale (built from sources {got}, current "
+                                      f"{source_hash(name)}): rebuild with make -C oracle")

@@ -63,5 +63,5 @@ def test_layout_and_capacity_mirror(port):
 def test_header_structs_match_ctypes_layout():
     # offsets of the C structs must match the ctypes mirrors (plain C, no padding surprises)
     assert ctypes.sizeof(p.StepArgs) == 32
-    assert ctypes.sizeof(p.StepOut) == 64
+    assert ctypes.sizeof(p.StepOut) == 72
     assert p.Desc.flags.offset > p.Desc.nccl_id.offset

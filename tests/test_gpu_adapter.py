@@ -19,6 +19,8 @@ EXE = os.path.join(ROOT, "oracle", "_ref", "adapter_parity")
 
 @pytest.mark.skipif(not os.path.exists(EXE), reason="oracle/_ref/adapter_parity not built")
 def test_cpp_dropin_matches_reference_step():
+    from tests.helpers import assert_fresh_binary
+    assert_fresh_binary(EXE)
     p = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

@@ -22,6 +22,8 @@ EXE = os.path.join(ROOT, "oracle", "_ref", "trainer_parity")
 
 @pytest.mark.skipif(not os.path.exists(EXE), reason="oracle/_ref/trainer_parity not built")
 def test_gpu_train_matches_reference_train():
+    from tests.helpers import assert_fresh_binary
+    assert_fresh_binary(EXE)
     p = subprocess.run([EXE], capture_output=True, text=True, timeout=900)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

@@ -19,6 +19,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <optional>
 #include <string>
@@ -199,12 +200,19 @@ inline StepResult distributed_partial_step(std::vector<CenterShard>& shards,
   // one cached session per thread, rebuilt when the shape or the step-invariant config changes
   thread_local std::unique_ptr<Session> cached;
   thread_local std::string key;
+  // keyed on the exact bits of every double (std::to_string keeps 6 decimals), with the
+  // filter's presence encoded separately from its threshold
+  auto bits = [](double v) {
+    uint64_t u;
+    std::memcpy(&u, &v, sizeof u);
+    return std::to_string(u);
+  };
   const std::string k = std::to_string(layout.num_classes) + "/" + std::to_string(K) + "/" +
                         std::to_string(dim) + "/" + std::to_string(batch.batch()) + "/" +
-                        std::to_string(cfg.r) + "/" + std::to_string((int)cfg.margin.kind) + "/" +
-                        std::to_string(cfg.margin.scale) + "/" + std::to_string(cfg.margin.margin) +
-                        "/" + std::to_string(cfg.filter_threshold.value_or(-1.0)) + "/" +
-                        std::to_string(cfg.momentum) + "/" + std::to_string(cfg.weight_decay);
+                        bits(cfg.r) + "/" + std::to_string((int)cfg.margin.kind) + "/" +
+                        bits(cfg.margin.scale) + "/" + bits(cfg.margin.margin) + "/" +
+                        (cfg.filter_threshold ? "f" + bits(*cfg.filter_threshold) : "nf") + "/" +
+                        bits(cfg.momentum) + "/" + bits(cfg.weight_decay);
   if (!cached || key != k) {
     cached.reset();
     cached = std::make_unique<Session>(layout, dim, cfg, std::max<int64_t>(batch.batch(), 1));

@@ -21,7 +21,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pfc_gpu.h"
@@ -37,6 +40,22 @@ namespace pfc {
 namespace {
 
 thread_local std::string g_create_error;
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (device, kernel): a process may hold
+// contexts on several devices (and create them from several threads), so the attribute is
+// set once per pair under a lock rather than once per process.
+cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, fn})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({dev, fn});
+  return e;
+}
 
 
 // ------------------------------------------------------------------ TMA descriptor encode
@@ -338,12 +357,7 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
   auto kern = umma_gemm_kernel<BN, STAGES, NWG, A_MN, B_MN, Epi, CG>;
   constexpr int smem = umma_smem_bytes<BN, STAGES, NWG, Epi, CG>();
   static_assert(smem <= 232448, "shared memory budget");
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem)) return e;
   const int total = g.total();
   if (total <= 0) return cudaSuccess;
   constexpr int kCl = CG > Epi::kCluster ? CG : Epi::kCluster;
@@ -380,13 +394,8 @@ template <bool A_MN, bool B_MN, class Epi>
 cudaError_t launch_simt(Ctx* c, const float* A, int lda, const float* Bm, int ldb,
                         const GemmGeom& g, const Epi& epi) {
   auto kern = simt_gemm_kernel<A_MN, B_MN, Epi>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimtSmemBytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), kSimtSmemBytes))
+    return e;
   if (g.total() <= 0) return cudaSuccess;
   kern<<<g.total(), 128, kSimtSmemBytes, c->stream>>>(A, lda, Bm, ldb, g, epi);
   c->launches++;
@@ -456,12 +465,8 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   while (P2 < B) P2 <<= 1;
   // keys + sorted unique labels (int32) + the staged batch labels (int64)
   const size_t sort_smem = (2 * sizeof(int32_t) + sizeof(int64_t)) * (size_t)P2;
-  static bool sort_cfg = false;
-  if (!sort_cfg) {
-    CUDA_TRY(c, cudaFuncSetAttribute(positives_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((2 * sizeof(int32_t) + sizeof(int64_t)) * kMaxSortBatch)));
-    sort_cfg = true;
-  }
+  CUDA_TRY(c, ensure_smem_attr(reinterpret_cast<const void*>(positives_kernel),
+                               (int)((2 * sizeof(int32_t) + sizeof(int64_t)) * kMaxSortBatch)));
   c->sort_smem = sort_smem;
   positives_kernel<<<1, 1024, sort_smem, s>>>(
       c->st, c->sp, a->seed, a->stream_id, (float)a->lr, c->reset_status ? 1 : 0, x, lab, dx_full,
@@ -2058,6 +2063,8 @@ int pfc_gpu_trainer_get_backbone(void* tr, double* w1, double* b1, double* w2, d
   auto* t = static_cast<Trainer*>(tr);
   Ctx* c = t->c;
   cudaStream_t s = c->stream;
+  // a pending non-finite product surfaces here, before anything (a checkpoint) is written
+  if (int rc = trainer_check(t, t->B)) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(w1, t->w1, sizeof(double) * t->H * t->in_dim, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaMemcpyAsync(b1, t->b1, sizeof(double) * t->H, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaMemcpyAsync(w2, t->w2, sizeof(double) * t->E * t->H, cudaMemcpyDeviceToHost, s));
@@ -2141,6 +2148,9 @@ int pfc_gpu_trainer_apply_gradient(void* tr, double lr) {
   CUDA_TRY(c, bb_matmul<kBbPlain>(t, dout, B, 1, t->hidden, 1, B, t->dw2, E, H, B, nullptr, 2));
   CUDA_TRY(c, bb_matmul<kBbTanhGrad>(t, t->w2, 1, H, dout, B, 1, t->dhid, H, B, E, t->hidden, 3));
   CUDA_TRY(c, bb_matmul<kBbPlain>(t, t->dhid, B, 1, t->inputs, 1, B, t->dw1, H, I, B, nullptr, 4));
+  // matmul's require_finite throws before apply_gradient touches w1/w2 (matrix.hpp:103,
+  // trainer.hpp:98-124): the products' flags are read before the SGD rows run
+  if (int rc = trainer_check(t, B)) return rc;
   // SGD, w2 rows then w1 rows (trainer.hpp:113-124)
   bb_sgd_rows_kernel<<<(unsigned)E, 128, 0, c->stream>>>(t->w2, t->b2, t->dw2, dout, (int)H, (int)B, lr);
   bb_sgd_rows_kernel<<<(unsigned)H, 128, 0, c->stream>>>(t->w1, t->b1, t->dw1, t->dhid, (int)I, (int)B, lr);
@@ -2148,7 +2158,6 @@ int pfc_gpu_trainer_apply_gradient(void* tr, double lr) {
   CUDA_TRY(c, cudaGetLastError());
   t->stepped = false;
   t->B = 0;
-  // the products' finiteness is checked before the next forward's features are used
   return PFC_OK;
 }
 

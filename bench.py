@@ -50,10 +50,14 @@ def parse():
     ap.add_argument("--dim", type=int, default=512)
     ap.add_argument("--shards", type=int, default=8)
     ap.add_argument("--r", type=float, default=0.1)
+    ap.add_argument("--margin", default="arcface", choices=["arcface", "cosface"],
+                    help="ArcFace s=64 m=0.5 (configs[0-2,4]) or CosFace s=64 m=0.4 (configs[3])")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-diag", action="store_true", help="skip timing the diagnostics call")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="launch without programmatic dependent launch (A/B timing)")
     return ap.parse_args()
 
 
@@ -113,7 +117,13 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_reference_time(C_full, K, D, B, r, steps, warmup):
+def margin_args(name):
+    """(oracle margin name, s, m, description) of a --margin choice."""
+    return {"arcface": ("arcface", 64.0, 0.5, "arcface s=64 m=0.5"),
+            "cosface": ("cosface", 64.0, 0.4, "cosface s=64 m=0.4")}[name]
+
+
+def cpu_reference_time(C_full, K, D, B, r, steps, warmup, margin="arcface"):
     """The reference's own pfc::distributed_partial_step (oracle/_ref/libpfc_ref.so: the
     unmodified headers compiled in place, reference flags) on the host cores, AT THE STATED
     WORKLOAD (no scaling): C_full classes in K shards, the global batch B of the bench input
@@ -126,7 +136,8 @@ def cpu_reference_time(C_full, K, D, B, r, steps, warmup):
     import numpy as np
     cores = os.cpu_count() or 1
     os.environ["PFC_SIM_THREADS"] = str(cores)
-    cfg = OracleCfg(r=r, margin="arcface", scale=64.0, m=0.5, lr=0.1)
+    mname, ms_, mm, mdesc = margin_args(margin)
+    cfg = OracleCfg(r=r, margin=mname, scale=ms_, m=mm, lr=0.1)
     P = Oracle("port")
     X, labels = P.bench_inputs(C_full, D, B, 1, 0)
     if not ref_available():
@@ -155,7 +166,7 @@ def cpu_reference_time(C_full, K, D, B, r, steps, warmup):
     threads = min(K, cores)
     return {"value": B / t, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": (f"reference distributed_partial_step at the full workload C={C_full}, K={K}, "
-                       f"B={B}, d={D}, r={r}, ArcFace s=64 m=0.5 (no scaling); best of {steps} "
+                       f"B={B}, d={D}, r={r}, {mdesc} (no scaling); best of {steps} "
                        f"step(s) after {warmup} warm-up: {t:.2f} s/step (all: "
                        f"{', '.join(f'{x:.2f}' for x in times)}); PFC_SIM_THREADS={cores} host "
                        f"cores, {threads} busy (one thread per shard); host init of the "
@@ -171,7 +182,8 @@ def run_reference(args, ws, rank):
     # them (one warm-up, then the best of two) keeps the run within a few minutes
     steps = 2
     warm = 1
-    cb = cpu_reference_time(args.classes, args.shards, args.dim, args.batch, args.r, steps, warm)
+    cb = cpu_reference_time(args.classes, args.shards, args.dim, args.batch, args.r, steps, warm,
+                            args.margin)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": warm, "ms_per_step": cb["step_s"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -196,7 +208,7 @@ def workload_name(args):
 def workload_config(args):
     return {"workload": workload_name(args),
             "classes": args.classes, "dim": args.dim, "global_batch": args.batch, "r": args.r,
-            "reference_shards": args.shards, "margin": "arcface s=64 m=0.5",
+            "reference_shards": args.shards, "margin": margin_args(args.margin)[3],
             "parallelism": f"class-sharded x{args.gpus}",
             "l2": "no flush: per-step working set (W+mom 8.2 GB, W^ 205 MB, E 410 MB) >> 126 MB L2"}
 
@@ -222,9 +234,13 @@ def main():
     B, D, C_, K = args.batch, args.dim, args.classes, args.shards
     assert B % ws == 0 and K % ws == 0
     bl = B // ws
-    cfg = p.StepConfig(r=args.r, margin=p.MarginConfig.arcface_style(64.0, 0.5), lr=0.1)
+    _, ms_, mm, _ = margin_args(args.margin)
+    mcfg = (p.MarginConfig.arcface_style(ms_, mm) if args.margin == "arcface"
+            else p.MarginConfig(p.ADDITIVE_COSINE, ms_, mm))
+    cfg = p.StepConfig(r=args.r, margin=mcfg, lr=0.1)
     sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, precision=p.PRECISION_BF16,
-                        device=local, rank=rank, world_size=ws, nccl_id=nccl_id)
+                        device=local, rank=rank, world_size=ws, nccl_id=nccl_id,
+                        flags=p.FLAG_NO_PDL if args.no_pdl else 0)
     sh.init_center_shards(1)
     ncols = sh.capacity * len(sh.local_shards)
     nsteps = args.warmup + args.steps
@@ -414,7 +430,7 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:  # one step of the stated workload (about a minute of host time), no warm-up
             line["cpu_baseline"] = {k: v for k, v in cpu_reference_time(
-                C_, K, D, B, args.r, 1, 0).items() if k in ("value", "unit", "cores", "kind", "sample")}
+                C_, K, D, B, args.r, 1, 0, args.margin).items() if k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # the baseline is reported, never the target
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "none",
                                     "sample": f"unavailable: {e}"}

@@ -59,7 +59,7 @@ typedef struct {
   int64_t num_classes;     /* C  (ShardLayout::num_classes) */
   int64_t dim;             /* D  (embedding dimension) */
   int64_t num_shards;      /* K  (ShardLayout::num_shards; the reference's shard count) */
-  int64_t max_batch;       /* largest global batch B the context will see (<= 8192) */
+  int64_t max_batch;       /* largest global batch B the context will see (<= 2^20) */
   double r;                /* StepConfig::r */
   int32_t margin_kind;     /* pfc_margin_kind */
   double margin_scale;     /* MarginConfig::scale */
@@ -84,6 +84,12 @@ typedef struct {
                                                 offset, rerun per row if a row underflows) */
 #define PFC_FLAG_DEBUG_LOGITS 8              /* test hook: keep the last step's logits
                                                 (pfc_gpu_debug_logits) */
+#define PFC_FLAG_NO_PDL 32                   /* launch the step's kernels without programmatic
+                                                dependent launch (A/B timing) */
+#define PFC_FLAG_GUARD 16                    /* test hook: every device buffer of the context
+                                                sits between two 4 KB guard regions filled with
+                                                a pattern; pfc_gpu_check_guards reports any
+                                                guard byte a kernel overwrote */
 
 typedef struct {
   uint64_t seed;       /* iteration_rng.seed()      (rng.hpp:44) */
@@ -239,14 +245,18 @@ int pfc_gpu_trainer_diagnostics(void* trainer, const int64_t* class_identity,
 /* distributed_partial_step on the forward batch; d_features stay on the device */
 int pfc_gpu_trainer_step(void* trainer, const pfc_gpu_step_args* args, pfc_gpu_step_out* out);
 /* Backbone::apply_gradient(inputs, act, d_features, lr) (trainer.hpp:99-125) with the cached
- * activations and the step's d_features; asynchronous: a non-finite product is reported by the
- * next forward-dependent call with the reference's "matmul: non-finite entry" text */
+ * activations and the step's d_features; a non-finite gradient product raises the reference's
+ * "matmul: non-finite entry" NumericalError before w1 / w2 change (the SGD rows run only after
+ * the products' finiteness flags are read) */
 int pfc_gpu_trainer_apply_gradient(void* trainer, double lr);
 /* forward-only embeddings of point_ids[n] into emb (embed x n fp64, host), chunked by max_batch
  * (evaluation: nearest-centre accuracy, verification); discards the cached activations */
 int pfc_gpu_trainer_embed(void* trainer, const int64_t* point_ids, int64_t n, double* emb);
 
 /* ---- bench / test helpers --------------------------------------------------------------- */
+/* PFC_FLAG_GUARD contexts: synchronises the device, compares every guard region with its
+ * pattern; *corrupted = the number of changed regions (PFC_ERR_CUDA naming them if any). */
+int pfc_gpu_check_guards(void* ctx, int64_t* corrupted);
 /* Synthetic inputs of the bench convention on the device:
  * labels[b] = SeededRng(seed, make_stream("bench-labels", step)).next_below(C) and
  * X[b][d] = SeededRng(seed, make_stream("bench-x", step)).next_normal() (b-major, d inner). */

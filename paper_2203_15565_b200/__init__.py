@@ -270,6 +270,7 @@ class StepOut(C.Structure):
 
 PRECISION_BF16, PRECISION_FP32 = 0, 1
 FLAG_FORCE_SEQUENTIAL_SAMPLER, FLAG_NO_GRAPH, FLAG_EXACT_SOFTMAX, FLAG_DEBUG_LOGITS = 1, 2, 4, 8
+FLAG_GUARD, FLAG_NO_PDL = 16, 32
 
 _lib = None
 
@@ -322,6 +323,7 @@ def load_library(path: str | None = None) -> C.CDLL:
         "pfc_gpu_write_shards": (C.c_int, [vp, C.c_char_p, C.c_int]),
         "pfc_gpu_mics": (C.c_int, [vp, vp]),
         "pfc_gpu_read_shards": (C.c_int, [vp, C.c_char_p, i64, C.POINTER(i64)]),
+        "pfc_gpu_check_guards": (C.c_int, [vp, C.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -369,7 +371,7 @@ class CenterShards:
                  world_size: int = 1, nccl_id: bytes | None = None, flags: int = 0):
         cfg.margin.validate()
         lib = load_library()
-        self.layout, self.dim, self.cfg = layout, dim, cfg
+        self.layout, self.dim, self.cfg, self.precision = layout, dim, cfg, precision
         self.world_size, self.rank = world_size, rank
         self._nccl_id = (C.c_uint8 * 128)(*nccl_id) if nccl_id else None
         d = Desc(layout.num_classes, dim, layout.num_shards, max_batch, cfg.r, cfg.margin.kind,
@@ -429,6 +431,12 @@ class CenterShards:
 
     def stream(self) -> int:
         return _lib.pfc_gpu_stream(self._h)
+
+    def check_guards(self) -> int:
+        """FLAG_GUARD contexts: number of guard regions a kernel overwrote (raises naming them)."""
+        n = C.c_int64()
+        _check(load_library().pfc_gpu_check_guards(self._h, C.byref(n)), self._h)
+        return n.value
 
     def debug_logits(self, batch: int) -> np.ndarray:
         """Last step's logits z of this rank (FLAG_DEBUG_LOGITS): [B][local shards][cap] float32,

@@ -30,6 +30,18 @@ __host__ __device__ __forceinline__ uint64_t rng_draw(uint64_t key, uint64_t cou
   return mix64(key + kPhi * counter);
 }
 
+// Programmatic dependent launch (PDL): the step's kernels are launched with programmatic
+// stream serialisation, so kernel N+1's CTAs may be scheduled while kernel N drains.  Every
+// kernel first waits for its predecessor grid to complete (griddepcontrol.wait: completion and
+// memory visibility; a no-op without the launch attribute), then lets its own dependents start
+// launching.  Only launch latency and prologues overlap; no data is read early.
+__device__ __forceinline__ void pdl_entry() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // Device status block, read back once per step (SURVEY.md §5 failure detection).
 struct StepStatus {
   double loss;
@@ -41,12 +53,12 @@ struct StepStatus {
   int32_t nonfinite_loss;
   int32_t nonfinite_dx;
   int32_t rejection_shards;   // count of shards that needed the sequential sampler
-  int32_t batch_too_large;
+  int32_t reserved0;
   int32_t underflow_row;      // first row whose exp(z - offset) sum underflowed, else INT32_MAX
   uint32_t fin_blocks;        // finalize_stats blocks done (last one reduces the loss)
 };
 
-// Per-step scalars, written on the device by step_begin (thread 0 of positives_kernel, the only
+// Per-step scalars, written on the device by step_begin (thread 0 of mark_kernel, the only
 // graph node whose arguments change between steps) and read by the kernels that need them.
 struct StepParams {
   uint64_t seed;    // iteration_rng.seed()
@@ -64,7 +76,7 @@ struct ShardMeta {        // per local shard
   int32_t need;           // cap - npos negatives to draw
   int32_t pool;           // N = owned - npos
   int32_t full;           // 1 -> full-sampling branch (ascending complement, no RNG)
-  int32_t ustart;         // index of the first positive in the sorted-unique label list
+  int32_t ustart;         // set label bits below the shard (its positives start at rank 0)
   int32_t reject;         // 1 -> a modulo rejection happened: sequential fallback
 };
 

@@ -39,7 +39,7 @@ namespace pfc {
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ bool status_failed(const StepStatus* st) {
-  return st->label_oob || st->capacity_shard >= 0 || st->batch_too_large ||
+  return st->label_oob || st->capacity_shard >= 0 ||
          st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx ||
          st->underflow_row != 0x7fffffff;
 }
@@ -383,6 +383,9 @@ struct DxPartEpi : NoSetup {
 #ifndef PFC_DW_CAP
 #define PFC_DW_CAP 6
 #endif
+#ifndef PFC_DW_EXP
+#define PFC_DW_EXP 0  // timing probes of the update epilogue (profiles/micro/dwexp.sh); 0 = product
+#endif
 namespace dw_ring {
 constexpr int kNC = 8;                      // 32-dim chunks per 256-dim tile half
 constexpr int kItems = 2 * kNC;             // W chunk c (dot pass), then W + momentum chunk c
@@ -514,7 +517,11 @@ struct DwUpdateEpi {
       rwn[u] = s_row_n[u * 4 + sub];
     }
     const int dbase = t.col0 + q4;
+#if PFC_DW_EXP == 3  // timing probe: no positive corrections (wrong values)
+    const bool anyp = false;
+#else
     const bool anyp = __any_sync(0xffffffffu, ps[0] >= 0 || ps[1] >= 0);  // positives are rare
+#endif
     if constexpr (kPair) {  // this tile's exchange: the peer's 8 half-dots arrive as 32 tx bytes
       if (lane == 0) pfc_sm100::mbar_arrive_expect_tx(&mb[(t.iter & 1) * 16 + wg * 4 + q], 32u);
     }
@@ -548,6 +555,12 @@ struct DwUpdateEpi {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float v[16];
+#if PFC_DW_EXP == 1  // timing probe: half the accumulator reads (wrong values)
+        if (h == 1) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        } else
+#endif
         src.load16(c0 + 16 * h, v);
         if (mine) {
 #pragma unroll
@@ -594,7 +607,9 @@ struct DwUpdateEpi {
               pfc_sm100::st_async_f32(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hr + u * 4 + sub), prank),
                                       dot[u], rbar);
           }
+#if PFC_DW_EXP != 4  // timing probe 4: no wait for the peer's half-dots (wrong values)
           pfc_sm100::mbar_wait_cluster(&mb[par * 16 + e], (uint32_t)((it >> 1) & 1));
+#endif
 #pragma unroll
           for (int u = 0; u < 2; ++u) dot[u] += hr[u * 4 + sub];
         }
@@ -633,8 +648,18 @@ struct DwUpdateEpi {
               wv[e] = wv[e] - lr * vv;                              // shardsim.hpp:156
             }
             const size_t o = (size_t)rw[u] * D + d;
+#if PFC_DW_EXP == 2  // timing probe: no W / momentum stores
+            if (mv[0] == 1234.5f)
+#endif
+            {
+#if PFC_DW_EXP == 5  // probe: streaming (evict-first) stores
+            __stcs(reinterpret_cast<float4*>(Mom + o), make_float4(mv[0], mv[1], mv[2], mv[3]));
+            __stcs(reinterpret_cast<float4*>(W + o), make_float4(wv[0], wv[1], wv[2], wv[3]));
+#else
             *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
             *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+#endif
+            }
           }
         }
       }

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
   __syncthreads();
   tc_fence_after();
   if constexpr (Epi::kCluster > 1 || CG == 2) cluster_sync_all();  // peer barriers initialised
+  pdl_entry();  // the prologue above overlapped the previous kernel's drain
   const uint32_t tmem_base = *tmem_slot;
   const int total = g.total();
   // persistent schedule over tiles (CG = 2: over pair tiles, one per cluster)
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(128)
   float* sB = sA + KC * 129;                        // [KC][BN]
   float* sAcc = sB + KC * BN;                       // [128][65]
   uint8_t* epi_smem = reinterpret_cast<uint8_t*>(sAcc + 128 * 65);
+  pdl_entry();
   const int tid = threadIdx.x;
   TileInfo ti = g.tile(blockIdx.x);
   float acc[BN];

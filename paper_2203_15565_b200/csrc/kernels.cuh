@@ -5,7 +5,7 @@
 namespace pfc {
 
 __device__ __forceinline__ bool sampler_failed(const StepStatus* st) {
-  return st->label_oob || st->capacity_shard >= 0 || st->batch_too_large;
+  return st->label_oob || st->capacity_shard >= 0;
 }
 __device__ __forceinline__ bool step_failed(const StepStatus* st) {
   return sampler_failed(st) || st->masked_row != 0x7fffffff || st->nonfinite_loss || st->nonfinite_dx;
@@ -53,6 +53,7 @@ __device__ __forceinline__ void store_out(float* p, float v) { *p = v; }
 // FeatureBatch layout (D x B fp64, types.hpp:14-26) -> rows [B][D] fp32.  32x32 tiles.
 __global__ void x_from_dxb_kernel(const double* __restrict__ xdb, int D, int B,
                                   float* __restrict__ X) {
+  pdl_entry();
   __shared__ float tile[32][33];
   const int b0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -69,6 +70,7 @@ __global__ void x_from_dxb_kernel(const double* __restrict__ xdb, int D, int B,
 // rows [B][D] fp32 -> D x B fp64 (StepResult::d_features layout).
 __global__ void dx_to_dxb_kernel(const float* __restrict__ dX, int D, int B,
                                  double* __restrict__ out) {
+  pdl_entry();
   __shared__ float tile[32][33];
   const int b0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -104,6 +106,7 @@ __device__ __forceinline__ void normalize_x_rows(const float* __restrict__ xs, i
 template <typename OT>
 __global__ void normalize_x_kernel(const float* __restrict__ x, int B, int D, int Dp,
                                    OT* __restrict__ xh, float* __restrict__ xnorm) {
+  pdl_entry();
   normalize_x_rows(x, B, D, Dp, xh, xnorm, (int)blockIdx.x);
 }
 
@@ -115,6 +118,7 @@ __global__ void gather_w_kernel(const float* __restrict__ W, int D, int Dp,
                                 int64_t cls_lo, int64_t rows, OT* __restrict__ wh,
                                 float* __restrict__ wnorm, int32_t* __restrict__ lrow,
                                 int32_t* __restrict__ pslot, const StepStatus* st) {
+  pdl_entry();
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c >= ncols_pad) return;
   if (lane == 0 && c < ncols) pslot[c] = -1;
@@ -183,35 +187,49 @@ __global__ void gather_w_kernel(const float* __restrict__ W, int D, int Dp,
   }
 }
 
-// Sum the per-(column slice) sums of E = exp(z - o) of each row, in a fixed order.
-// Pass 1: grid (rows/128, segments), thread = row (coalesced over b); pass 2: thread = row.
-constexpr int kMergeSegs = 64;
+// Sum the per-(column slice) sums of E = exp(z - o) of each row, in a fixed order: a block owns
+// kRowsPerBlk rows; thread (g, r) sums slices t = g, g + kSliceGroups, ... of row r (coalesced over
+// the rows of one slice, loads batched 8 deep, one fp32/fp64 running sum per thread), then the
+// kSliceGroups partials are added in ascending g in fp64.  One launch replaces the former
+// slices -> segments -> row kernels.
+constexpr int kRowsPerBlk = 16, kSliceGroups = 16;  // 256 threads
 template <typename ST>
-__global__ void __launch_bounds__(128) sum_slices_kernel(const ST* __restrict__ ps, int T, int B,
-                                                         ST* __restrict__ seg) {
-  const int b = blockIdx.x * 128 + threadIdx.x;
-  if (b >= B) return;
-  const int per = (T + gridDim.y - 1) / gridDim.y;
-  const int t0 = blockIdx.y * per, t1 = min(T, t0 + per);
-  ST s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-  int t = t0;
-  for (; t + 4 <= t1; t += 4) {
-    s0 += ps[(size_t)t * B + b];
-    s1 += ps[(size_t)(t + 1) * B + b];
-    s2 += ps[(size_t)(t + 2) * B + b];
-    s3 += ps[(size_t)(t + 3) * B + b];
+__device__ __forceinline__ double row_slice_sum(const ST* __restrict__ ps, int T, int B, int b0,
+                                                double* red /* [kSliceGroups][kRowsPerBlk] */) {
+  const int r = threadIdx.x % kRowsPerBlk, g = threadIdx.x / kRowsPerBlk;
+  const int b = b0 + r;
+  ST acc = 0;
+  if (b < B) {
+    int t = g;
+    for (; t + 7 * kSliceGroups < T; t += 8 * kSliceGroups) {
+      ST v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ps[(size_t)(t + u * kSliceGroups) * B + b];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; t < T; t += kSliceGroups) acc += ps[(size_t)t * B + b];
   }
-  for (; t < t1; ++t) s0 += ps[(size_t)t * B + b];
-  seg[(size_t)blockIdx.y * B + b] = (s0 + s1) + (s2 + s3);
+  red[g * kRowsPerBlk + r] = (double)acc;
+  __syncthreads();
+  double S = 0.0;
+  if (g == 0) {
+#pragma unroll
+    for (int q = 0; q < kSliceGroups; ++q) S += red[q * kRowsPerBlk + r];
+  }
+  return S;  // valid in threads g == 0
 }
+
+// Rank-local row sums for the cross-rank exchange (world > 1): ls[b] = sum over this rank's slices.
 template <typename ST>
-__global__ void sum_segments_kernel(const ST* __restrict__ seg, int nseg, int B,
-                                    ST* __restrict__ ls) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  double s = 0.0;
-  for (int i = 0; i < nseg; ++i) s += (double)seg[(size_t)i * B + b];
-  ls[b] = (ST)s;
+__global__ void __launch_bounds__(256) local_sums_kernel(const ST* __restrict__ ps, int T, int B,
+                                                         ST* __restrict__ ls) {
+  pdl_entry();
+  __shared__ double red[kSliceGroups * kRowsPerBlk];
+  const int b0 = blockIdx.x * kRowsPerBlk;
+  const double S = row_slice_sum(ps, T, B, b0, red);
+  const int b = b0 + (int)threadIdx.x;
+  if (threadIdx.x < kRowsPerBlk && b < B) ls[b] = (ST)S;
 }
 
 // Per-row softmax offset of the exact mode: o_b = max over the row's unmasked logits on this
@@ -222,6 +240,7 @@ __global__ void row_offset_kernel(const float* __restrict__ part_m, int T, int B
                                   const int32_t* __restrict__ pos_col,
                                   const double* __restrict__ zpos, MarginDev mg,
                                   float* __restrict__ offr) {
+  pdl_entry();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   float m = -INFINITY;
@@ -235,34 +254,30 @@ __global__ void row_offset_kernel(const float* __restrict__ part_m, int T, int B
 // terms, the row scale of G and the positive's correction:
 //   S = sum_r ls[r];  loss_b = log S + o - z_pos;  rowscale = s / (B S)
 //   delta_b = ((p_pos - 1)/B) margin'(c_pos) - rowscale * E_pos(stored)   (owner rank only)
-// With one rank (seg != nullptr) the rank-local sum is formed here from the nseg segment sums
-// (same order and rounding as sum_segments_kernel).  The last block to finish reduces loss_row
-// in a fixed order into the step's loss (was loss_reduce_kernel).
+// With one rank (ps != nullptr) the rank-local sum is formed here from the T slice sums
+// (row_slice_sum).  A block owns kRowsPerBlk rows; the last block to finish reduces loss_row in
+// a fixed order into the step's loss.
 template <typename ST>
 __global__ void __launch_bounds__(256) finalize_stats_kernel(
-    const ST* __restrict__ ls, int R, const ST* __restrict__ seg, int nseg, int B,
+    const ST* __restrict__ ls, int R, const ST* __restrict__ ps, int T, int B,
     const double* __restrict__ zpos, const double* __restrict__ cpos,
     const float* __restrict__ epos, const int32_t* __restrict__ pos_col,
     const int* __restrict__ hasval, int has_filter, MarginDev mg, const float* __restrict__ offr,
     ST* __restrict__ rowscale, ST* __restrict__ delta, double* __restrict__ loss_row,
     StepStatus* st) {
-  // one warp per row: lanes sum the segments (fixed lane order + fixed shuffle tree), lane 0
-  // finishes the row
-  const int lane = threadIdx.x & 31;
-  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const bool live = b < B && !sampler_failed(st);
+  pdl_entry();
+  __shared__ double red[kSliceGroups * kRowsPerBlk];
+  const int b0 = blockIdx.x * kRowsPerBlk;
+  const bool ok = !sampler_failed(st);
   double S = 0.0;
-  if (live) {
-    if (seg) {
-      double s = 0.0;
-      for (int i = lane; i < nseg; i += 32) s += (double)seg[(size_t)i * B + b];
-      s = warp_sum(s);
-      S = (double)(ST)s;
-    } else {
-      for (int r = 0; r < R; ++r) S += (double)ls[(size_t)r * B + b];
-    }
+  if (ps) {
+    S = row_slice_sum(ps, T, B, b0, red);
+    S = (double)(ST)S;  // the rank-local sum in the statistics type, as exchanged with R > 1
+  } else if (threadIdx.x < kRowsPerBlk && b0 + (int)threadIdx.x < B) {
+    for (int r = 0; r < R; ++r) S += (double)ls[(size_t)r * B + b0 + threadIdx.x];
   }
-  if (live && lane == 0) {
+  const int b = b0 + (int)threadIdx.x;
+  if (ok && threadIdx.x < kRowsPerBlk && b < B) {
     [&] {
       rowscale[b] = 0;
       delta[b] = 0;
@@ -297,7 +312,6 @@ __global__ void __launch_bounds__(256) finalize_stats_kernel(
   __syncthreads();
   if (!last) return;
   __threadfence();
-  __shared__ double red[8];
   double acc = 0.0;
   for (int i = threadIdx.x; i < B; i += blockDim.x) acc += ((volatile double*)loss_row)[i];
   acc = warp_sum(acc);
@@ -316,10 +330,24 @@ __global__ void __launch_bounds__(256) finalize_stats_kernel(
 }
 
 // rowscale_b * x^_b in the GEMM operand type: the dW GEMM's B operand (G = diag(rowscale) E).
+// Also resets the draws' per-position list heads (off the critical path, on the forked stream):
+// the walk no longer reads them, and resetting only the entries this step's draws set keeps them
+// all -1 between steps without a memset over every pool position.
 template <typename ST, typename OT>
 __global__ void xs_kernel(const StepParams* __restrict__ sp, const float* __restrict__ xnorm,
                           const ST* __restrict__ rowscale, int B, int D, int Dp,
-                          OT* __restrict__ xs) {
+                          OT* __restrict__ xs, const ShardMeta* __restrict__ meta, int nk, int cap,
+                          const int32_t* __restrict__ jv, int32_t* __restrict__ head,
+                          int64_t pool_stride, const StepStatus* st) {
+  pdl_entry();
+  if (!sampler_failed(st)) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < (int64_t)nk * cap;
+         g += (int64_t)gridDim.x * blockDim.x) {
+      const int kk = (int)(g / cap), i = (int)(g % cap);
+      const ShardMeta& m = meta[kk];
+      if (!m.full && i < m.need) head[(int64_t)kk * pool_stride + jv[g]] = -1;
+    }
+  }
   const int b = blockIdx.x;
   const float* x = sp->x + (size_t)b * D;
   const float n = xnorm[b];
@@ -340,6 +368,7 @@ __global__ void __launch_bounds__(256) poscorr_kernel(
     int B, const StepParams* __restrict__ sp, const float* __restrict__ xnorm, int D,
     const float* __restrict__ delta_f, const double* __restrict__ delta_d,
     float* __restrict__ poscorr, int32_t* __restrict__ pslot, const StepStatus* st) {
+  pdl_entry();
   const int kk = blockIdx.y, i = blockIdx.x;
   if (sampler_failed(st)) return;
   if (i >= meta[kk].npos) return;
@@ -391,6 +420,7 @@ __global__ void __launch_bounds__(256) dx_finalize_kernel(
     const ST* __restrict__ delta, const int32_t* __restrict__ pos_col,
     const int32_t* __restrict__ lrow, const float* __restrict__ wnorm,
     const float* __restrict__ W, int B, int D, StepStatus* st) {
+  pdl_entry();
   const int b = blockIdx.x;
   __shared__ double red[8];
   const float* __restrict__ X = sp->x;
@@ -418,7 +448,18 @@ __global__ void __launch_bounds__(256) dx_finalize_kernel(
     float acc = 0.f;
     xh[i] = 0.f;
     if (d < D) {
-      for (int s = 0; s < S; ++s) acc += part[((size_t)s * B + b) * D + d];
+      // ascending splits; loads issued 8 at a time (independent L2 round trips)
+      const float* p = part + (size_t)b * D + d;
+      const size_t stride = (size_t)B * D;
+      int s = 0;
+      for (; s + 8 <= S; s += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = p[(size_t)(s + u) * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+      }
+      for (; s < S; ++s) acc += p[(size_t)s * stride];
       acc *= rs;
       if (wpos) acc += dl * (wpos[d] * winv);
       xh[i] = X[(size_t)b * D + d] * inv;
@@ -454,6 +495,7 @@ __global__ void dw_rows_update_kernel(const float* __restrict__ dwt, const int32
                                       float* __restrict__ W, float* __restrict__ Mom,
                                       const StepParams* __restrict__ sp, float mu, float wd,
                                       const StepStatus* st) {
+  pdl_entry();
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c >= ncols) return;
   if (sampler_failed(st) || st->masked_row != 0x7fffffff || st->nonfinite_loss ||

@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -158,7 +159,13 @@ struct Ctx {
   float* M = nullptr;
   // sampler
   int64_t* labels = nullptr;  // global batch labels (world > 1 / host path)
-  int64_t* uniq = nullptr;
+  int64_t* labs = nullptr;    // the step's labels as the sampler copied them (device)
+  uint32_t* bits = nullptr;   // [nwords] label bitmap over all C classes (all-zero between steps)
+  int32_t* ccnt = nullptr;    // [nchunk] set bits per chunk of chunk_words words (zero between steps)
+  int32_t* rej = nullptr;     // [nk] a draw of the shard saw a modulo rejection
+  long long* oobs = nullptr;  // [2] smallest negative / >= C label of the step (LLONG_MAX: none)
+  int64_t nwords = 0;
+  int chunk_words = 1024, nchunk = 1;
   ShardMeta* meta = nullptr;
   int32_t* buf_cls = nullptr;
   int32_t* pos_col = nullptr;
@@ -189,7 +196,6 @@ struct Ctx {
   int32_t* lrow = nullptr;
   // softmax statistics (fixed-offset form, see epilogues.cuh)
   void* part_s = nullptr;  // [T * NWG][maxB] sums of E per column slice
-  void* seg_s = nullptr;   // [kMergeSegs][maxB]
   void* ls = nullptr;      // [R][maxB] rank-local sums
   void* rowscale = nullptr;
   void* delta = nullptr;
@@ -219,8 +225,7 @@ struct Ctx {
   StepStatus* st_host = nullptr;
   StepParams* sp = nullptr;
   bool reset_status = true;  // false while asynchronous device steps are in flight
-  size_t sort_smem = 0;  // dynamic shared memory of positives_kernel at the captured batch size
-  // CUDA graph of the device step (one per batch size); positives_kernel (which opens the step)
+  // CUDA graph of the device step (one per batch size); sampler_kernel (which opens the step)
   // is the node whose arguments change per step
   // captured steps: slot 0 = device-resident I/O (pfc_gpu_step_device), slot 1 = the host
   // drop-in with its copies inside the graph (pfc_gpu_step with pinned host buffers)
@@ -229,7 +234,6 @@ struct Ctx {
     cudaGraphExec_t gexec = nullptr;
     cudaGraphNode_t gbegin = nullptr;
     cudaGraphNode_t cp_x = nullptr, cp_dx = nullptr;  // slot 1 memcpy nodes
-    size_t psmem = 0;  // the step-opening node's dynamic shared memory (captured)
     const void* cp_ptr[3] = {nullptr, nullptr, nullptr};  // host pointers the nodes hold
     int64_t gB = -1;
     int64_t glaunches = 0;
@@ -255,8 +259,19 @@ struct Ctx {
   int64_t lastB = 0;
   int64_t launches = 0;
   PhaseTimer pt;
+  bool pdl = true;  // launch the step's kernels with programmatic stream serialisation
   std::vector<void*> allocs;
+  struct Guard {
+    uint8_t* base;  // [kGuardBytes guard][user bytes][kGuardBytes guard] (PFC_FLAG_GUARD)
+    size_t user;
+  };
+  std::vector<Guard> guards;
 };
+
+// PFC_FLAG_GUARD (the out-of-bounds write check that stands in for compute-sanitizer, which
+// this pool does not allow): every context buffer sits between two guard regions
+constexpr size_t kGuardBytes = 4096;
+constexpr int kGuardByte = 0xA5;
 
 // Largest margin scale that keeps the fixed softmax offset o = max(0, s - 40): above it every
 // step takes per-row offsets from a max-only pass (epilogues.cuh header).
@@ -334,10 +349,23 @@ inline int comm_reduce_scatter(Ctx* c, const void* send, void* recv, size_t coun
 template <typename T>
 cudaError_t dalloc(Ctx* c, T** p, size_t n) {
   void* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, n * sizeof(T) + 256);
+  const size_t user = n * sizeof(T) + 256;
+  if (c->d.flags & PFC_FLAG_GUARD) {  // [guard][buffer][guard], guards filled with the pattern
+    cudaError_t e = cudaMalloc(&q, user + 2 * kGuardBytes);
+    if (e != cudaSuccess) return e;
+    c->allocs.push_back(q);
+    uint8_t* b = static_cast<uint8_t*>(q);
+    cudaMemset(b, kGuardByte, kGuardBytes);
+    cudaMemset(b + kGuardBytes, 0, user);
+    cudaMemset(b + kGuardBytes + user, kGuardByte, kGuardBytes);
+    c->guards.push_back({b, user});
+    *p = reinterpret_cast<T*>(b + kGuardBytes);
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMalloc(&q, user);
   if (e == cudaSuccess) {
     c->allocs.push_back(q);
-    cudaMemset(q, 0, n * sizeof(T) + 256);
+    cudaMemset(q, 0, user);
   }
   *p = static_cast<T*>(q);
   return e;
@@ -348,6 +376,29 @@ void phase(Ctx* c, const char* name) {
   c->pt.names[c->pt.n] = name;
   cudaEventRecord(c->pt.ev[c->pt.n + 1], c->stream);
   c->pt.n++;
+}
+
+// PDL on the device path only: with the host drop-in's copy nodes forked around the kernels,
+// programmatic edges measured slower end to end (360k: 0.39 vs 0.31 ms per step).
+inline bool use_pdl(const Ctx* c) { return c->pdl && !c->e2e.on; }
+
+// Launch a step kernel with programmatic stream serialisation (PDL, common.cuh pdl_entry):
+// its CTAs may be scheduled while the previous kernel on the stream drains.
+template <typename... KArgs, typename... Args>
+cudaError_t klaunch(Ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                    cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = use_pdl(c) ? 1 : 0;
+  c->launches++;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------------ GEMM launchers
@@ -373,20 +424,21 @@ cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, co
     cfg.blockDim = dim3(32 * PFC_CTRL_WARPS + 128 * NWG);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kCl;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = use_pdl(c) ? 2 : 1;
     c->launches++;
     return cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epi);
   } else {
     const int grid = total < c->num_sms ? total : c->num_sms;
-    kern<<<grid, 32 * PFC_CTRL_WARPS + 128 * NWG, smem, c->stream>>>(ta, tb, g, epi);
-    c->launches++;
-    return cudaGetLastError();
+    return klaunch(c, kern, dim3(grid), dim3(32 * PFC_CTRL_WARPS + 128 * NWG), smem, c->stream,
+                   ta, tb, g, epi);
   }
 }
 
@@ -397,9 +449,8 @@ cudaError_t launch_simt(Ctx* c, const float* A, int lda, const float* Bm, int ld
   if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), kSimtSmemBytes))
     return e;
   if (g.total() <= 0) return cudaSuccess;
-  kern<<<g.total(), 128, kSimtSmemBytes, c->stream>>>(A, lda, Bm, ldb, g, epi);
-  c->launches++;
-  return cudaGetLastError();
+  return klaunch(c, kern, dim3(g.total()), dim3(128), kSimtSmemBytes, c->stream, A, lda, Bm, ldb,
+                 g, epi);
 }
 
 int ensure_maps(Ctx* c, int64_t B) {
@@ -420,6 +471,72 @@ int ensure_maps(Ctx* c, int64_t B) {
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
   return PFC_OK;
+}
+
+// The sampler's arguments for this step (sampler.cu SamplerArgs).
+SamplerArgs sampler_args(Ctx* c, const pfc_gpu_step_args* a, const float* x, const int64_t* lab,
+                         float* dx_full, int64_t B, int normalize) {
+  SamplerArgs sa{};
+  sa.st = c->st;
+  sa.sp = c->sp;
+  sa.seed = a->seed;
+  sa.stream = a->stream_id;
+  sa.lr = (float)a->lr;
+  sa.reset = c->reset_status ? 1 : 0;
+  sa.x = x;
+  sa.labels_in = lab;
+  sa.dx = dx_full;
+  sa.B = (int)B;
+  sa.C = c->C;
+  sa.K = (int)c->K;
+  sa.blk = c->blk;
+  sa.cap = (int)c->cap;
+  sa.k0 = (int)c->k0;
+  sa.nk = (int)c->nk;
+  sa.force_sequential = (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0;
+  sa.normalize = normalize;
+  sa.D = (int)c->D;
+  sa.Dp = (int)c->Dp;
+  sa.xh = c->xh;
+  sa.xnorm = c->xnorm;
+  sa.bits = c->bits;
+  sa.ccnt = c->ccnt;
+  sa.chunk_words = c->chunk_words;
+  sa.nchunk = c->nchunk;
+  sa.oobs = c->oobs;
+  sa.rej = c->rej;
+  sa.labs = c->labs;
+  sa.zpos = c->zpos;
+  sa.hasval = c->d.has_filter ? c->hasval : nullptr;
+  sa.meta = c->meta;
+  sa.buf_cls = c->buf_cls;
+  sa.pos_col = c->pos_col;
+  sa.head = c->head;
+  sa.nxt = c->nxt;
+  sa.jv = c->jv;
+  sa.pool_scratch = c->pool_scratch;
+  sa.pool_stride = c->pool_stride;
+  return sa;
+}
+
+// The three sampler kernels (sampler.cu): mark opens the step (no programmatic edge: it
+// follows work outside the step), fill and walk follow it with PDL.  Grid-stride loops over one
+// CTA of 1024 threads per SM.
+cudaError_t launch_sampler(Ctx* c, SamplerArgs& sa) {
+  const size_t smem = sampler_smem_bytes(c->nchunk, (int)c->nk);
+  const int smax = (int)sampler_smem_bytes(kMaxSamplerChunks, kMaxSamplerLocalShards);
+  const void* fill = c->bf16 ? reinterpret_cast<const void*>(fill_kernel<__nv_bfloat16>)
+                             : reinterpret_cast<const void*>(fill_kernel<float>);
+  if (cudaError_t e = ensure_smem_attr(fill, smax)) return e;
+  if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(walk_kernel), smax)) return e;
+  const dim3 grid((unsigned)c->num_sms), blk(kSamplerThreads);
+  mark_kernel<<<grid, blk, 0, c->stream>>>(sa);
+  c->launches++;
+  if (cudaError_t e = cudaGetLastError()) return e;
+  cudaError_t e = c->bf16 ? klaunch(c, fill_kernel<__nv_bfloat16>, grid, blk, smem, c->stream, sa)
+                          : klaunch(c, fill_kernel<float>, grid, blk, smem, c->stream, sa);
+  if (e != cudaSuccess) return e;
+  return klaunch(c, walk_kernel, grid, blk, smem, c->stream, sa);
 }
 
 int dx_splits(Ctx* c, int64_t B) {
@@ -460,44 +577,19 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     CUDA_TRY(c, cudaEventRecord(c->ev_x, c->s2));
   }
   // ---- sampler (build_buffers, sampler.hpp:63-126); its first kernel also opens the step.
-  // (host drop-in: `lab` is the caller's page-locked labels, read by the sampler over PCIe)
-  int P2 = 1;
-  while (P2 < B) P2 <<= 1;
-  // keys + sorted unique labels (int32) + the staged batch labels (int64)
-  const size_t sort_smem = (2 * sizeof(int32_t) + sizeof(int64_t)) * (size_t)P2;
-  CUDA_TRY(c, ensure_smem_attr(reinterpret_cast<const void*>(positives_kernel),
-                               (int)((2 * sizeof(int32_t) + sizeof(int64_t)) * kMaxSortBatch)));
-  c->sort_smem = sort_smem;
-  positives_kernel<<<1, 1024, sort_smem, s>>>(
-      c->st, c->sp, a->seed, a->stream_id, (float)a->lr, c->reset_status ? 1 : 0, x, lab, dx_full,
-      (int)B, c->C, (int)c->K, c->blk, (int)c->cap, (int)c->k0, (int)c->nk, c->uniq, c->meta,
-      c->buf_cls, c->pos_col, (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0);
-  c->launches++;
-  CUDA_TRY(c, cudaMemsetAsync(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride, s));
-  const int64_t nd = c->nk * c->cap;
-  OT* xh = static_cast<OT*>(c->xh);
-  const int nbd = (int)ceil_div(nd, bs);
-  // draws + (trailing blocks) x^ = x / |x|   (shardsim.hpp:196-232)
-  draws_kernel<OT><<<(unsigned)(nbd + (e2e ? 0 : ceil_div(B * 32, bs))), bs, 0, s>>>(
-      c->meta, (int)c->nk, (int)c->cap, c->sp, (int)c->k0, c->pool_stride, c->head, c->nxt,
-      c->jv, c->st, nbd, (int)B, (int)c->D, (int)c->Dp, xh, c->xnorm);
-  // chain walk + (trailing blocks, one per shard) the exact sequential fallback
-  walk_kernel<<<(unsigned)(nbd + c->nk), bs, 0, s>>>(c->meta, (int)c->nk, (int)c->cap,
-                                                     c->pool_stride, c->head, c->nxt, c->jv,
-                                                     c->buf_cls, c->st, nbd, c->sp, (int)c->k0,
-                                                     c->pool_scratch);
-  c->launches += 2;
+  // (host drop-in: `lab` is the caller's page-locked labels, read once over PCIe by the sampler)
+  {
+    SamplerArgs sa = sampler_args(c, a, x, lab, dx_full, B, e2e ? 0 : 1);
+    CUDA_TRY(c, launch_sampler(c, sa));
+  }
   phase(c, "sampler");
   // ---- gather + normalise sampled centres
   OT* wh = static_cast<OT*>(c->wh);
-  gather_w_kernel<OT><<<(unsigned)ceil_div(c->ncols_pad * 32, bs), bs, 0, s>>>(
-      c->W, (int)c->D, (int)c->Dp, c->buf_cls, (int)c->ncols, (int)c->ncols_pad, c->cls_lo,
-      c->rows, wh, c->wnorm, c->lrow, c->pslot, c->st);
-  c->launches++;
-  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, klaunch(c, gather_w_kernel<OT>, dim3((unsigned)ceil_div(c->ncols_pad * 32, bs)),
+                      dim3(bs), 0, s, c->W, (int)c->D, (int)c->Dp, c->buf_cls, (int)c->ncols,
+                      (int)c->ncols_pad, c->cls_lo, c->rows, wh, c->wnorm, c->lrow, c->pslot,
+                      (const StepStatus*)c->st));
   phase(c, "gather");
-  CUDA_TRY(c, cudaMemsetAsync(c->zpos, 0, sizeof(double) * B, s));
-  if (c->d.has_filter) CUDA_TRY(c, cudaMemsetAsync(c->hasval, 0, sizeof(int) * B, s));
 
   constexpr int BN = kUmma ? kBN : kSimtBN;
   constexpr int FBN = kUmma ? kFwdBN : kSimtBN;  // logits GEMM tile width
@@ -524,10 +616,8 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     if (filt) err = go(MaxEpi<true>{{}, (int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, c->zpos});
     else err = go(MaxEpi<false>{{}, (int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, c->zpos});
     CUDA_TRY(c, err);
-    row_offset_kernel<<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(pm, gf.n_tiles * NWG, (int)B,
-                                                              c->pos_col, c->zpos, c->mg, c->offr);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, klaunch(c, row_offset_kernel, dim3((unsigned)ceil_div(B, bs)), dim3(bs), 0, s,
+                        pm, gf.n_tiles * NWG, (int)B, c->pos_col, c->zpos, c->mg, c->offr));
     if (c->R > 1) COMM_TRY(comm_all_reduce(c, c->offr, c->offr, B, kF32, kMax, s));
     phase(c, "row_offsets");
   }
@@ -555,17 +645,10 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- softmax statistics: slices -> rank-local sum -> ranks (collectives 1 + 2) -> loss
   const int T = gf.n_tiles * NWG;
   ST* ls = static_cast<ST*>(c->ls);
-  const int nseg = (int)std::min<int64_t>(kMergeSegs, T);
-  ST* seg = static_cast<ST*>(c->seg_s);
-  sum_slices_kernel<ST><<<dim3((unsigned)ceil_div(B, 128), (unsigned)nseg), 128, 0, s>>>(
-      ps, T, (int)B, seg);
-  c->launches++;
+  const unsigned nrb = (unsigned)ceil_div(B, kRowsPerBlk);
   if (c->R > 1) {  // the rank-local sums are exchanged; with one rank finalize forms them
-    sum_segments_kernel<ST><<<(unsigned)ceil_div(B, bs), bs, 0, s>>>(seg, nseg, (int)B,
-                                                                     ls + c->rank * B);
-    c->launches++;
-  }
-  if (c->R > 1) {
+    CUDA_TRY(c, klaunch(c, local_sums_kernel<ST>, dim3(nrb), dim3(256), 0, s, ps, T, (int)B,
+                        ls + c->rank * B));
     const CommDt dt = sizeof(ST) == 8 ? kF64 : kF32;
     COMM_TRY(comm_all_gather(c, ls + c->rank * B, ls, B, dt, s));
     COMM_TRY(comm_all_reduce(c, c->zpos, c->zpos, B, kF64, kSum, s));
@@ -573,10 +656,11 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   }
   ST* rsc = static_cast<ST*>(c->rowscale);
   ST* dlt = static_cast<ST*>(c->delta);
-  finalize_stats_kernel<ST><<<(unsigned)ceil_div(B * 32, 256), 256, 0, s>>>(
-      ls, c->R, c->R > 1 ? nullptr : seg, nseg, (int)B, c->zpos, c->cpos, c->epos, c->pos_col,
-      c->hasval, filt ? 1 : 0, c->mg, offr, rsc, dlt, c->loss_row, c->st);
-  c->launches++;
+  CUDA_TRY(c, klaunch(c, finalize_stats_kernel<ST>, dim3(nrb), dim3(256), 0, s, (const ST*)ls,
+                      (int)c->R, (const ST*)(c->R > 1 ? nullptr : ps), T, (int)B,
+                      (const double*)c->zpos, (const double*)c->cpos, (const float*)c->epos,
+                      (const int32_t*)c->pos_col, (const int*)c->hasval, filt ? 1 : 0, c->mg,
+                      offr, rsc, dlt, c->loss_row, c->st));
   CUDA_TRY(c, cudaGetLastError());
   phase(c, "softmax_stats");
   // X^s and the positive corrections feed only the dW GEMM: they run on a forked stream,
@@ -584,7 +668,9 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
   CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_fork, 0));
   xs_kernel<ST, OT><<<(unsigned)B, 128, 0, c->s2>>>(c->sp, c->xnorm, rsc, (int)B, (int)c->D,
-                                                    (int)c->Dp, static_cast<OT*>(c->xs));
+                                                    (int)c->Dp, static_cast<OT*>(c->xs), c->meta,
+                                                    (int)c->nk, (int)c->cap, c->jv, c->head,
+                                                    c->pool_stride, c->st);
   poscorr_kernel<<<dim3((unsigned)c->pmax, (unsigned)c->nk), 256, 0, c->s2>>>(
       c->meta, (int)c->cap, (int)c->pmax, c->pos_col, (int)B, c->sp, c->xnorm, (int)c->D,
       std::is_same<ST, float>::value ? reinterpret_cast<const float*>(dlt) : nullptr,
@@ -604,17 +690,17 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
                                        (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
     const int dpt = (int)ceil_div(c->D, 256);
-#define PFC_FIN(N)                                                                               \
-  dx_finalize_kernel<N, ST><<<(unsigned)B, 256, 0, s>>>(c->dx_part, gx.splits, c->sp, c->xnorm, \
-                                                        rsc, dlt, c->pos_col, c->lrow, c->wnorm, \
-                                                        c->W, (int)B, (int)c->D, c->st)
-    if (dpt <= 1) PFC_FIN(1);
-    else if (dpt <= 2) PFC_FIN(2);
-    else if (dpt <= 4) PFC_FIN(4);
-    else PFC_FIN(8);
+#define PFC_FIN(N)                                                                           \
+  klaunch(c, dx_finalize_kernel<N, ST>, dim3((unsigned)B), dim3(256), 0, s,                 \
+          (const float*)c->dx_part, gx.splits, (const StepParams*)c->sp,                     \
+          (const float*)c->xnorm, (const ST*)rsc, (const ST*)dlt, (const int32_t*)c->pos_col, \
+          (const int32_t*)c->lrow, (const float*)c->wnorm, (const float*)c->W, (int)B,        \
+          (int)c->D, c->st)
+    if (dpt <= 1) CUDA_TRY(c, PFC_FIN(1));
+    else if (dpt <= 2) CUDA_TRY(c, PFC_FIN(2));
+    else if (dpt <= 4) CUDA_TRY(c, PFC_FIN(4));
+    else CUDA_TRY(c, PFC_FIN(8));
 #undef PFC_FIN
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
   }
   if (e2e) {  // d_features: [sum over ranks], -> D x B fp64, download; overlaps the dW GEMM
     CUDA_TRY(c, cudaEventRecord(c->ev_dx, s));
@@ -665,11 +751,11 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
       err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xs,
                                      (int)c->Dp, gw, DwStoreEpi{{}, (int)c->ncols, (int)c->D, c->dwt});
       if (err == cudaSuccess) {
-        dw_rows_update_kernel<<<(unsigned)ceil_div(c->ncols * 32, bs), bs, 0, s>>>(
-            c->dwt, c->lrow, c->wnorm, c->pslot, c->poscorr, (int)c->ncols, (int)c->D, c->W, c->M,
-            c->sp, (float)c->d.momentum, (float)c->d.weight_decay, c->st);
-        c->launches++;
-        err = cudaGetLastError();
+        err = klaunch(c, dw_rows_update_kernel, dim3((unsigned)ceil_div(c->ncols * 32, bs)),
+                      dim3(bs), 0, s, (const float*)c->dwt, (const int32_t*)c->lrow,
+                      (const float*)c->wnorm, (const int32_t*)c->pslot, (const float*)c->poscorr,
+                      (int)c->ncols, (int)c->D, c->W, c->M, (const StepParams*)c->sp,
+                      (float)c->d.momentum, (float)c->d.weight_decay, (const StepStatus*)c->st);
       }
     }
     CUDA_TRY(c, err);
@@ -733,7 +819,7 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
       if (ty != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams kp{};
       if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
-          kp.func == reinterpret_cast<void*>(positives_kernel))
+          kp.func == reinterpret_cast<void*>(mark_kernel))
         G.gbegin = nd;
     }
     if (!G.gbegin) return fail(c, PFC_ERR_CUDA, "graph capture lost the step-opening node");
@@ -745,30 +831,21 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
     G.gwire = c->step_wire_bytes - wire0;
     c->step_nccl_bytes = bytes0;
     c->step_wire_bytes = wire0;
-    G.psmem = c->sort_smem;
     G.cp_ptr[0] = G.cp_ptr[1] = G.cp_ptr[2] = nullptr;
   }
   // per step, only the step-opening kernel's arguments (and the host drop-in's host pointers)
   // change; the other arguments and the launch shape are the captured ones
-  StepStatus* st = c->st;
-  StepParams* sp = c->sp;
-  uint64_t seed = a->seed, stream = a->stream_id;
-  float lr = (float)a->lr;
-  int reset = c->reset_status ? 1 : 0;
-  int iB = (int)B, iK = (int)c->K, icap = (int)c->cap, ik0 = (int)c->k0, ink = (int)c->nk;
-  int64_t C = c->C, blk = c->blk;
-  int64_t* uniq = c->uniq;
-  ShardMeta* meta = c->meta;
-  int32_t* buf_cls = c->buf_cls;
-  int32_t* pos_col = c->pos_col;
-  int force = (c->d.flags & PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER) ? 1 : 0;
-  void* args[] = {&st, &sp, &seed, &stream, &lr, &reset, &x, &lab, &dx_full, &iB, &C, &iK,
-                  &blk, &icap, &ik0, &ink, &uniq, &meta, &buf_cls, &pos_col, &force};
+  // the fill / walk nodes read the per-step values from the StepParams block mark_kernel
+  // writes, so only the opening node's arguments change (the captured SamplerArgs of the other
+  // two nodes are identical for every step of this batch size except the fields below, which
+  // they do not use: seed, stream, lr, reset, labels_in)
+  SamplerArgs sa = sampler_args(c, a, x, lab, dx_full, B, c->e2e.on ? 0 : 1);
+  void* args[] = {&sa};
   cudaKernelNodeParams kp{};
-  kp.func = reinterpret_cast<void*>(positives_kernel);
-  kp.gridDim = dim3(1);
-  kp.blockDim = dim3(1024);
-  kp.sharedMemBytes = (unsigned)G.psmem;
+  kp.func = reinterpret_cast<void*>(mark_kernel);
+  kp.gridDim = dim3((unsigned)c->num_sms);
+  kp.blockDim = dim3(kSamplerThreads);
+  kp.sharedMemBytes = 0;
   kp.kernelParams = args;
   kp.extra = nullptr;
   CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(G.gexec, G.gbegin, &kp));
@@ -805,9 +882,6 @@ void trace_closed_form(Ctx* c, int64_t B, pfc_gpu_step_out* o) {
 int check_status(Ctx* c, int64_t step_index, int64_t B, pfc_gpu_step_out* out) {
   const StepStatus& st = *c->st_host;
   c->underflowed = false;
-  if (st.batch_too_large)
-    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu: global batch %lld exceeds the supported %d",
-                (long long)B, kMaxSortBatch);
   if (st.label_oob)
     return fail(c, PFC_ERR_CONTRACT, "build_buffers: label %lld outside [0, %lld)",
                 (long long)st.oob_label, (long long)c->C);
@@ -922,13 +996,17 @@ int validate_desc(const pfc_gpu_desc* d) {
   if (d->margin_kind < 0 || d->margin_kind > 2)
     return fail(nullptr, PFC_ERR_CONTRACT, "apply_margin: unknown kind");
   if (d->dim < 1) return fail(nullptr, PFC_ERR_SHAPE, "pfc_gpu_create: dim must be >= 1");
-  if (d->max_batch < 1 || d->max_batch > kMaxSortBatch)
+  if (d->max_batch < 1 || d->max_batch > kMaxBatch)
     return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: max_batch must be in [1, %d]",
-                kMaxSortBatch);
+                kMaxBatch);
   if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size ||
       d->num_shards % d->world_size != 0)
     return fail(nullptr, PFC_ERR_CONTRACT,
                 "pfc_gpu_create: world_size must divide num_shards and 0 <= rank < world_size");
+  if (d->num_shards / d->world_size > kMaxSamplerLocalShards)
+    return fail(nullptr, PFC_ERR_CONTRACT,
+                "pfc_gpu_create: at most %d reference shards per rank (num_shards / world_size)",
+                kMaxSamplerLocalShards);
   if (d->precision == PFC_PRECISION_BF16 && (d->dim % 4 != 0 || d->dim > 512))
     return fail(nullptr, PFC_ERR_CONFIG,
                 "pfc_gpu: the bf16 tcgen05 path needs dim %% 4 == 0 and dim <= 512 "
@@ -1149,6 +1227,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->mg.offd = std::max(0.0, desc->margin_scale - 40.0);  // E = exp(z - o) <= e^40
   c->mg.off = (float)c->mg.offd;
   c->exact = desc->margin_scale > kFixedOffsetMaxScale || (desc->flags & PFC_FLAG_EXACT_SOFTMAX);
+  c->pdl = !(desc->flags & PFC_FLAG_NO_PDL);
   int64_t B = c->maxB;
   auto bail = [&](int rc) {
     g_create_error = c->err;
@@ -1186,11 +1265,23 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->W, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
   CT(dalloc(c, &c->M, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
   CT(dalloc(c, &c->labels, (size_t)B));
-  CT(dalloc(c, &c->uniq, (size_t)B));
+  c->nwords = c->C / 32 + 1;  // covers bit C itself: bits_below(C) is the total count
+  while (ceil_div(c->nwords, c->chunk_words) > kMaxSamplerChunks) c->chunk_words *= 2;
+  c->nchunk = (int)ceil_div(c->nwords, c->chunk_words);
+  CT(dalloc(c, &c->labs, (size_t)B));
+  CT(dalloc(c, &c->bits, (size_t)c->nwords));
+  CT(dalloc(c, &c->ccnt, (size_t)c->nchunk));
+  CT(dalloc(c, &c->rej, (size_t)c->nk));
+  CT(dalloc(c, &c->oobs, 2));
+  {
+    const long long none[2] = {LLONG_MAX, LLONG_MAX};
+    CT(cudaMemcpy(c->oobs, none, sizeof none, cudaMemcpyHostToDevice));
+  }
   CT(dalloc(c, &c->meta, (size_t)c->nk));
   CT(dalloc(c, &c->buf_cls, (size_t)std::max<int64_t>(c->ncols, 1)));
   CT(dalloc(c, &c->pos_col, (size_t)B));
   CT(dalloc(c, &c->head, (size_t)(c->nk * c->pool_stride)));
+  CT(cudaMemset(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride));  // reset per draw after
   CT(dalloc(c, &c->nxt, (size_t)std::max<int64_t>(c->ncols, 1)));
   CT(dalloc(c, &c->jv, (size_t)std::max<int64_t>(c->ncols, 1)));
   CT(dalloc(c, &c->pool_scratch, (size_t)(c->nk * c->pool_stride)));
@@ -1202,7 +1293,6 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
   const int64_t Tf = c->bf16 ? ceil_div(std::max<int64_t>(c->ncols, 1), kFwdBN) * kFwdNWG : T;
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(Tf * B) * sb));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->seg_s), (size_t)(kMergeSegs * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->ls), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->rowscale), (size_t)B * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->delta), (size_t)B * sb));
@@ -1981,6 +2071,38 @@ int pfc_gpu_step_features(void* ctx, const double* xdb_dev, const int64_t* label
   if (dxdb_dev && dxdb_dev != c->xdb)
     CUDA_TRY(c, cudaMemcpyAsync(dxdb_dev, c->xdb, sizeof(double) * B * c->D, cudaMemcpyDeviceToDevice, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
+  return PFC_OK;
+}
+
+int pfc_gpu_check_guards(void* ctx, int64_t* corrupted) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  *corrupted = 0;
+  if (!(c->d.flags & PFC_FLAG_GUARD))
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_check_guards: context created without PFC_FLAG_GUARD");
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  std::vector<uint8_t> h(kGuardBytes);
+  std::string where;
+  for (size_t i = 0; i < c->guards.size(); ++i) {
+    const Ctx::Guard& g = c->guards[i];
+    for (int side = 0; side < 2; ++side) {
+      const uint8_t* at = side ? g.base + kGuardBytes + g.user : g.base;
+      CUDA_TRY(c, cudaMemcpy(h.data(), at, kGuardBytes, cudaMemcpyDeviceToHost));
+      size_t bad = 0, first = kGuardBytes;
+      for (size_t j = 0; j < kGuardBytes; ++j)
+        if (h[j] != (uint8_t)kGuardByte) {
+          ++bad;
+          if (first == kGuardBytes) first = j;
+        }
+      if (bad) {
+        ++*corrupted;
+        char buf[160];
+        snprintf(buf, sizeof buf, "%sbuffer #%zu (%zu bytes): %zu guard bytes %s it changed, first at %zu",
+                 where.empty() ? "" : "; ", i, g.user, bad, side ? "after" : "before", first);
+        where += buf;
+      }
+    }
+  }
+  if (*corrupted) return fail(c, PFC_ERR_CUDA, "out-of-bounds writes: %s", where.c_str());
   return PFC_OK;
 }
 

@@ -12,36 +12,62 @@
 //
 // A modulo rejection (probability <= n / 2^64 per draw) shifts every later counter; it is
 // detected per shard and that shard is redone by an exact sequential kernel on the device.
+#include <climits>
+
 #include "common.cuh"
 
 namespace pfc {
 
-constexpr int kMaxSortBatch = 8192;
+constexpr int kMaxBatch = 1 << 20;  // global batch rows (pfc_gpu_desc::max_batch)
 
-// first index with a[i] >= v in the sorted keys a[0..n)
-__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int64_t v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((int64_t)a[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
+// ---- build_buffers (sampler.hpp:63-126) in three kernels: a bitmap over the C classes instead
+// of a sort, and the parallel Fisher-Yates restatement.
+//   mark_kernel (opens the step): every valid label sets its class bit and, when the bit was new,
+//      counts it in its chunk (chunk_words words); the two smallest invalid labels are kept (the
+//      reference validates the sorted unique list: the smallest negative one, else the smallest
+//      one >= C); the labels are copied to the device (host drop-in: read once over PCIe)
+//   fill_kernel, every CTA redundantly: chunk prefixes in shared memory; validation; every
+//      shard's distinct-positive count against the capacity in ascending shard order
+//      (sampler.hpp:84-98); the local shards' metadata (CTA 0 publishes it); then the positives
+//      of the local shards ascending (a class's rank among the set bits of its shard is its
+//      buffer slot, sampler.hpp:100-104), each row's positive column (shardsim.hpp:207-213), the
+//      draws (counter RNG, rejection flag, per-position lists) and x^ = x / |x|
+//   walk_kernel: chain walk; the exact sequential sampler for shards that saw a modulo
+//      rejection; the bitmap and chunk counts are cleared again (all-zero between steps: no
+//      per-step pass over all C classes)
+// Grid-stride loops over one CTA of 1024 threads per SM; the kernels are chained by PDL.
+constexpr int kSamplerThreads = 1024;
+constexpr int kMaxSamplerChunks = 8192;       // chunk prefixes kept in shared memory
+constexpr int kMaxSamplerLocalShards = 2048;  // local shard metadata kept in shared memory
 
-// minimum over the block (every thread gets it); red: 32 shared slots
-__device__ __forceinline__ int64_t block_min_i64(int64_t v, int64_t* red) {
+__device__ __forceinline__ int warp_sum_i(int v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const int64_t w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w < v ? w : v;
-  }
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  int64_t r = red[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = red[w] < r ? red[w] : r;
-  __syncthreads();
-  return r;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
+
+// Set bits of the bitmap below class x (warp-collective): the chunk prefix plus a popcount of
+// the words of x's chunk before it (coalesced, 32 words per instruction).
+__device__ __forceinline__ int bits_below(const uint32_t* bits, const int32_t* bpre_s,
+                                          int chunk_words, int64_t x, int lane) {
+  const int64_t w = x >> 5;
+  const int64_t ch = w / chunk_words;
+  int cnt = 0;
+  // 8 independent loads in flight per lane (not one dependent L2 round trip per 32 words)
+  int64_t i = ch * chunk_words + lane;
+  for (; i + 7 * 32 < w; i += 8 * 32) {
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = bits[i + u * 32];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cnt += __popc(v[u]);
+  }
+  for (; i < w; i += 32) cnt += __popc(bits[i]);
+  if (lane == 0) cnt += __popc(bits[w] & ((1u << (x & 31)) - 1u));
+  return bpre_s[ch] + warp_sum_i(cnt);
+}
+
+__device__ int block_exclusive_scan(int v, int* smem_warp, int* total);
 
 // Exclusive block scan of one int per thread (blockDim.x == 1024).
 __device__ int block_exclusive_scan(int v, int* smem_warp, int* total) {
@@ -70,191 +96,6 @@ __device__ int block_exclusive_scan(int v, int* smem_warp, int* total) {
   return before;
 }
 
-// One CTA of 1024 threads: sort + unique the global batch labels, validate them, route
-// positives to shards (sampler.hpp:68-80), check capacity in the reference's shard order
-// (sampler.hpp:84-98), and locate every row's positive column (shardsim.hpp:207-213).
-// Its thread 0 first opens the step (step_begin: the step's parameters and a status reset), so
-// this kernel is the one node of the step's graph whose arguments change from step to step.
-__global__ void __launch_bounds__(1024) positives_kernel(
-    StepStatus* st, StepParams* sp, uint64_t seed, uint64_t stream, float lr, int reset,
-    const float* x, const int64_t* labels_in, float* dx, int B, int64_t C, int K, int64_t blk,
-    int cap, int k0, int nk, int64_t* __restrict__ uniq, ShardMeta* __restrict__ meta,
-    int32_t* __restrict__ buf_cls, int32_t* __restrict__ pos_col, int force_sequential) {
-  if (threadIdx.x == 0) step_begin(st, sp, seed, stream, lr, reset, x, labels_in, dx);
-  __syncthreads();  // the block sees the step's parameters and the reset status
-  // dynamic smem: keys[P] and the sorted unique labels us[P] (int32), then the batch labels[P]
-  // (int64), staged once: in the host drop-in they are read from the caller's page-locked buffer
-  // over PCIe (P = B rounded up to a power of 2)
-  extern __shared__ int32_t keys[];
-  __shared__ int warp_tmp[32];
-  __shared__ int nuniq_s;
-  __shared__ int64_t red[32];
-  if (B > kMaxSortBatch) {
-    if (threadIdx.x == 0) st->batch_too_large = 1;
-    return;
-  }
-  int P = 1;
-  while (P < B) P <<= 1;
-  int64_t* labels = reinterpret_cast<int64_t*>(keys + 2 * P);
-  // validation (sampler.hpp:72-78) reports the first invalid label of the SORTED unique list:
-  // the smallest negative one, else the smallest one >= C.  With every label in [0, C),
-  // C < 2^31, the sort and the searches below run on 32-bit keys.
-  int64_t mn = INT64_MAX, mc = INT64_MAX;
-  for (int i = threadIdx.x; i < B; i += blockDim.x) {
-    const int64_t y = labels_in[i];
-    labels[i] = y;
-    mn = y < mn ? y : mn;
-    if (y >= C && y < mc) mc = y;
-  }
-  mn = block_min_i64(mn, red);
-  mc = block_min_i64(mc, red);
-  if (mn < 0 || mc != INT64_MAX) {
-    if (threadIdx.x == 0) {
-      st->label_oob = 1;
-      st->oob_label = mn < 0 ? mn : mc;
-    }
-    return;
-  }
-  if (P <= (int)blockDim.x) {
-    // one key per thread: register bitonic sort, warp shuffles for partner distance < 32
-    const int i = threadIdx.x;
-    int32_t key = i < B ? (int32_t)labels[i] : INT32_MAX;
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        int32_t other;
-        if (j >= 32) {
-          if (i < P) keys[i] = key;
-          __syncthreads();
-          other = i < P ? keys[i ^ j] : key;
-          __syncthreads();
-        } else {
-          other = __shfl_xor_sync(0xffffffffu, key, j);
-        }
-        const bool asc = (i & k) == 0, lower = i < (i ^ j);
-        key = (asc == lower) ? min(key, other) : max(key, other);
-      }
-    }
-    if (i < P) keys[i] = key;
-    __syncthreads();
-  } else {
-    for (int i = threadIdx.x; i < P; i += blockDim.x) keys[i] = i < B ? (int32_t)labels[i] : INT32_MAX;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < P; i += blockDim.x) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const int32_t a = keys[i], b = keys[ixj];
-            const bool asc = (i & k) == 0;
-            if (asc ? (a > b) : (a < b)) {
-              keys[i] = b;
-              keys[ixj] = a;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-  }
-  // unique (sorted) into shared memory: each thread owns a contiguous run of keys
-  int32_t* us = keys + P;
-  __shared__ int bad_shard_s;
-  const int per = (B + blockDim.x - 1) / blockDim.x;
-  const int beg = threadIdx.x * per, end = min(B, beg + per);
-  int cnt = 0;
-  for (int i = beg; i < end; ++i) cnt += (i == 0 || keys[i] != keys[i - 1]);
-  int total = 0;
-  int pos = block_exclusive_scan(cnt, warp_tmp, &total);
-  for (int i = beg; i < end; ++i)
-    if (i == 0 || keys[i] != keys[i - 1]) us[pos++] = keys[i];
-  if (threadIdx.x == 0) {
-    nuniq_s = total;
-    bad_shard_s = K;
-  }
-  __syncthreads();
-  const int nu = nuniq_s;
-  // capacity checks for ALL shards; the first failing shard in ascending order wins
-  // (sampler.hpp:84-98)
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
-    const int np = lower_bound_i32(us, nu, hi) - lower_bound_i32(us, nu, lo);
-    if (np > cap || hi - lo < cap) atomicMin(&bad_shard_s, k);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && bad_shard_s < K) {
-    const int k = bad_shard_s;
-    const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
-    st->capacity_shard = k;
-    st->capacity_npos = lower_bound_i32(us, nu, hi) - lower_bound_i32(us, nu, lo);
-  }
-  __syncthreads();
-  if (bad_shard_s < K) return;
-  for (int kk = threadIdx.x; kk < nk; kk += blockDim.x) {
-    const int k = k0 + kk;
-    const int64_t lo = min((int64_t)k * blk, C), hi = min((int64_t)(k + 1) * blk, C);
-    const int us0 = lower_bound_i32(us, nu, lo), ue = lower_bound_i32(us, nu, hi);
-    ShardMeta m;
-    m.lo = lo;
-    m.hi = hi;
-    m.npos = ue - us0;
-    m.need = cap - m.npos;
-    m.pool = (int)(hi - lo) - m.npos;
-    m.full = (m.need == m.pool);
-    m.ustart = us0;
-    m.reject = force_sequential && !m.full && m.need > 0;
-    meta[kk] = m;
-  }
-  // positives first, ascending (sampler.hpp:100-104)
-  for (int i = threadIdx.x; i < nu; i += blockDim.x) {
-    const int32_t y = us[i];
-    const int k = (int)((uint32_t)y / (uint32_t)blk);
-    if (k >= k0 && k < k0 + nk) {
-      const int64_t lo = min((int64_t)k * blk, C);
-      const int u0 = lower_bound_i32(us, nu, lo);
-      buf_cls[(int64_t)(k - k0) * cap + (i - u0)] = y;
-    }
-  }
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    const int32_t y = (int32_t)labels[b];
-    const int k = (int)((uint32_t)y / (uint32_t)blk);
-    int col = -1;
-    if (k >= k0 && k < k0 + nk) {
-      const int64_t lo = min((int64_t)k * blk, C);
-      col = (k - k0) * cap + (lower_bound_i32(us, nu, y) - lower_bound_i32(us, nu, lo));
-    }
-    pos_col[b] = col;
-  }
-}
-
-// Per-draw counter RNG + modulo-rejection flag + per-position lists (j_s = p).  Blocks past
-// the draws (blockIdx.x >= nblk_draws) normalise the features instead (independent work that
-// shares the launch).
-template <typename OT>
-__global__ void draws_kernel(ShardMeta* __restrict__ meta, int nk, int cap,
-                             const StepParams* __restrict__ sp, int k0, int64_t pool_stride,
-                             int32_t* __restrict__ head, int32_t* __restrict__ nxt,
-                             int32_t* __restrict__ jv, const StepStatus* st, int nblk_draws,
-                             int B, int D, int Dp, OT* __restrict__ xh, float* __restrict__ xnorm) {
-  if ((int)blockIdx.x >= nblk_draws) {
-    normalize_x_rows(sp->x, B, D, Dp, xh, xnorm, (int)blockIdx.x - nblk_draws);
-    return;
-  }
-  if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)nk * cap) return;
-  const int kk = (int)(gid / cap), i = (int)(gid % cap);
-  const ShardMeta m = meta[kk];
-  if (m.full || i >= m.need) return;
-  const uint64_t key = rng_key(sp->seed, fork_stream(sp->stream, (uint64_t)(k0 + kk)));
-  const uint64_t n = (uint64_t)(m.pool - i);
-  const uint64_t r = rng_draw(key, (uint64_t)i + 1);
-  const uint64_t limit = UINT64_MAX - UINT64_MAX % n;  // rng.hpp:69
-  if (r >= limit) meta[kk].reject = 1;
-  const int32_t j = i + (int32_t)(r % n);
-  jv[gid] = j;
-  nxt[gid] = atomicExch(&head[(int64_t)kk * pool_stride + j], i);
-}
-
 // p-th element of [lo, hi) minus the sorted positives pos[0..npos)
 __device__ __forceinline__ int64_t pool_value(int64_t lo, const int32_t* pos, int npos,
                                               int64_t p) {
@@ -267,57 +108,11 @@ __device__ __forceinline__ int64_t pool_value(int64_t lo, const int32_t* pos, in
   return lo + p + a;
 }
 
-__device__ void sequential_fallback(ShardMeta* meta, int cap, const StepParams* sp, int k0,
-                                    int64_t pool_stride, int32_t* pool_scratch, int32_t* buf_cls,
-                                    StepStatus* st, int kk);
-
-// Chain walk of the parallel Fisher-Yates restatement; the last nk blocks run the exact
-// sequential sampler for shards that saw a modulo rejection (disjoint from the walked shards).
-__global__ void walk_kernel(ShardMeta* __restrict__ meta, int nk, int cap,
-                            int64_t pool_stride, const int32_t* __restrict__ head,
-                            const int32_t* __restrict__ nxt, const int32_t* __restrict__ jv,
-                            int32_t* __restrict__ buf_cls, StepStatus* st, int nblk_walk,
-                            const StepParams* __restrict__ sp, int k0,
-                            int32_t* __restrict__ pool_scratch) {
-  if (st->label_oob || st->capacity_shard >= 0 || st->batch_too_large) return;
-  if ((int)blockIdx.x >= nblk_walk) {
-    sequential_fallback(meta, cap, sp, k0, pool_stride, pool_scratch, buf_cls, st,
-                        (int)blockIdx.x - nblk_walk);
-    return;
-  }
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)nk * cap) return;
-  const int kk = (int)(gid / cap), i = (int)(gid % cap);
-  const ShardMeta m = meta[kk];
-  if (m.reject || i >= m.need) return;
-  int32_t* row = buf_cls + (int64_t)kk * cap;
-  int64_t p;
-  if (m.full) {
-    p = i;  // full sampling: ascending complement (sampler.hpp:106-115)
-  } else {
-    const int32_t* hd = head + (int64_t)kk * pool_stride;
-    const int32_t* nx = nxt + (int64_t)kk * cap;
-    int32_t pp = jv[(int64_t)kk * cap + i], t = i;
-    for (;;) {
-      int32_t best = -1;
-      for (int32_t s = hd[pp]; s >= 0; s = nx[s])
-        if (s < t && s > best) best = s;
-      if (best < 0) break;
-      pp = best;
-      t = best;
-    }
-    p = pp;
-  }
-  row[m.npos + i] = (int32_t)pool_value(m.lo, row, m.npos, p);
-}
-
-// Exact sequential sample_without_replacement for shards that saw a modulo rejection
-// (or when forced for testing).  One CTA per local shard (walk_kernel's trailing blocks).
-__device__ void sequential_fallback(ShardMeta* meta, int cap, const StepParams* sp, int k0,
+// Exact sequential sample_without_replacement for a shard that saw a modulo rejection (or when
+// forced for testing), by one CTA: the complement pool, then the reference's loop.
+__device__ void sequential_fallback(const ShardMeta& m, int cap, const StepParams* sp, int k0,
                                     int64_t pool_stride, int32_t* pool_scratch, int32_t* buf_cls,
                                     StepStatus* st, int kk) {
-  const ShardMeta m = meta[kk];
-  if (!m.reject) return;
   int32_t* row = buf_cls + (int64_t)kk * cap;
   int32_t* pool = pool_scratch + (int64_t)kk * pool_stride;
   for (int64_t p = threadIdx.x; p < m.pool; p += blockDim.x)
@@ -338,6 +133,237 @@ __device__ void sequential_fallback(ShardMeta* meta, int cap, const StepParams* 
       pool[j] = t;
       row[m.npos + i] = pool[i];
     }
+  }
+  __syncthreads();
+}
+
+struct SamplerArgs {
+  StepStatus* st;
+  StepParams* sp;
+  uint64_t seed, stream;
+  float lr;
+  int reset;
+  const float* x;
+  const int64_t* labels_in;  // device or page-locked host labels of the global batch
+  float* dx;
+  int B;
+  int64_t C;
+  int K;
+  int64_t blk;
+  int cap, k0, nk;
+  int force_sequential;
+  int normalize;             // 1: phase D also normalises the features (device path)
+  int D, Dp;
+  void* xh;                  // x^ in the GEMM operand type
+  float* xnorm;
+  uint32_t* bits;            // [nwords] class bitmap
+  int32_t* ccnt;             // [nchunk] set bits per chunk
+  int chunk_words, nchunk;
+  long long* oobs;           // [2] smallest negative / >= C label (LLONG_MAX: none)
+  int32_t* rej;              // [nk] modulo rejection seen by a draw
+  int64_t* labs;
+  double* zpos;
+  int* hasval;
+  ShardMeta* meta;           // [nk] published for the later kernels and pfc_gpu_get_buffers
+  int32_t* buf_cls;
+  int32_t* pos_col;
+  int32_t* head;
+  int32_t* nxt;
+  int32_t* jv;
+  int32_t* pool_scratch;
+  int64_t pool_stride;
+};
+
+__host__ __device__ constexpr size_t sampler_smem_bytes(int nchunk, int nk) {
+  return (size_t)nchunk * sizeof(int32_t) + (size_t)nk * sizeof(ShardMeta);
+}
+
+// Opens the step (thread 0: step_begin) and marks the labels.
+__global__ void __launch_bounds__(kSamplerThreads) mark_kernel(const SamplerArgs a) {
+  pdl_entry();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0) step_begin(a.st, a.sp, a.seed, a.stream, a.lr, a.reset, a.x, a.labels_in, a.dx);
+  for (int64_t b = tid; b < a.B; b += nthr) {
+    const int64_t y = a.labels_in[b];
+    a.labs[b] = y;
+    a.zpos[b] = 0.0;  // the logits epilogue writes the local positives' z_pos; 0 elsewhere
+    if (a.hasval) a.hasval[b] = 0;
+    if (y < 0) {
+      atomicMin(&a.oobs[0], (long long)y);
+    } else if (y >= a.C) {
+      atomicMin(&a.oobs[1], (long long)y);
+    } else {
+      const uint32_t bit = 1u << (y & 31);
+      if (!(atomicOr(&a.bits[y >> 5], bit) & bit)) atomicAdd(&a.ccnt[(y >> 5) / a.chunk_words], 1);
+    }
+  }
+  for (int64_t kk = tid; kk < a.nk; kk += nthr) a.rej[kk] = 0;
+}
+
+template <typename OT>
+__global__ void __launch_bounds__(kSamplerThreads, 1) fill_kernel(const SamplerArgs a) {
+  pdl_entry();
+  extern __shared__ __align__(16) uint8_t sampler_smem[];
+  ShardMeta* meta_s = reinterpret_cast<ShardMeta*>(sampler_smem);
+  int32_t* bpre_s = reinterpret_cast<int32_t*>(sampler_smem + (size_t)a.nk * sizeof(ShardMeta));
+  __shared__ int warp_tmp[32];
+  __shared__ int bad_shard_s;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gwarp = tid >> 5, nwarp = nthr >> 5;
+  StepStatus* st = a.st;
+  if (a.normalize) {  // independent of the labels: x^ = x / |x| first
+    const int nw = (int)nwarp;
+    for (int row0 = 0; row0 < a.B; row0 += nw)
+      normalize_x_rows(a.sp->x + (size_t)row0 * a.D, a.B - row0, a.D, a.Dp,
+                       static_cast<OT*>(a.xh) + (size_t)row0 * a.Dp, a.xnorm + row0,
+                       (int)blockIdx.x);
+  }
+  // ---- chunk prefixes, validation, capacity, local shard metadata (every CTA)
+  {
+    int carry = 0;
+    for (int base = 0; base < a.nchunk; base += blockDim.x) {
+      const int i = base + (int)threadIdx.x;
+      const int t = i < a.nchunk ? a.ccnt[i] : 0;
+      int tot = 0;
+      const int ex = block_exclusive_scan(t, warp_tmp, &tot);
+      if (i < a.nchunk) bpre_s[i] = carry + ex;
+      carry += tot;
+    }
+  }
+  if (threadIdx.x == 0) bad_shard_s = a.K;
+  const long long mn = a.oobs[0], mc = a.oobs[1];
+  __syncthreads();
+  const bool sticky = sampler_failed(st);  // an earlier asynchronous step's error stays first
+  const bool oob = mn != LLONG_MAX || mc != LLONG_MAX;
+  if (!sticky && !oob) {
+    // capacity checks for ALL shards, one warp per shard; the first failing shard wins
+    for (int k = wib; k < a.K; k += blockDim.x >> 5) {
+      const int64_t lo = min((int64_t)k * a.blk, a.C), hi = min((int64_t)(k + 1) * a.blk, a.C);
+      const int plo = bits_below(a.bits, bpre_s, a.chunk_words, lo, lane);
+      const int np = bits_below(a.bits, bpre_s, a.chunk_words, hi, lane) - plo;
+      if (np > a.cap || hi - lo < a.cap) {
+        if (lane == 0) atomicMin(&bad_shard_s, k);
+      } else if (k >= a.k0 && k < a.k0 + a.nk && lane == 0) {
+        ShardMeta m;
+        m.lo = lo;
+        m.hi = hi;
+        m.ustart = plo;
+        m.npos = np;
+        m.need = a.cap - np;
+        m.pool = (int)(hi - lo) - np;
+        m.full = (m.need == m.pool);
+        m.reject = a.force_sequential && !m.full && m.need > 0;
+        meta_s[k - a.k0] = m;
+      }
+    }
+  }
+  __syncthreads();
+  const int bad = bad_shard_s;
+  const bool ok = !sticky && !oob && bad == a.K;
+  if (blockIdx.x == 0) {
+    if (!sticky && threadIdx.x == 0) {
+      if (oob) {
+        st->label_oob = 1;
+        st->oob_label = mn != LLONG_MAX ? mn : mc;
+      } else if (bad < a.K) {
+        st->capacity_shard = bad;
+      }
+    }
+    if (!sticky && !oob && bad < a.K && wib == 0) {  // the failing shard's count, for the message
+      const int64_t lo = min((int64_t)bad * a.blk, a.C), hi = min((int64_t)(bad + 1) * a.blk, a.C);
+      const int np = bits_below(a.bits, bpre_s, a.chunk_words, hi, lane) -
+                     bits_below(a.bits, bpre_s, a.chunk_words, lo, lane);
+      if (lane == 0) st->capacity_npos = np;
+    }
+    if (ok)
+      for (int kk = threadIdx.x; kk < a.nk; kk += blockDim.x) a.meta[kk] = meta_s[kk];
+  }
+  if (!ok) return;
+  // ---- positives + positive columns (one warp per label), draws (one thread per draw)
+  for (int64_t b = gwarp; b < a.B; b += nwarp) {
+    const int64_t y = a.labs[b];
+    const int k = (int)(y / a.blk);
+    int col = -1;
+    if (k >= a.k0 && k < a.k0 + a.nk) {
+      const int kk = k - a.k0;
+      col = kk * a.cap + (bits_below(a.bits, bpre_s, a.chunk_words, y, lane) - meta_s[kk].ustart);
+      if (lane == 0) a.buf_cls[col] = (int32_t)y;
+    }
+    if (lane == 0) a.pos_col[b] = col;
+  }
+  const int64_t nd = (int64_t)a.nk * a.cap;
+  for (int64_t g = tid; g < nd; g += nthr) {
+    const int kk = (int)(g / a.cap), i = (int)(g % a.cap);
+    const ShardMeta& m = meta_s[kk];
+    if (m.full || i >= m.need) continue;
+    // per-step values from the StepParams block (only mark_kernel's arguments change per step)
+    const uint64_t key = rng_key(a.sp->seed, fork_stream(a.sp->stream, (uint64_t)(a.k0 + kk)));
+    const uint64_t n = (uint64_t)(m.pool - i);
+    const uint64_t r = rng_draw(key, (uint64_t)i + 1);
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % n;  // rng.hpp:69
+    if (r >= limit) a.rej[kk] = 1;
+    const int32_t j = i + (int32_t)(r % n);
+    a.jv[g] = j;
+    a.nxt[g] = atomicExch(&a.head[(int64_t)kk * a.pool_stride + j], i);
+  }
+}
+
+// Chain walk (+ the exact sequential fallback of rejected shards); clears the bitmap.
+__global__ void __launch_bounds__(kSamplerThreads) walk_kernel(const SamplerArgs a) {
+  pdl_entry();
+  extern __shared__ __align__(16) uint8_t sampler_smem[];
+  ShardMeta* meta_s = reinterpret_cast<ShardMeta*>(sampler_smem);
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = tid; b < a.B; b += nthr) {
+    const int64_t y = a.labs[b];
+    if (y >= 0 && y < a.C) {
+      a.bits[y >> 5] = 0u;
+      a.ccnt[(y >> 5) / a.chunk_words] = 0;
+    }
+  }
+  if (tid == 0) {
+    a.oobs[0] = LLONG_MAX;
+    a.oobs[1] = LLONG_MAX;
+  }
+  if (sampler_failed(a.st)) return;
+  for (int kk = threadIdx.x; kk < a.nk; kk += blockDim.x) {
+    ShardMeta m = a.meta[kk];
+    m.reject = m.reject || a.rej[kk];
+    meta_s[kk] = m;
+  }
+  __syncthreads();
+  for (int kk = blockIdx.x; kk < a.nk; kk += gridDim.x)
+    if (meta_s[kk].reject)  // block-uniform
+      sequential_fallback(meta_s[kk], a.cap, a.sp, a.k0, a.pool_stride, a.pool_scratch,
+                          a.buf_cls, a.st, kk);
+  const int64_t nd = (int64_t)a.nk * a.cap;
+  for (int64_t g = tid; g < nd; g += nthr) {
+    const int kk = (int)(g / a.cap), i = (int)(g % a.cap);
+    const ShardMeta& m = meta_s[kk];
+    if (m.reject || i >= m.need) continue;
+    int32_t* row = a.buf_cls + (int64_t)kk * a.cap;
+    int64_t p;
+    if (m.full) {
+      p = i;  // full sampling: ascending complement (sampler.hpp:106-115)
+    } else {
+      const int32_t* hd = a.head + (int64_t)kk * a.pool_stride;
+      const int32_t* nx = a.nxt + (int64_t)kk * a.cap;
+      int32_t pp = a.jv[g], t = i;
+      for (;;) {
+        int32_t best = -1;
+        for (int32_t s = hd[pp]; s >= 0; s = nx[s])
+          if (s < t && s > best) best = s;
+        if (best < 0) break;
+        pp = best;
+        t = best;
+      }
+      p = pp;
+    }
+    row[m.npos + i] = (int32_t)pool_value(m.lo, row, m.npos, p);
   }
 }
 

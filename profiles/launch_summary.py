@@ -1,5 +1,5 @@
 """Summarise an ncu launch list (ncu --metrics gpu__time_duration.sum --csv --log-file X) of
-bench.py: the kernels of the last step (from the last positives_kernel through the next dW
+bench.py: the kernels of the last step (from the last sampler_kernel through the next dW
 GEMM), their times and their shares of the serialised sum.
 Usage: python profiles/launch_summary.py <launches.csv> [header line ...]"""
 import csv
@@ -17,9 +17,9 @@ def main():
             unit = r["Metric Unit"]
             us = v / 1000.0 if unit == "ns" else (v * 1000.0 if unit == "ms" else v)
             rows.append((r["Kernel Name"], us))
-    starts = [i for i, (k, _) in enumerate(rows) if k.startswith("positives_kernel")]
+    starts = [i for i, (k, _) in enumerate(rows) if k.startswith("mark_kernel")]
     if not starts:
-        sys.exit("no positives_kernel in the launch list")
+        sys.exit("no mark_kernel in the launch list")
     i0 = starts[-1]
     step = []
     for k, us in rows[i0:]:

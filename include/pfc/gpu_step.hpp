@@ -132,10 +132,14 @@ class Session {
     if (cfg.margin.kind != cfg_.margin.kind || cfg.margin.scale != cfg_.margin.scale ||
         cfg.margin.margin != cfg_.margin.margin || cfg.r != cfg_.r ||
         cfg.filter_threshold != cfg_.filter_threshold || cfg.momentum != cfg_.momentum ||
-        cfg.weight_decay != cfg_.weight_decay)
-      throw ContractError(
-          "pfc::gpu::Session::step: StepConfig differs from the session's (only lr and "
-          "step_index may change between steps)");
+        cfg.weight_decay != cfg_.weight_decay) {
+      // the reference takes its StepConfig per call (shardsim.hpp:166-168)
+      pfc_gpu_step_config sc{cfg.r, static_cast<int32_t>(cfg.margin.kind), cfg.margin.scale,
+                             cfg.margin.margin, cfg.filter_threshold ? 1 : 0,
+                             cfg.filter_threshold.value_or(0.0), cfg.momentum, cfg.weight_decay};
+      check(pfc_gpu_set_step_config(ctx_, &sc), ctx_);
+      cfg_ = cfg;
+    }
     if (batch.dim() != dim_) throw ShapeError("pfc::gpu::Session::step: feature dim mismatch");
     std::optional<DiagnosticsSnapshot> diag;
     if (cfg.with_diagnostics) {
@@ -200,19 +204,9 @@ inline StepResult distributed_partial_step(std::vector<CenterShard>& shards,
   // one cached session per thread, rebuilt when the shape or the step-invariant config changes
   thread_local std::unique_ptr<Session> cached;
   thread_local std::string key;
-  // keyed on the exact bits of every double (std::to_string keeps 6 decimals), with the
-  // filter's presence encoded separately from its threshold
-  auto bits = [](double v) {
-    uint64_t u;
-    std::memcpy(&u, &v, sizeof u);
-    return std::to_string(u);
-  };
+  // keyed on the shape; a StepConfig change is applied by Session::step (per-call config)
   const std::string k = std::to_string(layout.num_classes) + "/" + std::to_string(K) + "/" +
-                        std::to_string(dim) + "/" + std::to_string(batch.batch()) + "/" +
-                        bits(cfg.r) + "/" + std::to_string((int)cfg.margin.kind) + "/" +
-                        bits(cfg.margin.scale) + "/" + bits(cfg.margin.margin) + "/" +
-                        (cfg.filter_threshold ? "f" + bits(*cfg.filter_threshold) : "nf") + "/" +
-                        bits(cfg.momentum) + "/" + bits(cfg.weight_decay);
+                        std::to_string(dim) + "/" + std::to_string(batch.batch());
   if (!cached || key != k) {
     cached.reset();
     cached = std::make_unique<Session>(layout, dim, cfg, std::max<int64_t>(batch.batch(), 1));

@@ -132,6 +132,24 @@ int pfc_gpu_nccl_unique_id(uint8_t out[128]);
 int pfc_gpu_loopback_id(uint8_t out[128]);
 const char* pfc_gpu_version(void);
 
+/* ---- per-step configuration ------------------------------------------------------------ */
+/* The StepConfig fields a context holds between steps (r, margin, filter, momentum, weight
+ * decay; StepConfig, shardsim.hpp:117-127).  The reference takes a StepConfig per call: a caller
+ * whose config changes between steps sets the new one here before the step (validated like
+ * pfc_gpu_create: MarginConfig::validate's ConfigError texts, r in (0, 1]).  A new r changes the
+ * buffer capacity (the column buffers grow when needed); the captured step graphs are rebuilt. */
+typedef struct {
+  double r;
+  int32_t margin_kind;
+  double margin_scale;
+  double margin_m;
+  int32_t has_filter;
+  double filter_threshold;
+  double momentum;
+  double weight_decay;
+} pfc_gpu_step_config;
+int pfc_gpu_set_step_config(void* ctx, const pfc_gpu_step_config* cfg);
+
 /* ---- shape queries (ShardLayout / buffer_capacity) ------------------------------------ */
 int64_t pfc_gpu_capacity(const void* ctx);
 int pfc_gpu_local_shards(const void* ctx, int64_t* first_shard, int64_t* num_local_shards);

@@ -124,6 +124,65 @@ int main(int argc, char** argv) {
           trace_ok ? "true" : "false", got.loss, want.loss, dl, dx, dw, pass ? "true" : "false");
     }
   }
+  // StepConfig per call (shardsim.hpp:166-168): r, margin, filter, momentum and weight decay
+  // change from step to step on one session (the capacity grows, shrinks, per-row offsets at
+  // s = 128), against the reference taking each config as given
+  for (int precision : {PFC_PRECISION_FP32, PFC_PRECISION_BF16}) {
+    const ShardLayout layout(20000, 4);
+    const int64_t D = 256, B = 96;
+    std::vector<CenterShard> ref = init_center_shards(layout, D, 3);
+    std::vector<CenterShard> dev = ref;
+    StepConfig cfgs[5];
+    cfgs[0].r = 0.1;
+    cfgs[0].margin = MarginConfig::arcface_style();
+    cfgs[1].r = 0.2;
+    cfgs[1].margin = MarginConfig::cosface_style();
+    cfgs[1].momentum = 0.5;
+    cfgs[2].r = 0.05;
+    cfgs[2].margin = MarginConfig::cosface_style();
+    // the filter in fp32 only: in bf16 the mask is decided on bf16-operand cosines and may flip
+    // within 2^-7 of tau (that contract is tests/test_gpu_edges.py::test_bf16_filter_contract)
+    if (precision == PFC_PRECISION_FP32) cfgs[2].filter_threshold = 0.1;
+    cfgs[2].weight_decay = 0.0;
+    cfgs[3].r = 0.3;
+    cfgs[3].margin = MarginConfig::cosface_style(128.0, 0.35);
+    cfgs[4] = cfgs[0];
+    const bool fp32 = precision == PFC_PRECISION_FP32;
+    gpu::Session session(layout, D, cfgs[0], B, precision);
+    session.upload(dev);
+    double worst_l = 0, worst_x = 0, worst_w = 0, fw = 1.0;
+    bool bufs = true, pass = true;
+    for (uint64_t step = 0; step < 5; ++step) {
+      StepConfig cfg = cfgs[step];
+      cfg.lr = 0.1;
+      const FeatureBatch batch = bench_batch(layout.num_classes, D, B, step);
+      const SeededRng it(1, make_stream("iteration", step));
+      const StepResult want = distributed_partial_step(ref, batch, cfg, it);
+      const StepResult got = session.step(batch, cfg, it);
+      session.download(dev);
+      for (size_t k = 0; k < want.buffers.size(); ++k)
+        bufs = bufs && want.buffers[k].class_indices == got.buffers[k].class_indices;
+      // the value bounds scale with s / 64 (logit rounding times s; W' by (s/64)^2, as in
+      // tests/test_gpu_edges.py)
+      // (W and momentum carry earlier steps' errors: the largest scale so far bounds W')
+      const double f = std::max(1.0, cfg.margin.scale / 64.0);
+      fw = std::max(fw, f);
+      const double dl = std::fabs(got.loss - want.loss) / std::fabs(want.loss);
+      const double dx = rel_fro(got.d_features, want.d_features);
+      const double dw = rel_max_shards(dev, ref);
+      worst_l = std::max(worst_l, dl);
+      worst_x = std::max(worst_x, dx);
+      worst_w = std::max(worst_w, dw);
+      pass = pass && dl <= (fp32 ? 1e-6 : 1e-4) * f && dx <= (fp32 ? 1e-5 : 1e-2) * f &&
+             dw <= (fp32 ? 1e-6 : 1e-3) * fw * fw;
+    }
+    pass = pass && bufs;
+    ok = ok && pass;
+    std::printf("{\"case\": \"step_config_per_call_%s\", \"steps\": 5, \"buffers_bit_exact\": %s, "
+                "\"loss_rel_max\": %.3e, \"dX_fro_max\": %.3e, \"W_maxmax\": %.3e, \"pass\": %s}\n",
+                fp32 ? "fp32" : "bf16", bufs ? "true" : "false", worst_l, worst_x, worst_w,
+                pass ? "true" : "false");
+  }
   // with_diagnostics (shardsim.hpp:401-410): apcs / amncs on the pre-update shards, with the
   // conflict split; the GPU values are exact up to fp32 storage of W
   {

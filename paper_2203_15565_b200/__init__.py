@@ -255,6 +255,13 @@ class Desc(C.Structure):
                 ("world_size", C.c_int32), ("nccl_id", C.c_void_p), ("flags", C.c_int32)]
 
 
+class StepConfigC(C.Structure):
+    _fields_ = [("r", C.c_double), ("margin_kind", C.c_int32), ("margin_scale", C.c_double),
+                ("margin_m", C.c_double), ("has_filter", C.c_int32),
+                ("filter_threshold", C.c_double), ("momentum", C.c_double),
+                ("weight_decay", C.c_double)]
+
+
 class StepArgs(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("stream_id", C.c_uint64), ("lr", C.c_double),
                 ("step_index", C.c_int64)]
@@ -324,6 +331,7 @@ def load_library(path: str | None = None) -> C.CDLL:
         "pfc_gpu_mics": (C.c_int, [vp, vp]),
         "pfc_gpu_read_shards": (C.c_int, [vp, C.c_char_p, i64, C.POINTER(i64)]),
         "pfc_gpu_check_guards": (C.c_int, [vp, C.POINTER(i64)]),
+        "pfc_gpu_set_step_config": (C.c_int, [vp, C.POINTER(StepConfigC)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -362,8 +370,9 @@ class CenterShards:
     """Device-resident replacement of ``std::vector<CenterShard>`` for one rank.
 
     Owns W and momentum of the reference shards [rank*K/world, (rank+1)*K/world) as fp32
-    row-major [classes x D] on this rank's GPU.  The step-invariant parts of StepConfig (r,
-    margin, filter, momentum, weight decay) are fixed here; lr and the iteration rng are per step.
+    row-major [classes x D] on this rank's GPU.  Every step takes its own StepConfig, like the
+    reference; a changed r / margin / filter / momentum / weight decay is applied before the step
+    (set_step_config), lr and the iteration rng ride with the step.
     """
 
     def __init__(self, layout: ShardLayout, dim: int, cfg: StepConfig, *, max_batch: int = 1024,
@@ -432,6 +441,23 @@ class CenterShards:
     def stream(self) -> int:
         return _lib.pfc_gpu_stream(self._h)
 
+    def set_step_config(self, cfg: StepConfig) -> None:
+        """The reference takes a StepConfig per call: apply r / margin / filter / momentum /
+        weight decay for the next steps (no-op when unchanged)."""
+        cfg.margin.validate()
+        c = self.cfg
+        if (cfg.margin == c.margin and cfg.r == c.r and cfg.filter_threshold == c.filter_threshold
+                and cfg.momentum == c.momentum and cfg.weight_decay == c.weight_decay):
+            return
+        sc = StepConfigC(cfg.r, cfg.margin.kind, cfg.margin.scale, cfg.margin.margin,
+                         0 if cfg.filter_threshold is None else 1,
+                         0.0 if cfg.filter_threshold is None else cfg.filter_threshold,
+                         cfg.momentum, cfg.weight_decay)
+        _check(load_library().pfc_gpu_set_step_config(self._h, C.byref(sc)), self._h)
+        self.cfg = StepConfig(r=cfg.r, margin=cfg.margin, filter_threshold=cfg.filter_threshold,
+                              momentum=cfg.momentum, weight_decay=cfg.weight_decay, lr=cfg.lr)
+        self.capacity = load_library().pfc_gpu_capacity(self._h)
+
     def check_guards(self) -> int:
         """FLAG_GUARD contexts: number of guard regions a kernel overwrote (raises naming them)."""
         n = C.c_int64()
@@ -480,6 +506,7 @@ class CenterShards:
                 raise ShapeError("pfc_gpu: out must be a contiguous float64 array shaped like the features")
             dx = out
         out = StepOut()
+        self.set_step_config(cfg)
         args = StepArgs(iteration_rng.seed, iteration_rng.stream_id, cfg.lr, cfg.step_index)
         _check(_lib.pfc_gpu_step(self._h, _ptr(x), _ptr(lab), lab.shape[0], C.byref(args),
                                  _ptr(dx), C.byref(out)), self._h)
@@ -507,6 +534,7 @@ class CenterShards:
             raise ShapeError(f"pfc_gpu: feature dim {x.shape[0]} != {self.dim}")
         dx = torch.empty_like(x) if out is None else out
         so = StepOut()
+        self.set_step_config(cfg)
         args = StepArgs(iteration_rng.seed, iteration_rng.stream_id, cfg.lr, cfg.step_index)
         torch.cuda.current_stream().synchronize()  # the library works on its own stream
         _check(_lib.pfc_gpu_step_features(self._h, x.data_ptr(), lab.data_ptr(), lab.shape[0],
@@ -553,6 +581,7 @@ class CenterShards:
 
     def step_device(self, x_local_ptr: int, labels_local_ptr: int, b_local: int, dx_local_ptr: int,
                     cfg: StepConfig, iteration_rng: SeededRng, sync: bool = True):
+        self.set_step_config(cfg)
         args = StepArgs(iteration_rng.seed, iteration_rng.stream_id, cfg.lr, cfg.step_index)
         out = StepOut()
         rc = _lib.pfc_gpu_step_device(self._h, C.c_void_p(x_local_ptr),
@@ -576,11 +605,6 @@ def distributed_partial_step(shards: CenterShards, features_dxb: np.ndarray, lab
     reference's closed-form trace and the local shards' SampleBuffers.
     """
     cfg.margin.validate()
-    if cfg.margin != shards.cfg.margin or cfg.r != shards.cfg.r or \
-            cfg.filter_threshold != shards.cfg.filter_threshold or \
-            cfg.momentum != shards.cfg.momentum or cfg.weight_decay != shards.cfg.weight_decay:
-        raise ContractError("distributed_partial_step: StepConfig differs from the one the "
-                            "device shards were created with (only lr / step_index may vary)")
     diag = None
     if cfg.with_diagnostics:
         # the reference reports them for the pre-update shards (shardsim.hpp:401-417); its label

@@ -552,23 +552,21 @@ struct DwUpdateEpi {
     };
     auto stage_chunk = [&](int c0) {
       __syncwarp();
+      float v0[16], v1[16];
+      src.load16x2(c0, v0, v1);  // 32 columns, one TMEM round trip
+#if PFC_DW_EXP != 6  // timing probe 6: no staging stores (wrong values)
+      if (mine) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float v[16];
-#if PFC_DW_EXP == 1  // timing probe: half the accumulator reads (wrong values)
-        if (h == 1) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        } else
-#endif
-        src.load16(c0 + 16 * h, v);
-        if (mine) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<float4*>(stage + li * 36 + 16 * h + 4 * j) =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        for (int j = 0; j < 4; ++j) {
+          *reinterpret_cast<float4*>(stage + li * 36 + 4 * j) =
+              make_float4(v0[4 * j], v0[4 * j + 1], v0[4 * j + 2], v0[4 * j + 3]);
+          *reinterpret_cast<float4*>(stage + li * 36 + 16 + 4 * j) =
+              make_float4(v1[4 * j], v1[4 * j + 1], v1[4 * j + 2], v1[4 * j + 3]);
         }
       }
+#else
+      if (v0[0] == 1234.5f && v1[3] == 7.f) stage[li] = 0.f;
+#endif
       __syncwarp();
     };
     auto dwt4 = [&](int u, int d) {
@@ -666,241 +664,6 @@ struct DwUpdateEpi {
       // refill the ring (reads of item k's sub-slots were consumed above: in-order issue)
       static_range<issued_before(k), issued_before(k + 1)>(issue);
     });
-  }
-};
-
-// ---------------------------------------------------------------------------------- DwRowEpi
-// Row-major variant of DwUpdateEpi for D in (384, 512]: a 4-CTA cluster owns a 128-class block,
-// CTA r the dims [128 r, 128 r + 128).  Warp (g, q) owns rows 32q + 8g .. +7 over the CTA's 128
-// dims and streams each row's 512 B span of W / momentum at once (lane l: dims 4l .. 4l+3) through
-// a ring of 512 B slots, so the 4 CTAs fetch a row's 2 KB together instead of in 8 chunks spread
-// over the tile (profiles/micro/rowupd.cu: row-major 6.2 TB/s vs chunk-major 4.7-5.1 TB/s at the
-// same bytes in flight).  A lane only reads the 16 bytes it copied itself, so the ring needs no
-// warp synchronisation.  A row's dot is a warp reduction; the 4 CTAs swap quarter-dots
-// (st.async into the peers' shared memory, 96 tx bytes per warp and tile).
-// EXPERIMENTAL (PFC_DW_ROW=1; off by default): parity-correct, but measured at 0.85-0.94 ms
-// against 0.46 ms for DwUpdateEpi. Per tile it is bound by instruction latency (row-by-row
-// dependent waits, warp reductions, ring address arithmetic), not by the memory order; see DESIGN.md.
-#ifndef PFC_DWR_SLOTS
-#define PFC_DWR_SLOTS 8
-#endif
-struct DwRowEpi {
-  static constexpr int kCluster = 4;
-  static constexpr bool kNext = true;
-  static constexpr int kRows = 8;                  // rows per warp
-  static constexpr int kItems = 3 * kRows;         // W row i (dot pass), then W row i + momentum row i
-  static constexpr int kSlots = PFC_DWR_SLOTS;     // ring slots of 512 B
-  static constexpr int kAhead = kSlots - 1;        // items in flight after the consumed one
-  // rows per ring wait: dot pass kGD rows (kGD items), update pass kGU rows (2 kGU items)
-  static constexpr int kGD = kAhead >= 4 ? 4 : (kAhead >= 2 ? 2 : 1);
-  static constexpr int kGU = kAhead >= 4 ? 2 : 1;
-  static_assert(kAhead >= 2 && kAhead <= kItems, "DwRowEpi ring");
-  static_assert(kItems % kSlots == 0, "slot of item k is k % kSlots in every tile");
-  static constexpr int kStageBytes = kRows * 128 * 4;       // dwt rows, float4 columns XOR-swizzled
-  static constexpr int kRingBytes = kSlots * 512;
-  static constexpr int kScalarBytes = 2 * 3 * kRows * 4;    // [2 tile parity][inv | row | pslot]
-  static constexpr int kWarpBytes = kStageBytes + kRingBytes + kScalarBytes;
-  // CTA-shared (in warpgroup 0's scratch): hq[2 parity][4 ranks][128 rows] + mbarriers [2][16 warps]
-  static constexpr int kSharedBytes = 2 * 4 * 128 * 4 + 2 * 16 * 8;
-  static constexpr int kSmem = ((4 * kWarpBytes + kSharedBytes + 127) / 128) * 128;
-  int ncols, D;
-  const float* wnorm;       // [ncols]
-  const int32_t* lrow;      // [ncols] local row of W
-  const int32_t* pslot;     // [ncols] positive-correction slot or -1
-  const float* poscorr;     // [slots][D]
-  float* W;
-  float* Mom;
-  const StepParams* sp;
-  float mu, wd;
-  const StepStatus* st;
-
-  struct Pre {
-    float inv;
-    int r, ps;
-  };
-  __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int wg) const {
-    Pre p{0.f, -1, -1};
-    const int lane = row & 31;
-    const int c = t.row0 + (row & ~31) + lane;
-    if ((lane >> 3) == wg && c < ncols) {  // only this warp's 8 rows
-      const float n = wnorm[c];
-      p.inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
-      p.r = lrow[c];
-      p.ps = pslot[c];
-    }
-    return p;
-  }
-  __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
-  __device__ __forceinline__ void finish(int, int) const {}
-  __device__ __forceinline__ static uint8_t* shared_area(uint8_t* wg0) { return wg0 + 4 * kWarpBytes; }
-  __device__ __forceinline__ void setup(uint8_t* epi_base) const {
-    uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 2 * 4 * 128 * 4);
-    for (int k = 0; k < 32; ++k) pfc_sm100::mbar_init(&mb[k], 1);  // local arrive + 96 tx bytes
-  }
-
-  template <int BN, int NWG, class Src>
-  __device__ __forceinline__ void run_next(const TileInfo& t, const Src& src, int row, int wg,
-                                           uint8_t* smem, const Pre& pre, const Pre& pre_next,
-                                           bool has_next) const {
-    static_assert(NWG == 4 && BN == 128, "DwRowEpi: 4 warpgroups, 128-dim tiles");
-    const int q = row >> 5, lane = row & 31;
-    uint8_t* wg0 = smem - wg * kSmem;
-    uint8_t* ws = smem + q * kWarpBytes;
-    float* stage = reinterpret_cast<float*>(ws);                       // [8][128]
-    const uint32_t ring_s = pfc_sm100::smem_u32(ws + kStageBytes);     // [kSlots][128]
-    const float* ring = reinterpret_cast<const float*>(ws + kStageBytes);
-    float* sc = reinterpret_cast<float*>(ws + kStageBytes + kRingBytes);
-    const int par = t.iter & 1;
-    float* s_inv = sc + par * 24;
-    int* s_row = reinterpret_cast<int*>(s_inv + 8);
-    int* s_ps = s_row + 8;
-    const int* s_row_n = reinterpret_cast<const int*>(sc + (par ^ 1) * 24 + 8);
-    float* hq = reinterpret_cast<float*>(shared_area(wg0));                          // [2][4][128]
-    uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + 2 * 4 * 128 * 4);  // [2][16]
-    const bool failed = status_failed(st);
-    const float lr = sp->lr;
-    const bool mine = (lane >> 3) == wg;
-    const int li = lane & 7;
-    const int e = wg * 4 + q;                     // this warp's barrier
-    const uint32_t rank = pfc_sm100::cluster_ctarank();
-    __syncwarp();  // the warp finished with the previous tile's scalars
-    if (mine) {
-      if (t.iter == 0) {
-        s_inv[li] = pre.inv;
-        s_row[li] = failed ? -1 : pre.r;
-        s_ps[li] = pre.ps;
-      }
-      float* sn = sc + (par ^ 1) * 24;
-      sn[li] = pre_next.inv;
-      reinterpret_cast<int*>(sn)[8 + li] = (failed || !has_next) ? -1 : pre_next.r;
-      reinterpret_cast<int*>(sn)[16 + li] = pre_next.ps;
-    }
-    if (lane == 0) pfc_sm100::mbar_arrive_expect_tx(&mb[par * 16 + e], 96u);
-    __syncwarp();
-    const int d = t.col0 + lane * 4;               // this lane's 4 dims
-    const bool dv = d < D;
-    // item k of the stream (k >= kItems: the next tile's item k - kItems; an empty group when
-    // there is none): W row k (k < 8), else W (even) / momentum (odd) row (k - 8) / 2
-    auto issue = [&](int k) {
-      const bool nx = k >= kItems;
-      const int kk = nx ? k - kItems : k;
-      const int r8 = kk < kRows ? kk : (kk - kRows) >> 1;
-      const bool mom = kk >= kRows && ((kk - kRows) & 1);
-      const int r = nx ? s_row_n[r8] : s_row[r8];
-      if (r >= 0 && dv)
-        pfc_sm100::cp_async16(ring_s + (uint32_t)((k % kSlots) * 512 + lane * 16),
-                              (mom ? Mom : W) + (size_t)r * D + d);
-      pfc_sm100::cp_async_commit();
-    };
-    auto slot4 = [&](int k) {
-      return *reinterpret_cast<const float4*>(ring + (k % kSlots) * 128 + lane * 4);
-    };
-    // dwt of this warp's rows, staged row-major: lane i's TMEM row is row 32q + 8wg + i
-#pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      float v[32];
-      src.load(c0, v);
-      if (mine) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int f = (c0 >> 2) + j;  // float4 column
-          *reinterpret_cast<float4*>(stage + li * 128 + ((f ^ li) << 2)) =
-              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        }
-      }
-    }
-    __syncwarp();
-    auto dwt4 = [&](int i) {
-      float4 a = *reinterpret_cast<const float4*>(stage + i * 128 + ((lane ^ i) << 2));
-      const int ps = s_ps[i];
-      if (ps >= 0 && dv) {
-        const float4 pc = *reinterpret_cast<const float4*>(poscorr + (size_t)ps * D + d);
-        a.x += pc.x; a.y += pc.y; a.z += pc.z; a.w += pc.w;
-      }
-      return a;
-    };
-    if (t.iter == 0)
-      for (int k = 0; k < kAhead; ++k) issue(k);  // otherwise issued by the previous tile
-    // ---- dot pass: the CTA's quarter of w . dwt per row, GD rows per ring wait (independent
-    // FMA / shuffle chains)
-    float dots[kRows];
-#pragma unroll
-    for (int i0 = 0; i0 < kRows; i0 += kGD) {
-      pfc_sm100::cp_async_wait<kAhead - kGD>();  // items i0 .. i0 + kGD - 1 landed
-      float4 w[kGD];
-#pragma unroll
-      for (int j = 0; j < kGD; ++j) w[j] = slot4(i0 + j);
-#pragma unroll
-      for (int j = 0; j < kGD; ++j) issue(i0 + j + kAhead);  // refills the slots just read
-      float p[kGD];
-#pragma unroll
-      for (int j = 0; j < kGD; ++j) {
-        const float4 a = dwt4(i0 + j);
-        p[j] = dv ? a.x * w[j].x + a.y * w[j].y + a.z * w[j].z + a.w * w[j].w : 0.f;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int j = 0; j < kGD; ++j) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
-#pragma unroll
-      for (int j = 0; j < kGD; ++j) dots[i0 + j] = p[j];
-    }
-    // ---- swap quarter-dots with the 3 peers; totals in rank order (identical on every CTA)
-    float* hp = hq + par * 512;
-    const int rbase = q * 32 + wg * 8;            // this warp's rows within the 128-row block
-    if (lane < 24) {
-      const int j = lane & 7;
-      float v = dots[0];
-#pragma unroll
-      for (int jj = 1; jj < kRows; ++jj) v = j == jj ? dots[jj] : v;
-      const uint32_t peer = (rank + 1 + (uint32_t)(lane >> 3)) & 3u;
-      const uint32_t rbar = pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[par * 16 + e]), peer);
-      pfc_sm100::st_async_f32(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hp + rank * 128 + rbase + j), peer),
-                              v, rbar);
-    }
-    pfc_sm100::mbar_wait_cluster(&mb[par * 16 + e], (uint32_t)((t.iter >> 1) & 1));
-    float rcp[kRows];
-#pragma unroll
-    for (int i = 0; i < kRows; ++i) {
-      float tot = 0.f;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) tot += (uint32_t)r == rank ? dots[i] : hp[r * 128 + rbase + i];
-      rcp[i] = tot * s_inv[i];  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
-    }
-    // ---- update pass: dW and the momentum-SGD update, GU rows (2 GU items) per ring wait
-#pragma unroll
-    for (int i0 = 0; i0 < kRows; i0 += kGU) {
-      const int k0 = kRows + 2 * i0;
-      pfc_sm100::cp_async_wait<kAhead - 2 * kGU>();
-      float4 wm[2 * kGU];
-#pragma unroll
-      for (int j = 0; j < 2 * kGU; ++j) wm[j] = slot4(k0 + j);
-#pragma unroll
-      for (int j = 0; j < 2 * kGU; ++j) issue(k0 + j + kAhead);
-#pragma unroll
-      for (int jr = 0; jr < kGU; ++jr) {
-        const int i = i0 + jr;
-        const int r = s_row[i];
-        if (r < 0 || !dv) continue;
-        const float4 a4 = dwt4(i);
-        const float inv = s_inv[i], cpj = rcp[i];
-        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-        const float4 w4 = wm[2 * jr], m4 = wm[2 * jr + 1];
-        float wv[4] = {w4.x, w4.y, w4.z, w4.w};
-        float mv[4] = {m4.x, m4.y, m4.z, m4.w};
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const float dw = (av[x] - cpj * (wv[x] * inv)) * inv;  // shardsim.hpp:382
-          const float g = dw + wd * wv[x];                       // shardsim.hpp:152-153
-          const float vv = mu * mv[x] + g;                       // shardsim.hpp:154
-          mv[x] = vv;
-          wv[x] = wv[x] - lr * vv;                               // shardsim.hpp:156
-        }
-        const size_t o = (size_t)r * D + d;
-        *reinterpret_cast<float4*>(Mom + o) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-        *reinterpret_cast<float4*>(W + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
-      }
-    }
   }
 };
 

@@ -89,6 +89,18 @@ struct TmemSrc {
   __device__ __forceinline__ void load16(int c0, float (&v)[16]) const {
     pfc_sm100::tmem_ld16(taddr + (uint32_t)c0, v);
   }
+  // 32 columns as two x16 loads behind one wait
+  __device__ __forceinline__ void load16x2(int c0, float (&v0)[16], float (&v1)[16]) const {
+    uint32_t r0[16], r1[16];
+    pfc_sm100::tmem_ld16_nowait(taddr + (uint32_t)c0, r0);
+    pfc_sm100::tmem_ld16_nowait(taddr + (uint32_t)c0 + 16u, r1);
+    pfc_sm100::tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v0[i] = __uint_as_float(r0[i]);
+      v1[i] = __uint_as_float(r1[i]);
+    }
+  }
 };
 
 #ifndef PFC_CTRL_WARPS

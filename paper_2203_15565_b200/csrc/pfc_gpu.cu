@@ -122,12 +122,6 @@ constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
 #define PFC_DIAG_CG 1
 #endif
 constexpr int kDiagCG = PFC_DIAG_CG;  // diagnostics / mics screening GEMMs likewise
-#ifndef PFC_DW_ROW
-#define PFC_DW_ROW 0  // 1: dW epilogue with a row-major W / momentum stream (DwRowEpi)
-#endif
-#ifndef PFC_DWR_STAGES
-#define PFC_DWR_STAGES 2  // operand stages of the DwRowEpi GEMM (32 KB each)
-#endif
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
 #endif  // dW GEMM operand ring depth (2: leaves shared memory to the W / momentum ring)
@@ -216,6 +210,7 @@ struct Ctx {
   int32_t* pslot = nullptr;  // [ncols]
   float* dwt = nullptr;      // fp32 validation path: [ncols][D]
   int64_t pmax = 1;
+  int64_t cap_alloc = 0;     // capacity the column buffers were allocated for
   float* dx_part = nullptr;  // [S][maxB][D]
   float* dX = nullptr;       // [maxB][D]
   int max_splits = 1;
@@ -726,15 +721,6 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
     cudaError_t err;
     if constexpr (kUmma) {
-#if PFC_DW_ROW
-      if (c->D > 384 && c->D <= 512) {  // row-major W / momentum stream, 4-CTA clusters
-        const GemmGeom gw4 = make_geom((int)c->ncols, (int)c->D, (int)B, 128, 1, 1);
-        err = launch_umma<128, PFC_DWR_STAGES, 4, false, true>(
-            c, c->tm_e_k, c->tm_xs_mn, gw4,
-            DwRowEpi{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr, c->W,
-                     c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay, c->st});
-      } else
-#endif
       if (gw.n_tiles == 2)
         err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
@@ -981,6 +967,93 @@ int host_validate(Ctx* c, const int64_t* labels, int64_t B) {
   return PFC_OK;
 }
 
+// buffer_capacity (sampler.hpp:50-57): ceil(C r - 1e-9) columns spread over K shards
+int64_t capacity_for(int64_t C, int64_t K, double r) {
+  const double want = (double)C * r;
+  const int64_t total = (int64_t)std::ceil(want - 1e-9);
+  return (total + K - 1) / K;
+}
+
+// the step-invariant margin state of c->d (softmax offset mode included)
+void set_margin_state(Ctx* c) {
+  c->mg.kind = c->d.margin_kind;
+  c->mg.s = (float)c->d.margin_scale;
+  c->mg.sd = c->d.margin_scale;
+  c->mg.md = c->d.margin_m;
+  c->mg.offd = std::max(0.0, c->d.margin_scale - 40.0);  // E = exp(z - o) <= e^40
+  c->mg.off = (float)c->mg.offd;
+  c->exact = c->d.margin_scale > kFixedOffsetMaxScale || (c->d.flags & PFC_FLAG_EXACT_SOFTMAX);
+}
+
+// capacity-derived geometry of c->cap
+void set_cap_geometry(Ctx* c) {
+  c->ncols = c->nk * c->cap;
+  c->ncols_pad = round_up(std::max<int64_t>(c->ncols, 1), 256);
+  c->pmax = std::max<int64_t>(1, std::min<int64_t>(c->cap, c->maxB));
+}
+
+void dfree(Ctx* c, void* p) {
+  if (!p) return;
+  for (size_t i = 0; i < c->guards.size(); ++i)
+    if (c->guards[i].base + kGuardBytes == p) {
+      p = c->guards[i].base;
+      c->guards.erase(c->guards.begin() + (long)i);
+      break;
+    }
+  for (size_t i = 0; i < c->allocs.size(); ++i)
+    if (c->allocs[i] == p) {
+      c->allocs.erase(c->allocs.begin() + (long)i);
+      cudaFree(p);
+      return;
+    }
+}
+
+// The buffers whose size follows the buffer capacity (c->ncols / c->ncols_pad / c->pmax);
+// (re)allocated at creation and when a later StepConfig needs more columns than allocated.
+cudaError_t alloc_cap_buffers(Ctx* c) {
+  void** old[] = {reinterpret_cast<void**>(&c->buf_cls), reinterpret_cast<void**>(&c->nxt),
+                  reinterpret_cast<void**>(&c->jv), &c->wh,
+                  reinterpret_cast<void**>(&c->wnorm), reinterpret_cast<void**>(&c->lrow),
+                  &c->part_s, reinterpret_cast<void**>(&c->dbgz), &c->G,
+                  reinterpret_cast<void**>(&c->poscorr), reinterpret_cast<void**>(&c->pslot),
+                  reinterpret_cast<void**>(&c->dwt)};
+  for (void** p : old) {
+    dfree(c, *p);
+    *p = nullptr;
+  }
+  const size_t ob = c->bf16 ? 2 : 4;  // operand bytes
+  const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
+  const int64_t B = c->maxB;
+  const int64_t n1 = std::max<int64_t>(c->ncols, 1);
+  const int BN = c->bf16 ? kBN : kSimtBN;
+  const int64_t Tf = c->bf16 ? ceil_div(n1, kFwdBN) * kFwdNWG : ceil_div(n1, BN);
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  A(dalloc(c, &c->buf_cls, (size_t)n1));
+  A(dalloc(c, &c->nxt, (size_t)n1));
+  A(dalloc(c, &c->jv, (size_t)n1));
+  A(dalloc(c, reinterpret_cast<uint8_t**>(&c->wh), (size_t)c->ncols_pad * c->Dp * ob));
+  A(dalloc(c, &c->wnorm, (size_t)c->ncols_pad));
+  A(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
+  A(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(Tf * B) * sb));
+  if (c->d.flags & PFC_FLAG_DEBUG_LOGITS) A(dalloc(c, &c->dbgz, (size_t)B * n1));
+  A(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
+  A(dalloc(c, &c->poscorr, (size_t)(c->nk * c->pmax * c->D)));
+  A(dalloc(c, &c->pslot, (size_t)n1));
+  if (!c->bf16) A(dalloc(c, &c->dwt, (size_t)n1 * c->D));
+  c->cap_alloc = c->cap;
+  return e;
+}
+
+void drop_graphs(Ctx* c) {
+  for (Ctx::GraphSlot& G : c->gs) {
+    if (G.gexec) cudaGraphExecDestroy(G.gexec);
+    if (G.graph) cudaGraphDestroy(G.graph);
+    G = Ctx::GraphSlot{};
+  }
+  c->tm_B = -1;  // tensor maps over the column buffers are re-encoded
+}
+
 int validate_desc(const pfc_gpu_desc* d) {
   if (!d) return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: null descriptor");
   if (d->num_classes < 1 || d->num_shards < 1)
@@ -1205,28 +1278,17 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->bf16 = desc->precision == PFC_PRECISION_BF16;
   c->Dp = round_up(c->D, 64);
   c->blk = ceil_div(c->C, c->K);
-  {
-    const double want = (double)c->C * desc->r;
-    const int64_t total = (int64_t)std::ceil(want - 1e-9);
-    c->cap = (total + c->K - 1) / c->K;  // buffer_capacity (sampler.hpp:50-57)
-  }
+  c->cap = capacity_for(c->C, c->K, desc->r);
   c->nk = c->K / c->R;
   c->k0 = (int64_t)c->rank * c->nk;
   c->cls_lo = std::min(c->k0 * c->blk, c->C);
   c->cls_hi = std::min((c->k0 + c->nk) * c->blk, c->C);
   c->rows = c->cls_hi - c->cls_lo;
-  c->ncols = c->nk * c->cap;
-  c->ncols_pad = round_up(std::max<int64_t>(c->ncols, 1), 256);
   c->ldg = round_up(desc->max_batch, 8);  // E^T row stride
   c->pool_stride = std::max<int64_t>(c->blk, 1);
   c->maxB = desc->max_batch;
-  c->mg.kind = desc->margin_kind;
-  c->mg.s = (float)desc->margin_scale;
-  c->mg.sd = desc->margin_scale;
-  c->mg.md = desc->margin_m;
-  c->mg.offd = std::max(0.0, desc->margin_scale - 40.0);  // E = exp(z - o) <= e^40
-  c->mg.off = (float)c->mg.offd;
-  c->exact = desc->margin_scale > kFixedOffsetMaxScale || (desc->flags & PFC_FLAG_EXACT_SOFTMAX);
+  set_cap_geometry(c);
+  set_margin_state(c);
   c->pdl = !(desc->flags & PFC_FLAG_NO_PDL);
   int64_t B = c->maxB;
   auto bail = [&](int rc) {
@@ -1259,8 +1321,6 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
     CT(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   const size_t ob = c->bf16 ? 2 : 4;  // operand bytes
   const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
-  const int BN = c->bf16 ? kBN : kSimtBN;
-  const int64_t T = ceil_div(std::max<int64_t>(c->ncols, 1), BN);
   c->max_splits = c->bf16 ? 32 : 64;
   CT(dalloc(c, &c->W, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
   CT(dalloc(c, &c->M, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
@@ -1278,21 +1338,13 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
     CT(cudaMemcpy(c->oobs, none, sizeof none, cudaMemcpyHostToDevice));
   }
   CT(dalloc(c, &c->meta, (size_t)c->nk));
-  CT(dalloc(c, &c->buf_cls, (size_t)std::max<int64_t>(c->ncols, 1)));
   CT(dalloc(c, &c->pos_col, (size_t)B));
   CT(dalloc(c, &c->head, (size_t)(c->nk * c->pool_stride)));
   CT(cudaMemset(c->head, 0xFF, sizeof(int32_t) * c->nk * c->pool_stride));  // reset per draw after
-  CT(dalloc(c, &c->nxt, (size_t)std::max<int64_t>(c->ncols, 1)));
-  CT(dalloc(c, &c->jv, (size_t)std::max<int64_t>(c->ncols, 1)));
   CT(dalloc(c, &c->pool_scratch, (size_t)(c->nk * c->pool_stride)));
   CT(dalloc(c, &c->X, (size_t)B * c->D));
   CT(dalloc(c, &c->xnorm, (size_t)B));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->xh), (size_t)B * c->Dp * ob));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->wh), (size_t)c->ncols_pad * c->Dp * ob));
-  CT(dalloc(c, &c->wnorm, (size_t)c->ncols_pad));
-  CT(dalloc(c, &c->lrow, (size_t)c->ncols_pad));
-  const int64_t Tf = c->bf16 ? ceil_div(std::max<int64_t>(c->ncols, 1), kFwdBN) * kFwdNWG : T;
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->part_s), (size_t)(Tf * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->ls), (size_t)(c->R * B) * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->rowscale), (size_t)B * sb));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->delta), (size_t)B * sb));
@@ -1302,14 +1354,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->hasval, (size_t)B));
   CT(dalloc(c, &c->loss_row, (size_t)B));
   CT(dalloc(c, &c->offr, (size_t)B));
-  if (desc->flags & PFC_FLAG_DEBUG_LOGITS)
-    CT(dalloc(c, &c->dbgz, (size_t)B * std::max<int64_t>(c->ncols, 1)));
-  CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
   CT(dalloc(c, reinterpret_cast<uint8_t**>(&c->xs), (size_t)B * c->Dp * ob));
-  c->pmax = std::max<int64_t>(1, std::min<int64_t>(c->cap, B));
-  CT(dalloc(c, &c->poscorr, (size_t)(c->nk * c->pmax * c->D)));
-  CT(dalloc(c, &c->pslot, (size_t)std::max<int64_t>(c->ncols, 1)));
-  if (!c->bf16) CT(dalloc(c, &c->dwt, (size_t)std::max<int64_t>(c->ncols, 1) * c->D));
+  CT(alloc_cap_buffers(c));
   CT(dalloc(c, &c->dx_part, (size_t)c->max_splits * B * c->D));
   CT(dalloc(c, &c->dX, (size_t)B * c->D));
   CT(dalloc(c, &c->xdb, (size_t)B * c->D));
@@ -1348,10 +1394,7 @@ int pfc_gpu_destroy(void* ctx) {
   if (!ctx) return PFC_OK;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (Ctx::GraphSlot& G : c->gs) {
-    if (G.gexec) cudaGraphExecDestroy(G.gexec);
-    if (G.graph) cudaGraphDestroy(G.graph);
-  }
+  drop_graphs(c);
   for (cudaEvent_t e : {c->ev_s, c->ev_x, c->ev_dx, c->ev_out})
     if (e) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
@@ -1369,6 +1412,38 @@ int pfc_gpu_destroy(void* ctx) {
 }
 
 int64_t pfc_gpu_capacity(const void* ctx) { return static_cast<const Ctx*>(ctx)->cap; }
+
+int pfc_gpu_set_step_config(void* ctx, const pfc_gpu_step_config* sc) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  pfc_gpu_desc d = c->d;
+  d.r = sc->r;
+  d.margin_kind = sc->margin_kind;
+  d.margin_scale = sc->margin_scale;
+  d.margin_m = sc->margin_m;
+  d.has_filter = sc->has_filter ? 1 : 0;
+  d.filter_threshold = sc->has_filter ? sc->filter_threshold : 0.0;
+  d.momentum = sc->momentum;
+  d.weight_decay = sc->weight_decay;
+  if (int rc = validate_desc(&d)) return fail(c, rc, "%s", g_create_error.c_str());
+  const pfc_gpu_desc& o = c->d;
+  if (d.r == o.r && d.margin_kind == o.margin_kind && d.margin_scale == o.margin_scale &&
+      d.margin_m == o.margin_m && d.has_filter == o.has_filter &&
+      d.filter_threshold == o.filter_threshold && d.momentum == o.momentum &&
+      d.weight_decay == o.weight_decay)
+    return PFC_OK;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // no step in flight uses the old state
+  CUDA_TRY(c, cudaStreamSynchronize(c->s2));
+  c->d = d;
+  set_margin_state(c);
+  const int64_t cap = capacity_for(c->C, c->K, d.r);
+  if (cap != c->cap) {
+    c->cap = cap;
+    set_cap_geometry(c);
+    if (cap > c->cap_alloc) CUDA_TRY(c, alloc_cap_buffers(c));
+  }
+  drop_graphs(c);  // the captured epilogue parameters and column geometry are stale
+  return PFC_OK;
+}
 
 int pfc_gpu_local_shards(const void* ctx, int64_t* first, int64_t* n) {
   const Ctx* c = static_cast<const Ctx*>(ctx);

@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-diag", action="store_true", help="skip timing the diagnostics call")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32"],
+                    help="tcgen05 engine: bf16 operands (the headline) or tf32 (tighter values)")
     ap.add_argument("--no-pdl", action="store_true",
                     help="launch without programmatic dependent launch (A/B timing)")
     return ap.parse_args()
@@ -238,7 +240,8 @@ def main():
     mcfg = (p.MarginConfig.arcface_style(ms_, mm) if args.margin == "arcface"
             else p.MarginConfig(p.ADDITIVE_COSINE, ms_, mm))
     cfg = p.StepConfig(r=args.r, margin=mcfg, lr=0.1)
-    sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, precision=p.PRECISION_BF16,
+    prec = p.PRECISION_TF32 if args.precision == "tf32" else p.PRECISION_BF16
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, precision=prec,
                         device=local, rank=rank, world_size=ws, nccl_id=nccl_id,
                         flags=p.FLAG_NO_PDL if args.no_pdl else 0)
     sh.init_center_shards(1)
@@ -295,7 +298,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": workload_config(args), "gpu_launches": int(launches * args.steps),
             "last_loss": out.loss, "clocks": clk}
     if args.profile:

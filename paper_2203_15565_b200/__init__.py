@@ -275,7 +275,7 @@ class StepOut(C.Structure):
                 ("nccl_bytes", C.c_uint64), ("wire_bytes", C.c_uint64)]
 
 
-PRECISION_BF16, PRECISION_FP32 = 0, 1
+PRECISION_BF16, PRECISION_FP32, PRECISION_TF32 = 0, 1, 2
 FLAG_FORCE_SEQUENTIAL_SAMPLER, FLAG_NO_GRAPH, FLAG_EXACT_SOFTMAX, FLAG_DEBUG_LOGITS = 1, 2, 4, 8
 FLAG_GUARD, FLAG_NO_PDL = 16, 32
 

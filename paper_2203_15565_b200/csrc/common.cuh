@@ -7,6 +7,17 @@
 
 namespace pfc {
 
+// Operand type of the TF32 precision mode: fp32 storage holding values already rounded to tf32
+// (cvt.rna), so the tensor core's tf32 read of the operand is exact and unbiased.
+struct alignas(4) tf32_t {
+  float v;
+};
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
 
 // reference rng.hpp:17-24 (murmur3 finaliser)

@@ -55,8 +55,10 @@ __device__ __forceinline__ float round_to(const __nv_bfloat16*, float v) {
   return __bfloat162float(__float2bfloat16_rn(v));
 }
 __device__ __forceinline__ float round_to(const float*, float v) { return v; }
+__device__ __forceinline__ float round_to(const tf32_t*, float v) { return to_tf32(v); }
 __device__ __forceinline__ void store_out1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 __device__ __forceinline__ void store_out1(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_out1(tf32_t* p, float v) { p->v = to_tf32(v); }
 
 struct NoSetup {
   static constexpr int kCluster = 1;

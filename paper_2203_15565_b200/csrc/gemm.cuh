@@ -54,17 +54,19 @@ struct GemmGeom {
   }
 };
 
-inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest, int BM = 128) {
+// BK: K elements per stage (one 128-byte swizzle row: 64 bf16 or 32 tf32 operands)
+inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest, int BM = 128,
+                          int BK = 64) {
   GemmGeom g{};
   g.BM = BM;
   g.M = M;
   g.N = N;
   g.K = K;
   g.BN = BN;
-  g.BK = 64;
+  g.BK = BK;
   g.m_tiles = (M + BM - 1) / BM;
   g.n_tiles = (N + BN - 1) / BN;
-  g.kb_total = (K + 63) / 64;
+  g.kb_total = (K + BK - 1) / BK;
   if (splits < 1) splits = 1;
   if (splits > g.kb_total) splits = g.kb_total;
   g.kb_per_split = (g.kb_total + splits - 1) / splits;
@@ -111,14 +113,24 @@ struct TmemSrc {
 // rows of B (both signal the leader's full barrier), so per CTA the operand bytes per FLOP drop
 // by a third (A 128 + B 128 rows per 128 x BN block instead of 128 + BN); each CTA's TMEM holds
 // its 128 accumulator rows, so the epilogue functors are the same as for CG = 1.
-template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi, int CG = 1>
+// OT: operand type -- __nv_bfloat16 (kind::f16) or float (kind::tf32; the TF32 precision mode).
+// Every stage holds one 128-byte swizzle row of K per operand row either way (64 bf16 or 32 fp32
+// elements), so the shared-memory layout and the descriptors' byte strides are the same; an
+// MN-major atom is 128 B of M/N by one stage of K (8 KB bf16, 4 KB tf32).
+template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi, int CG = 1,
+          class OT = __nv_bfloat16>
 __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, const GemmGeom g,
                      const __grid_constant__ Epi epi) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using namespace pfc_sm100;
+  constexpr bool kTf32 = sizeof(OT) == 4;
+  constexpr int KB = 128 / (int)sizeof(OT);          // K elements per stage
+  constexpr uint32_t ATOM = 128u * (uint32_t)KB;     // MN-major atom bytes (128 B x KB rows)
+  constexpr uint32_t KSTEP = 32u / sizeof(OT) * 128u;  // MN-major bytes per MMA K step
   static_assert(CG == 1 || CG == 2, "CG");
+  static_assert(!kTf32 || CG == 1, "the tf32 engine runs single-CTA MMAs");
   static_assert(CG == 1 || Epi::kCluster == 1, "a CTA-pair GEMM has no epilogue cluster");
   constexpr int BNL = BN / CG;  // rows of B this CTA loads
   constexpr uint32_t A_BYTES = 128 * 64 * 2;
@@ -192,7 +204,7 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
           const uint32_t s = kbc % STAGES, ph = (kbc / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[s], STAGE_BYTES * CG);
-          const int k0 = kb * 64;
+          const int k0 = kb * KB;
           uint8_t* a = sA + s * A_BYTES;
           uint8_t* b = sB + s * B_BYTES;
           auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1) {
@@ -203,20 +215,21 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
             load(&tmA, a, k0, ti.row0);
           } else {
 #pragma unroll
-            for (int i = 0; i < 2; ++i) load(&tmA, a + i * 8192, ti.row0 + 64 * i, k0);
+            for (int i = 0; i < 128 / KB; ++i) load(&tmA, a + i * ATOM, ti.row0 + KB * i, k0);
           }
           if (!B_MN) {
             load(&tmB, b, k0, bcol);
           } else {
 #pragma unroll
-            for (int i = 0; i < BNL / 64; ++i) load(&tmB, b + i * 8192, bcol + 64 * i, k0);
+            for (int i = 0; i < BNL / KB; ++i) load(&tmB, b + i * ATOM, bcol + KB * i, k0);
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = kTf32 ? make_idesc_tf32(128, BN, A_MN, B_MN)
+                                       : make_idesc_bf16(128 * CG, BN, A_MN, B_MN);
       uint32_t kbc = 0, it = 0;
       for (int t = first; t < total; t += stride, ++it) {
         const TileInfo ti = g.tile(t);
@@ -231,13 +244,18 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
           const uint32_t b_base = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = A_MN ? make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(a_base + k * 32, 0, 1024);
-            const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
-                                     : make_sdesc_sw128(b_base + k * 32, 0, 1024);
+          for (int k = 0; k < 4; ++k) {  // 4 MMAs of 32 bytes of K each
+            // MN-major tf32 operands use the 32-byte-atom 128B swizzle (4-row K groups, SBO
+            // 512 B); everything else the 16-byte-atom one (8-row groups, SBO 1024 B)
+            auto mn_desc = [&](uint32_t base) {
+              return kTf32 ? make_sdesc_sw128_32b(base + k * KSTEP, ATOM, 512)
+                           : make_sdesc_sw128(base + k * KSTEP, ATOM, 1024);
+            };
+            const uint64_t ad = A_MN ? mn_desc(a_base) : make_sdesc_sw128(a_base + k * 32, 0, 1024);
+            const uint64_t bd = B_MN ? mn_desc(b_base) : make_sdesc_sw128(b_base + k * 32, 0, 1024);
             const uint32_t acc = (kb > ti.kb0 || k > 0) ? 1u : 0u;
-            if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, acc);
+            if constexpr (kTf32) umma_tf32(d_tmem, ad, bd, idesc, acc);
+            else if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, acc);
             else umma_bf16(d_tmem, ad, bd, idesc, acc);
           }
           if constexpr (CG == 2) umma_commit_pair(&empty[s]);

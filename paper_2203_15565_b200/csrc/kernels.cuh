@@ -49,6 +49,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __device__ __forceinline__ void store_out(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 __device__ __forceinline__ void store_out(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_out(tf32_t* p, float v) { p->v = to_tf32(v); }
 
 // FeatureBatch layout (D x B fp64, types.hpp:14-26) -> rows [B][D] fp32.  32x32 tiles.
 __global__ void x_from_dxb_kernel(const double* __restrict__ xdb, int D, int B,

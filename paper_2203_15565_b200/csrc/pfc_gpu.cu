@@ -80,16 +80,19 @@ PFN_encodeTiled_t get_encode() {
 // 2-D bf16 tensor [outer][inner] with row stride ld (elements); box {box_inner, box_outer}.
 // Loads use {64, rows} with 128B swizzle (UMMA operand atoms); the G^T store uses {32, 128}
 // with 64B swizzle (matching the epilogue's smem staging).
+// elem: 2 (bf16) or 4 (fp32 operands of the tf32 engine; box_inner then 32 for 128 B rows).
 bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
               uint32_t box_outer, uint32_t box_inner = 64,
-              CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+              CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B, int elem = 2) {
   PFN_encodeTiled_t enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * (uint64_t)elem};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+  const CUtensorMapDataType dt =
+      elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  return enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -142,7 +145,9 @@ struct Ctx {
   int64_t C, D, K, Dp, blk, cap, k0, nk, cls_lo, cls_hi, rows, ncols, ncols_pad, ldg;
   int64_t pool_stride, maxB;
   int R, rank;
-  bool bf16;
+  bool bf16;          // tcgen05 kind::f16 engine (bf16 operands)
+  bool tf32 = false;  // tcgen05 kind::tf32 engine (fp32 operands)
+  bool umma = false;  // either tcgen05 engine (else the fp32 SIMT validation engine)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t s2 = nullptr;                      // forked stream inside the step
@@ -397,10 +402,11 @@ cudaError_t klaunch(Ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 }
 
 // ------------------------------------------------------------------ GEMM launchers
-template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi, int CG = 1>
+template <int BN, int STAGES, int NWG, bool A_MN, bool B_MN, class Epi, int CG = 1,
+          class OT = __nv_bfloat16>
 cudaError_t launch_umma(Ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, const GemmGeom& g,
                         const Epi& epi) {
-  auto kern = umma_gemm_kernel<BN, STAGES, NWG, A_MN, B_MN, Epi, CG>;
+  auto kern = umma_gemm_kernel<BN, STAGES, NWG, A_MN, B_MN, Epi, CG, OT>;
   constexpr int smem = umma_smem_bytes<BN, STAGES, NWG, Epi, CG>();
   static_assert(smem <= 232448, "shared memory budget");
   if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem)) return e;
@@ -449,20 +455,26 @@ cudaError_t launch_simt(Ctx* c, const float* A, int lda, const float* Bm, int ld
 }
 
 int ensure_maps(Ctx* c, int64_t B) {
-  if (!c->bf16 || c->tm_B == B) return PFC_OK;
+  if (!c->umma || c->tm_B == B) return PFC_OK;
   bool ok = true;
+  const int el = c->tf32 ? 4 : 2;       // operand bytes
+  const uint32_t kb = 128 / (uint32_t)el;  // elements per 128-byte swizzle row
+  const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  // MN-major operands: tf32 needs the 32-byte-atom variant (gemm.cuh make_sdesc_sw128_32b)
+  const auto swm = c->tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   // logits GEMM (M = b, N = classes): A = X^ [B][Dp], B = W^ [ncols][Dp], both K-major;
-  // its epilogue stores E^T [ncols][ldg] (per-warp box 32 b x 32 classes, 64B swizzle)
-  ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128);
-  ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kFwdBN / kFwdCG);
-  ok &= make_map(&c->tm_e_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  // its epilogue stores E^T [ncols][ldg] (bf16: per-warp box 32 b x 32 classes, 64B swizzle)
+  ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128, kb, sw, el);
+  ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kFwdBN / kFwdCG, kb, sw, el);
+  if (c->bf16)
+    ok &= make_map(&c->tm_e_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   // dX GEMM (M = b, N = d, K = classes): A = E^T read MN-major (b contiguous); B = W^ MN-major
-  ok &= make_map(&c->tm_e_mn, c->G, B, c->ncols, c->ldg, 64);
-  ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, 64);
+  ok &= make_map(&c->tm_e_mn, c->G, B, c->ncols, c->ldg, kb, kb, swm, el);
+  ok &= make_map(&c->tm_w_mn, c->wh, c->Dp, c->ncols, c->Dp, kb, kb, swm, el);
   // dW GEMM (M = classes, N = d, K = b): A = E^T K-major (whole class blocks contiguous);
   // B = rowscale * x^ MN-major
-  ok &= make_map(&c->tm_e_k, c->G, B, c->ncols, c->ldg, 128);
-  ok &= make_map(&c->tm_xs_mn, c->xs, c->Dp, B, c->Dp, 64);
+  ok &= make_map(&c->tm_e_k, c->G, B, c->ncols, c->ldg, 128, kb, sw, el);
+  ok &= make_map(&c->tm_xs_mn, c->xs, c->Dp, B, c->Dp, kb, kb, swm, el);
   if (!ok) return fail(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   c->tm_B = B;
   return PFC_OK;
@@ -520,22 +532,24 @@ SamplerArgs sampler_args(Ctx* c, const pfc_gpu_step_args* a, const float* x, con
 cudaError_t launch_sampler(Ctx* c, SamplerArgs& sa) {
   const size_t smem = sampler_smem_bytes(c->nchunk, (int)c->nk);
   const int smax = (int)sampler_smem_bytes(kMaxSamplerChunks, kMaxSamplerLocalShards);
-  const void* fill = c->bf16 ? reinterpret_cast<const void*>(fill_kernel<__nv_bfloat16>)
-                             : reinterpret_cast<const void*>(fill_kernel<float>);
+  const void* fill = c->bf16   ? reinterpret_cast<const void*>(fill_kernel<__nv_bfloat16>)
+                     : c->tf32 ? reinterpret_cast<const void*>(fill_kernel<tf32_t>)
+                               : reinterpret_cast<const void*>(fill_kernel<float>);
   if (cudaError_t e = ensure_smem_attr(fill, smax)) return e;
   if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(walk_kernel), smax)) return e;
   const dim3 grid((unsigned)c->num_sms), blk(kSamplerThreads);
   mark_kernel<<<grid, blk, 0, c->stream>>>(sa);
   c->launches++;
   if (cudaError_t e = cudaGetLastError()) return e;
-  cudaError_t e = c->bf16 ? klaunch(c, fill_kernel<__nv_bfloat16>, grid, blk, smem, c->stream, sa)
-                          : klaunch(c, fill_kernel<float>, grid, blk, smem, c->stream, sa);
+  cudaError_t e = c->bf16   ? klaunch(c, fill_kernel<__nv_bfloat16>, grid, blk, smem, c->stream, sa)
+                  : c->tf32 ? klaunch(c, fill_kernel<tf32_t>, grid, blk, smem, c->stream, sa)
+                            : klaunch(c, fill_kernel<float>, grid, blk, smem, c->stream, sa);
   if (e != cudaSuccess) return e;
   return klaunch(c, walk_kernel, grid, blk, smem, c->stream, sa);
 }
 
 int dx_splits(Ctx* c, int64_t B) {
-  if (c->bf16) {
+  if (c->umma) {
     const int64_t tiles = ceil_div(B, 128 * kDxCG) * kDxCG * ceil_div(c->D, kBN);  // CTAs per split
     int64_t s = c->num_sms / (tiles > 0 ? tiles : 1);
     if (s < 1) s = 1;
@@ -553,6 +567,11 @@ int dx_splits(Ctx* c, int64_t B) {
 template <typename ST, typename OT, bool kUmma>
 int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
                  const pfc_gpu_step_args* a, float* dx_full) {
+  // tcgen05 engine: bf16 operands (kind::f16) or fp32 operands (kind::tf32, the TF32 mode)
+  constexpr bool kTf = kUmma && sizeof(OT) == 4;
+  constexpr int BKU = kUmma ? 128 / (int)sizeof(OT) : 64;  // K elements per GEMM stage
+  constexpr int FCG = kTf ? 1 : kFwdCG;
+  constexpr int XCG = kTf ? 1 : kDxCG;
   cudaStream_t s = c->stream;
   const int bs = 256;
   if (int rc = ensure_maps(c, B)) return rc;
@@ -594,7 +613,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const float tau = (float)c->d.filter_threshold;
   const bool filt = c->d.has_filter != 0;
   if (e2e) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_x, 0));
-  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, FBN, 1, 0, kUmma ? 128 * kFwdCG : 128);
+  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, FBN, 1, 0, kUmma ? 128 * FCG : 128, BKU);
   const bool exact = exact_now(c);
   if (exact) {
     // ---- per-row offsets: max-only pass of the logits GEMM -> o_b (rank max: collective 1,
@@ -604,7 +623,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     auto go = [&](auto e) {
       if constexpr (kUmma)
-        return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), kFwdCG>(c, c->tm_x_k, c->tm_w_k, gf, e);
+        return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), FCG, OT>(c, c->tm_x_k, c->tm_w_k, gf, e);
       else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
                                             (const float*)c->wh, (int)c->Dp, gf, e);
     };
@@ -622,16 +641,16 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     auto go = [&](auto e) {
       if constexpr (kUmma)
-        return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), kFwdCG>(c, c->tm_x_k, c->tm_w_k, gf, e);
+        return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), FCG, OT>(c, c->tm_x_k, c->tm_w_k, gf, e);
       else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
                                             (const float*)c->wh, (int)c->Dp, gf, e);
     };
     if (filt)
-      err = go(FwdEpi<ST, OT, true, kUmma>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
+      err = go(FwdEpi<ST, OT, true, kUmma && !kTf>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
                                            c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E,
                                            offr, c->dbgz});
     else
-      err = go(FwdEpi<ST, OT, false, kUmma>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
+      err = go(FwdEpi<ST, OT, false, kUmma && !kTf>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
                                             c->mg, tau, ps, c->zpos, c->cpos, c->epos, c->hasval, E,
                                             offr, c->dbgz});
     CUDA_TRY(c, err);
@@ -677,10 +696,10 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   // ---- dX = rowscale * E W^ + delta w^_pos (split-K), tangent projection (shardsim.hpp:363-376)
   {
     const int S = dx_splits(c, B);
-    const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0, kUmma ? 128 * kDxCG : 128);
+    const GemmGeom gx = make_geom((int)B, (int)c->D, (int)c->ncols, BN, S, 0, kUmma ? 128 * XCG : 128, BKU);
     DxPartEpi e{{}, (int)B, (int)c->D, c->dx_part};
     cudaError_t err;
-    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, true, true, DxPartEpi, kDxCG>(c, c->tm_e_mn, c->tm_w_mn, gx, e);
+    if constexpr (kUmma) err = launch_umma<kBN, 4, 1, true, true, DxPartEpi, XCG, OT>(c, c->tm_e_mn, c->tm_w_mn, gx, e);
     else err = launch_simt<true, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->wh,
                                        (int)c->Dp, gx, e);
     CUDA_TRY(c, err);
@@ -718,17 +737,17 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));  // X^s and the positive corrections
   // ---- dwt = E^T (rowscale x^) + positive corrections; center_proj; fused momentum-SGD
   {
-    const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1);
+    const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1, 128, BKU);
     cudaError_t err;
     if constexpr (kUmma) {
       if (gw.n_tiles == 2)
-        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true>(
+        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true, DwUpdateEpi<true>, 1, OT>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                               c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
                               c->st});
       else
-        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true>(
+        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true, DwUpdateEpi<false>, 1, OT>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
             DwUpdateEpi<false>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
                                c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
@@ -759,6 +778,7 @@ int run_step(Ctx* c, const float* x, const int64_t* lab, int64_t B, const pfc_gp
   auto pipeline = [&]() {
     c->launches = 0;
     if (c->bf16) return run_pipeline<float, __nv_bfloat16, true>(c, x, lab, B, a, dx_full);
+    if (c->tf32) return run_pipeline<float, tf32_t, true>(c, x, lab, B, a, dx_full);
     return run_pipeline<double, float, false>(c, x, lab, B, a, dx_full);
   };
   if (!graph) {
@@ -1022,11 +1042,11 @@ cudaError_t alloc_cap_buffers(Ctx* c) {
     *p = nullptr;
   }
   const size_t ob = c->bf16 ? 2 : 4;  // operand bytes
-  const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
+  const size_t sb = c->umma ? 4 : 8;  // statistics bytes
   const int64_t B = c->maxB;
   const int64_t n1 = std::max<int64_t>(c->ncols, 1);
-  const int BN = c->bf16 ? kBN : kSimtBN;
-  const int64_t Tf = c->bf16 ? ceil_div(n1, kFwdBN) * kFwdNWG : ceil_div(n1, BN);
+  const int BN = c->umma ? kBN : kSimtBN;
+  const int64_t Tf = c->umma ? ceil_div(n1, kFwdBN) * kFwdNWG : ceil_div(n1, BN);
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   A(dalloc(c, &c->buf_cls, (size_t)n1));
@@ -1040,7 +1060,7 @@ cudaError_t alloc_cap_buffers(Ctx* c) {
   A(dalloc(c, reinterpret_cast<uint8_t**>(&c->G), (size_t)c->ncols_pad * c->ldg * ob));
   A(dalloc(c, &c->poscorr, (size_t)(c->nk * c->pmax * c->D)));
   A(dalloc(c, &c->pslot, (size_t)n1));
-  if (!c->bf16) A(dalloc(c, &c->dwt, (size_t)n1 * c->D));
+  if (!c->umma) A(dalloc(c, &c->dwt, (size_t)n1 * c->D));
   c->cap_alloc = c->cap;
   return e;
 }
@@ -1080,9 +1100,11 @@ int validate_desc(const pfc_gpu_desc* d) {
     return fail(nullptr, PFC_ERR_CONTRACT,
                 "pfc_gpu_create: at most %d reference shards per rank (num_shards / world_size)",
                 kMaxSamplerLocalShards);
-  if (d->precision == PFC_PRECISION_BF16 && (d->dim % 4 != 0 || d->dim > 512))
+  if (d->precision < PFC_PRECISION_BF16 || d->precision > PFC_PRECISION_TF32)
+    return fail(nullptr, PFC_ERR_CONFIG, "pfc_gpu_create: unknown precision %d", d->precision);
+  if (d->precision != PFC_PRECISION_FP32 && (d->dim % 4 != 0 || d->dim > 512))
     return fail(nullptr, PFC_ERR_CONFIG,
-                "pfc_gpu: the bf16 tcgen05 path needs dim %% 4 == 0 and dim <= 512 "
+                "pfc_gpu: the tcgen05 paths (bf16, tf32) need dim %% 4 == 0 and dim <= 512 "
                 "(use PFC_PRECISION_FP32 otherwise)");
   if (d->num_classes >= (int64_t)INT32_MAX)
     return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: num_classes must be < 2^31");
@@ -1276,6 +1298,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->R = desc->world_size;
   c->rank = desc->rank;
   c->bf16 = desc->precision == PFC_PRECISION_BF16;
+  c->tf32 = desc->precision == PFC_PRECISION_TF32;
+  c->umma = c->bf16 || c->tf32;
   c->Dp = round_up(c->D, 64);
   c->blk = ceil_div(c->C, c->K);
   c->cap = capacity_for(c->C, c->K, desc->r);
@@ -1320,8 +1344,8 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   for (cudaEvent_t* e : {&c->ev_s, &c->ev_x, &c->ev_dx, &c->ev_out})
     CT(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   const size_t ob = c->bf16 ? 2 : 4;  // operand bytes
-  const size_t sb = c->bf16 ? 4 : 8;  // statistics bytes
-  c->max_splits = c->bf16 ? 32 : 64;
+  const size_t sb = c->umma ? 4 : 8;  // statistics bytes
+  c->max_splits = c->umma ? 32 : 64;
   CT(dalloc(c, &c->W, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
   CT(dalloc(c, &c->M, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
   CT(dalloc(c, &c->labels, (size_t)B));

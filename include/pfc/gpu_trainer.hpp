@@ -67,6 +67,16 @@ class DeviceTrainer {
     return o.loss;
   }
   void apply_gradient(double lr) { check(pfc_gpu_trainer_apply_gradient(t_, lr), ctx_); }
+  void nearest_center(const std::vector<int64_t>& ids, std::vector<int64_t>& best) {
+    check(pfc_gpu_trainer_nearest_center(t_, ids.data(), static_cast<int64_t>(ids.size()),
+                                         best.data()),
+          ctx_);
+  }
+  void pair_cosines(const std::vector<int64_t>& ids, std::vector<double>& out) {
+    check(pfc_gpu_trainer_pair_cosines(t_, ids.data(), static_cast<int64_t>(ids.size()),
+                                       out.data()),
+          ctx_);
+  }
   Matrix embed(const std::vector<int64_t>& ids) {
     Matrix m(embed_, static_cast<int64_t>(ids.size()));
     if (!ids.empty())
@@ -398,39 +408,32 @@ inline TrainResult train(const SyntheticDataset& ds, const TrainConfig& cfg,
   result.mics_max = *std::max_element(mics_values.begin(), mics_values.end());
   host_state();
 
-  // nearest-centre training accuracy (trainer.hpp:520-546) over device embeddings
+  // nearest-centre training accuracy (trainer.hpp:519-547): the O(n C D) scan runs on the
+  // device (pfc_gpu_trainer_nearest_center, fp64 in the reference's order)
   {
-    const Matrix centers = pfc::detail::gather_unit_centers(result.shards);  // C x D
-    const Matrix emb = l2_normalize_columns(tr.embed(train_points));
+    std::vector<int64_t> best(static_cast<size_t>(n_train));
+    tr.nearest_center(train_points, best);
     int64_t correct = 0;
-    for (int64_t b = 0; b < n_train; ++b) {
-      double best = -2.0;
-      int64_t best_class = -1;
-      for (int64_t c = 0; c < classes; ++c) {
-        double cosv = 0.0;
-        for (int64_t d = 0; d < cfg.embed_dim; ++d) cosv += emb(d, b) * centers(c, d);
-        if (cosv > best) {
-          best = cosv;
-          best_class = c;
-        }
-      }
-      correct += best_class == ds.observed_labels[train_points[static_cast<size_t>(b)]];
-    }
+    for (int64_t b = 0; b < n_train; ++b)
+      correct += best[static_cast<size_t>(b)] ==
+                 ds.observed_labels[train_points[static_cast<size_t>(b)]];
     result.train_accuracy = static_cast<double>(correct) / static_cast<double>(n_train);
   }
 
-  // open-set verification on the held-out identities (trainer.hpp:548-577)
+  // open-set verification on the held-out identities (trainer.hpp:548-577): the pair cosines
+  // come from the device (pfc_gpu_trainer_pair_cosines); scores are split by identity in the
+  // reference's (i, j) order and scored by the host project's own verify_tar_at_far
   if (!eval_points.empty()) {
     const auto n_eval = static_cast<int64_t>(eval_points.size());
-    const Matrix emb = l2_normalize_columns(tr.embed(eval_points));
+    std::vector<double> pair_cos(static_cast<size_t>(n_eval * (n_eval - 1) / 2));
+    tr.pair_cosines(eval_points, pair_cos);
     std::vector<double> genuine, impostor;
+    size_t at = 0;
     for (int64_t i = 0; i < n_eval; ++i)
-      for (int64_t j = i + 1; j < n_eval; ++j) {
-        double c = 0.0;
-        for (int64_t d = 0; d < cfg.embed_dim; ++d) c += emb(d, i) * emb(d, j);
+      for (int64_t j = i + 1; j < n_eval; ++j, ++at) {
         const bool same = ds.true_identities[eval_points[static_cast<size_t>(i)]] ==
                           ds.true_identities[eval_points[static_cast<size_t>(j)]];
-        (same ? genuine : impostor).push_back(c);
+        (same ? genuine : impostor).push_back(pair_cos[at]);
       }
     if (!genuine.empty() && !impostor.empty()) {
       try {

@@ -274,6 +274,19 @@ int pfc_gpu_trainer_apply_gradient(void* trainer, double lr);
  * (evaluation: nearest-centre accuracy, verification); discards the cached activations */
 int pfc_gpu_trainer_embed(void* trainer, const int64_t* point_ids, int64_t n, double* emb);
 
+/* Evaluation of the trained model on the device (trainer.hpp:519-577), fp64 in the reference's
+ * operation order (separate multiply / add, d ascending), on the points' normalised embeddings
+ * (l2_normalize_columns of Backbone::forward) and the context's current centres:
+ *   nearest_center: best_class[n] = the first class with the largest cosine to the point's
+ *                   embedding over all C unit centres (the training-accuracy scan, 532-545);
+ *   pair_cosines:   cos_out[n (n-1) / 2] = the cosines of every pair i < j in (i, j)
+ *                   lexicographic order (the verification score loop, 553-561).
+ * Single-rank contexts (all classes local); embed_dim <= 512 for nearest_center. */
+int pfc_gpu_trainer_nearest_center(void* trainer, const int64_t* point_ids, int64_t n,
+                                   int64_t* best_class);
+int pfc_gpu_trainer_pair_cosines(void* trainer, const int64_t* point_ids, int64_t n,
+                                 double* cos_out);
+
 /* ---- bench / test helpers --------------------------------------------------------------- */
 /* PFC_FLAG_GUARD contexts: synchronises the device, compares every guard region with its
  * pattern; *corrupted = the number of changed regions (PFC_ERR_CUDA naming them if any). */

@@ -75,4 +75,91 @@ __global__ void bb_gather_kernel(const double* __restrict__ points, int64_t npts
   if (d == 0 && labels) labels[b] = plabels[p];
 }
 
+// ---- evaluation of the trained model (trainer.hpp:519-577) on the device, in fp64 with the
+// reference's operation order (products and sums as separate IEEE operations, d ascending), so
+// the cosines equal the reference's host loops bit for bit on the same embeddings and centres.
+
+// l2_normalize_columns (matrix.hpp:118-143) of a chunk of embeddings: feat is E x m (the step's
+// FeatureBatch layout); out rows [m][E] (row-major per point).
+__global__ void eval_normalize_kernel(const double* __restrict__ feat, int E, int m,
+                                      double* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= m) return;
+  double s = 0.0;
+  for (int d = 0; d < E; ++d) {
+    const double x = feat[(int64_t)d * m + b];
+    s = __dadd_rn(s, __dmul_rn(x, x));
+  }
+  const double inv = 1.0 / fmax(sqrt(s), 1e-12);
+  for (int d = 0; d < E; ++d) out[(int64_t)b * E + d] = __dmul_rn(feat[(int64_t)d * m + b], inv);
+}
+
+// unit_center (metrics.hpp:20-31): per class, 1 / max(|w|, 1e-12) of its fp32 row (as fp64)
+__global__ void eval_center_inv_kernel(const float* __restrict__ W, int64_t C, int D,
+                                       double* __restrict__ winv) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= C) return;
+  double s = 0.0;
+  for (int d = 0; d < D; ++d) {
+    const double x = (double)W[r * D + d];
+    s = __dadd_rn(s, __dmul_rn(x, x));
+  }
+  winv[r] = 1.0 / fmax(sqrt(s), 1e-12);
+}
+
+// Nearest unit centre of each point (trainer.hpp:532-545): one block per point, threads over
+// classes, cos = sum_d emb_d (w_d inv) in d order; the first class with the largest cosine wins
+// (the reference's strict > scan from best = -2); NaN never wins.
+__global__ void __launch_bounds__(256) eval_argmax_kernel(const double* __restrict__ emb, int E,
+                                                          const float* __restrict__ W,
+                                                          const double* __restrict__ winv,
+                                                          int64_t C, int64_t* __restrict__ best) {
+  __shared__ double se[512];
+  __shared__ double bv[256];
+  __shared__ int64_t bc[256];
+  const int b = blockIdx.x;
+  for (int d = threadIdx.x; d < E; d += blockDim.x) se[d] = emb[(int64_t)b * E + d];
+  __syncthreads();
+  double v = -2.0;
+  int64_t c_best = -1;
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+    const float* w = W + c * E;
+    const double inv = winv[c];
+    double cs = 0.0;
+    for (int d = 0; d < E; ++d) cs = __dadd_rn(cs, __dmul_rn(se[d], __dmul_rn((double)w[d], inv)));
+    if (cs > v) {  // classes ascend within the thread: strict > keeps the first
+      v = cs;
+      c_best = c;
+    }
+  }
+  bv[threadIdx.x] = v;
+  bc[threadIdx.x] = c_best;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double ov = bv[threadIdx.x + o];
+      const int64_t oc = bc[threadIdx.x + o];
+      const bool take = oc >= 0 && (ov > bv[threadIdx.x] ||
+                                    (ov == bv[threadIdx.x] && (bc[threadIdx.x] < 0 || oc < bc[threadIdx.x])));
+      if (take) {
+        bv[threadIdx.x] = ov;
+        bc[threadIdx.x] = oc;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) best[b] = bc[0];
+}
+
+// Cosines of all pairs i < j (trainer.hpp:553-561), in (i, j) lexicographic order.
+__global__ void eval_pairs_kernel(const double* __restrict__ emb, int E, int64_t n, int64_t i0,
+                                  double* __restrict__ out) {
+  const int64_t i = i0 + blockIdx.y;
+  const int64_t j = i + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double cs = 0.0;
+  for (int d = 0; d < E; ++d) cs = __dadd_rn(cs, __dmul_rn(emb[i * E + d], emb[j * E + d]));
+  out[i * n - i * (i + 1) / 2 + (j - i - 1)] = cs;
+}
+
 }  // namespace pfc

@@ -2382,6 +2382,93 @@ int pfc_gpu_trainer_apply_gradient(void* tr, double lr) {
   return PFC_OK;
 }
 
+// normalised embeddings [n][E] of the points into a device buffer (chunked forward)
+int trainer_embed_device(Trainer* t, const int64_t* point_ids, int64_t n, double* emb) {
+  Ctx* c = t->c;
+  for (int64_t at = 0; at < n; at += t->maxB) {
+    const int64_t m = std::min<int64_t>(t->maxB, n - at);
+    if (int rc = trainer_forward(t, point_ids + at, m)) return rc;
+    if (int rc = trainer_check(t, m)) return rc;
+    eval_normalize_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, c->stream>>>(
+        t->feat, (int)t->E, (int)m, emb + at * t->E);
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  t->B = 0;  // the cached activations are not a training batch
+  return PFC_OK;
+}
+
+int pfc_gpu_trainer_nearest_center(void* tr, const int64_t* point_ids, int64_t n,
+                                   int64_t* best_class) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  if (n <= 0) return PFC_OK;
+  if (t->E > 512)
+    return fail(c, PFC_ERR_CONTRACT, "pfc_gpu_trainer_nearest_center: embed_dim %lld > 512",
+                (long long)t->E);
+  double *emb = nullptr, *winv = nullptr;
+  int64_t* best = nullptr;
+  cudaStream_t s = c->stream;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(s);
+    cudaFree(emb);
+    cudaFree(winv);
+    cudaFree(best);
+  };
+  cudaError_t e = cudaMalloc(&emb, sizeof(double) * n * t->E);
+  if (e == cudaSuccess) e = cudaMalloc(&winv, sizeof(double) * std::max<int64_t>(c->rows, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&best, sizeof(int64_t) * n);
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(c, PFC_ERR_CUDA, "pfc_gpu_trainer_nearest_center: %s", cudaGetErrorString(e));
+  }
+  int rc = trainer_embed_device(t, point_ids, n, emb);
+  if (rc == PFC_OK) {
+    eval_center_inv_kernel<<<(unsigned)ceil_div(std::max<int64_t>(c->rows, 1), 128), 128, 0, s>>>(
+        c->W, c->rows, (int)c->D, winv);
+    eval_argmax_kernel<<<(unsigned)n, 256, 0, s>>>(emb, (int)t->E, c->W, winv, c->rows, best);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(best_class, best, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = fail(c, PFC_ERR_CUDA, "pfc_gpu_trainer_nearest_center: %s", cudaGetErrorString(e));
+  }
+  cleanup();
+  return rc;
+}
+
+int pfc_gpu_trainer_pair_cosines(void* tr, const int64_t* point_ids, int64_t n, double* cos_out) {
+  auto* t = static_cast<Trainer*>(tr);
+  Ctx* c = t->c;
+  if (n < 2) return PFC_OK;
+  const int64_t np = n * (n - 1) / 2;
+  double *emb = nullptr, *out = nullptr;
+  cudaStream_t s = c->stream;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(s);
+    cudaFree(emb);
+    cudaFree(out);
+  };
+  cudaError_t e = cudaMalloc(&emb, sizeof(double) * n * t->E);
+  if (e == cudaSuccess) e = cudaMalloc(&out, sizeof(double) * np);
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(c, PFC_ERR_CUDA, "pfc_gpu_trainer_pair_cosines: %s", cudaGetErrorString(e));
+  }
+  int rc = trainer_embed_device(t, point_ids, n, emb);
+  if (rc == PFC_OK) {
+    for (int64_t i0 = 0; i0 < n && e == cudaSuccess; i0 += 65535) {  // rows i0.. (grid.y limit)
+      const int64_t ni = std::min<int64_t>(65535, n - i0);
+      dim3 grid((unsigned)ceil_div(n, 128), (unsigned)ni);
+      eval_pairs_kernel<<<grid, 128, 0, s>>>(emb, (int)t->E, n, i0, out);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(cos_out, out, sizeof(double) * np, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = fail(c, PFC_ERR_CUDA, "pfc_gpu_trainer_pair_cosines: %s", cudaGetErrorString(e));
+  }
+  cleanup();
+  return rc;
+}
+
 int pfc_gpu_trainer_embed(void* tr, const int64_t* point_ids, int64_t n, double* emb) {
   auto* t = static_cast<Trainer*>(tr);
   Ctx* c = t->c;

@@ -62,6 +62,7 @@ __device__ __forceinline__ void store_out1(tf32_t* p, float v) { p->v = to_tf32(
 
 struct NoSetup {
   static constexpr int kCluster = 1;
+  static constexpr int kExtraSmem = 0;  // CTA-shared epilogue bytes past the NWG per-WG areas
   static constexpr bool kNext = false;  // true: run_next() also receives the next tile's Pre
   __device__ __forceinline__ void setup(uint8_t*) const {}
 };
@@ -422,17 +423,25 @@ __device__ __forceinline__ void static_range(F&& f) {
 }
 }  // namespace dw_ring
 
-template <bool kPair>
+// NC: CTAs per class block (a cluster): the dim blocks of 256 (D <= 256 * NC, up to 1024).  Each
+// CTA sends its rows' partial dots to the other NC - 1 and sums all NC in cluster-rank order, so
+// every CTA of the cluster forms the same center_proj.
+template <int NC>
 struct DwUpdateEpi {
-  static constexpr int kCluster = kPair ? 2 : 1;
+  static_assert(NC >= 1 && NC <= 4, "DwUpdateEpi: 1-4 dim blocks");
+  static constexpr bool kPair = NC > 1;
+  static constexpr int kCluster = NC;
   static constexpr bool kNext = true;
   static constexpr int kStageFloats = 8 * 36;             // TMEM chunk of the warp's 8 rows
   static constexpr int kRingFloats = dw_ring::kCap * 256;  // 6 x 1 KB
   static constexpr int kWarpFloats = kStageFloats + kRingFloats + 2 * 3 * 8;  // + [2][inv|row|pslot]
   static constexpr int kWarpBytes = kWarpFloats * 4;
-  // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][128 rows] + mbarriers [2][16 warps]
-  static constexpr int kSharedBytes = 2 * 128 * 4 + 2 * 16 * 8;
-  static constexpr int kSmem = ((4 * kWarpBytes + kSharedBytes + 127) / 128) * 128;
+  // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][NC source rank][128 rows] + mbarriers
+  // [2][16 warps]
+  static constexpr int kHremFloats = 2 * NC * 128;
+  static constexpr int kSharedBytes = kHremFloats * 4 + 2 * 16 * 8;
+  static constexpr int kSmem = ((4 * kWarpBytes + 127) / 128) * 128;  // per warpgroup
+  static constexpr int kExtraSmem = ((kSharedBytes + 127) / 128) * 128;  // once, after all 4
   int ncols, D;
   const float* wnorm;       // [ncols]
   const int32_t* lrow;      // [ncols] local row of W
@@ -463,11 +472,11 @@ struct DwUpdateEpi {
   __device__ __forceinline__ void prefetch(const TileInfo&, int, int, const Pre&) const {}
   __device__ __forceinline__ void finish(int, int) const {}
 
-  __device__ __forceinline__ static uint8_t* shared_area(uint8_t* wg0) { return wg0 + 4 * kWarpBytes; }
+  __device__ __forceinline__ static uint8_t* shared_area(uint8_t* wg0) { return wg0 + 4 * kSmem; }
   __device__ __forceinline__ void setup(uint8_t* epi_base) const {
     if constexpr (kPair) {
-      uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(epi_base) + 2 * 128 * 4);
-      for (int k = 0; k < 32; ++k) pfc_sm100::mbar_init(&mb[k], 1);  // local arrive + 32 tx bytes
+      uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(epi_base) + kHremFloats * 4);
+      for (int k = 0; k < 32; ++k) pfc_sm100::mbar_init(&mb[k], 1);  // local arrive + tx bytes
     }
   }
 
@@ -490,8 +499,8 @@ struct DwUpdateEpi {
     int* s_row = reinterpret_cast<int*>(s_inv + 8);
     int* s_ps = s_row + 8;
     int* s_row_n = reinterpret_cast<int*>(sc + ((t.iter & 1) ^ 1) * 24 + 8);
-    float* hrem = reinterpret_cast<float*>(shared_area(wg0));                   // [2][128]
-    uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + 2 * 128 * 4);  // [2][16]
+    float* hrem = reinterpret_cast<float*>(shared_area(wg0));                      // [2][NC][128]
+    uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + kHremFloats * 4);  // [2][16]
     const bool failed = status_failed(st);
     const float lr = sp->lr;
     const bool mine = (lane >> 3) == wg;  // this lane's TMEM row is one of the warp's 8
@@ -524,8 +533,9 @@ struct DwUpdateEpi {
 #else
     const bool anyp = __any_sync(0xffffffffu, ps[0] >= 0 || ps[1] >= 0);  // positives are rare
 #endif
-    if constexpr (kPair) {  // this tile's exchange: the peer's 8 half-dots arrive as 32 tx bytes
-      if (lane == 0) pfc_sm100::mbar_arrive_expect_tx(&mb[(t.iter & 1) * 16 + wg * 4 + q], 32u);
+    if constexpr (kPair) {  // this tile's exchange: each peer's 8 partial dots arrive as 32 tx bytes
+      if (lane == 0)
+        pfc_sm100::mbar_arrive_expect_tx(&mb[(t.iter & 1) * 16 + wg * 4 + q], 32u * (NC - 1));
     }
     // this lane's 16-byte piece of row (u*4+sub) in ring sub-slot p
     const uint32_t ring_s = pfc_sm100::smem_u32(ring);
@@ -598,20 +608,31 @@ struct DwUpdateEpi {
         }
         if constexpr (kPair) {
           const int it = t.iter, par = it & 1, e = wg * 4 + q;
-          float* hr = hrem + par * 128 + q * 32 + wg * 8;  // this warp's 8 rows
+          const uint32_t me = pfc_sm100::cluster_ctarank();
+          // this warp's 8 rows in the slot of source rank r: hrem[par][r][q*32 + wg*8 + ...]
+          auto slot = [&](uint32_t r) { return hrem + (par * NC + (int)r) * 128 + q * 32 + wg * 8; };
           if ((lane & 7) == 0) {
-            const uint32_t prank = pfc_sm100::cluster_ctarank() ^ 1u;
-            const uint32_t rbar = pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[par * 16 + e]), prank);
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
-              pfc_sm100::st_async_f32(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(hr + u * 4 + sub), prank),
-                                      dot[u], rbar);
+            for (int pr = 1; pr < NC; ++pr) {
+              const uint32_t peer = (me + (uint32_t)pr) % (uint32_t)NC;
+              const uint32_t rbar = pfc_sm100::mapa_shared(pfc_sm100::smem_u32(&mb[par * 16 + e]), peer);
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+                pfc_sm100::st_async_f32(pfc_sm100::mapa_shared(pfc_sm100::smem_u32(slot(me) + u * 4 + sub), peer),
+                                        dot[u], rbar);
+            }
           }
-#if PFC_DW_EXP != 4  // timing probe 4: no wait for the peer's half-dots (wrong values)
+#if PFC_DW_EXP != 4  // timing probe 4: no wait for the peers' partial dots (wrong values)
           pfc_sm100::mbar_wait_cluster(&mb[par * 16 + e], (uint32_t)((it >> 1) & 1));
 #endif
+          // every CTA sums the NC partial dots in rank order: the same center_proj everywhere
 #pragma unroll
-          for (int u = 0; u < 2; ++u) dot[u] += hr[u * 4 + sub];
+          for (int u = 0; u < 2; ++u) {
+            float tot = 0.f;
+#pragma unroll
+            for (int r = 0; r < NC; ++r) tot += r == (int)me ? dot[u] : slot((uint32_t)r)[u * 4 + sub];
+            dot[u] = tot;
+          }
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {

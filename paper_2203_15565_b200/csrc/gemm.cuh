@@ -80,7 +80,7 @@ constexpr int kEpiSmemBytes = 20 * 1024;  // SIMT engine epilogue scratch
 template <int BN, int STAGES, int NWG, class Epi, int CG = 1>
 constexpr int umma_smem_bytes() {
   return 1024 /*align slack*/ + STAGES * (128 * 64 * 2 + (BN / CG) * 64 * 2) + 1024 /*barriers*/ +
-         NWG * Epi::kSmem;
+         NWG * Epi::kSmem + Epi::kExtraSmem;
 }
 
 struct TmemSrc {

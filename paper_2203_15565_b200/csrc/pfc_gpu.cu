@@ -740,18 +740,21 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     const GemmGeom gw = make_geom((int)c->ncols, (int)c->D, (int)B, BN, 1, 1, 128, BKU);
     cudaError_t err;
     if constexpr (kUmma) {
-      if (gw.n_tiles == 2)
-        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true, DwUpdateEpi<true>, 1, OT>(
+      // one cluster CTA per 256-dim block of a class block (tile order n fastest)
+      auto dw = [&](auto nc) {
+        constexpr int NC = decltype(nc)::value;
+        return launch_umma<kBN, PFC_DW_STAGES, 4, false, true, DwUpdateEpi<NC>, 1, OT>(
             c, c->tm_e_k, c->tm_xs_mn, gw,
-            DwUpdateEpi<true>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
-                              c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                              c->st});
-      else
-        err = launch_umma<kBN, PFC_DW_STAGES, 4, false, true, DwUpdateEpi<false>, 1, OT>(
-            c, c->tm_e_k, c->tm_xs_mn, gw,
-            DwUpdateEpi<false>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
-                               c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                               c->st});
+            DwUpdateEpi<NC>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
+                            c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
+                            c->st});
+      };
+      switch (gw.n_tiles) {
+        case 1: err = dw(std::integral_constant<int, 1>{}); break;
+        case 2: err = dw(std::integral_constant<int, 2>{}); break;
+        case 3: err = dw(std::integral_constant<int, 3>{}); break;
+        default: err = dw(std::integral_constant<int, 4>{}); break;
+      }
     } else {
       err = launch_simt<false, true>(c, (const float*)c->G, (int)c->ldg, (const float*)c->xs,
                                      (int)c->Dp, gw, DwStoreEpi{{}, (int)c->ncols, (int)c->D, c->dwt});
@@ -1102,9 +1105,9 @@ int validate_desc(const pfc_gpu_desc* d) {
                 kMaxSamplerLocalShards);
   if (d->precision < PFC_PRECISION_BF16 || d->precision > PFC_PRECISION_TF32)
     return fail(nullptr, PFC_ERR_CONFIG, "pfc_gpu_create: unknown precision %d", d->precision);
-  if (d->precision != PFC_PRECISION_FP32 && (d->dim % 4 != 0 || d->dim > 512))
+  if (d->precision != PFC_PRECISION_FP32 && (d->dim % 4 != 0 || d->dim > 1024))
     return fail(nullptr, PFC_ERR_CONFIG,
-                "pfc_gpu: the tcgen05 paths (bf16, tf32) need dim %% 4 == 0 and dim <= 512 "
+                "pfc_gpu: the tcgen05 paths (bf16, tf32) need dim %% 4 == 0 and dim <= 1024 "
                 "(use PFC_PRECISION_FP32 otherwise)");
   if (d->num_classes >= (int64_t)INT32_MAX)
     return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: num_classes must be < 2^31");

@@ -40,6 +40,25 @@ def test_create_without_gpu_fails_loudly():
         p.CenterShards(p.ShardLayout(100, 1), 8, p.StepConfig(r=0.5), max_batch=8)
 
 
+def test_create_validates_before_touching_a_device():
+    """pfc_gpu_create checks the descriptor before any CUDA call (the reference's error types,
+    and the tensor-core paths' dim limit) -- runnable without a GPU."""
+    if not os.path.exists(p.LIB_PATH):
+        pytest.skip("not built")
+    cfg = p.StepConfig(r=0.1)
+    for prec in (p.PRECISION_BF16, p.PRECISION_TF32):
+        with pytest.raises(p.ConfigError, match="dim <= 1024"):
+            p.CenterShards(p.ShardLayout(1000, 2), 1028, cfg, max_batch=8, precision=prec)
+        with pytest.raises(p.ConfigError, match="dim % 4 == 0"):
+            p.CenterShards(p.ShardLayout(1000, 2), 130, cfg, max_batch=8, precision=prec)
+    with pytest.raises(p.ConfigError, match="unknown precision"):
+        p.CenterShards(p.ShardLayout(1000, 2), 128, cfg, max_batch=8, precision=7)
+    with pytest.raises(p.ContractError, match="max_batch"):
+        p.CenterShards(p.ShardLayout(1000, 2), 128, cfg, max_batch=(1 << 20) + 1)
+    with pytest.raises(p.ContractError, match="sampling ratio"):
+        p.CenterShards(p.ShardLayout(1000, 2), 128, p.StepConfig(r=1.5), max_batch=8)
+
+
 def test_rng_mirror_matches_oracle(port):
     for tag, a, b in [("iteration", 0, 0), ("center-init", 77, 0), ("x", 3, 9)]:
         assert p.make_stream(tag, a, b) == port.make_stream(tag, a, b)

@@ -6,9 +6,9 @@ same ones; they cover the paths the hand-picked cases may miss:
     straddle the batch end);
   * D not a multiple of 64;
   * K = 1..7, r up to 1.0 (full sampling), CosFace / ArcFace / plain margins, the filter.
-bf16 is checked where its contract applies (128 <= D <= 512, no filter: bf16 flips the filter's
-mask decisions within its rounding of tau, and tiny D is a smoke bound only; D > 512 must be
-refused with ConfigError); fp32 everywhere.
+bf16 and tf32 are checked where their contracts apply (128 <= D <= 1024, no filter: the tensor-core
+paths flip the filter's mask decisions within their rounding of tau, and tiny D is a smoke bound
+only; D > 1024 must be refused with ConfigError); fp32 everywhere.
 """
 import json
 import math
@@ -27,7 +27,9 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
-TOL = {p.PRECISION_FP32: (1e-6, 1e-5, 3e-5, 1e-6), p.PRECISION_BF16: (1e-4, 1e-2, 1e-2, 1e-3)}
+TOL = {p.PRECISION_FP32: (1e-6, 1e-5, 3e-5, 1e-6), p.PRECISION_BF16: (1e-4, 1e-2, 1e-2, 1e-3),
+       p.PRECISION_TF32: (2e-5, 1e-3, 2.5e-3, 2e-4)}
+PREC_NAME = {p.PRECISION_FP32: "fp32", p.PRECISION_BF16: "bf16", p.PRECISION_TF32: "tf32"}
 RESULTS = os.path.join(os.path.dirname(os.path.dirname(__file__)), "gpurun_out", "fuzz.jsonl")
 
 
@@ -92,12 +94,12 @@ def test_fuzz_step_matches_oracle(case, port):
         ref = port.step(oracle_cfg(mg, m, r, tau), C_, K, D, W, M, Xs, ls, 1, st)
         refs.append((Xs, ls, st, ref, shards_to_rows(W, C_, K, D), shards_to_rows(M, C_, K, D)))
     precisions = [p.PRECISION_FP32]
-    if D > 512:  # the bf16 path refuses it (dW covers two 256-dim halves); fp32 runs it
-        with pytest.raises(p.ConfigError, match="dim <= 512"):
+    if D > 1024:  # the tensor-core paths refuse it (dW clusters cover four 256-dim blocks)
+        with pytest.raises(p.ConfigError, match="dim <= 1024"):
             make_shards(W0, np.zeros_like(W0), C_, K, D, step_cfg(mg, m, r, tau), B,
                         p.PRECISION_BF16)
     elif D >= 128 and tau is None:
-        precisions.append(p.PRECISION_BF16)
+        precisions += [p.PRECISION_BF16, p.PRECISION_TF32]
     for precision in precisions:
         tl, tdf, tdm, tw = TOL[precision]
         sh = make_shards(W0, np.zeros_like(W0), C_, K, D, step_cfg(mg, m, r, tau), B, precision)
@@ -110,7 +112,7 @@ def test_fuzz_step_matches_oracle(case, port):
                 assert np.array_equal(buf.class_indices, ref["buffers"][k]), (name, step, k)
                 assert buf.num_positives == ref["npos"][k]
             Wd, Md = device_rows(sh, C_, K, D)
-            rec = {"case": name, "precision": "fp32" if precision else "bf16", "step": step,
+            rec = {"case": name, "precision": PREC_NAME[precision], "step": step,
                    "loss_rel": abs(res.loss - ref["loss"]) / abs(ref["loss"]),
                    "dX_fro": rel_fro(res.d_features, ref["dX"]),
                    "dX_maxmax": rel_max(res.d_features, ref["dX"]),

@@ -96,6 +96,10 @@ STEP_CASES = [  # name, C, K, B, D, r, margin, m, tau, steps
     # 256 < D < 512: the second CTA of the dW pair owns a partial dim half
     ("arc_d384_pair", 5000, 2, 96, 384, 0.2, "arcface", 0.5, None, 2),
     ("cos_d260_pair_ragged", 3000, 3, 72, 260, 0.3, "cosface", 0.4, None, 2),
+    # D > 512: dW clusters of 3 / 4 CTAs, one per 256-dim block (the last one partial at D = 1000)
+    ("arc_d768_nc3", 8000, 2, 128, 768, 0.2, "arcface", 0.5, None, 2),
+    ("cos_d1000_nc4_ragged", 6000, 3, 96, 1000, 0.25, "cosface", 0.4, None, 2),
+    ("arc_d1024_nc4", 8000, 2, 128, 1024, 0.2, "arcface", 0.5, None, 1),
     # largest batch class: B = 8191 (odd, > 1024: shared-memory bitonic sort, ragged E rows)
     ("arc_b8191", 60000, 4, 8191, 128, 0.25, "arcface", 0.5, None, 1),
 ]
@@ -105,7 +109,7 @@ TOL = {  # precision -> (loss rel, dX fro, dX max/max, W' max/max)
     p.PRECISION_BF16: (1e-4, 1e-2, 1e-2, 1e-3),
     # tcgen05 kind::tf32 on operands pre-rounded to tf32 (10-bit mantissa): the north star's
     # 1e-3 on gradients holds on tensor cores (measured worst: dX fro 8.4e-4, max/max 1.2e-3)
-    p.PRECISION_TF32: (2e-5, 1e-3, 2.5e-3, 1e-4),
+    p.PRECISION_TF32: (2e-5, 1e-3, 2.5e-3, 2e-4),
 }
 PREC_NAME = {p.PRECISION_FP32: "fp32", p.PRECISION_BF16: "bf16", p.PRECISION_TF32: "tf32"}
 # bf16 operands perturb each logit by ~s * 2^-9 / sqrt(D) and each update by the same

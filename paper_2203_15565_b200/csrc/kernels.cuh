@@ -193,7 +193,8 @@ __global__ void gather_w_kernel(const float* __restrict__ W, int D, int Dp,
 // the rows of one slice, loads batched 8 deep, one fp32/fp64 running sum per thread), then the
 // kSliceGroups partials are added in ascending g in fp64.  One launch replaces the former
 // slices -> segments -> row kernels.
-constexpr int kRowsPerBlk = 16, kSliceGroups = 16;  // 256 threads
+constexpr int kRowsPerBlk = 16, kSliceGroups = 64;  // 1024 threads: ~T / 64 loads per thread
+constexpr int kStatsThreads = kRowsPerBlk * kSliceGroups;
 template <typename ST>
 __device__ __forceinline__ double row_slice_sum(const ST* __restrict__ ps, int T, int B, int b0,
                                                 double* red /* [kSliceGroups][kRowsPerBlk] */) {
@@ -223,7 +224,7 @@ __device__ __forceinline__ double row_slice_sum(const ST* __restrict__ ps, int T
 
 // Rank-local row sums for the cross-rank exchange (world > 1): ls[b] = sum over this rank's slices.
 template <typename ST>
-__global__ void __launch_bounds__(256) local_sums_kernel(const ST* __restrict__ ps, int T, int B,
+__global__ void __launch_bounds__(kStatsThreads) local_sums_kernel(const ST* __restrict__ ps, int T, int B,
                                                          ST* __restrict__ ls) {
   pdl_entry();
   __shared__ double red[kSliceGroups * kRowsPerBlk];
@@ -259,7 +260,7 @@ __global__ void row_offset_kernel(const float* __restrict__ part_m, int T, int B
 // (row_slice_sum).  A block owns kRowsPerBlk rows; the last block to finish reduces loss_row in
 // a fixed order into the step's loss.
 template <typename ST>
-__global__ void __launch_bounds__(256) finalize_stats_kernel(
+__global__ void __launch_bounds__(kStatsThreads) finalize_stats_kernel(
     const ST* __restrict__ ls, int R, const ST* __restrict__ ps, int T, int B,
     const double* __restrict__ zpos, const double* __restrict__ cpos,
     const float* __restrict__ epos, const int32_t* __restrict__ pos_col,

@@ -661,7 +661,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   ST* ls = static_cast<ST*>(c->ls);
   const unsigned nrb = (unsigned)ceil_div(B, kRowsPerBlk);
   if (c->R > 1) {  // the rank-local sums are exchanged; with one rank finalize forms them
-    CUDA_TRY(c, klaunch(c, local_sums_kernel<ST>, dim3(nrb), dim3(256), 0, s, ps, T, (int)B,
+    CUDA_TRY(c, klaunch(c, local_sums_kernel<ST>, dim3(nrb), dim3(kStatsThreads), 0, s, ps, T, (int)B,
                         ls + c->rank * B));
     const CommDt dt = sizeof(ST) == 8 ? kF64 : kF32;
     COMM_TRY(comm_all_gather(c, ls + c->rank * B, ls, B, dt, s));
@@ -670,7 +670,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   }
   ST* rsc = static_cast<ST*>(c->rowscale);
   ST* dlt = static_cast<ST*>(c->delta);
-  CUDA_TRY(c, klaunch(c, finalize_stats_kernel<ST>, dim3(nrb), dim3(256), 0, s, (const ST*)ls,
+  CUDA_TRY(c, klaunch(c, finalize_stats_kernel<ST>, dim3(nrb), dim3(kStatsThreads), 0, s, (const ST*)ls,
                       (int)c->R, (const ST*)(c->R > 1 ? nullptr : ps), T, (int)B,
                       (const double*)c->zpos, (const double*)c->cpos, (const float*)c->epos,
                       (const int32_t*)c->pos_col, (const int*)c->hasval, filt ? 1 : 0, c->mg,

@@ -81,6 +81,9 @@ CASES = [  # name, C, K, D, B, precision, flags, extra
     ("bf16_filter", 10000, 2, 256, 192, p.PRECISION_BF16, 0,
      {"margin": "cosface", "m": 0.4, "r": 0.3, "tau": 0.1}),
     ("bf16_full_fc", 6000, 4, 128, 96, p.PRECISION_BF16, 0, {"margin": "cosface", "m": 0.4, "r": 1.0}),
+    ("tf32_d512_graph", 20000, 2, 512, 256, p.PRECISION_TF32, 0, {}),
+    ("bf16_d768_nc3", 8000, 2, 768, 128, p.PRECISION_BF16, 0, {}),
+    ("tf32_d1000_nc4_eager", 6000, 3, 1000, 96, p.PRECISION_TF32, p.FLAG_NO_GRAPH, {}),
     ("fp32_graph", 9000, 3, 256, 96, p.PRECISION_FP32, 0, {}),
     ("fp32_eager_d200", 7001, 3, 200, 77, p.PRECISION_FP32, p.FLAG_NO_GRAPH, {}),
 ]

@@ -32,7 +32,8 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
-TOL = {p.PRECISION_FP32: (1e-6, 1e-5, 3e-5, 1e-6), p.PRECISION_BF16: (1e-4, 1e-2, 1e-2, 1e-3)}
+TOL = {p.PRECISION_FP32: (1e-6, 1e-5, 3e-5, 1e-6), p.PRECISION_BF16: (1e-4, 1e-2, 1e-2, 1e-3),
+       p.PRECISION_TF32: (2e-5, 1e-3, 2.5e-3, 2e-4)}
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 RESULTS = os.path.join(os.path.dirname(os.path.dirname(__file__)), "gpurun_out", "multirank.jsonl")
 
@@ -67,12 +68,12 @@ def shard_block(W, C_, K, D, k):
         off += n
 
 
-def protocol_bytes(R, B, D, bf16, filt, exact, host):
+def protocol_bytes(R, B, D, f32_stats, filt, exact, host):
     """Closed form of the collectives one step issues (pfc_gpu.cu run_pipeline / step entry
     points), per rank = the larger of send / receive buffer of each call, and the ring model of
     the reference's cost model summed over ranks ((R-1) S per gather / scatter, 2 (R-1) S per
     all-reduce, costmodel.hpp:37-69)."""
-    sb = 4 if bf16 else 8
+    sb = 4 if f32_stats else 8  # the tensor-core modes exchange fp32 statistics, fp32 mode fp64
     calls = [("ag", R * B * sb), ("ar", 8 * B)]          # row sums (rank-major), z_pos
     if filt:
         calls.append(("ar", 4 * B))                      # positive-present flags
@@ -93,6 +94,8 @@ CASES = [  # name, C, K, D, B, r, margin, s, m, tau, precision, R list
     ("cos_filter_fp32", 12000, 4, 256, 128, 0.3, "cosface", 64.0, 0.4, 0.08, p.PRECISION_FP32, (2, 4)),
     ("cos_s256_exact", 16000, 4, 256, 128, 0.2, "cosface", 256.0, 0.4, None, p.PRECISION_FP32, (2, 4)),
     ("full_fc_r1", 6000, 4, 128, 96, 1.0, "cosface", 64.0, 0.4, None, p.PRECISION_BF16, (4,)),
+    ("arc_40k_tf32", 40000, 8, 512, 256, 0.1, "arcface", 64.0, 0.5, None, p.PRECISION_TF32, (2, 8)),
+    ("cos_d768_bf16", 12000, 4, 768, 128, 0.2, "cosface", 64.0, 0.4, None, p.PRECISION_BF16, (2,)),
 ]
 
 
@@ -137,8 +140,8 @@ def test_loopback_ranks_match_oracle(case, port):
         host = run_ranks(R, lambda rk: rank(rk, False))
         dev = run_ranks(R, lambda rk: rank(rk, True))
         exact = s > 64.0
-        nccl_h, wire_h = protocol_bytes(R, B, D, prec == p.PRECISION_BF16, tau is not None, exact, True)
-        nccl_d, wire_d = protocol_bytes(R, B, D, prec == p.PRECISION_BF16, tau is not None, exact, False)
+        nccl_h, wire_h = protocol_bytes(R, B, D, prec != p.PRECISION_FP32, tau is not None, exact, True)
+        nccl_d, wire_d = protocol_bytes(R, B, D, prec != p.PRECISION_FP32, tau is not None, exact, False)
         losses = [h[0][0] for h in host]
         assert len(set(losses)) == 1, losses  # every rank reports the same global loss
         dX = host[0][0][1]

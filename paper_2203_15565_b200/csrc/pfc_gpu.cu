@@ -164,7 +164,7 @@ struct Ctx {
   int32_t* rej = nullptr;     // [nk] a draw of the shard saw a modulo rejection
   long long* oobs = nullptr;  // [2] smallest negative / >= C label of the step (LLONG_MAX: none)
   int64_t nwords = 0;
-  int chunk_words = 1024, nchunk = 1;
+  int chunk_words = 32, nchunk = 1;
   ShardMeta* meta = nullptr;
   int32_t* buf_cls = nullptr;
   int32_t* pos_col = nullptr;
@@ -531,12 +531,14 @@ SamplerArgs sampler_args(Ctx* c, const pfc_gpu_step_args* a, const float* x, con
 // CTA of 1024 threads per SM.
 cudaError_t launch_sampler(Ctx* c, SamplerArgs& sa) {
   const size_t smem = sampler_smem_bytes(c->nchunk, (int)c->nk);
+  const size_t wsmem = walk_smem_bytes((int)c->nk);
   const int smax = (int)sampler_smem_bytes(kMaxSamplerChunks, kMaxSamplerLocalShards);
+  const int wmax = (int)walk_smem_bytes(kMaxSamplerLocalShards);
   const void* fill = c->bf16   ? reinterpret_cast<const void*>(fill_kernel<__nv_bfloat16>)
                      : c->tf32 ? reinterpret_cast<const void*>(fill_kernel<tf32_t>)
                                : reinterpret_cast<const void*>(fill_kernel<float>);
   if (cudaError_t e = ensure_smem_attr(fill, smax)) return e;
-  if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(walk_kernel), smax)) return e;
+  if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(walk_kernel), wmax)) return e;
   const dim3 grid((unsigned)c->num_sms), blk(kSamplerThreads);
   mark_kernel<<<grid, blk, 0, c->stream>>>(sa);
   c->launches++;
@@ -545,7 +547,7 @@ cudaError_t launch_sampler(Ctx* c, SamplerArgs& sa) {
                   : c->tf32 ? klaunch(c, fill_kernel<tf32_t>, grid, blk, smem, c->stream, sa)
                             : klaunch(c, fill_kernel<float>, grid, blk, smem, c->stream, sa);
   if (e != cudaSuccess) return e;
-  return klaunch(c, walk_kernel, grid, blk, smem, c->stream, sa);
+  return klaunch(c, walk_kernel, grid, blk, wsmem, c->stream, sa);
 }
 
 int dx_splits(Ctx* c, int64_t B) {

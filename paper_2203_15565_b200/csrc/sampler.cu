@@ -37,7 +37,7 @@ constexpr int kMaxBatch = 1 << 20;  // global batch rows (pfc_gpu_desc::max_batc
 //      per-step pass over all C classes)
 // Grid-stride loops over one CTA of 1024 threads per SM; the kernels are chained by PDL.
 constexpr int kSamplerThreads = 1024;
-constexpr int kMaxSamplerChunks = 8192;       // chunk prefixes kept in shared memory
+constexpr int kMaxSamplerChunks = 16384;      // chunk prefixes kept in shared memory
 constexpr int kMaxSamplerLocalShards = 2048;  // local shard metadata kept in shared memory
 
 __device__ __forceinline__ int warp_sum_i(int v) {
@@ -53,6 +53,14 @@ __device__ __forceinline__ int bits_below(const uint32_t* bits, const int32_t* b
   const int64_t w = x >> 5;
   const int64_t ch = w / chunk_words;
   int cnt = 0;
+  if (chunk_words == 32) {  // one word per lane: a single round trip
+    const int64_t i = ch * 32 + lane;
+    if (i <= w) {
+      const uint32_t v = bits[i];
+      cnt = __popc(i < w ? v : (v & ((1u << (x & 31)) - 1u)));
+    }
+    return bpre_s[ch] + warp_sum_i(cnt);
+  }
   // 8 independent loads in flight per lane (not one dependent L2 round trip per 32 words)
   int64_t i = ch * chunk_words + lane;
   for (; i + 7 * 32 < w; i += 8 * 32) {
@@ -65,6 +73,22 @@ __device__ __forceinline__ int bits_below(const uint32_t* bits, const int32_t* b
   for (; i < w; i += 32) cnt += __popc(bits[i]);
   if (lane == 0) cnt += __popc(bits[w] & ((1u << (x & 31)) - 1u));
   return bpre_s[ch] + warp_sum_i(cnt);
+}
+
+// bits_below at two points with both loads in flight together (the capacity check's shard
+// bounds); the per-lane counts (<= 32 each) travel packed through one warp sum.
+__device__ __forceinline__ int2 bits_below2(const uint32_t* bits, const int32_t* bpre_s,
+                                            int chunk_words, int64_t x0, int64_t x1, int lane) {
+  if (chunk_words != 32)
+    return make_int2(bits_below(bits, bpre_s, chunk_words, x0, lane),
+                     bits_below(bits, bpre_s, chunk_words, x1, lane));
+  const int64_t w0 = x0 >> 5, w1 = x1 >> 5;
+  const int64_t i0 = (w0 & ~31ll) + lane, i1 = (w1 & ~31ll) + lane;
+  const uint32_t v0 = i0 <= w0 ? bits[i0] : 0u, v1 = i1 <= w1 ? bits[i1] : 0u;
+  const int c0 = __popc(i0 < w0 ? v0 : (v0 & ((1u << (x0 & 31)) - 1u)));
+  const int c1 = __popc(i1 < w1 ? v1 : (v1 & ((1u << (x1 & 31)) - 1u)));
+  const int t = warp_sum_i(c0 | (c1 << 16));
+  return make_int2(bpre_s[w0 >> 5] + (t & 0xffff), bpre_s[w1 >> 5] + (t >> 16));
 }
 
 __device__ int block_exclusive_scan(int v, int* smem_warp, int* total);
@@ -178,6 +202,13 @@ __host__ __device__ constexpr size_t sampler_smem_bytes(int nchunk, int nk) {
   return (size_t)nchunk * sizeof(int32_t) + (size_t)nk * sizeof(ShardMeta);
 }
 
+// walk_kernel: shard metadata, each local shard's offset into the staged positives, and the
+// positives themselves when they fit (kWalkPositives), for pool_value's binary searches
+constexpr int kWalkPositives = 8192;
+__host__ __device__ constexpr size_t walk_smem_bytes(int nk) {
+  return (size_t)nk * (sizeof(ShardMeta) + sizeof(int32_t)) + (size_t)kWalkPositives * sizeof(int32_t);
+}
+
 // Opens the step (thread 0: step_begin) and marks the labels.
 __global__ void __launch_bounds__(kSamplerThreads) mark_kernel(const SamplerArgs a) {
   pdl_entry();
@@ -201,6 +232,39 @@ __global__ void __launch_bounds__(kSamplerThreads) mark_kernel(const SamplerArgs
   for (int64_t kk = tid; kk < a.nk; kk += nthr) a.rej[kk] = 0;
 }
 
+// fill_kernel's second half: positives + positive columns (one warp per label), draws (one
+// thread per draw)
+__device__ __forceinline__ void draw_phase(const SamplerArgs& a, const ShardMeta* meta_s,
+                                           const int32_t* bpre_s, int lane, int64_t gwarp,
+                                           int64_t nwarp, int64_t tid, int64_t nthr) {
+  for (int64_t b = gwarp; b < a.B; b += nwarp) {
+    const int64_t y = a.labs[b];
+    const int k = (int)(y / a.blk);
+    int col = -1;
+    if (k >= a.k0 && k < a.k0 + a.nk) {
+      const int kk = k - a.k0;
+      col = kk * a.cap + (bits_below(a.bits, bpre_s, a.chunk_words, y, lane) - meta_s[kk].ustart);
+      if (lane == 0) a.buf_cls[col] = (int32_t)y;
+    }
+    if (lane == 0) a.pos_col[b] = col;
+  }
+  const int64_t nd = (int64_t)a.nk * a.cap;
+  for (int64_t g = tid; g < nd; g += nthr) {
+    const int kk = (int)(g / a.cap), i = (int)(g % a.cap);
+    const ShardMeta& m = meta_s[kk];
+    if (m.full || i >= m.need) continue;
+    // per-step values from the StepParams block (only mark_kernel's arguments change per step)
+    const uint64_t key = rng_key(a.sp->seed, fork_stream(a.sp->stream, (uint64_t)(a.k0 + kk)));
+    const uint64_t n = (uint64_t)(m.pool - i);
+    const uint64_t r = rng_draw(key, (uint64_t)i + 1);
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % n;  // rng.hpp:69
+    if (r >= limit) a.rej[kk] = 1;
+    const int32_t j = i + (int32_t)(r % n);
+    a.jv[g] = j;
+    a.nxt[g] = atomicExch(&a.head[(int64_t)kk * a.pool_stride + j], i);
+  }
+}
+
 template <typename OT>
 __global__ void __launch_bounds__(kSamplerThreads, 1) fill_kernel(const SamplerArgs a) {
   pdl_entry();
@@ -214,23 +278,23 @@ __global__ void __launch_bounds__(kSamplerThreads, 1) fill_kernel(const SamplerA
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t gwarp = tid >> 5, nwarp = nthr >> 5;
   StepStatus* st = a.st;
-  if (a.normalize) {  // independent of the labels: x^ = x / |x| first
-    const int nw = (int)nwarp;
-    for (int row0 = 0; row0 < a.B; row0 += nw)
-      normalize_x_rows(a.sp->x + (size_t)row0 * a.D, a.B - row0, a.D, a.Dp,
-                       static_cast<OT*>(a.xh) + (size_t)row0 * a.Dp, a.xnorm + row0,
-                       (int)blockIdx.x);
-  }
-  // ---- chunk prefixes, validation, capacity, local shard metadata (every CTA)
+  // ---- chunk prefixes (each thread a run of up to 16 consecutive chunks, one block scan),
+  // validation, capacity, local shard metadata (every CTA)
   {
-    int carry = 0;
-    for (int base = 0; base < a.nchunk; base += blockDim.x) {
-      const int i = base + (int)threadIdx.x;
-      const int t = i < a.nchunk ? a.ccnt[i] : 0;
-      int tot = 0;
-      const int ex = block_exclusive_scan(t, warp_tmp, &tot);
-      if (i < a.nchunk) bpre_s[i] = carry + ex;
-      carry += tot;
+    const int per = (a.nchunk + kSamplerThreads - 1) / kSamplerThreads;
+    const int i0 = (int)threadIdx.x * per;
+    int v[kMaxSamplerChunks / kSamplerThreads];
+    int run = 0;
+#pragma unroll
+    for (int u = 0; u < kMaxSamplerChunks / kSamplerThreads; ++u) {
+      v[u] = (u < per && i0 + u < a.nchunk) ? a.ccnt[i0 + u] : 0;
+      run += v[u];
+    }
+    int ex = block_exclusive_scan(run, warp_tmp, nullptr);
+#pragma unroll
+    for (int u = 0; u < kMaxSamplerChunks / kSamplerThreads; ++u) {
+      if (u < per && i0 + u < a.nchunk) bpre_s[i0 + u] = ex;
+      ex += v[u];
     }
   }
   if (threadIdx.x == 0) bad_shard_s = a.K;
@@ -242,8 +306,8 @@ __global__ void __launch_bounds__(kSamplerThreads, 1) fill_kernel(const SamplerA
     // capacity checks for ALL shards, one warp per shard; the first failing shard wins
     for (int k = wib; k < a.K; k += blockDim.x >> 5) {
       const int64_t lo = min((int64_t)k * a.blk, a.C), hi = min((int64_t)(k + 1) * a.blk, a.C);
-      const int plo = bits_below(a.bits, bpre_s, a.chunk_words, lo, lane);
-      const int np = bits_below(a.bits, bpre_s, a.chunk_words, hi, lane) - plo;
+      const int2 pb = bits_below2(a.bits, bpre_s, a.chunk_words, lo, hi, lane);
+      const int plo = pb.x, np = pb.y - pb.x;
       if (np > a.cap || hi - lo < a.cap) {
         if (lane == 0) atomicMin(&bad_shard_s, k);
       } else if (k >= a.k0 && k < a.k0 + a.nk && lane == 0) {
@@ -281,33 +345,13 @@ __global__ void __launch_bounds__(kSamplerThreads, 1) fill_kernel(const SamplerA
     if (ok)
       for (int kk = threadIdx.x; kk < a.nk; kk += blockDim.x) a.meta[kk] = meta_s[kk];
   }
-  if (!ok) return;
-  // ---- positives + positive columns (one warp per label), draws (one thread per draw)
-  for (int64_t b = gwarp; b < a.B; b += nwarp) {
-    const int64_t y = a.labs[b];
-    const int k = (int)(y / a.blk);
-    int col = -1;
-    if (k >= a.k0 && k < a.k0 + a.nk) {
-      const int kk = k - a.k0;
-      col = kk * a.cap + (bits_below(a.bits, bpre_s, a.chunk_words, y, lane) - meta_s[kk].ustart);
-      if (lane == 0) a.buf_cls[col] = (int32_t)y;
-    }
-    if (lane == 0) a.pos_col[b] = col;
-  }
-  const int64_t nd = (int64_t)a.nk * a.cap;
-  for (int64_t g = tid; g < nd; g += nthr) {
-    const int kk = (int)(g / a.cap), i = (int)(g % a.cap);
-    const ShardMeta& m = meta_s[kk];
-    if (m.full || i >= m.need) continue;
-    // per-step values from the StepParams block (only mark_kernel's arguments change per step)
-    const uint64_t key = rng_key(a.sp->seed, fork_stream(a.sp->stream, (uint64_t)(a.k0 + kk)));
-    const uint64_t n = (uint64_t)(m.pool - i);
-    const uint64_t r = rng_draw(key, (uint64_t)i + 1);
-    const uint64_t limit = UINT64_MAX - UINT64_MAX % n;  // rng.hpp:69
-    if (r >= limit) a.rej[kk] = 1;
-    const int32_t j = i + (int32_t)(r % n);
-    a.jv[g] = j;
-    a.nxt[g] = atomicExch(&a.head[(int64_t)kk * a.pool_stride + j], i);
+  if (ok) draw_phase(a, meta_s, bpre_s, lane, gwarp, nwarp, tid, nthr);
+  if (a.normalize) {  // x^ = x / |x| last: only the GEMMs after the sampler read it
+    const int nw = (int)nwarp;
+    for (int row0 = 0; row0 < a.B; row0 += nw)
+      normalize_x_rows(a.sp->x + (size_t)row0 * a.D, a.B - row0, a.D, a.Dp,
+                       static_cast<OT*>(a.xh) + (size_t)row0 * a.Dp, a.xnorm + row0,
+                       (int)blockIdx.x);
   }
 }
 
@@ -316,6 +360,9 @@ __global__ void __launch_bounds__(kSamplerThreads) walk_kernel(const SamplerArgs
   pdl_entry();
   extern __shared__ __align__(16) uint8_t sampler_smem[];
   ShardMeta* meta_s = reinterpret_cast<ShardMeta*>(sampler_smem);
+  int32_t* off_s = reinterpret_cast<int32_t*>(sampler_smem + (size_t)a.nk * sizeof(ShardMeta));
+  int32_t* pos_s = off_s + a.nk;
+  __shared__ int warp_tmp[32];
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b = tid; b < a.B; b += nthr) {
@@ -340,6 +387,25 @@ __global__ void __launch_bounds__(kSamplerThreads) walk_kernel(const SamplerArgs
     if (meta_s[kk].reject)  // block-uniform
       sequential_fallback(meta_s[kk], a.cap, a.sp, a.k0, a.pool_stride, a.pool_scratch,
                           a.buf_cls, a.st, kk);
+  // the local shards' positives (fill_kernel wrote them) into shared memory when they fit:
+  // pool_value's binary search then costs no dependent global round trips
+  int npos_all = 0;
+  for (int base = 0; base < a.nk; base += blockDim.x) {
+    const int kk = base + (int)threadIdx.x;
+    int tot = 0;
+    const int ex = block_exclusive_scan(kk < a.nk ? meta_s[kk].npos : 0, warp_tmp, &tot);
+    if (kk < a.nk) off_s[kk] = npos_all + ex;
+    npos_all += tot;
+  }
+  const bool staged = npos_all <= kWalkPositives;
+  if (staged) {
+    const int lane = threadIdx.x & 31;
+    for (int kk = threadIdx.x >> 5; kk < a.nk; kk += blockDim.x >> 5) {
+      const int32_t* src = a.buf_cls + (int64_t)kk * a.cap;
+      for (int i = lane; i < meta_s[kk].npos; i += 32) pos_s[off_s[kk] + i] = src[i];
+    }
+  }
+  __syncthreads();
   const int64_t nd = (int64_t)a.nk * a.cap;
   for (int64_t g = tid; g < nd; g += nthr) {
     const int kk = (int)(g / a.cap), i = (int)(g % a.cap);
@@ -363,7 +429,7 @@ __global__ void __launch_bounds__(kSamplerThreads) walk_kernel(const SamplerArgs
       }
       p = pp;
     }
-    row[m.npos + i] = (int32_t)pool_value(m.lo, row, m.npos, p);
+    row[m.npos + i] = (int32_t)pool_value(m.lo, staged ? pos_s + off_s[kk] : row, m.npos, p);
   }
 }
 

@@ -89,6 +89,9 @@ typedef struct {
                                                 (pfc_gpu_debug_logits) */
 #define PFC_FLAG_NO_PDL 32                   /* launch the step's kernels without programmatic
                                                 dependent launch (A/B timing) */
+#define PFC_FLAG_WIDE_SAMPLER_CHUNKS 64      /* test hook: 1024-word label-bitmap chunks (the
+                                                sampler's multi-word rank path, used by default
+                                                only past 16.7M classes) */
 #define PFC_FLAG_GUARD 16                    /* test hook: every device buffer of the context
                                                 sits between two 4 KB guard regions filled with
                                                 a pattern; pfc_gpu_check_guards reports any

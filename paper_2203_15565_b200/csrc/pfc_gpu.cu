@@ -1355,6 +1355,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->M, (size_t)std::max<int64_t>(c->rows, 1) * c->D));
   CT(dalloc(c, &c->labels, (size_t)B));
   c->nwords = c->C / 32 + 1;  // covers bit C itself: bits_below(C) is the total count
+  if (c->d.flags & PFC_FLAG_WIDE_SAMPLER_CHUNKS) c->chunk_words = 1024;
   while (ceil_div(c->nwords, c->chunk_words) > kMaxSamplerChunks) c->chunk_words *= 2;
   c->nchunk = (int)ceil_div(c->nwords, c->chunk_words);
   CT(dalloc(c, &c->labs, (size_t)B));

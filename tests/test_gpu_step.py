@@ -43,15 +43,18 @@ def test_bench_inputs_match_oracle(port):
         np.testing.assert_allclose(x.cpu().numpy(), X.T.astype(np.float32), rtol=1e-6, atol=1e-6)
 
 
-@pytest.mark.parametrize("name", ["cpu_ref_10k", "glint360k_k8", "glint360k_k1", "webface2m_k8",
-                                  "webface2m_k1", "fullfc_360k_k8", "stress10m_k8"])
-def test_sampler_bit_exact_baseline_configs(name, port):
-    """build_buffers parity (order included) on all BASELINE configs, two steps each."""
+@pytest.mark.parametrize("name,flags", [(n, 0) for n in [
+    "cpu_ref_10k", "glint360k_k8", "glint360k_k1", "webface2m_k8", "webface2m_k1",
+    "fullfc_360k_k8", "stress10m_k8"]] + [("webface2m_k8", p.FLAG_WIDE_SAMPLER_CHUNKS),
+                                          ("stress10m_k8", p.FLAG_WIDE_SAMPLER_CHUNKS)])
+def test_sampler_bit_exact_baseline_configs(name, flags, port):
+    """build_buffers parity (order included) on all BASELINE configs, two steps each (and with
+    the 1024-word bitmap chunks the sampler switches to past 16.7M classes)."""
     entries = [e for e in golden("sampler.json")["baseline"] if e["name"] == name]
     e0 = entries[0]
     C_, K, B, r = e0["C"], e0["K"], e0["B"], e0["r"]
     D = 64  # sampling does not depend on D; keeps W small at 10M classes
-    sh = p.CenterShards(p.ShardLayout(C_, K), D, p.StepConfig(r=r), max_batch=B)
+    sh = p.CenterShards(p.ShardLayout(C_, K), D, p.StepConfig(r=r), max_batch=B, flags=flags)
     sh.init_center_shards(1)
     x = torch.empty(B, D, device="cuda")
     lab = torch.empty(B, dtype=torch.int64, device="cuda")
@@ -72,7 +75,7 @@ def test_sampler_small_and_forced_sequential(port):
         if "error" in e or e["B"] == 0:
             continue
         C_, K, B, r = e["C"], e["K"], e["B"], e["r"]
-        for flags in (0, p.FLAG_FORCE_SEQUENTIAL_SAMPLER):
+        for flags in (0, p.FLAG_FORCE_SEQUENTIAL_SAMPLER, p.FLAG_WIDE_SAMPLER_CHUNKS):
             sh = p.CenterShards(p.ShardLayout(C_, K), 8, p.StepConfig(r=r), max_batch=max(B, 1),
                                 flags=flags)
             sh.init_center_shards(1)

@@ -46,7 +46,12 @@ typedef enum {
 typedef enum { /* MarginKind, margin.hpp:11 */
   PFC_MARGIN_PLAIN = 0,
   PFC_MARGIN_ADDITIVE_COSINE = 1, /* CosFace-style */
-  PFC_MARGIN_ADDITIVE_ANGULAR = 2 /* ArcFace-style */
+  PFC_MARGIN_ADDITIVE_ANGULAR = 2, /* ArcFace-style */
+  PFC_MARGIN_COMBINED = 3          /* extension, not a reference MarginKind: the combined margin
+                                      s (cos(m1 theta + m2) - m3) on the positive, s cos elsewhere
+                                      (m2 = margin_m; m1 = margin_m1 in (0, 2], m3 = margin_m3 in
+                                      [0, 1); theta = acos of the cosine clamped like ArcFace).
+                                      (1, m, 0) is ArcFace and (1, 0, m) CosFace up to the clamp */
 } pfc_margin_kind;
 
 typedef enum {
@@ -78,6 +83,8 @@ typedef struct {
   const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from pfc_gpu_nccl_unique_id (world_size > 1),
                               or a loopback id from pfc_gpu_loopback_id */
   int32_t flags;           /* PFC_FLAG_* */
+  double margin_m1;        /* PFC_MARGIN_COMBINED only (ignored otherwise): angular factor m1 */
+  double margin_m3;        /* PFC_MARGIN_COMBINED only (ignored otherwise): cosine margin m3 */
 } pfc_gpu_desc;
 
 #define PFC_FLAG_FORCE_SEQUENTIAL_SAMPLER 1 /* test hook: always use the exact sequential FY */
@@ -153,6 +160,8 @@ typedef struct {
   double filter_threshold;
   double momentum;
   double weight_decay;
+  double margin_m1;  /* PFC_MARGIN_COMBINED only */
+  double margin_m3;
 } pfc_gpu_step_config;
 int pfc_gpu_set_step_config(void* ctx, const pfc_gpu_step_config* cfg);
 

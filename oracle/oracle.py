@@ -36,11 +36,12 @@ class StepCfgC(C.Structure):
     _fields_ = [("r", C.c_double), ("margin_kind", C.c_int32), ("margin_scale", C.c_double),
                 ("margin_m", C.c_double), ("has_filter", C.c_int32),
                 ("filter_threshold", C.c_double), ("lr", C.c_double), ("momentum", C.c_double),
-                ("weight_decay", C.c_double), ("step_index", C.c_int64)]
+                ("weight_decay", C.c_double), ("step_index", C.c_int64),
+                ("margin_m1", C.c_double), ("margin_m3", C.c_double)]
 
 
 MARGIN_KINDS = {"plain": 0, "cosface": 1, "additive_cosine": 1, "arcface": 2,
-                "additive_angular": 2}
+                "additive_angular": 2, "combined": 3}  # combined: extension (pfc_oracle.c MK_COMB)
 
 
 @dataclass
@@ -54,12 +55,15 @@ class OracleCfg:
     momentum: float = 0.9
     weight_decay: float = 5e-4
     step_index: int = -1
+    m1: float = 1.0  # combined margin only (m = m2)
+    m3: float = 0.0
 
     def c(self) -> StepCfgC:
         return StepCfgC(self.r, MARGIN_KINDS[self.margin], self.scale, self.m,
                         0 if self.filter_threshold is None else 1,
                         0.0 if self.filter_threshold is None else self.filter_threshold,
-                        self.lr, self.momentum, self.weight_decay, self.step_index)
+                        self.lr, self.momentum, self.weight_decay, self.step_index, self.m1,
+                        self.m3)
 
 
 def _ptr(a: np.ndarray | None):
@@ -113,6 +117,8 @@ class Oracle:
             self._f("bench_inputs", None, [i64, i64, i64, u64, u64, vp, vp])
             self._f("apply_margin", dbl, [dbl, C.c_int, C.c_int, dbl, dbl])
             self._f("margin_derivative", dbl, [dbl, C.c_int, C.c_int, dbl, dbl])
+            self._f("apply_margin_combined", dbl, [dbl, C.c_int, dbl, dbl, dbl, dbl])
+            self._f("margin_derivative_combined", dbl, [dbl, C.c_int, dbl, dbl, dbl])
 
     def _f(self, name, res, args):
         fn = getattr(self.lib, self.p + name)

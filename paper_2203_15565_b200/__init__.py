@@ -114,14 +114,18 @@ class SeededRng:
 
 # ----------------------------------------------------------------------------- config types
 PLAIN, ADDITIVE_COSINE, ADDITIVE_ANGULAR = 0, 1, 2
+COMBINED = 3  # extension (PFC_MARGIN_COMBINED): not a reference MarginKind
 
 
 @dataclass(frozen=True)
 class MarginConfig:
-    """margin.hpp:17-37"""
+    """margin.hpp:17-37.  COMBINED (an extension beyond the reference) adds m1 and m3:
+    s (cos(m1 theta + margin) - m3) on the positive entry; m1 / m3 are ignored otherwise."""
     kind: int = ADDITIVE_COSINE
     scale: float = 64.0
     margin: float = 0.4
+    m1: float = 1.0
+    m3: float = 0.0
 
     @staticmethod
     def plain() -> "MarginConfig":
@@ -135,6 +139,13 @@ class MarginConfig:
     def arcface_style(s: float = 64.0, m: float = 0.5) -> "MarginConfig":
         return MarginConfig(ADDITIVE_ANGULAR, s, m)
 
+    @staticmethod
+    def combined(s: float = 64.0, m1: float = 1.0, m2: float = 0.3,
+                 m3: float = 0.2) -> "MarginConfig":
+        """The combined (m1, m2, m3) margin; (1, m, 0) is ArcFace, (1, 0, m) CosFace up to the
+        ArcFace clamp of the cosine."""
+        return MarginConfig(COMBINED, s, m2, m1, m3)
+
     def validate(self) -> None:
         if not self.scale > 0.0:
             raise ConfigError("margin: scale must be positive")
@@ -142,6 +153,10 @@ class MarginConfig:
             raise ConfigError("margin: m must be in [0, 1)")
         if self.kind == PLAIN and (self.scale != 1.0 or self.margin != 0.0):
             raise ConfigError("margin: plain kind requires s=1, m=0")
+        if self.kind == COMBINED and not 0.0 < self.m1 <= 2.0:
+            raise ConfigError("margin: m1 must be in (0, 2]")
+        if self.kind == COMBINED and not 0.0 <= self.m3 < 1.0:
+            raise ConfigError("margin: m3 must be in [0, 1)")
 
 
 @dataclass
@@ -252,14 +267,16 @@ class Desc(C.Structure):
                 ("has_filter", C.c_int32), ("filter_threshold", C.c_double),
                 ("momentum", C.c_double), ("weight_decay", C.c_double),
                 ("precision", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32),
-                ("world_size", C.c_int32), ("nccl_id", C.c_void_p), ("flags", C.c_int32)]
+                ("world_size", C.c_int32), ("nccl_id", C.c_void_p), ("flags", C.c_int32),
+                ("margin_m1", C.c_double), ("margin_m3", C.c_double)]
 
 
 class StepConfigC(C.Structure):
     _fields_ = [("r", C.c_double), ("margin_kind", C.c_int32), ("margin_scale", C.c_double),
                 ("margin_m", C.c_double), ("has_filter", C.c_int32),
                 ("filter_threshold", C.c_double), ("momentum", C.c_double),
-                ("weight_decay", C.c_double)]
+                ("weight_decay", C.c_double), ("margin_m1", C.c_double),
+                ("margin_m3", C.c_double)]
 
 
 class StepArgs(C.Structure):
@@ -387,7 +404,8 @@ class CenterShards:
                  cfg.margin.scale, cfg.margin.margin, 0 if cfg.filter_threshold is None else 1,
                  0.0 if cfg.filter_threshold is None else cfg.filter_threshold, cfg.momentum,
                  cfg.weight_decay, precision, device, rank, world_size,
-                 C.cast(self._nccl_id, C.c_void_p) if self._nccl_id else None, flags)
+                 C.cast(self._nccl_id, C.c_void_p) if self._nccl_id else None, flags,
+                 cfg.margin.m1, cfg.margin.m3)
         h = C.c_void_p()
         _check(lib.pfc_gpu_create(C.byref(d), C.byref(h)), None)
         self._h = h
@@ -452,7 +470,7 @@ class CenterShards:
         sc = StepConfigC(cfg.r, cfg.margin.kind, cfg.margin.scale, cfg.margin.margin,
                          0 if cfg.filter_threshold is None else 1,
                          0.0 if cfg.filter_threshold is None else cfg.filter_threshold,
-                         cfg.momentum, cfg.weight_decay)
+                         cfg.momentum, cfg.weight_decay, cfg.margin.m1, cfg.margin.m3)
         _check(load_library().pfc_gpu_set_step_config(self._h, C.byref(sc)), self._h)
         self.cfg = StepConfig(r=cfg.r, margin=cfg.margin, filter_threshold=cfg.filter_threshold,
                               momentum=cfg.momentum, weight_decay=cfg.weight_decay, lr=cfg.lr)

@@ -91,12 +91,13 @@ struct ShardMeta {        // per local shard
   int32_t reject;         // 1 -> a modulo rejection happened: sequential fallback
 };
 
-enum MarginKindDev : int { kPlain = 0, kAddCos = 1, kAddAng = 2 };
+enum MarginKindDev : int { kPlain = 0, kAddCos = 1, kAddAng = 2, kComb = 3 };
 
 struct MarginDev {
   int kind;
   float s;       // scale (1 for plain)
   double sd, md; // scale, margin in fp64 for the positive logit
+  double m1d, m3d;  // combined margin (kComb): s (cos(m1 theta + m) - m3); 1 and 0 otherwise
   float off;     // fixed softmax offset o = max(0, s - 40): exp(z - o) never overflows (z <= s)
   double offd;
 };
@@ -109,6 +110,7 @@ __device__ __forceinline__ double margin_pos(const MarginDev& mg, double c) {
   if (mg.kind == kAddCos) return mg.sd * (c - mg.md);
   const double lo = -1.0 + kAngularClamp, hi = 1.0 - kAngularClamp;
   const double cc = c < lo ? lo : (hi < c ? hi : c);
+  if (mg.kind == kComb) return mg.sd * (cos(mg.m1d * acos(cc) + mg.md) - mg.m3d);
   return mg.sd * cos(acos(cc) + mg.md);
 }
 // margin_derivative for the positive entry (margin.hpp:58-72).
@@ -117,6 +119,7 @@ __device__ __forceinline__ double margin_deriv_pos(const MarginDev& mg, double c
   if (mg.kind == kAddCos) return mg.sd;
   if (c <= -1.0 + kAngularClamp || c >= 1.0 - kAngularClamp) return 0.0;
   const double th = acos(c);
+  if (mg.kind == kComb) return mg.sd * mg.m1d * sin(mg.m1d * th + mg.md) / sqrt(1.0 - c * c);
   return mg.sd * sin(th + mg.md) / sqrt(1.0 - c * c);
 }
 

@@ -1005,6 +1005,9 @@ void set_margin_state(Ctx* c) {
   c->mg.s = (float)c->d.margin_scale;
   c->mg.sd = c->d.margin_scale;
   c->mg.md = c->d.margin_m;
+  const bool comb = c->d.margin_kind == PFC_MARGIN_COMBINED;
+  c->mg.m1d = comb ? c->d.margin_m1 : 1.0;
+  c->mg.m3d = comb ? c->d.margin_m3 : 0.0;
   c->mg.offd = std::max(0.0, c->d.margin_scale - 40.0);  // E = exp(z - o) <= e^40
   c->mg.off = (float)c->mg.offd;
   c->exact = c->d.margin_scale > kFixedOffsetMaxScale || (c->d.flags & PFC_FLAG_EXACT_SOFTMAX);
@@ -1091,8 +1094,14 @@ int validate_desc(const pfc_gpu_desc* d) {
     return fail(nullptr, PFC_ERR_CONFIG, "margin: m must be in [0, 1)");
   if (d->margin_kind == PFC_MARGIN_PLAIN && (d->margin_scale != 1.0 || d->margin_m != 0.0))
     return fail(nullptr, PFC_ERR_CONFIG, "margin: plain kind requires s=1, m=0");
-  if (d->margin_kind < 0 || d->margin_kind > 2)
+  if (d->margin_kind < 0 || d->margin_kind > 3)
     return fail(nullptr, PFC_ERR_CONTRACT, "apply_margin: unknown kind");
+  if (d->margin_kind == PFC_MARGIN_COMBINED) {  // extension (pfc_gpu.h)
+    if (!(d->margin_m1 > 0.0 && d->margin_m1 <= 2.0))
+      return fail(nullptr, PFC_ERR_CONFIG, "margin: m1 must be in (0, 2]");
+    if (!(d->margin_m3 >= 0.0 && d->margin_m3 < 1.0))
+      return fail(nullptr, PFC_ERR_CONFIG, "margin: m3 must be in [0, 1)");
+  }
   if (d->dim < 1) return fail(nullptr, PFC_ERR_SHAPE, "pfc_gpu_create: dim must be >= 1");
   if (d->max_batch < 1 || d->max_batch > kMaxBatch)
     return fail(nullptr, PFC_ERR_CONTRACT, "pfc_gpu_create: max_batch must be in [1, %d]",
@@ -1450,6 +1459,8 @@ int pfc_gpu_set_step_config(void* ctx, const pfc_gpu_step_config* sc) {
   d.margin_kind = sc->margin_kind;
   d.margin_scale = sc->margin_scale;
   d.margin_m = sc->margin_m;
+  d.margin_m1 = sc->margin_m1;
+  d.margin_m3 = sc->margin_m3;
   d.has_filter = sc->has_filter ? 1 : 0;
   d.filter_threshold = sc->has_filter ? sc->filter_threshold : 0.0;
   d.momentum = sc->momentum;
@@ -1457,7 +1468,8 @@ int pfc_gpu_set_step_config(void* ctx, const pfc_gpu_step_config* sc) {
   if (int rc = validate_desc(&d)) return fail(c, rc, "%s", g_create_error.c_str());
   const pfc_gpu_desc& o = c->d;
   if (d.r == o.r && d.margin_kind == o.margin_kind && d.margin_scale == o.margin_scale &&
-      d.margin_m == o.margin_m && d.has_filter == o.has_filter &&
+      d.margin_m == o.margin_m && d.margin_m1 == o.margin_m1 && d.margin_m3 == o.margin_m3 &&
+      d.has_filter == o.has_filter &&
       d.filter_threshold == o.filter_threshold && d.momentum == o.momentum &&
       d.weight_decay == o.weight_decay)
     return PFC_OK;

@@ -224,3 +224,40 @@ def test_mics_matches_reference_golden(port, golden_dir):
         assert port.mics(cs["C"], cs["K"], cs["D"], W).tolist() == cs["mics"], cs["name"]
     with pytest.raises(OracleError, match="mics: needs at least two classes"):
         port.mics(1, 1, 4, port.init_centers(1, 1, 4, 1))
+
+
+def test_combined_margin_identities(port):
+    """The combined-margin extension (pfc_oracle.c MK_COMB) is pinned to the reference's own
+    margins through its identities: (1, m, 0) is ArcFace operation for operation (bit-equal,
+    clamp region included) and (1, 0, m) is CosFace up to the ArcFace clamp of the cosine."""
+    for c in (-1.0, -0.999999995, -0.7, -0.1, 0.0, 0.2, 0.55, 0.9999, 1.0):
+        for is_pos in (0, 1):
+            assert port._apply_margin_combined(c, is_pos, 64.0, 1.0, 0.5, 0.0) == \
+                port._apply_margin(c, is_pos, 2, 64.0, 0.5)
+            assert port._margin_derivative_combined(c, is_pos, 64.0, 1.0, 0.5) == \
+                port._margin_derivative(c, is_pos, 2, 64.0, 0.5)
+            if abs(c) < 1.0 - 1e-7:
+                assert port._apply_margin_combined(c, is_pos, 64.0, 1.0, 0.0, 0.4) == \
+                    pytest.approx(port._apply_margin(c, is_pos, 1, 64.0, 0.4), abs=1e-12)
+    # m1 scales the angle: d/dc of s (cos(m1 acos c + m2) - m3) by central differences
+    for c in (-0.6, 0.1, 0.7):
+        h = 1e-6
+        num = (port._apply_margin_combined(c + h, 1, 64.0, 0.9, 0.4, 0.15) -
+               port._apply_margin_combined(c - h, 1, 64.0, 0.9, 0.4, 0.15)) / (2 * h)
+        assert port._margin_derivative_combined(c, 1, 64.0, 0.9, 0.4) == pytest.approx(num, rel=1e-6)
+
+
+def test_combined_margin_step_arcface_point(port):
+    """A whole oracle step with combined (1, 0.5, 0) equals the ArcFace step bit for bit."""
+    from oracle.oracle import OracleCfg
+    C_, K, D, B = 600, 2, 16, 32
+    X, labels = port.bench_inputs(C_, D, B, 1, 0)
+    out = []
+    for cfg in (OracleCfg(r=0.3, margin="arcface", scale=64.0, m=0.5),
+                OracleCfg(r=0.3, margin="combined", scale=64.0, m=0.5, m1=1.0, m3=0.0)):
+        W = port.init_centers(C_, K, D, 1)
+        M = np.zeros_like(W)
+        ref = port.step(cfg, C_, K, D, W, M, X, labels, 1, 7)
+        out.append((ref["loss"], ref["dX"], W))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])

@@ -96,6 +96,10 @@ typedef struct {
                                                 (pfc_gpu_debug_logits) */
 #define PFC_FLAG_NO_PDL 32                   /* launch the step's kernels without programmatic
                                                 dependent launch (A/B timing) */
+#define PFC_FLAG_FORCE_COLLECTIVES 128     /* test hook: world_size 1 still runs every collective
+                                                of the N > 1 path, through a 1-rank group
+                                                (nccl_id: a real ncclUniqueId, or a loopback
+                                                id): real NCCL calls on a one-GPU box */
 #define PFC_FLAG_WIDE_SAMPLER_CHUNKS 64      /* test hook: 1024-word label-bitmap chunks (the
                                                 sampler's multi-word rank path, used by default
                                                 only past 16.7M classes) */

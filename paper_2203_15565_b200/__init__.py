@@ -294,7 +294,7 @@ class StepOut(C.Structure):
 
 PRECISION_BF16, PRECISION_FP32, PRECISION_TF32 = 0, 1, 2
 FLAG_FORCE_SEQUENTIAL_SAMPLER, FLAG_NO_GRAPH, FLAG_EXACT_SOFTMAX, FLAG_DEBUG_LOGITS = 1, 2, 4, 8
-FLAG_GUARD, FLAG_NO_PDL, FLAG_WIDE_SAMPLER_CHUNKS = 16, 32, 64
+FLAG_GUARD, FLAG_NO_PDL, FLAG_WIDE_SAMPLER_CHUNKS, FLAG_FORCE_COLLECTIVES = 16, 32, 64, 128
 
 _lib = None
 

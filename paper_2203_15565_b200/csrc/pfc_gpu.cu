@@ -145,6 +145,7 @@ struct Ctx {
   int64_t C, D, K, Dp, blk, cap, k0, nk, cls_lo, cls_hi, rows, ncols, ncols_pad, ldg;
   int64_t pool_stride, maxB;
   int R, rank;
+  bool coll = false;  // R > 1, or PFC_FLAG_FORCE_COLLECTIVES: the collectives run (1-rank group)
   bool bf16;          // tcgen05 kind::f16 engine (bf16 operands)
   bool tf32 = false;  // tcgen05 kind::tf32 engine (fp32 operands)
   bool umma = false;  // either tcgen05 engine (else the fp32 SIMT validation engine)
@@ -634,7 +635,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     CUDA_TRY(c, err);
     CUDA_TRY(c, klaunch(c, row_offset_kernel, dim3((unsigned)ceil_div(B, bs)), dim3(bs), 0, s,
                         pm, gf.n_tiles * NWG, (int)B, c->pos_col, c->zpos, c->mg, c->offr));
-    if (c->R > 1) COMM_TRY(comm_all_reduce(c, c->offr, c->offr, B, kF32, kMax, s));
+    if (c->coll) COMM_TRY(comm_all_reduce(c, c->offr, c->offr, B, kF32, kMax, s));
     phase(c, "row_offsets");
   }
   const float* offr = exact ? c->offr : nullptr;
@@ -662,7 +663,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const int T = gf.n_tiles * NWG;
   ST* ls = static_cast<ST*>(c->ls);
   const unsigned nrb = (unsigned)ceil_div(B, kRowsPerBlk);
-  if (c->R > 1) {  // the rank-local sums are exchanged; with one rank finalize forms them
+  if (c->coll) {  // the rank-local sums are exchanged; with one rank finalize forms them
     CUDA_TRY(c, klaunch(c, local_sums_kernel<ST>, dim3(nrb), dim3(kStatsThreads), 0, s, ps, T, (int)B,
                         ls + c->rank * B));
     const CommDt dt = sizeof(ST) == 8 ? kF64 : kF32;
@@ -673,7 +674,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   ST* rsc = static_cast<ST*>(c->rowscale);
   ST* dlt = static_cast<ST*>(c->delta);
   CUDA_TRY(c, klaunch(c, finalize_stats_kernel<ST>, dim3(nrb), dim3(kStatsThreads), 0, s, (const ST*)ls,
-                      (int)c->R, (const ST*)(c->R > 1 ? nullptr : ps), T, (int)B,
+                      (int)c->R, (const ST*)(c->coll ? nullptr : ps), T, (int)B,
                       (const double*)c->zpos, (const double*)c->cpos, (const float*)c->epos,
                       (const int32_t*)c->pos_col, (const int*)c->hasval, filt ? 1 : 0, c->mg,
                       offr, rsc, dlt, c->loss_row, c->st));
@@ -721,7 +722,7 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   if (e2e) {  // d_features: [sum over ranks], -> D x B fp64, download; overlaps the dW GEMM
     CUDA_TRY(c, cudaEventRecord(c->ev_dx, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_dx, 0));
-    if (c->R > 1)  // the drop-in returns the FULL summed d_features on every rank
+    if (c->coll)  // the drop-in returns the FULL summed d_features on every rank
       COMM_TRY(comm_all_reduce(c, c->dX, c->dX, B * c->D, kF32, kSum, c->s2));
     dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
     dx_to_dxb_kernel<<<grid, blk, 0, c->s2>>>(c->dX, (int)c->D, (int)B, c->xdb);
@@ -1310,6 +1311,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   c->D = desc->dim;
   c->K = desc->num_shards;
   c->R = desc->world_size;
+  c->coll = c->R > 1 || (desc->flags & PFC_FLAG_FORCE_COLLECTIVES);
   c->rank = desc->rank;
   c->bf16 = desc->precision == PFC_PRECISION_BF16;
   c->tf32 = desc->precision == PFC_PRECISION_TF32;
@@ -1402,7 +1404,7 @@ int pfc_gpu_create(const pfc_gpu_desc* desc, void** ctx_out) {
   CT(dalloc(c, &c->sp, 1));
   CT(cudaMallocHost(&c->st_host, sizeof(StepStatus)));
   for (int i = 0; i <= PhaseTimer::kMax; ++i) CT(cudaEventCreate(&c->pt.ev[i]));
-  if (c->R > 1) {
+  if (c->coll) {
     if (!desc->nccl_id) return bail(fail(c, PFC_ERR_NCCL, "world_size > 1 needs nccl_id"));
     std::string e;
     if (is_loop_id(desc->nccl_id)) {  // R ranks as R contexts of this process (comm.cuh)
@@ -1762,7 +1764,7 @@ static int step_from_X(Ctx* c, int64_t B, const pfc_gpu_step_args* a, pfc_gpu_st
   dim3 grid((unsigned)ceil_div(B, 32), (unsigned)ceil_div(c->D, 32)), blk(32, 8);
   if (int rc = run_step(c, c->X, c->labels, B, a, c->dX)) return rc;
   c->reset_status = true;
-  if (c->R > 1) {  // the drop-in returns the FULL summed d_features on every rank
+  if (c->coll) {  // the drop-in returns the FULL summed d_features on every rank
     COMM_TRY(comm_all_reduce(c, c->dX, c->dX, B * c->D, kF32, kSum, s));
   }
   dx_to_dxb_kernel<<<grid, blk, 0, s>>>(c->dX, (int)c->D, (int)B, c->xdb);
@@ -1847,7 +1849,7 @@ static int step_device_once(Ctx* c, const float* x_local, const int64_t* labels_
   const float* x = x_local;
   const int64_t* lab = labels_local;
   float* dxf = dx_local;
-  if (c->R > 1) {  // feature all-gather (rank-major, all_gather_features shardsim.hpp:86-115)
+  if (c->coll) {  // feature all-gather (rank-major, all_gather_features shardsim.hpp:86-115)
     COMM_TRY(comm_all_gather(c, x_local, c->X, b_local * c->D, kF32, s));
     COMM_TRY(comm_all_gather(c, labels_local, c->labels, b_local, kI64, s));
     x = c->X;
@@ -1856,7 +1858,7 @@ static int step_device_once(Ctx* c, const float* x_local, const int64_t* labels_
   }
   if (int rc = run_step(c, x, lab, B, a, dxf)) return rc;
   c->reset_status = false;  // errors stay on the device until a synchronous check
-  if (c->R > 1)  // collective 3 (shardsim.hpp:387-399) as a reduce-scatter to the owners
+  if (c->coll)  // collective 3 (shardsim.hpp:387-399) as a reduce-scatter to the owners
     COMM_TRY(comm_reduce_scatter(c, c->dX, dx_local, b_local * c->D, kF32, kSum, s));
   if (!out) return PFC_OK;
   CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(StepStatus), cudaMemcpyDeviceToHost, s));
@@ -1890,7 +1892,7 @@ static int diagnostics_device(Ctx* c, int64_t B, bool split, pfc_gpu_diag_out* o
   const int rc = c->bf16 ? run_diagnostics<__nv_bfloat16, true>(c, B, split)
                          : run_diagnostics<float, false>(c, B, split);
   if (rc) return rc;
-  if (c->R > 1) {  // merge over ranks: maxima, sibling flags, the owner's apcs term
+  if (c->coll) {  // merge over ranks: maxima, sibling flags, the owner's apcs term
     COMM_TRY(comm_all_reduce(c, c->demax, c->demax, B * 3, kU64, kMax, s));
     COMM_TRY(comm_all_reduce(c, c->dhasc, c->dhasc, B, kI32, kMax, s));
     COMM_TRY(comm_all_reduce(c, c->dapcs, c->dapcs, B, kF64, kSum, s));

@@ -226,3 +226,55 @@ def test_loopback_northstar_golden(R, port):
         f.write(json.dumps(rec) + "\n")
     assert rec["loss_rel"] <= tl and rec["dX_fro"] <= tdf and rec["dX_max"] <= tdm, rec
     assert rec["W_max"] <= tw, rec
+
+
+@pytest.mark.parametrize("transport", ["nccl", "loopback"])
+@pytest.mark.parametrize("precision", [p.PRECISION_BF16, p.PRECISION_FP32], ids=["bf16", "fp32"])
+def test_collective_path_one_rank(transport, precision, port):
+    """The N > 1 collective path on a real NCCL communicator (NCCL never ran).
+
+    NCCL will not put two ranks on one GPU, so PFC_FLAG_FORCE_COLLECTIVES runs every collective
+    of the rank path -- all-gather of X and labels, the statistics all-gather, z_pos and flag
+    all-reduces, the per-row offset max, the dX all-reduce (host drop-in, inside the captured
+    graph) and the dX reduce-scatter (device path), the diagnostics merges -- through a 1-rank
+    communicator.  Same values as the plain one-rank context (bit-identical: every 1-rank
+    collective is a copy); the byte counters follow the protocol closed form at R = 1."""
+    C_, K, D, B = 16000, 4, 256, 128
+    tau = 0.05 if precision == p.PRECISION_FP32 else None
+    for s in (64.0, 128.0):  # fixed offset, then per-row offsets (the max all-reduce)
+        cfg = p.StepConfig(r=0.2, margin=p.MarginConfig.cosface_style(s, 0.4), filter_threshold=tau,
+                           lr=0.1)
+        W0 = port.init_centers(C_, K, D, 1)
+        X, labels = port.bench_inputs(C_, D, B, 1, 0)
+        outs = []
+        for flags in (0, p.FLAG_FORCE_COLLECTIVES):
+            nid = None
+            if flags:
+                nid = p.nccl_unique_id() if transport == "nccl" else p.loopback_id()
+            sh = p.CenterShards(p.ShardLayout(C_, K), D, cfg, max_batch=B, precision=precision,
+                                world_size=1, nccl_id=nid, flags=flags)
+            for k in range(K):
+                sh.set_shard(k, shard_block(W0, C_, K, D, k))
+            st = sh.step_host(X, labels, cfg, p.SeededRng(1, port.make_stream("iteration", 0)))
+            xl = torch.from_numpy(np.ascontiguousarray(X.T)).float().cuda()
+            ll = torch.from_numpy(labels.copy()).cuda()
+            dx = torch.empty(B, D, device="cuda")
+            torch.cuda.synchronize()
+            o = sh.step_device(xl.data_ptr(), ll.data_ptr(), B, dx.data_ptr(), cfg,
+                               p.SeededRng(1, port.make_stream("iteration", 1)))
+            dg = sh.diagnostics(X, labels)
+            outs.append((st.loss, st.d_features, o.loss, dx.cpu().numpy(),
+                         [sh.get_shard(k)[0] for k in range(K)], dg, st.nccl_bytes,
+                         o.nccl_bytes))
+            sh.close()
+        a, b = outs
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+        assert a[2] == b[2] and np.array_equal(a[3], b[3])
+        assert all(np.array_equal(x, y) for x, y in zip(a[4], b[4]))
+        assert a[5] == b[5]
+        exact = s > 64.0
+        assert (a[6], a[7]) == (0, 0)
+        assert b[6] == protocol_bytes(1, B, D, precision != p.PRECISION_FP32, tau is not None,
+                                      exact, True)[0]
+        assert b[7] == protocol_bytes(1, B, D, precision != p.PRECISION_FP32, tau is not None,
+                                      exact, False)[0]

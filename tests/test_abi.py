@@ -57,6 +57,16 @@ def test_create_validates_before_touching_a_device():
         p.CenterShards(p.ShardLayout(1000, 2), 128, cfg, max_batch=(1 << 20) + 1)
     with pytest.raises(p.ContractError, match="sampling ratio"):
         p.CenterShards(p.ShardLayout(1000, 2), 128, p.StepConfig(r=1.5), max_batch=8)
+    # the combined-margin extension's parameters (checked by the library itself, not only by
+    # MarginConfig.validate)
+    for m1, m3, msg in ((0.0, 0.2, r"m1 must be in \(0, 2\]"), (1.0, 1.0, r"m3 must be in \[0, 1\)")):
+        d = p.Desc(1000, 128, 2, 8, 0.1, p.COMBINED, 64.0, 0.3, 0, 0.0, 0.9, 5e-4,
+                   p.PRECISION_BF16, 0, 0, 1, None, 0, m1, m3)
+        h = ctypes.c_void_p()
+        lib = p.load_library()
+        assert lib.pfc_gpu_create(ctypes.byref(d), ctypes.byref(h)) == 4  # PFC_ERR_CONFIG
+        import re
+        assert re.search(msg, lib.pfc_gpu_last_error(None).decode())
 
 
 def test_rng_mirror_matches_oracle(port):
@@ -84,3 +94,35 @@ def test_header_structs_match_ctypes_layout():
     assert ctypes.sizeof(p.StepArgs) == 32
     assert ctypes.sizeof(p.StepOut) == 72
     assert p.Desc.flags.offset > p.Desc.nccl_id.offset
+
+
+def test_header_structs_match_c_compiler(tmp_path):
+    """sizeof / offsetof of every struct in include/pfc_gpu.h, as gcc lays them out, against the
+    ctypes mirrors the Python package and INTEGRATION.md's bindings use."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    mirrors = {"pfc_gpu_desc": p.Desc, "pfc_gpu_step_config": p.StepConfigC,
+               "pfc_gpu_step_args": p.StepArgs, "pfc_gpu_step_out": p.StepOut}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pfc_gpu.h"', 'int main(void) {']
+    for cname, py in mirrors.items():
+        lines.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ['  return 0;', '}']
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "abi"
+    subprocess.check_call(["gcc", "-std=c11", "-I", inc, str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    got = {}
+    for line in out:
+        if line:
+            c, f, v = line.split()
+            got[(c, f)] = int(v)
+    for cname, py in mirrors.items():
+        assert got[(cname, "sizeof")] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)

@@ -384,7 +384,7 @@ def main():
     # ---- diagnostics (with_diagnostics): apcs + exact amncs over all C
     #      classes (a 2 B d C screening GEMM); wall time of the host call, X / labels from host
     if not args.no_diag:
-        X0 = xs[0].t().double().cpu().numpy()
+        X0 = np.ascontiguousarray(xs[0].t().double().cpu().numpy())  # FeatureBatch: D x B rows
         L0 = ls[0].cpu().numpy()
         sh.diagnostics(X0, L0)  # builds the all-class operand once
         torch.cuda.synchronize()

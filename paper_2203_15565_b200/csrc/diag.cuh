@@ -149,10 +149,17 @@ struct DiagMaxEpi : NoSetup {
       if (!rv || colb >= rows) continue;
       if (!cid) {  // no split: one bucket; the per-column work runs only near the maximum
         float cm = -INFINITY;
+        if (colb + 32 <= rows && (lab < colb || lab >= colb + 32)) {
+          // every column valid (the common case): a plain 32-way max, no per-column index tests
+          float m4[4] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int64_t j = colb + q;
-          cm = (j < rows && j != lab) ? fmaxf(cm, v[q]) : cm;
+          for (int q = 4; q < 32; ++q) m4[q & 3] = fmaxf(m4[q & 3], v[q]);
+          cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        } else {
+          const int nv = (int)(rows - colb < 32 ? rows - colb : 32);
+          const int lq = (lab >= colb && lab < colb + 32) ? (int)(lab - colb) : -1;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) cm = (q < nv && q != lq) ? fmaxf(cm, v[q]) : cm;
         }
         if (cm > rm[0]) {
           rm[0] = cm;

@@ -73,3 +73,25 @@ def test_sampler_fuzz(flags, port):
                 assert np.array_equal(b.class_indices, want[k]), (C_, K, r, len(lab), k)
                 assert b.num_positives == npos[k]
         sh.close()
+
+
+@pytest.mark.parametrize("flags", [0, p.FLAG_WIDE_SAMPLER_CHUNKS], ids=["chunk32", "chunk1024"])
+def test_sampler_positives_beyond_shared_staging(flags, port):
+    """More distinct positives across the local shards (10000) than the chain walk stages in
+    shared memory (kWalkPositives = 8192): the walk's complement lookups fall back to the
+    positives in global memory; buffers still bit-exact."""
+    C_, K, B, r = 400000, 2, 16384, 0.1
+    rng = np.random.default_rng(3)
+    pool = np.concatenate([rng.choice(200000, 5000, replace=False),
+                           200000 + rng.choice(200000, 5000, replace=False)])
+    lab = pool[rng.integers(0, pool.size, B)].astype(np.int64)
+    lab[:pool.size] = pool  # every pool class present
+    stream = port.make_stream("fuzz", 99)
+    want, npos = port.build_buffers(C_, K, lab, r, 5, stream)
+    assert npos.sum() == 10000
+    sh = p.CenterShards(p.ShardLayout(C_, K), 8, p.StepConfig(r=r), max_batch=B, flags=flags)
+    X = np.random.default_rng(0).standard_normal((8, B))
+    p.distributed_partial_step(sh, X, lab, p.StepConfig(r=r, lr=0.0), p.SeededRng(5, stream))
+    for k, b in enumerate(sh.buffers()):
+        assert np.array_equal(b.class_indices, want[k]) and b.num_positives == npos[k]
+    sh.close()

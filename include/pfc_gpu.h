@@ -56,7 +56,7 @@ typedef enum { /* MarginKind, margin.hpp:11 */
 
 typedef enum {
   PFC_PRECISION_BF16 = 0, /* tcgen05 kind::f16 GEMMs, fp32 accumulate, fp32 master W / momentum;
-                             needs dim % 4 == 0 and dim <= 512 (pfc_gpu_create: PFC_ERR_CONFIG) */
+                             needs dim % 4 == 0 and dim <= 1024 (pfc_gpu_create: PFC_ERR_CONFIG) */
   PFC_PRECISION_FP32 = 1, /* fp32 validation mode: SIMT fp32 GEMMs, fp64 softmax / gradient stage */
   PFC_PRECISION_TF32 = 2  /* tcgen05 kind::tf32 GEMMs on fp32 operands (10-bit mantissa inputs, fp32
                              accumulate, fp32 E), fp32 master W / momentum: the tensor-core mode for

@@ -69,7 +69,7 @@ struct NoSetup {
 
 // ------------------------------------------------------------------------------------ FwdEpi
 #ifndef PFC_FWD_STBUF
-#define PFC_FWD_STBUF 2
+#define PFC_FWD_STBUF 1
 #endif
 template <typename ST, typename OT, bool kFilter, bool kTma>
 struct alignas(64) FwdEpi : NoSetup {

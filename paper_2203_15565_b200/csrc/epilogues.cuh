@@ -392,27 +392,31 @@ struct DxPartEpi : NoSetup {
 namespace dw_ring {
 constexpr int kNC = 8;                      // 32-dim chunks per 256-dim tile half
 constexpr int kItems = 2 * kNC;             // W chunk c (dot pass), then W + momentum chunk c
-constexpr int kCap = PFC_DW_CAP;            // ring capacity in 1 KB sub-slots (8 rows x 128 B)
 constexpr int kTileSlots = kNC * 1 + kNC * 2;
-static_assert(kTileSlots % kCap == 0, "ring positions must repeat every tile");
 __host__ __device__ constexpr int size(int i) { return (i % kItems) < kNC ? 1 : 2; }
-__host__ __device__ constexpr int pos(int i) {                  // first sub-slot of item i
-  int p = 0;
-  for (int j = 0; j < i % kItems; ++j) p += size(j);
-  return p % kCap;
-}
-// Greedy issue over the endless item stream (tile after tile): items issued before item k is
-// consumed, in steady state (the previous tile already issued this tile's first items).
-__host__ __device__ constexpr int issued_before(int k) {
-  int issued = 0, used = 0;
-  for (int c = 0;; ++c) {
-    while (issued < 3 * kItems && used + size(issued) <= kCap) used += size(issued++);
-    if (c == kItems + k) return issued - kItems;
-    used -= size(c);
+// Cap: ring capacity in 1 KB sub-slots (8 rows x 128 B)
+template <int Cap>
+struct Ring {
+  static constexpr int kCap = Cap;
+  static_assert(kTileSlots % kCap == 0, "ring positions must repeat every tile");
+  __host__ __device__ static constexpr int pos(int i) {  // first sub-slot of item i
+    int p = 0;
+    for (int j = 0; j < i % kItems; ++j) p += size(j);
+    return p % kCap;
   }
-}
-constexpr int kHead = issued_before(0);     // items of a tile in flight when it starts
-static_assert(issued_before(kItems) - kItems == kHead, "periodic steady state");
+  // Greedy issue over the endless item stream (tile after tile): items issued before item k is
+  // consumed, in steady state (the previous tile already issued this tile's first items).
+  __host__ __device__ static constexpr int issued_before(int k) {
+    int issued = 0, used = 0;
+    for (int c = 0;; ++c) {
+      while (issued < 3 * kItems && used + size(issued) <= kCap) used += size(issued++);
+      if (c == kItems + k) return issued - kItems;
+      used -= size(c);
+    }
+  }
+  static constexpr int kHead = issued_before(0);  // items of a tile in flight when it starts
+  static_assert(issued_before(kItems) - kItems == kHead, "periodic steady state");
+};
 // compile-time loop: f(std::integral_constant<int, I>) for I in [A, B)
 template <int A, int B, class F>
 __device__ __forceinline__ void static_range(F&& f) {
@@ -426,14 +430,17 @@ __device__ __forceinline__ void static_range(F&& f) {
 // NC: CTAs per class block (a cluster): the dim blocks of 256 (D <= 256 * NC, up to 1024).  Each
 // CTA sends its rows' partial dots to the other NC - 1 and sums all NC in cluster-rank order, so
 // every CTA of the cluster forms the same center_proj.
-template <int NC>
+// Cap: the W / momentum ring per warp in KB (6 with 2 operand stages at B <= 1024; 3 with 3
+// stages when the GEMM's K = B is larger and its operand stream needs the deeper pipeline).
+template <int NC, int Cap = PFC_DW_CAP>
 struct DwUpdateEpi {
   static_assert(NC >= 1 && NC <= 4, "DwUpdateEpi: 1-4 dim blocks");
   static constexpr bool kPair = NC > 1;
   static constexpr int kCluster = NC;
   static constexpr bool kNext = true;
   static constexpr int kStageFloats = 8 * 36;             // TMEM chunk of the warp's 8 rows
-  static constexpr int kRingFloats = dw_ring::kCap * 256;  // 6 x 1 KB
+  using R = dw_ring::Ring<Cap>;
+  static constexpr int kRingFloats = Cap * 256;  // Cap x 1 KB
   static constexpr int kWarpFloats = kStageFloats + kRingFloats + 2 * 3 * 8;  // + [2][inv|row|pslot]
   static constexpr int kWarpBytes = kWarpFloats * 4;
   // CTA-shared (in warpgroup 0's scratch): hrem[2 parity][NC source rank][128 rows] + mbarriers
@@ -489,6 +496,7 @@ struct DwUpdateEpi {
                                            bool has_next) const {
     static_assert(NWG == 4 && BN == 256, "DwUpdateEpi: 4 warpgroups, 256-dim tiles");
     using namespace dw_ring;
+    constexpr int kCap = R::kCap, kHead = R::kHead;
     const int q = row >> 5, lane = row & 31;
     uint8_t* wg0 = smem - wg * kSmem;
     float* ws = reinterpret_cast<float*>(smem + q * kWarpBytes);
@@ -546,7 +554,7 @@ struct DwUpdateEpi {
       constexpr int i = decltype(ic)::value;
       constexpr int ii = i % kItems;
       constexpr int c = ii < kNC ? ii : ii - kNC;
-      constexpr int p = pos(i);
+      constexpr int p = R::pos(i);
       const int d = dbase + c * 32;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -640,14 +648,14 @@ struct DwUpdateEpi {
           rcp[u] = dot[u] * rinv[u];  // center_proj_j = w^_j . dwt_j (shardsim.hpp:361-362)
         }
       }
-      pfc_sm100::cp_async_wait<issued_before(k) - k - 1>();  // item k landed (this lane's pieces)
+      pfc_sm100::cp_async_wait<R::issued_before(k) - k - 1>();  // item k landed (this lane's pieces)
       stage_chunk(c * 32);
       if (d < D) {
         if constexpr (k < kNC) {  // dot pass: half-dot w . dwt over this CTA's dims
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const float4 a = dwt4(u, d);
-            const float4 w = ring4(pos(k), u);
+            const float4 w = ring4(R::pos(k), u);
             dot[u] += a.x * w.x + a.y * w.y + a.z * w.z + a.w * w.w;
           }
         } else {  // update pass: dW and the momentum-SGD update of the sampled rows
@@ -655,7 +663,7 @@ struct DwUpdateEpi {
           for (int u = 0; u < 2; ++u) {
             if (rw[u] < 0) continue;
             const float4 a4 = dwt4(u, d);
-            const float4 w4 = ring4(pos(k), u), m4 = ring4((pos(k) + 1) % kCap, u);
+            const float4 w4 = ring4(R::pos(k), u), m4 = ring4((R::pos(k) + 1) % kCap, u);
             const float av[4] = {a4.x, a4.y, a4.z, a4.w};
             float wv[4] = {w4.x, w4.y, w4.z, w4.w};
             float mv[4] = {m4.x, m4.y, m4.z, m4.w};
@@ -685,7 +693,7 @@ struct DwUpdateEpi {
         }
       }
       // refill the ring (reads of item k's sub-slots were consumed above: in-order issue)
-      static_range<issued_before(k), issued_before(k + 1)>(issue);
+      static_range<R::issued_before(k), R::issued_before(k + 1)>(issue);
     });
   }
 };

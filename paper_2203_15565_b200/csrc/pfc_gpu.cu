@@ -125,6 +125,7 @@ constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
 #define PFC_DIAG_CG 1
 #endif
 constexpr int kDiagCG = PFC_DIAG_CG;  // diagnostics / mics screening GEMMs likewise
+constexpr int64_t kDwDeepBatch = 1024;  // dW GEMM: 3 operand stages + 3 KB ring above this batch
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
 #endif  // dW GEMM operand ring depth (2: leaves shared memory to the W / momentum ring)
@@ -744,13 +745,24 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     if constexpr (kUmma) {
       // one cluster CTA per 256-dim block of a class block (tile order n fastest)
+      // operand pipeline vs W / momentum ring: the GEMM's K is the batch, so past B = 1024 its
+      // operand stream needs a third stage (10M / B = 2048: dW 3.21 vs 3.49 ms), paid for with
+      // a 3 KB ring (2M / B = 1024 keeps 2 stages + 6 KB: 0.475 vs 0.488 ms)
+      const bool deep = B > kDwDeepBatch;
       auto dw = [&](auto nc) {
         constexpr int NC = decltype(nc)::value;
-        return launch_umma<kBN, PFC_DW_STAGES, 4, false, true, DwUpdateEpi<NC>, 1, OT>(
-            c, c->tm_e_k, c->tm_xs_mn, gw,
-            DwUpdateEpi<NC>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot, c->poscorr,
-                            c->W, c->M, c->sp, (float)c->d.momentum, (float)c->d.weight_decay,
-                            c->st});
+        auto go = [&](auto e) {
+          using E = decltype(e);
+          constexpr int S = E::R::kCap == PFC_DW_CAP ? PFC_DW_STAGES : 3;
+          return launch_umma<kBN, S, 4, false, true, E, 1, OT>(c, c->tm_e_k, c->tm_xs_mn, gw, e);
+        };
+        if (deep)
+          return go(DwUpdateEpi<NC, 3>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot,
+                                       c->poscorr, c->W, c->M, c->sp, (float)c->d.momentum,
+                                       (float)c->d.weight_decay, c->st});
+        return go(DwUpdateEpi<NC>{(int)c->ncols, (int)c->D, c->wnorm, c->lrow, c->pslot,
+                                  c->poscorr, c->W, c->M, c->sp, (float)c->d.momentum,
+                                  (float)c->d.weight_decay, c->st});
       };
       switch (gw.n_tiles) {
         case 1: err = dw(std::integral_constant<int, 1>{}); break;

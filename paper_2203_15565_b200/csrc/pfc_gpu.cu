@@ -125,7 +125,7 @@ constexpr int kDxCG = PFC_DX_CG;    // dX GEMM likewise
 #define PFC_DIAG_CG 1
 #endif
 constexpr int kDiagCG = PFC_DIAG_CG;  // diagnostics / mics screening GEMMs likewise
-constexpr int64_t kDwDeepBatch = 1024;  // dW GEMM: 3 operand stages + 3 KB ring above this batch
+constexpr int64_t kDwDeepBatch = 1024;  // dW GEMM: 3 operand stages + 3 KB ring above 2 KB of E^T per row
 #ifndef PFC_DW_STAGES
 #define PFC_DW_STAGES 2
 #endif  // dW GEMM operand ring depth (2: leaves shared memory to the W / momentum ring)
@@ -745,10 +745,11 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     cudaError_t err;
     if constexpr (kUmma) {
       // one cluster CTA per 256-dim block of a class block (tile order n fastest)
-      // operand pipeline vs W / momentum ring: the GEMM's K is the batch, so past B = 1024 its
-      // operand stream needs a third stage (10M / B = 2048: dW 3.21 vs 3.49 ms), paid for with
-      // a 3 KB ring (2M / B = 1024 keeps 2 stages + 6 KB: 0.475 vs 0.488 ms)
-      const bool deep = B > kDwDeepBatch;
+      // operand pipeline vs W / momentum ring: the GEMM's K is the batch, so past 2 KB of E^T
+      // per class row (bf16 B > 1024, tf32 B > 512) its operand stream needs a third stage
+      // (10M / B = 2048: dW 3.26 vs 3.52 ms; tf32 2M: 0.612 vs 0.675 ms), paid for with a 3 KB
+      // ring (bf16 2M / B = 1024 keeps 2 stages + 6 KB: 0.475 vs 0.488 ms)
+      const bool deep = B * (int64_t)sizeof(OT) > kDwDeepBatch * 2;  // K bytes per E^T row
       auto dw = [&](auto nc) {
         constexpr int NC = decltype(nc)::value;
         auto go = [&](auto e) {

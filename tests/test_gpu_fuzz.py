@@ -54,7 +54,8 @@ def _cases(n=16, seed=2203):
     return out
 
 
-CASES = _cases()
+# PFC_FUZZ_CASES / PFC_FUZZ_SEED widen the sweep for a one-off run (profiles/r2/fuzz_wide.txt)
+CASES = _cases(int(os.environ.get("PFC_FUZZ_CASES", "16")), int(os.environ.get("PFC_FUZZ_SEED", "2203")))
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
@@ -102,6 +103,16 @@ def test_fuzz_step_matches_oracle(case, port):
         precisions += [p.PRECISION_BF16, p.PRECISION_TF32]
     for precision in precisions:
         tl, tdf, tdm, tw = TOL[precision]
+        if precision != p.PRECISION_FP32 and D < 512:
+            # the tensor-core contract is stated at D >= 512; a cosine of unit vectors whose
+            # D elements are rounded independently errs as 1 / sqrt(D), so below 512 every bound
+            # scales by sqrt(512 / D) (the 120-case sweep, profiles/r2/fuzz_wide.txt)
+            f = math.sqrt(512.0 / D)
+            tl, tdf, tdm, tw = tl * f, tdf * f, tdm * f, tw * f
+        if precision != p.PRECISION_FP32 and B < 64:
+            # W' is compared as max/max of the whole centres; its error is the operands'
+            # rounding times the UPDATE, which grows as 1 / B (two steps with momentum)
+            tw *= 64.0 / B
         sh = make_shards(W0, np.zeros_like(W0), C_, K, D, step_cfg(mg, m, r, tau), B, precision)
         for step, (Xs, ls, st, ref, Wr, Mr) in enumerate(refs):
             rows = np.unique(ref["buffers"].ravel())

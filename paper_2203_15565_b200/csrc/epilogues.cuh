@@ -432,10 +432,18 @@ __device__ __forceinline__ void static_range(F&& f) {
 // every CTA of the cluster forms the same center_proj.
 // Cap: the W / momentum ring per warp in KB (6 with 2 operand stages at B <= 1024; 3 with 3
 // stages when the GEMM's K = B is larger and its operand stream needs the deeper pipeline).
-template <int NC, int Cap = PFC_DW_CAP>
-struct DwUpdateEpi {
+struct DwHalfMap {
+  CUtensorMap tm_a16;  // E^T K-major, 16-row boxes (the producer's half-tile A loads)
+};
+struct DwNoHalfMap {};
+template <int NC, int Cap = PFC_DW_CAP, bool Half = false>
+struct DwUpdateEpi : std::conditional_t<Half, DwHalfMap, DwNoHalfMap> {
   static_assert(NC >= 1 && NC <= 4, "DwUpdateEpi: 1-4 dim blocks");
   static constexpr bool kPair = NC > 1;
+  // half tiles (the schedule's tail, GemmGeom::half_m0): 64 class rows, 16 at the top of each
+  // TMEM lane quadrant, 4 per warp (lanes 4 wg .. 4 wg + 3) instead of 8
+  // (a separate instantiation: the full-tile schedule keeps the plain 8-rows-per-warp path)
+  static constexpr bool kHalfTiles = Half;
   static constexpr int kCluster = NC;
   static constexpr bool kNext = true;
   static constexpr int kStageFloats = 8 * 36;             // TMEM chunk of the warp's 8 rows
@@ -463,12 +471,20 @@ struct DwUpdateEpi {
   struct Pre {
     float inv;
     int r, ps;
+    int li;  // this lane's row slot among the warp's rows, -1: not one of them
   };
+  // lane -> row of a tile: full tiles 32 q + lane (warp wg: lanes 8 wg ..), half tiles 16 q + lane
+  // for lane < 16 (warp wg: lanes 4 wg ..)
+  __device__ __forceinline__ static int slot_of(const TileInfo& t, int lane, int wg) {
+    if (!Half || t.h == 128) return (lane >> 3) == wg ? (lane & 7) : -1;
+    return (lane < 16 && (lane >> 2) == wg) ? (lane & 3) : -1;
+  }
   __device__ __forceinline__ Pre preload(const TileInfo& t, int row, int wg) const {
-    Pre p{0.f, -1, -1};
-    const int lane = row & 31;
-    const int c = t.row0 + (row & ~31) + lane;
-    if ((lane >> 3) == wg && c < ncols) {  // only this warp's 8 rows
+    Pre p{0.f, -1, -1, -1};
+    const int lane = row & 31, q = row >> 5;
+    const int c = t.row0 + ((!Half || t.h == 128) ? 32 : 16) * q + lane;
+    p.li = slot_of(t, lane, wg);
+    if (p.li >= 0 && c < ncols) {  // only this warp's rows
       const float n = wnorm[c];
       p.inv = 1.0f / (n > 1e-12f ? n : 1e-12f);
       p.r = lrow[c];
@@ -511,16 +527,40 @@ struct DwUpdateEpi {
     uint64_t* mb = reinterpret_cast<uint64_t*>(shared_area(wg0) + kHremFloats * 4);  // [2][16]
     const bool failed = status_failed(st);
     const float lr = sp->lr;
-    const bool mine = (lane >> 3) == wg;  // this lane's TMEM row is one of the warp's 8
-    const int li = lane & 7;
+    const int li = slot_of(t, lane, wg);
+    const bool mine = li >= 0;  // this lane's TMEM row is one of the warp's rows
+    float* sn = sc + ((t.iter & 1) ^ 1) * 24;
     __syncwarp();  // the warp finished with the previous tile's scalars
-    if (mine) {
+    if constexpr (Half) {
+      if (lane < 8) {  // slots a half tile leaves empty stay invalid rows
+        if (t.iter == 0) {
+          s_inv[lane] = 0.f;
+          s_row[lane] = -1;
+          s_ps[lane] = -1;
+        }
+        sn[lane] = 0.f;
+        reinterpret_cast<int*>(sn)[8 + lane] = -1;
+        reinterpret_cast<int*>(sn)[16 + lane] = -1;
+      }
+      __syncwarp();
+    }
+    if constexpr (Half) {  // each tile's own lane -> slot map (the slots were cleared above)
+      if (t.iter == 0 && pre.li >= 0) {  // later tiles' scalars were stored by the tile before
+        s_inv[pre.li] = pre.inv;
+        s_row[pre.li] = failed ? -1 : pre.r;
+        s_ps[pre.li] = pre.ps;
+      }
+      if (has_next && pre_next.li >= 0) {
+        sn[pre_next.li] = pre_next.inv;
+        reinterpret_cast<int*>(sn)[8 + pre_next.li] = failed ? -1 : pre_next.r;
+        reinterpret_cast<int*>(sn)[16 + pre_next.li] = pre_next.ps;
+      }
+    } else if (mine) {  // full tiles only: one map, every slot of the warp written
       if (t.iter == 0) {  // later tiles' scalars were stored by the tile before them
         s_inv[li] = pre.inv;
         s_row[li] = failed ? -1 : pre.r;
         s_ps[li] = pre.ps;
       }
-      float* sn = sc + ((t.iter & 1) ^ 1) * 24;
       sn[li] = pre_next.inv;
       reinterpret_cast<int*>(sn)[8 + li] = (failed || !has_next) ? -1 : pre_next.r;
       reinterpret_cast<int*>(sn)[16 + li] = pre_next.ps;

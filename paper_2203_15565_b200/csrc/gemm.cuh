@@ -14,6 +14,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -24,7 +26,16 @@ struct TileInfo {
   int row0, col0;
   int kb0, kb1;
   int iter;  // this CTA's tile counter (0, 1, 2, ...)
+  int h;     // valid rows: BM, or BM / 2 for a half tile (16 rows at the top of each TMEM
+             // lane quadrant; the dW GEMM's tail, GemmGeom::half_m0)
 };
+
+// Epi::kHalfTiles (optional, false when absent): the GEMM may be given half tiles, whose A rows
+// the producer loads through Epi::tm_a16 (16-row boxes)
+template <class E, class = void>
+struct kHalfTilesOf : std::false_type {};
+template <class E>
+struct kHalfTilesOf<E, std::void_t<decltype(E::kHalfTiles)>> : std::bool_constant<E::kHalfTiles> {};
 
 struct GemmGeom {
   int M, N, K;
@@ -32,7 +43,10 @@ struct GemmGeom {
   int n_fastest;  // tile order: 0 -> m fastest, 1 -> n fastest
   int BN, BK;
   int BM;         // 128, or 256 for a CTA-pair GEMM (the kernel adds 128 x cluster rank)
+  int half_m0;    // m tiles from here on are half tiles of BM / 2 rows (m_tiles: none)
   __host__ __device__ int total() const { return m_tiles * n_tiles * splits; }
+  // kHalf: the GEMM may have half tiles (half_m0 < m_tiles); without it every tile is BM rows
+  template <bool kHalf = false>
   __host__ __device__ TileInfo tile(int t) const {
     TileInfo ti;
     const int mn = m_tiles * n_tiles;
@@ -45,7 +59,13 @@ struct GemmGeom {
       ti.m_tile = r % m_tiles;
       ti.n_tile = r / m_tiles;
     }
-    ti.row0 = ti.m_tile * BM;
+    if constexpr (kHalf) {
+      ti.h = ti.m_tile < half_m0 ? BM : BM / 2;
+      ti.row0 = ti.m_tile < half_m0 ? ti.m_tile * BM : half_m0 * BM + (ti.m_tile - half_m0) * (BM / 2);
+    } else {
+      ti.h = BM;
+      ti.row0 = ti.m_tile * BM;
+    }
     ti.col0 = ti.n_tile * BN;
     ti.kb0 = ti.split * kb_per_split;
     ti.kb1 = ti.kb0 + kb_per_split < kb_total ? ti.kb0 + kb_per_split : kb_total;
@@ -72,6 +92,7 @@ inline GemmGeom make_geom(int M, int N, int K, int BN, int splits, int n_fastest
   g.kb_per_split = (g.kb_total + splits - 1) / splits;
   g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
   g.n_fastest = n_fastest;
+  g.half_m0 = g.m_tiles;
   return g;
 }
 
@@ -187,7 +208,7 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
   // persistent schedule over tiles (CG = 2: over pair tiles, one per cluster)
   const int first = (int)blockIdx.x / CG, stride = (int)gridDim.x / CG;
   auto tile_at = [&](int t) {
-    TileInfo ti = g.tile(t);
+    TileInfo ti = g.template tile<kHalfTilesOf<Epi>::value>(t);
     ti.row0 += (int)rank * 128;
     return ti;
   };
@@ -200,10 +221,11 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
       for (int t = first; t < total; t += stride) {
         const TileInfo ti = tile_at(t);
         const int bcol = ti.col0 + (int)rank * BNL;
+        const bool half = kHalfTilesOf<Epi>::value && ti.h != g.BM;  // (Epi::kHalfTiles GEMMs only)
         for (int kb = ti.kb0; kb < ti.kb1; ++kb, ++kbc) {
           const uint32_t s = kbc % STAGES, ph = (kbc / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[s], STAGE_BYTES * CG);
+          if (leader) mbar_arrive_expect_tx(&full[s], (half ? STAGE_BYTES - A_BYTES / 2 : STAGE_BYTES) * CG);
           const int k0 = kb * KB;
           uint8_t* a = sA + s * A_BYTES;
           uint8_t* b = sB + s * B_BYTES;
@@ -211,7 +233,14 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
             if constexpr (CG == 2) tma_load_2d_pair(m, full_c + s * 8u, dst, c0, c1);
             else tma_load_2d(m, &full[s], dst, c0, c1);
           };
-          if (!A_MN) {
+          if constexpr (kHalfTilesOf<Epi>::value) {
+            if (half) {  // 16 class rows at the top of each 32-row TMEM lane quadrant
+#pragma unroll
+              for (int q = 0; q < 4; ++q) load(&epi.tm_a16, a + q * 32 * 128, k0, ti.row0 + 16 * q);
+            } else {
+              load(&tmA, a, k0, ti.row0);
+            }
+          } else if (!A_MN) {
             load(&tmA, a, k0, ti.row0);
           } else {
 #pragma unroll
@@ -232,7 +261,7 @@ __global__ void __launch_bounds__(32 * PFC_CTRL_WARPS + 128 * NWG, 1)
                                        : make_idesc_bf16(128 * CG, BN, A_MN, B_MN);
       uint32_t kbc = 0, it = 0;
       for (int t = first; t < total; t += stride, ++it) {
-        const TileInfo ti = g.tile(t);
+        const TileInfo ti = g.template tile<kHalfTilesOf<Epi>::value>(t);
         const uint32_t as = it & 1, aph = (it >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();

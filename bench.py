@@ -82,20 +82,31 @@ class ClockSampler:
 
     def __init__(self, device):
         self.device, self.rows, self.proc = device, [], None
+        self.window = None
 
     def start(self):
+        """Started before the warm-up: nvidia-smi's own start-up (which can stall the GPU for a
+        few ms) must not land in the timed region; stop() keeps the samples taken inside it."""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device),
                                           f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=subprocess.PIPE, text=True)
+                                          "-lms", "50"], stdout=subprocess.PIPE, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 3.0:  # first sample = it runs
+                time.sleep(0.01)
+            time.sleep(0.2)
         except FileNotFoundError:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, t0, t1):
+        """the timed region (perf_counter), padded by one sampling period"""
+        self.window = (t0 - 0.05, t1 + 0.05)
 
     def stop(self):
         if not self.proc:
@@ -103,6 +114,11 @@ class ClockSampler:
         time.sleep(0.25)
         self.proc.terminate()
         self.t.join(timeout=2)
+        rows = self.rows
+        if self.window:
+            inside = [r for r in rows if self.window[0] <= r[0] <= self.window[1]]
+            rows = inside or rows
+        self.rows = [r for _, r in rows]
         sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -274,23 +290,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    clocks = ClockSampler(local)
+    clocks.start()
     losses = []
     for i in range(args.warmup):
         losses.append(step(i, True).loss)
     launches = sh.launches_per_step()
-    torch.cuda.synchronize()
-    barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
+    t_start = time.perf_counter()
     e0.record(stream)
     for i in range(args.warmup, nsteps):
         step(i, False)
     e1.record(stream)
     out = sh.sync()  # validates the last step's device status (loss finite, no errors)
     torch.cuda.synchronize()
+    clocks.mark(t_start, time.perf_counter())
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)

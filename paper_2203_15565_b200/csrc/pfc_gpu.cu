@@ -108,6 +108,7 @@ constexpr int kBN = 256;  // tcgen05 tile 128 x 256
 #define PFC_FWD_NWG 2
 #endif
 constexpr int kFwdBN = PFC_FWD_BN;    // logits GEMM tile width (classes)
+constexpr int kNarrowBN = 128;        // ... when kFwdBN-wide tiles would fill at most half the SMs
 constexpr int kFwdNWG = PFC_FWD_NWG;  // logits GEMM epilogue warpgroups (kFwdBN / 64 / kFwdNWG chunks)
 #ifndef PFC_FWD_CG
 #define PFC_FWD_CG 1
@@ -252,7 +253,7 @@ struct Ctx {
   cudaEvent_t ev_s = nullptr, ev_x = nullptr, ev_dx = nullptr, ev_out = nullptr;
   // tensor maps cached per batch
   int64_t tm_B = -1;
-  CUtensorMap tm_x_k, tm_w_k, tm_e_st, tm_e_k, tm_e_k16, tm_w_mn, tm_e_mn, tm_xs_mn;
+  CUtensorMap tm_x_k, tm_w_k, tm_w_k128, tm_e_st, tm_e_k, tm_e_k16, tm_w_mn, tm_e_mn, tm_xs_mn;
   // collectives: NCCL communicator, or the loopback group (comm.cuh)
   ncclComm_t comm = nullptr;
   std::shared_ptr<LoopGroup> loop;
@@ -468,6 +469,7 @@ int ensure_maps(Ctx* c, int64_t B) {
   // its epilogue stores E^T [ncols][ldg] (bf16: per-warp box 32 b x 32 classes, 64B swizzle)
   ok &= make_map(&c->tm_x_k, c->xh, c->Dp, B, c->Dp, 128, kb, sw, el);
   ok &= make_map(&c->tm_w_k, c->wh, c->Dp, c->ncols, c->Dp, kFwdBN / kFwdCG, kb, sw, el);
+  ok &= make_map(&c->tm_w_k128, c->wh, c->Dp, c->ncols, c->Dp, kNarrowBN / kFwdCG, kb, sw, el);
   if (c->bf16)
     ok &= make_map(&c->tm_e_st, c->G, B, c->ncols, c->ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   // dX GEMM (M = b, N = d, K = classes): A = E^T read MN-major (b contiguous); B = W^ MN-major
@@ -566,6 +568,11 @@ int dx_splits(Ctx* c, int64_t B) {
   return (int)std::min<int64_t>(s, c->max_splits);
 }
 
+// The logits GEMM with kFwdBN-wide tiles fills at most half the SMs: use kNarrowBN tiles.
+bool logits_narrow(const Ctx* c, int64_t B) {
+  return ceil_div(B, 128) * ceil_div(c->ncols, kFwdBN) * 2 <= c->num_sms;
+}
+
 // Small column counts leave most clusters idle in the dW GEMM (one per 128-class block): when
 // even twice as many blocks fit in one round, every block becomes two half tiles (64 rows, 16 per
 // TMEM lane quadrant, 4 per warp), which halves the round (10k: 0.077 -> 0.073 ms per step).  A
@@ -630,7 +637,10 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   const float tau = (float)c->d.filter_threshold;
   const bool filt = c->d.has_filter != 0;
   if (e2e) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_x, 0));
-  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, FBN, 1, 0, kUmma ? 128 * FCG : 128, BKU);
+  // small problems (the 10k CPU-reference workload: 4 tiles) take narrow tiles: twice the CTAs
+  const bool narrow = kUmma && logits_narrow(c, B);
+  const GemmGeom gf = make_geom((int)B, (int)c->ncols, (int)c->Dp, narrow ? kNarrowBN : FBN, 1, 0,
+                                kUmma ? 128 * FCG : 128, BKU);
   const bool exact = exact_now(c);
   if (exact) {
     // ---- per-row offsets: max-only pass of the logits GEMM -> o_b (rank max: collective 1,
@@ -639,10 +649,12 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
     float* pm = reinterpret_cast<float*>(c->part_s);
     cudaError_t err;
     auto go = [&](auto e) {
-      if constexpr (kUmma)
+      if constexpr (kUmma) {
+        if (narrow)
+          return launch_umma<kNarrowBN, kFwdStages, kFwdNWG, false, false, decltype(e), FCG, OT>(c, c->tm_x_k, c->tm_w_k128, gf, e);
         return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), FCG, OT>(c, c->tm_x_k, c->tm_w_k, gf, e);
-      else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
-                                            (const float*)c->wh, (int)c->Dp, gf, e);
+      } else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
+                                              (const float*)c->wh, (int)c->Dp, gf, e);
     };
     if (filt) err = go(MaxEpi<true>{{}, (int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, c->zpos});
     else err = go(MaxEpi<false>{{}, (int)B, (int)c->ncols, c->pos_col, c->mg, tau, pm, c->zpos});
@@ -657,10 +669,12 @@ int run_pipeline(Ctx* c, const float* x, const int64_t* lab, int64_t B,
   {
     cudaError_t err;
     auto go = [&](auto e) {
-      if constexpr (kUmma)
+      if constexpr (kUmma) {
+        if (narrow)
+          return launch_umma<kNarrowBN, kFwdStages, kFwdNWG, false, false, decltype(e), FCG, OT>(c, c->tm_x_k, c->tm_w_k128, gf, e);
         return launch_umma<kFwdBN, kFwdStages, kFwdNWG, false, false, decltype(e), FCG, OT>(c, c->tm_x_k, c->tm_w_k, gf, e);
-      else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
-                                            (const float*)c->wh, (int)c->Dp, gf, e);
+      } else return launch_simt<false, false>(c, (const float*)c->xh, (int)c->Dp,
+                                              (const float*)c->wh, (int)c->Dp, gf, e);
     };
     if (filt)
       err = go(FwdEpi<ST, OT, true, kUmma && !kTf>{{}, c->tm_e_st, (int)B, (int)c->ncols, (int)c->ldg, c->pos_col,
@@ -1094,7 +1108,8 @@ cudaError_t alloc_cap_buffers(Ctx* c) {
   const int64_t B = c->maxB;
   const int64_t n1 = std::max<int64_t>(c->ncols, 1);
   const int BN = c->umma ? kBN : kSimtBN;
-  const int64_t Tf = c->umma ? ceil_div(n1, kFwdBN) * kFwdNWG : ceil_div(n1, BN);
+  // (narrow logits tiles, logits_narrow, need the finer slice count)
+  const int64_t Tf = c->umma ? ceil_div(n1, kNarrowBN) * kFwdNWG : ceil_div(n1, BN);
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   A(dalloc(c, &c->buf_cls, (size_t)n1));
